@@ -1,0 +1,343 @@
+#!/usr/bin/env python
+"""Benchmark: GAT layer fwd+bwd edges/s (GTEPS) on B200 -- BASELINE.json `metric`.
+
+Workload (BASELINE.json configs[1]): 2-layer GAT training step on a
+synthetic Reddit-shaped graph -- V = 233,000, E = 114,000,000 (Chung-Lu power law,
+Zipf weights, max in-degree ~2e4), layer 1 602 -> 8 heads x 32, layer 2 256 -> 8 x 32,
+fp32, random-init weights, synthetic features.  One step = forward (both layers) +
+loss (sum of exits) + backward with recomputation + SGD update.
+
+  value  = E * layers * steps / device time of the K timed steps (inputs resident in HBM)
+  e2e    = the same metric through the public API with HOST buffers: every step copies the
+           features host->device (pinned) and reads loss + parameter gradients back
+  roofline  -> the dominant fused kernel: algorithmic bytes per launch / its CUDA-event
+               time inside the timed region, vs MEASURED_PEAKS.json hbm_gbs
+  cpu_baseline -> the oracle's f32 OpenMP port of the spec executor on a bounded sample
+
+Multi-GPU (torchrun, N > 1): weak scaling -- the graph grows with N (V*N, E*N), destination
+rows are partitioned into N edge-balanced blocks (gnncg_partition_rows), every rank
+all-gathers the transformed features each layer over NCCL (paper_2110_09524_b200.dist).
+
+`--impl reference` times the CPU port of the reference path (oracle/) on the host cores.
+"""
+from __future__ import annotations
+
+import argparse
+import json
+import os
+import statistics
+import subprocess
+import sys
+import time
+
+ROOT = os.path.dirname(os.path.abspath(__file__))
+sys.path.insert(0, ROOT)
+
+METRIC = "GAT layer fwd+bwd edges/sec (GTEPS) at 1/2/4/8 B200; fused-kernel HBM GB/s vs peak"
+UNIT = "GTEPS"
+REDDIT = dict(V=233_000, E=114_000_000, offset=1100, dims=[(602, 8, 32), (256, 8, 32)])
+CPU_SCALE = 50  # bounded CPU sample: same generator and dims with V, E (and the degree cap) / 50
+
+
+def parse():
+    ap = argparse.ArgumentParser()
+    ap.add_argument("--gpus", type=int, default=1)
+    ap.add_argument("--steps", type=int, default=10)
+    ap.add_argument("--warmup", type=int, default=3)
+    ap.add_argument("--impl", choices=["ours", "reference"], default="ours")
+    ap.add_argument("--no-cpu-baseline", action="store_true")
+    ap.add_argument("--no-e2e", action="store_true")
+    ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--scale", type=float, default=1.0, help="shrink V and E (debug only)")
+    return ap.parse_args()
+
+
+def measured_peaks():
+    path = os.path.join(ROOT, "MEASURED_PEAKS.json")
+    if os.path.exists(path):
+        with open(path) as f:
+            d = json.load(f)
+        return float(d["hbm_gbs"]), "measured (MEASURED_PEAKS.json hbm_gbs)"
+    return 6650.0, "fallback (B200_PROFILING.md 6.65 TB/s)"
+
+
+# ----------------------------------------------------------------------------- bytes model
+def gat_kernel_bytes(V: int, E: int, h: int, f: int) -> dict:
+    """Algorithmic HBM bytes per launch (fp32), per-edge-gather model of SURVEY §8d / DESIGN.md §4.
+    The per-row terms include the 8 B work item and the 8 B offsets pair."""
+    hf = h * f
+    return {
+        # K2: nbr, A_l[u], Ht[u] per edge; item, off, A_r[v] in; out, m, d out per row
+        "gat_fwd": E * (4 + 4 * h + 4 * hf) + V * (16 + 4 * h + 4 * hf + 8 * h),
+        # K3: nbr, A_l[u], Ht[u] per edge; item, off, A_r/m/d/dOut in, c/dA_r out per row
+        "gat_bwd_dst": E * (4 + 4 * h + 4 * hf) + V * (16 + 12 * h + 4 * hf + 8 * h),
+        # K4: nbr, A_r/m/d/c[v], dOut[v] per edge; item, off, A_l/Ht/dA_r in, dHt/dAl out per row
+        "gat_bwd_src": E * (4 + 16 * h + 4 * hf) + V * (16 + 8 * h + 8 * hf + 4 * h),
+    }
+
+
+# ----------------------------------------------------------------------------- clocks
+class ClockSampler:
+    Q = ("index,clocks.sm,clocks.max.sm,power.draw,clocks_event_reasons.active,"
+         "clocks_event_reasons.hw_slowdown,clocks_event_reasons.hw_thermal_slowdown,"
+         "clocks_event_reasons.sw_thermal_slowdown,clocks_event_reasons.sw_power_cap")
+
+    def __init__(self, gpu_index: int):
+        self.idx = gpu_index
+        self.p = None
+
+    def start(self):
+        try:
+            self.p = subprocess.Popen(["nvidia-smi", f"--id={self.idx}", f"--query-gpu={self.Q}",
+                                       "--format=csv,noheader,nounits", "-lms", "200"], stdout=subprocess.PIPE,
+                                      stderr=subprocess.DEVNULL, text=True)
+        except OSError:
+            self.p = None
+
+    def stop(self):
+        if self.p is None:
+            return {"sm_mhz": None, "sm_max_mhz": None, "reasons": ["nvidia-smi unavailable"]}
+        self.p.terminate()
+        out, _ = self.p.communicate(timeout=10)
+        sm, mx, reasons = [], [], set()
+        names = ["hw_slowdown", "hw_thermal_slowdown", "sw_thermal_slowdown", "sw_power_cap"]
+        for line in out.strip().splitlines():
+            parts = [x.strip() for x in line.split(",")]
+            if len(parts) < 9:
+                continue
+            try:
+                sm.append(float(parts[1]))
+                mx.append(float(parts[2]))
+            except ValueError:
+                continue
+            for n, v in zip(names, parts[5:9]):
+                if v.lower().startswith("active"):
+                    reasons.add(n)
+        return {"sm_mhz": statistics.median(sm) if sm else None, "sm_max_mhz": max(mx) if mx else None,
+                "reasons": sorted(reasons), "samples": len(sm)}
+
+
+# ----------------------------------------------------------------------------- CPU arms
+def cpu_sample_step(scale: int = CPU_SCALE, steps: int = 3, warmup: int = 1):
+    """The oracle's f32 OpenMP port (vertex_balanced, recompute backward)
+    on the Reddit-shaped generator scaled by 1/scale.  Returns (GTEPS, seconds/step, info)."""
+    import numpy as np
+
+    from oracle import oracle as O
+    from paper_2110_09524_b200.graph import chung_lu_edges_host
+
+    V, E = REDDIT["V"] // scale, REDDIT["E"] // scale
+    src, dst = chung_lu_edges_host(V, E, max(1, REDDIT["offset"] // scale), 0)
+    g = O.host_graph(V, src, dst)
+    rng = np.random.default_rng(0)
+    H = rng.uniform(-1, 1, (V, REDDIT["dims"][0][0])).astype(np.float32)
+    params = []
+    for fin, h, f in REDDIT["dims"]:
+        s = 1 / np.sqrt(h * f)
+        params.append((rng.uniform(-s, s, (fin, h * f)).astype(np.float32),
+                       rng.uniform(-1 / np.sqrt(f), 1 / np.sqrt(f), (h, f)).astype(np.float32),
+                       rng.uniform(-1 / np.sqrt(f), 1 / np.sqrt(f), (h, f)).astype(np.float32), h, f))
+
+    def step():
+        xs, fws = [H], []
+        for W, al, ar, h, f in params:
+            fw = O.gat_layer_fwd_f32_omp(g, xs[-1], W, al, ar, h, f)
+            xs.append(fw["out"])
+            fws.append(fw)
+        grad = np.ones_like(xs[-1])
+        for i in reversed(range(len(params))):
+            W, al, ar, h, f = params[i]
+            bw = O.gat_layer_bwd_f32_omp(g, xs[i], W, al, ar, h, f, fws[i], grad, need_dH=i > 0)
+            grad = bw["dH"]
+            for p_, dp in ((W, bw["dW"]), (al, bw["dal"]), (ar, bw["dar"])):
+                p_ -= np.float32(1e-4) * dp  # SGD, as in the GPU step
+
+    for _ in range(warmup):
+        step()
+    t0 = time.perf_counter()
+    for _ in range(steps):
+        step()
+    dt = (time.perf_counter() - t0) / steps
+    layers = len(REDDIT["dims"])
+    info = dict(V=V, E=E, cores=O.num_threads(),
+                sample=f"Reddit-shaped Chung-Lu scaled 1/{scale}: V={V}, E={E} (mean in-degree {E / V:.0f}), "
+                       f"dims 602->8x32->8x32, 2-layer fwd+bwd+SGD, f32, {steps} timed steps")
+    return layers * E / dt / 1e9, dt, info
+
+
+def run_reference(args):
+    rank = int(os.environ.get("RANK", "0"))
+    if rank != 0:
+        return
+    gteps, dt, info = cpu_sample_step(steps=args.steps, warmup=args.warmup)
+    line = {"impl": "reference", "metric": METRIC, "value": gteps, "unit": UNIT, "n_gpus": args.gpus,
+            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
+            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "GAT 2-layer fwd+bwd, Reddit-shaped (configs[1]) -- CPU port on a bounded sample",
+                       "V": info["V"], "E": info["E"], "layers": 2, "dims": "602->8x32, 256->8x32"},
+            "cpu_baseline": {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port",
+                             "sample": info["sample"]},
+            "e2e": {"value": gteps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    print(json.dumps(line), flush=True)
+
+
+# ----------------------------------------------------------------------------- GPU arm
+def run_ours(args):
+    import torch
+    import torch.distributed as dist
+
+    from paper_2110_09524_b200 import _lib
+    from paper_2110_09524_b200.graph import DeviceGraph
+    from paper_2110_09524_b200.models import GAT
+    from paper_2110_09524_b200.ops import PROBE
+
+    world = int(os.environ.get("WORLD_SIZE", "1"))
+    rank = int(os.environ.get("RANK", "0"))
+    local = int(os.environ.get("LOCAL_RANK", "0"))
+    torch.cuda.set_device(local)
+    dev = torch.device("cuda", local)
+    if world > 1:
+        dist.init_process_group("nccl", device_id=dev)
+    V = int(REDDIT["V"] * args.scale)
+    E = int(REDDIT["E"] * args.scale)
+    offset = max(1, int(REDDIT["offset"] * args.scale))
+    dims = REDDIT["dims"]
+    layers = len(dims)
+
+    t_build = time.perf_counter()
+    if world > 1:
+        from paper_2110_09524_b200.dist import PartitionedGAT, partitioned_chung_lu
+
+        pg = partitioned_chung_lu(V * world, E * world, offset=offset * world, seed=0, rank=rank, world=world,
+                                  device=dev)
+        model = PartitionedGAT(pg, dims, seed=1, chunk=args.chunk)
+        E_total = E * world
+        V_local = pg.num_local
+    else:
+        g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
+        model = GAT(g, dims, seed=1, chunk=args.chunk)
+        E_total = E
+        V_local = V
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+    H = torch.rand(V_local, dims[0][0], generator=gen, device=dev).mul_(2).sub_(1)
+    torch.cuda.synchronize()
+    build_s = time.perf_counter() - t_build
+
+    def barrier():
+        if world > 1:
+            dist.barrier(device_ids=[local])
+        torch.cuda.synchronize()
+
+    lr = 1e-4
+    for _ in range(args.warmup):
+        model.train_step(H, lr=lr)
+    barrier()
+    launches0 = _lib.lib().gnncg_launch_count()
+    clocks = ClockSampler(local)
+    clocks.start()
+    PROBE.reset()
+    PROBE.enabled = True
+    start, end = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+    barrier()
+    start.record()
+    for _ in range(args.steps):
+        model.train_step(H, lr=lr)
+    end.record()
+    barrier()
+    PROBE.enabled = False
+    clk = clocks.stop()
+    launches = int(_lib.lib().gnncg_launch_count() - launches0)
+    ms = start.elapsed_time(end)
+    totals = PROBE.collect()
+    if world > 1:
+        t = torch.tensor([ms], device=dev)
+        dist.all_reduce(t, op=dist.ReduceOp.MAX)
+        ms = float(t.item())
+    ms_step = ms / args.steps
+    value = E_total * layers * args.steps / (ms / 1e3) / 1e9
+
+    # --- per-kernel roofline (rank 0's graph; bytes summed over the layers) -----------
+    peak, peak_src = measured_peaks()
+    h, f = dims[0][1], dims[0][2]
+    per_launch = gat_kernel_bytes(V_local if world > 1 else V, E, h, f)
+    kernels = {}
+    for name, (tot_ms, cnt) in sorted(totals.items()):
+        k = {"ms_per_launch": tot_ms / max(cnt, 1), "launches": cnt, "share_of_step": tot_ms / ms}
+        if name in per_launch:
+            k["bytes_per_launch"] = per_launch[name]
+            k["GBps"] = per_launch[name] / (k["ms_per_launch"] / 1e3) / 1e9
+            k["frac"] = k["GBps"] / peak
+        kernels[name] = k
+    dominant = max((n for n in kernels if n in per_launch), key=lambda n: kernels[n]["share_of_step"])
+    traffic = None
+    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+    if os.path.exists(tpath):
+        with open(tpath) as fh:
+            traffic = json.load(fh).get(dominant)
+    roofline = {"bound": "hbm", "kernel": dominant, "achieved": kernels[dominant]["GBps"], "peak": peak,
+                "unit": "GB/s", "frac": kernels[dominant]["frac"], "traffic": traffic, "peak_source": peak_src}
+
+    # --- end-to-end through the public API with host buffers ----------------------------
+    e2e = None
+    if not args.no_e2e:
+        H_host = torch.empty(H.shape, dtype=torch.float32, pin_memory=True)
+        H_host.copy_(H.cpu())
+        out_bufs = None
+        s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
+        H_dev = torch.empty_like(H)
+        barrier()
+        s.record()
+        for _ in range(args.steps):
+            H_dev.copy_(H_host, non_blocking=True)
+            loss, grads = model.train_step(H_dev, lr=lr)
+            res = [loss] + [t for gr in grads for t in (gr.dW, gr.da_l, gr.da_r)]
+            if out_bufs is None:
+                out_bufs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
+            for hb, t in zip(out_bufs, res):
+                hb.copy_(t, non_blocking=True)
+        e.record()
+        barrier()
+        ems = s.elapsed_time(e)
+        if world > 1:
+            t = torch.tensor([ems], device=dev)
+            dist.all_reduce(t, op=dist.ReduceOp.MAX)
+            ems = float(t.item())
+        e2e = {"value": E_total * layers * args.steps / (ems / 1e3) / 1e9, "unit": UNIT,
+               "h2d_bytes_per_step": H.numel() * 4, "d2h_bytes_per_step": sum(b.numel() * 4 for b in out_bufs),
+               "ms_per_step": ems / args.steps}
+
+    cpu = None
+    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+        gteps, dt, info = cpu_sample_step()
+        cpu = {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port", "sample": info["sample"],
+               "s_per_step": dt}
+
+    if rank == 0:
+        line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Chung-Lu graph, uniform features, "
+                "random-init weights)",
+                "config": {"workload": "GAT 2-layer fwd+bwd+SGD, Reddit-shaped (BASELINE configs[1])",
+                           "V": V * world, "E": E_total, "layers": layers, "dims": "602->8x32, 256->8x32",
+                           "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0", "parallelism":
+                           f"row-partition x{world}" if world > 1 else "single GPU",
+                           "l2": "inputs larger than L2 (H 561 MB, index 912 MB per direction)",
+                           "chunk": args.chunk or 2048, "graph_build_s": build_s},
+                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                "gpu_launches": launches, "clocks": clk}
+        print(json.dumps(line), flush=True)
+    if world > 1:
+        dist.destroy_process_group()
+
+
+def main():
+    args = parse()
+    if args.impl == "reference":
+        run_reference(args)
+    else:
+        run_ours(args)
+
+
+if __name__ == "__main__":
+    main()

@@ -1,0 +1,227 @@
+/* SPDX-License-Identifier: Apache-2.0
+ *
+ * gnncg_b200.h -- C ABI of the B200-native (sm_100a) fused GNN layer path.
+ *
+ * This is the drop-in boundary for the reference's fused-layer path.  The
+ * reference ("gnncg", /root/reference/proj) specifies -- but does not ship -- an
+ * executor that runs the fused GAT / EdgeConv / GMMConv graph regions over its
+ * dual index.  Every entry point below replaces one operation
+ * of that executor or of the graph/tensor layer it sits on; the replaced
+ * interface is cited (file:line) beside each declaration.
+ *
+ * Conventions (identical to the reference's data model):
+ *   - an index is gnncg::AdjIndex (graph.hpp:19-29) split to SoA:
+ *       off[rows+1] = AdjIndex::offsets, nbr[E] = entries[i].vertex,
+ *       eid[E] = entries[i].edge; rows are sorted by edge id (graph.hpp:26).
+ *   - tensors are row-major gnncg::Tensor<float> (tensor.hpp:20-35); multi-head
+ *     features are flattened head-major, cols = h*f, column j -> head j/f
+ *     (tensor.hpp:17-19,99-121).
+ *   - LeakyReLU(z) = z > 0 ? z : slope*z (tensor.hpp:75), slope default 0.2.
+ *   - every pointer argument is DEVICE memory unless the name ends in _host.
+ *   - calls are asynchronous on the given stream (a cudaStream_t passed as
+ *     void*; NULL = legacy default stream).  The library never allocates device
+ *     memory inside compute calls; scratch comes from the caller's workspace,
+ *     sized by the matching *_workspace() query.
+ *   - errors: the return value is a gnncg_status; gnncg_last_error() returns a
+ *     thread-local message.  Shape errors correspond to the reference's
+ *     TensorError (tensor.hpp:13-15), range errors to GraphError (graph.hpp:14-16).
+ *     There is no CPU fallback: without an sm_100 device every compute call
+ *     returns GNNCG_ERR_NO_DEVICE.
+ *
+ * Row partitioning (multi-GPU): a call may process a contiguous block of
+ * destination rows.  "Destination-side" tensors (indexed by an index row of
+ * csr_dst: out, m, d, A_r, dOut, c, dA_r) are LOCAL (row 0 = first row of the
+ * block); "source-side" tensors (indexed by a neighbour id of csr_dst: Ht, A_l)
+ * are GLOBAL.  A single-GPU caller simply passes the whole graph.
+ */
+#ifndef GNNCG_B200_H_
+#define GNNCG_B200_H_
+
+#include <stddef.h>
+#include <stdint.h>
+
+#ifdef __cplusplus
+extern "C" {
+#endif
+
+typedef enum gnncg_status {
+  GNNCG_OK = 0,
+  GNNCG_ERR_SHAPE = 1,       /* TensorError: shape / width mismatch (tensor.hpp:13-15) */
+  GNNCG_ERR_RANGE = 2,       /* GraphError: endpoint out of range (graph.cpp:37-39) */
+  GNNCG_ERR_NO_DEVICE = 3,   /* no sm_100 device visible: no CPU fallback exists */
+  GNNCG_ERR_CUDA = 4,        /* CUDA runtime / launch failure */
+  GNNCG_ERR_WORKSPACE = 5,   /* caller workspace smaller than the *_workspace() query */
+  GNNCG_ERR_UNSUPPORTED = 6, /* shape outside the compiled kernel variants */
+  GNNCG_ERR_ARG = 7          /* null pointer / invalid argument */
+} gnncg_status;
+
+/* One adjacency index (AdjIndex, graph.hpp:19-29), possibly a row block of it. */
+typedef struct gnncg_index {
+  int64_t num_rows;    /* rows processed (block length; V for a whole index) */
+  int64_t num_edges;   /* off[num_rows] - off[0]; off[0] must be 0 (rebased block) */
+  const uint64_t* off; /* num_rows + 1 */
+  const uint32_t* nbr; /* AdjEntry::vertex */
+  const uint32_t* eid; /* AdjEntry::edge; may be NULL where unused */
+} gnncg_index_t;
+
+/* Edge-balance schedule over one index: "unified thread mapping" work items
+ * (one warp each).  Rows with more than `chunk` edges are split into several
+ * items whose partial results are merged deterministically in chunk order --
+ * the reference's ReductionBuffer contract applied to the
+ * fused region, which the online-softmax merge makes legal for GAT
+ * (cf. SPEC.md:267-268).  Built on the host by gnncg_sched_build_host(). */
+typedef struct gnncg_sched {
+  int64_t num_items;       /* total work items */
+  int64_t num_split_items; /* items [0, num_split_items) belong to split rows */
+  int64_t num_split_rows;
+  int32_t chunk;           /* max edges per item */
+  int32_t reserved;
+  const uint32_t* items;       /* 2*num_items: (row, chunk index) pairs */
+  const uint32_t* split_rows;  /* num_split_rows row ids */
+  const uint32_t* split_first; /* num_split_rows+1 item offsets into [0, num_split_items) */
+} gnncg_sched_t;
+
+/* ---------------------------------------------------------------- runtime */
+const char* gnncg_last_error(void);
+const char* gnncg_version(void);
+/* GNNCG_OK iff an sm_100 (B200) device is current. */
+int gnncg_device_check(void);
+/* Number of kernels this library has launched in the process (instrumentation). */
+uint64_t gnncg_launch_count(void);
+
+/* ------------------------------------------------------- graph store (K9)
+ * Replaces build_index (graph.cpp:14-28) and the Graph ctor (graph.cpp:32-45).
+ * Counting sort by key vertex, stable in edge id -> bit-identical to the
+ * reference's AdjIndex.  key/other/off/nbr/eid are device arrays.  Returns
+ * GNNCG_ERR_RANGE if any endpoint >= V (the reference's GraphError). */
+size_t gnncg_csr_build_workspace(int64_t num_vertices, int64_t num_edges);
+int gnncg_csr_build(int64_t num_vertices, int64_t num_edges, const uint32_t* key, const uint32_t* other,
+                    uint64_t* off, uint32_t* nbr, uint32_t* eid, void* workspace, size_t workspace_bytes,
+                    void* stream);
+
+/* degree_stats (graph.cpp:47-57) over a device index: out_host[0] = max degree
+ * of `idx` (blocking call; stream is synchronised). */
+int gnncg_max_degree(const gnncg_index_t* idx, uint64_t* max_degree_host, void* stream);
+
+/* Row-block partitioner (new): P contiguous row blocks with
+ * balanced edge counts, bound[p] = lower_bound(off, ceil(p*E/P)), bound[P] = V.
+ * off_host/bound_host are host arrays. */
+int gnncg_partition_rows(int64_t num_rows, const uint64_t* off_host, int32_t parts, uint64_t* bound_host);
+
+/* Deterministic Chung-Lu edge generator (device): edge e draws its destination
+ * and source independently from the integer weight CDF `cdf` (device, V entries,
+ * inclusive prefix sums of positive weights), using the counter-based hash
+ * splitmix64(seed, e).  Same edge list for the same (cdf, seed) on any device. */
+int gnncg_gen_chung_lu(int64_t num_vertices, int64_t num_edges, const uint64_t* cdf, uint64_t seed, uint32_t* src,
+                       uint32_t* dst, void* stream);
+
+/* Schedule construction on the host from a host copy of the offsets.
+ * First call with items_host == NULL to get the counts, then with arrays sized
+ * 2*num_items, num_split_rows, num_split_rows+1. */
+int gnncg_sched_build_host(int64_t num_rows, const uint64_t* off_host, int32_t chunk, int64_t* num_items,
+                           int64_t* num_split_items, int64_t* num_split_rows, uint32_t* items_host,
+                           uint32_t* split_rows_host, uint32_t* split_first_host);
+
+/* ------------------------------------------------- dense transforms (K1/K5)
+ * C[M,N] = op(A)[M,K] * op(B)[K,N], fp32 in / fp32 accumulate / fp32 out.
+ * trans_a = 0: A is M x K (lda >= K);  trans_a = 1: A is K x M (lda >= M).
+ * trans_b = 0: B is K x N (ldb >= N);  trans_b = 1: B is N x K (ldb >= K).
+ * (0,0) = matmul (tensor.cpp:8-24); (0,1) = matmul_nt (tensor.cpp:26-42);
+ * (1,0) = matmul_tn (tensor.cpp:44-60).  Deterministic (fixed-order split-K). */
+size_t gnncg_gemm_workspace(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K);
+int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, void* workspace, size_t workspace_bytes,
+               void* stream);
+
+/* ------------------------------------------------------------------ GAT
+ * Reorganized attention LPs:
+ *   A_l[v,k] = <Ht[v,k,:], a_l[k,:]>, A_r[v,k] = <Ht[v,k,:], a_r[k,:]>. */
+int gnncg_gat_attn_dots(int64_t num_rows, int heads, int f, const float* Ht, const float* a_l, const float* a_r,
+                        float* Al, float* Ar, void* stream);
+
+/* Scratch for the split-row partials of all GAT kernels over these schedules. */
+size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* src_sched, int heads, int f);
+
+/* K2: the fused region Scatter(u_add_v) -> ApplyEdge(LeakyReLU) ->
+ * ReduceScatter(edge-softmax RS1/RS2) -> Aggregate(sum) in ONE kernel
+ * (PAPER.md:316-319,555-558), vertex-balanced with the
+ * edge-balance split of `sched`.  Stashes only m, d (V x h).
+ *   out[v,k,:] = sum_e softmax_v(LReLU(A_l[u,k] + A_r[v,k])) * Ht[u,k,:]
+ * Empty rows: out = 0, m = d = 0. */
+int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int heads, int f, float slope,
+                  const float* Ht, const float* Al, const float* Ar, float* out, float* m, float* d,
+                  void* workspace, size_t workspace_bytes, void* stream);
+
+/* K3: backward pass 1 over csr_dst (derive_backward + plan_recompute,
+ * SPEC.md:187-195,273-281,352-360): edge values recomputed from (A_l, A_r, m, d);
+ *   c[v,k]   = sum_e alpha_e <dOut[v,k,:], Ht[u,k,:]>
+ *   dA_r[v,k] = sum_e LReLU'(z_e) alpha_e (dalpha_e - c[v,k]) */
+int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int heads, int f, float slope,
+                      const float* Ht, const float* Al, const float* Ar, const float* m, const float* d,
+                      const float* dOut, float* c, float* dAr, void* workspace, size_t workspace_bytes,
+                      void* stream);
+
+/* K4: backward pass 2 over csc_src (Scatter backward = Gather over out-edges,
+ * PAPER.md:638-649).  Rows are GLOBAL source ids u; neighbours are LOCAL
+ * destination rows of the block [row_base, row_base + num_local_rows).
+ *   dA_l[u,k] = sum_e LReLU'(z_e) alpha_e (dalpha_e - c[v,k])
+ *   dHt[u,:]  = sum_e alpha_e dOut[v,:] + dA_l[u] (x) a_l + dA_r[u] (x) a_r
+ * (the dA_r term only for u inside the local block).  In a multi-GPU run the
+ * outputs are partial sums to be reduce-scattered (they are linear). */
+int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int heads, int f, float slope,
+                      int64_t row_base, int64_t num_local_rows, const float* Ht, const float* Al, const float* Ar,
+                      const float* m, const float* d, const float* c, const float* dOut, const float* dAr,
+                      const float* a_l, const float* a_r, float* dHt, float* dAl, void* workspace,
+                      size_t workspace_bytes, void* stream);
+
+/* da_l[k,:] = sum_v dA_l[v,k] Ht[v,k,:] ; da_r likewise (LP parameter grads). */
+size_t gnncg_gat_attn_grad_workspace(int64_t num_rows, int heads, int f);
+int gnncg_gat_attn_grad(int64_t num_rows, int heads, int f, const float* Ht, const float* dAl, const float* dAr,
+                        float* da_l, float* da_r, void* workspace, size_t workspace_bytes, void* stream);
+
+/* -------------------------------------------------------------- EdgeConv
+ * K6 (reorganized per SPEC.md:261): Th = H Theta, Ph = H Phi
+ * precomputed (packed as Y = [Th | Ph], row stride ldy).
+ *   out[v,c] = max_e ((Th[u,c] - Th[v,c]) + Ph[v,c])  evaluated in fp32 RN
+ *   argmax[v,c] = edge id of the lowest-eid maximiser, or
+ *   0xFFFFFFFF with out = 0 for an empty row.  Bit-exact.
+ * Th is indexed by global ids, Ph / out / argmax by local rows. */
+int gnncg_edgeconv_fwd(const gnncg_index_t* csr_dst, int channels, int64_t row_base, const float* Th,
+                       int64_t ld_th, const float* Ph, int64_t ld_ph, float* out, uint32_t* argmax, void* stream);
+
+/* K7: Gather(max) backward by argmax routing, atomic-free
+ * (inverse-argmax gather over csc_src, needs csc_src.eid):
+ *   dTh[u,c] = sum_{(v,e) in out(u), argmax[v,c]==e} g[v,c] - [deg_in(u)>0] g[u,c]
+ *   dPh[u,c] = [deg_in(u)>0] g[u,c] */
+int gnncg_edgeconv_bwd(const gnncg_index_t* csc_src, const gnncg_index_t* csr_dst, int channels,
+                       const uint32_t* argmax, const float* grad, float* dTh, int64_t ld_dth, float* dPh,
+                       int64_t ld_dph, void* stream);
+
+/* --------------------------------------------------------------- GMMConv
+ * K8: Y = H [W | P_l | P_r] packed, row stride
+ * ldy = K*f + 2r: hW = Y[:, :K*f], pl = Y[:, K*f:K*f+r], pr = Y[:, K*f+r:].
+ *   w_k(m) = exp(-1/2 sum_d (m_d - mu_kd)^2 sinv_kd^2),  m = pl[u] + pr[v]
+ *   out[v,:] = (1/K) sum_e sum_k w_k hW[u,k,:] */
+int gnncg_gmm_fwd(const gnncg_index_t* csr_dst, int kernels, int r, int f, const float* Y, int64_t ldy,
+                  const float* mu, const float* sinv, float* out, void* stream);
+
+size_t gnncg_gmm_bwd_workspace(const gnncg_index_t* csr_dst, int kernels, int r);
+/* Backward: dY (same packing as Y) and parameter grads dmu, dsinv (K x r).
+ * pass 1 over csr_dst -> d pr, dmu, dsinv ; pass 2 over csc_src -> d hW, d pl. */
+int gnncg_gmm_bwd(const gnncg_index_t* csr_dst, const gnncg_index_t* csc_src, int kernels, int r, int f,
+                  const float* Y, int64_t ldy, const float* mu, const float* sinv, const float* dOut, float* dY,
+                  float* dmu, float* dsinv, void* workspace, size_t workspace_bytes, void* stream);
+
+/* ------------------------------------------------- training-step helpers */
+/* params -= lr * grad  (train_step). */
+int gnncg_sgd_update(int64_t n, float lr, const float* grad, float* param, void* stream);
+/* x[0..n) = value (x 16-byte aligned); e.g. the all-ones seed gradient. */
+int gnncg_fill(int64_t n, float value, float* x, void* stream);
+/* *out = sum of x[0..n) (loss = sum of exits); fixed-order, bitwise reproducible. */
+size_t gnncg_sum_workspace(void);
+int gnncg_sum(int64_t n, const float* x, float* out, void* workspace, size_t workspace_bytes, void* stream);
+
+#ifdef __cplusplus
+}
+#endif
+#endif /* GNNCG_B200_H_ */

@@ -1,0 +1,143 @@
+"""ctypes binding of include/gnncg_b200.h (libgnncg_b200.so, built in-tree).
+
+The product path has exactly one compute backend: the sm_100a kernels in this
+library.  If the library is missing or no B200 is visible, every call raises --
+there is no CPU fallback.
+"""
+from __future__ import annotations
+
+import ctypes as C
+import os
+
+_HERE = os.path.dirname(os.path.abspath(__file__))
+LIB_PATH = os.path.join(_HERE, "libgnncg_b200.so")
+
+i32, i64, u32, u64, f32, sz, vp = C.c_int, C.c_int64, C.c_uint32, C.c_uint64, C.c_float, C.c_size_t, C.c_void_p
+
+
+class GnncgError(RuntimeError):
+    """Base error of the C ABI (status != GNNCG_OK)."""
+
+    status = -1
+
+
+class TensorError(GnncgError):
+    """Shape mismatch -- the reference's gnncg::TensorError (tensor.hpp:13-15)."""
+
+    status = 1
+
+
+class GraphError(GnncgError):
+    """Endpoint out of range -- the reference's gnncg::GraphError (graph.hpp:14-16)."""
+
+    status = 2
+
+
+class DeviceError(GnncgError):
+    """No sm_100 device: the library has no CPU fallback."""
+
+    status = 3
+
+
+class CudaError(GnncgError):
+    status = 4
+
+
+class WorkspaceError(GnncgError):
+    status = 5
+
+
+class UnsupportedError(GnncgError):
+    status = 6
+
+
+class ArgumentError(GnncgError):
+    status = 7
+
+
+_ERRORS = {c.status: c for c in (TensorError, GraphError, DeviceError, CudaError, WorkspaceError, UnsupportedError,
+                                 ArgumentError)}
+
+
+class Index(C.Structure):
+    """gnncg_index_t -- one AdjIndex (graph.hpp:19-29) split to SoA."""
+
+    _fields_ = [("num_rows", i64), ("num_edges", i64), ("off", vp), ("nbr", vp), ("eid", vp)]
+
+
+class Sched(C.Structure):
+    """gnncg_sched_t -- edge-balance work items of the unified thread mapping."""
+
+    _fields_ = [("num_items", i64), ("num_split_items", i64), ("num_split_rows", i64), ("chunk", i32),
+                ("reserved", i32), ("items", vp), ("split_rows", vp), ("split_first", vp)]
+
+
+P = C.POINTER
+_SIGS = {
+    "gnncg_last_error": ([], C.c_char_p),
+    "gnncg_version": ([], C.c_char_p),
+    "gnncg_device_check": ([], i32),
+    "gnncg_launch_count": ([], u64),
+    "gnncg_csr_build_workspace": ([i64, i64], sz),
+    "gnncg_csr_build": ([i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_max_degree": ([P(Index), P(u64), vp], i32),
+    "gnncg_partition_rows": ([i64, vp, i32, vp], i32),
+    "gnncg_gen_chung_lu": ([i64, i64, vp, u64, vp, vp, vp], i32),
+    "gnncg_sched_build_host": ([i64, vp, i32, P(i64), P(i64), P(i64), vp, vp, vp], i32),
+    "gnncg_gemm_workspace": ([i32, i32, i64, i64, i64], sz),
+    "gnncg_gemm": ([i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], i32),
+    "gnncg_gat_attn_dots": ([i64, i32, i32, vp, vp, vp, vp, vp, vp], i32),
+    "gnncg_gat_workspace": ([P(Sched), P(Sched), i32, i32], sz),
+    "gnncg_gat_fwd": ([P(Index), P(Sched), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_gat_bwd_dst": ([P(Index), P(Sched), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_gat_bwd_src": ([P(Index), P(Sched), i32, i32, f32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                           vp, vp, sz, vp], i32),
+    "gnncg_gat_attn_grad_workspace": ([i64, i32, i32], sz),
+    "gnncg_gat_attn_grad": ([i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_edgeconv_fwd": ([P(Index), i32, i64, vp, i64, vp, i64, vp, vp, vp], i32),
+    "gnncg_edgeconv_bwd": ([P(Index), P(Index), i32, vp, vp, vp, i64, vp, i64, vp], i32),
+    "gnncg_gmm_fwd": ([P(Index), i32, i32, i32, vp, i64, vp, vp, vp, vp], i32),
+    "gnncg_gmm_bwd_workspace": ([P(Index), i32, i32], sz),
+    "gnncg_gmm_bwd": ([P(Index), P(Index), i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_sgd_update": ([i64, f32, vp, vp, vp], i32),
+    "gnncg_fill": ([i64, f32, vp, vp], i32),
+    "gnncg_sum_workspace": ([], sz),
+    "gnncg_sum": ([i64, vp, vp, vp, sz, vp], i32),
+}
+
+EXPORTED = tuple(_SIGS)
+
+_lib = None
+
+
+def lib():
+    """Load libgnncg_b200.so (in-tree) and declare every exported signature."""
+    global _lib
+    if _lib is None:
+        if not os.path.exists(LIB_PATH):
+            raise DeviceError(f"{LIB_PATH} is missing: run __graft_entry__.build() (no CPU fallback exists)")
+        L = C.CDLL(LIB_PATH)
+        for name, (args, res) in _SIGS.items():
+            fn = getattr(L, name)
+            fn.argtypes = args
+            fn.restype = res
+        _lib = L
+    return _lib
+
+
+def last_error() -> str:
+    return lib().gnncg_last_error().decode(errors="replace")
+
+
+def check(rc: int, what: str = ""):
+    if rc != 0:
+        cls = _ERRORS.get(rc, GnncgError)
+        raise cls(f"{what}: {last_error()}" if what else last_error())
+
+
+def call(name: str, *args):
+    check(getattr(lib(), name)(*args), name)
+
+
+def require_device():
+    check(lib().gnncg_device_check(), "gnncg_device_check")

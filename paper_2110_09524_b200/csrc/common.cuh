@@ -1,0 +1,103 @@
+// SPDX-License-Identifier: Apache-2.0
+// Shared helpers for the sm_100a kernels behind include/gnncg_b200.h.
+#pragma once
+
+#include <cuda_runtime.h>
+#include <stdint.h>
+
+#include <cstdio>
+#include <string>
+
+#include "gnncg_b200.h"
+
+namespace gnncg_b200 {
+
+// Thread-local error message behind gnncg_last_error().
+void set_error(const char* fmt, ...);
+int fail(int status, const char* fmt, ...);
+
+inline cudaStream_t as_stream(void* s) { return reinterpret_cast<cudaStream_t>(s); }
+
+// Every compute entry point starts with this: no device => no CPU fallback.
+int require_device();
+
+#define GNNCG_CUDA_TRY(expr)                                                                   \
+  do {                                                                                         \
+    cudaError_t err__ = (expr);                                                                \
+    if (err__ != cudaSuccess)                                                                  \
+      return ::gnncg_b200::fail(GNNCG_ERR_CUDA, "%s:%d %s: %s", __FILE__, __LINE__, #expr,     \
+                                cudaGetErrorString(err__));                                    \
+  } while (0)
+
+// Counts every kernel this library launches (gnncg_launch_count()).
+void note_launch();
+
+#define GNNCG_LAUNCH_CHECK()                     \
+  do {                                           \
+    ::gnncg_b200::note_launch();                 \
+    GNNCG_CUDA_TRY(cudaGetLastError());          \
+  } while (0)
+
+#define GNNCG_REQUIRE(cond, status, ...)                \
+  do {                                                  \
+    if (!(cond)) return ::gnncg_b200::fail(status, __VA_ARGS__); \
+  } while (0)
+
+#define GNNCG_DEVICE_GUARD()                   \
+  do {                                         \
+    int rc__ = ::gnncg_b200::require_device(); \
+    if (rc__ != GNNCG_OK) return rc__;         \
+  } while (0)
+
+constexpr int kWarp = 32;
+
+__device__ __forceinline__ float lrelu(float z, float slope) { return z > 0.f ? z : slope * z; }
+__device__ __forceinline__ float lrelu_grad(float z, float slope) { return z > 0.f ? 1.f : slope; }
+
+__device__ __forceinline__ float warp_max(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v = fmaxf(v, __shfl_xor_sync(0xffffffffu, v, o));
+  return v;
+}
+__device__ __forceinline__ float warp_sum(float v) {
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) v += __shfl_xor_sync(0xffffffffu, v, o);
+  return v;
+}
+
+// Vector of VW consecutive floats (VW in {1,2,4}), read-only path.
+template <int VW>
+struct Vec {
+  float x[VW];
+};
+
+template <int VW>
+__device__ __forceinline__ Vec<VW> ldg_vec(const float* p) {
+  Vec<VW> r;
+  if constexpr (VW == 4) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+  } else if constexpr (VW == 2) {
+    const float2 t = __ldg(reinterpret_cast<const float2*>(p));
+    r.x[0] = t.x; r.x[1] = t.y;
+  } else {
+    r.x[0] = __ldg(p);
+  }
+  return r;
+}
+
+template <int VW>
+__device__ __forceinline__ void st_vec(float* p, const Vec<VW>& v) {
+  if constexpr (VW == 4) {
+    *reinterpret_cast<float4*>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
+  } else if constexpr (VW == 2) {
+    *reinterpret_cast<float2*>(p) = make_float2(v.x[0], v.x[1]);
+  } else {
+    *p = v.x[0];
+  }
+}
+
+__host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
+inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
+
+}  // namespace gnncg_b200

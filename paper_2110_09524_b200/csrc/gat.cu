@@ -1,0 +1,864 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// GAT fused graph region on sm_100a: forward (K2) and the two-pass recompute
+// backward (K3 over csr_dst, K4 over csc_src), plus the reorganized attention
+// LPs and their parameter gradients.
+//
+// Semantics follow the reference's specification (the executor that would run
+// this region, src/executor.cpp, is absent from the reference):
+//   fused region 
+//   edge-softmax      RS1 (max) / RS2 (sum)
+//   recompute plan    stash m, d (O(|V|)); recompute scores and weights
+//   backward rules    PAPER.md:615-662 ; empty rows SPEC.md:213
+//
+// Unified thread mapping: one warp per work item (a whole
+// destination row, or a <= chunk-edge slice of a hub row; see gnncg_sched_t).
+// Inside a work item the warp alternates two lane mappings:
+//   * edge mapping   -- lane j owns edge j of a 32-edge block: gathers the
+//     neighbour id and the h attention logits, evaluates LeakyReLU / exp for all
+//     heads, writes the 32 x h edge weights to a per-warp shared-memory table;
+//   * column mapping -- lane owns NV vectors of VW consecutive feature columns
+//     (coalesced 16-byte loads); walks the 32 edges, gathering the neighbour's
+//     feature row and FMA-ing it with the edge weight read from shared memory.
+// No per-edge value ever reaches HBM; only O(|V| h) statistics are stashed.
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace gnncg_b200 {
+namespace {
+
+constexpr int MAXH = 8;          // compiled head limit
+constexpr int TS = MAXH + 1;     // padded row of the per-warp edge tables (bank-conflict free)
+constexpr int WARPS = 8;         // warps per CTA
+constexpr int THREADS = WARPS * kWarp;
+
+struct WarpSmem {
+  uint32_t nb[kWarp];
+  float t0[kWarp * TS];
+  float t1[kWarp * TS];
+  float red[8 * kWarp];
+  float stat[4][MAXH];
+};
+
+struct Item {
+  uint32_t row;
+  uint64_t e0, e1;
+  bool split;
+};
+
+__device__ __forceinline__ Item decode_item(const uint32_t* __restrict__ items, const uint64_t* __restrict__ off,
+                                            int64_t wi, int64_t num_split_items, int chunk) {
+  Item it;
+  it.row = __ldg(items + 2 * wi);
+  const uint32_t ch = __ldg(items + 2 * wi + 1);
+  const uint64_t rb = __ldg(off + it.row), re = __ldg(off + it.row + 1);
+  it.e0 = rb + (uint64_t)ch * (uint64_t)chunk;
+  it.e1 = min(re, it.e0 + (uint64_t)chunk);
+  it.split = wi < num_split_items;
+  return it;
+}
+
+// h per-vertex values p[0..h) into registers (vectorised when possible).
+__device__ __forceinline__ void load_heads(const float* __restrict__ p, int h, float (&v)[MAXH]) {
+  if (h == 8) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else if (h == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+#pragma unroll
+    for (int k = 4; k < MAXH; ++k) v[k] = 0.f;
+  } else {
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) v[k] = k < h ? __ldg(p + k) : 0.f;
+  }
+}
+
+// Sum, for head `k`, of red[] entries belonging to that head (vector index
+// range [k*f/VW, (k+1)*f/VW) of the flattened lane-vector numbering).
+template <int VW>
+__device__ __forceinline__ float head_sum(const float* red, int k, int f) {
+  const int per = f / VW;
+  float s = 0.f;
+  for (int q = k * per; q < (k + 1) * per; ++q) s += red[q];
+  return s;
+}
+
+struct GatParams {
+  const uint64_t* off;
+  const uint32_t* nbr;
+  const uint32_t* items;
+  int64_t num_items, num_split_items;
+  int chunk, h, f;
+  float slope;
+  const float *Ht, *Al, *Ar, *m, *d, *c, *dOut, *dAr, *a_l, *a_r;
+  float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
+  float* part;  // split-row partials
+  int64_t row_base, num_local;
+};
+
+// ---------------------------------------------------------------------------
+// K2: forward.
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS) gat_fwd_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+
+  float arv[MAXH];
+  load_heads(p.Ar + (int64_t)it.row * h, h, arv);
+
+  // RS1/RS2 over the item's edges, lanes over edges (online max/sum, merged once).
+  float M[MAXH], S[MAXH];
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) { M[k] = -FLT_MAX; S[k] = 0.f; }
+  for (uint64_t e = it.e0 + lane; e < it.e1; e += 32) {
+    const uint32_t u = __ldg(p.nbr + e);
+    float al[MAXH];
+    load_heads(p.Al + (int64_t)u * h, h, al);
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) {
+      if (k < h) {
+        const float s = lrelu(al[k] + arv[k], slope);
+        if (s > M[k]) { S[k] = S[k] * __expf(M[k] - s) + 1.f; M[k] = s; }
+        else S[k] += __expf(s - M[k]);
+      }
+    }
+  }
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) {
+    if (k < h) {
+      const float mk = warp_max(M[k]);
+      S[k] = warp_sum(S[k] * __expf(M[k] - mk));
+      M[k] = mk;
+    }
+  }
+
+  // Aggregate: column mapping over 32-edge blocks.
+  int colv[NV], hdv[NV];
+  bool okv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    colv[i] = (i * 32 + lane) * VW;
+    okv[i] = colv[i] < hf;
+    hdv[i] = okv[i] ? colv[i] / f : 0;
+  }
+  Vec<VW> acc[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) acc[i].x[q] = 0.f;
+
+  constexpr int U = NV >= 4 ? 2 : 4;
+  for (uint64_t base = it.e0; base < it.e1; base += 32) {
+    const int n = (int)min((uint64_t)32, it.e1 - base);
+    if (lane < n) {
+      const uint32_t u = __ldg(p.nbr + base + lane);
+      sm.nb[lane] = u;
+      float al[MAXH];
+      load_heads(p.Al + (int64_t)u * h, h, al);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k)
+        if (k < h) sm.t0[lane * TS + k] = __expf(lrelu(al[k] + arv[k], slope) - M[k]);
+    }
+    __syncwarp();
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> x[U][NV];
+      float a[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const float* row = p.Ht + (int64_t)sm.nb[j + t] * hf;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          if (okv[i]) x[t][i] = ldg_vec<VW>(row + colv[i]);
+          else
+#pragma unroll
+            for (int q = 0; q < VW; ++q) x[t][i].x[q] = 0.f;
+          a[t][i] = sm.t0[(j + t) * TS + hdv[i]];
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+#pragma unroll
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a[t][i], x[t][i].x[q], acc[i].x[q]);
+    }
+    for (; j < n; ++j) {
+      const float* row = p.Ht + (int64_t)sm.nb[j] * hf;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        if (okv[i]) {
+          const Vec<VW> x = ldg_vec<VW>(row + colv[i]);
+          const float a = sm.t0[j * TS + hdv[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x.x[q], acc[i].x[q]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+
+  const bool empty = it.e0 == it.e1;
+  if (lane == 0) {
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k)
+      if (k < h) { sm.stat[0][k] = empty ? 0.f : M[k]; sm.stat[1][k] = S[k]; }
+  }
+  __syncwarp();
+  if (!it.split) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (okv[i]) {
+        const float den = sm.stat[1][hdv[i]];
+        const float inv = den > 0.f ? 1.f / den : 0.f;
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
+        st_vec<VW>(p.out + (int64_t)it.row * hf + colv[i], o);
+      }
+    }
+    if (lane < h) {
+      p.mo[(int64_t)it.row * h + lane] = sm.stat[0][lane];
+      p.dd[(int64_t)it.row * h + lane] = sm.stat[1][lane];
+    }
+  } else {
+    float* part = p.part + wi * (int64_t)(hf + 2 * h);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (okv[i]) st_vec<VW>(part + colv[i], acc[i]);
+    if (lane < h) {
+      part[hf + lane] = sm.stat[0][lane];
+      part[hf + h + lane] = sm.stat[1][lane];
+    }
+  }
+}
+
+// Merge of split-row partials (forward): online-softmax combination in chunk order.
+__global__ void gat_fwd_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
+                                     const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
+  __shared__ float st[WARPS][2][MAXH];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
+  if (sr >= num_split_rows) return;
+  const int h = p.h, f = p.f, hf = h * f;
+  const int64_t stride = hf + 2 * h;
+  const uint32_t row = split_rows[sr];
+  const int64_t i0 = split_first[sr], i1 = split_first[sr + 1];
+  if (lane < h) {
+    float mk = -FLT_MAX;
+    for (int64_t it = i0; it < i1; ++it) mk = fmaxf(mk, p.part[it * stride + hf + lane]);
+    float sk = 0.f;
+    for (int64_t it = i0; it < i1; ++it)
+      sk += p.part[it * stride + hf + h + lane] * __expf(p.part[it * stride + hf + lane] - mk);
+    st[w][0][lane] = mk;
+    st[w][1][lane] = sk;
+    p.mo[(int64_t)row * h + lane] = mk;
+    p.dd[(int64_t)row * h + lane] = sk;
+  }
+  __syncwarp();
+  for (int c = lane; c < hf; c += 32) {
+    const int hd = c / f;
+    const float mk = st[w][0][hd], sk = st[w][1][hd];
+    float s = 0.f;
+    for (int64_t it = i0; it < i1; ++it) s += p.part[it * stride + c] * __expf(p.part[it * stride + hf + hd] - mk);
+    p.out[(int64_t)row * hf + c] = sk > 0.f ? s / sk : 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: backward pass 1 over csr_dst.  Per destination v, with alpha recomputed:
+//   c = sum alpha <g, x_u> = <g, sum alpha x_u>,   P = <g, sum LReLU'(z) alpha x_u>,
+//   Q = sum LReLU'(z) alpha,   dA_r = P - c Q
+// (the column phase only accumulates sum alpha x_u and sum gate*alpha x_u; the
+// dot with g = dOut[v] happens once per row, not per edge).
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS) gat_bwd_dst_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+
+  float arv[MAXH], mv[MAXH], invd[MAXH], Q[MAXH];
+  load_heads(p.Ar + (int64_t)it.row * h, h, arv);
+  load_heads(p.m + (int64_t)it.row * h, h, mv);
+  load_heads(p.d + (int64_t)it.row * h, h, invd);
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) { invd[k] = invd[k] > 0.f ? 1.f / invd[k] : 0.f; Q[k] = 0.f; }
+
+  int colv[NV], hdv[NV];
+  bool okv[NV];
+  Vec<VW> g[NV], y[NV], z[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    colv[i] = (i * 32 + lane) * VW;
+    okv[i] = colv[i] < hf;
+    hdv[i] = okv[i] ? colv[i] / f : 0;
+    if (okv[i]) g[i] = ldg_vec<VW>(p.dOut + (int64_t)it.row * hf + colv[i]);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      if (!okv[i]) g[i].x[q] = 0.f;
+      y[i].x[q] = 0.f;
+      z[i].x[q] = 0.f;
+    }
+  }
+
+  constexpr int U = NV >= 4 ? 2 : 4;
+  for (uint64_t base = it.e0; base < it.e1; base += 32) {
+    const int n = (int)min((uint64_t)32, it.e1 - base);
+    if (lane < n) {
+      const uint32_t u = __ldg(p.nbr + base + lane);
+      sm.nb[lane] = u;
+      float al[MAXH];
+      load_heads(p.Al + (int64_t)u * h, h, al);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        if (k < h) {
+          const float zz = al[k] + arv[k];
+          const float a = __expf(lrelu(zz, slope) - mv[k]) * invd[k];
+          const float ga = lrelu_grad(zz, slope) * a;
+          sm.t0[lane * TS + k] = a;
+          sm.t1[lane * TS + k] = ga;
+          Q[k] += ga;
+        }
+      }
+    }
+    __syncwarp();
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> x[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const float* row = p.Ht + (int64_t)sm.nb[j + t] * hf;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          if (okv[i]) x[t][i] = ldg_vec<VW>(row + colv[i]);
+          else
+#pragma unroll
+            for (int q = 0; q < VW; ++q) x[t][i].x[q] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[(j + t) * TS + hdv[i]], ga = sm.t1[(j + t) * TS + hdv[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            y[i].x[q] = fmaf(a, x[t][i].x[q], y[i].x[q]);
+            z[i].x[q] = fmaf(ga, x[t][i].x[q], z[i].x[q]);
+          }
+        }
+    }
+    for (; j < n; ++j) {
+      const float* row = p.Ht + (int64_t)sm.nb[j] * hf;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        if (okv[i]) {
+          const Vec<VW> x = ldg_vec<VW>(row + colv[i]);
+          const float a = sm.t0[j * TS + hdv[i]], ga = sm.t1[j * TS + hdv[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            y[i].x[q] = fmaf(a, x.x[q], y[i].x[q]);
+            z[i].x[q] = fmaf(ga, x.x[q], z[i].x[q]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k)
+    if (k < h) Q[k] = warp_sum(Q[k]);
+
+  // c and P per head: per-lane partial dots -> shared -> head sums.
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float cp = 0.f, pp = 0.f;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) { cp = fmaf(g[i].x[q], y[i].x[q], cp); pp = fmaf(g[i].x[q], z[i].x[q], pp); }
+    sm.t0[i * 32 + lane] = cp;   // tables are free now; reuse as reduction scratch
+    sm.t1[i * 32 + lane] = pp;
+  }
+  __syncwarp();
+  if (lane < h) {
+    const float ck = head_sum<VW>(sm.t0, lane, f), pk = head_sum<VW>(sm.t1, lane, f);
+    float qk = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k)
+      if (k == lane) qk = Q[k];
+    if (!it.split) {
+      p.co[(int64_t)it.row * h + lane] = ck;
+      p.dAro[(int64_t)it.row * h + lane] = pk - ck * qk;
+    } else {
+      float* part = p.part + wi * (int64_t)(3 * h);
+      part[lane] = ck;
+      part[h + lane] = pk;
+      part[2 * h + lane] = qk;
+    }
+  }
+}
+
+__global__ void gat_bwd_dst_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
+                                         const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
+  const int64_t sr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
+  const int h = p.h;
+  if (sr >= num_split_rows * h) return;
+  const int64_t r = sr / h;
+  const int k = (int)(sr % h);
+  const uint32_t row = split_rows[r];
+  float c = 0.f, P = 0.f, Q = 0.f;
+  for (int64_t it = split_first[r]; it < split_first[r + 1]; ++it) {
+    c += p.part[it * 3 * h + k];
+    P += p.part[it * 3 * h + h + k];
+    Q += p.part[it * 3 * h + 2 * h + k];
+  }
+  p.co[(int64_t)row * h + k] = c;
+  p.dAro[(int64_t)row * h + k] = P - c * Q;
+}
+
+// ---------------------------------------------------------------------------
+// K4: backward pass 2 over csc_src.  Per source u (global), over out-edges to
+// local destinations v, alpha and the gate recomputed:
+//   dHt[u] = sum alpha dOut[v]                      (Aggregate backward)
+//   dA_l[u] = <x_u, sum gate*alpha dOut[v]> - sum gate*alpha c[v]
+// then the LP epilogue dHt[u] += dA_l[u] (x) a_l + dA_r[u] (x) a_r.
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS) gat_bwd_src_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+  const int64_t u = it.row;
+
+  float alv[MAXH], T[MAXH];
+  load_heads(p.Al + u * h, h, alv);
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) T[k] = 0.f;
+
+  int colv[NV], hdv[NV];
+  bool okv[NV];
+  Vec<VW> x[NV], acc[NV], wv[NV];
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    colv[i] = (i * 32 + lane) * VW;
+    okv[i] = colv[i] < hf;
+    hdv[i] = okv[i] ? colv[i] / f : 0;
+    if (okv[i]) x[i] = ldg_vec<VW>(p.Ht + u * hf + colv[i]);
+#pragma unroll
+    for (int q = 0; q < VW; ++q) {
+      if (!okv[i]) x[i].x[q] = 0.f;
+      acc[i].x[q] = 0.f;
+      wv[i].x[q] = 0.f;
+    }
+  }
+
+  constexpr int U = NV >= 4 ? 2 : 4;
+  for (uint64_t base = it.e0; base < it.e1; base += 32) {
+    const int n = (int)min((uint64_t)32, it.e1 - base);
+    if (lane < n) {
+      const uint32_t v = __ldg(p.nbr + base + lane);
+      sm.nb[lane] = v;
+      float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
+      load_heads(p.Ar + (int64_t)v * h, h, arv);
+      load_heads(p.m + (int64_t)v * h, h, mv);
+      load_heads(p.d + (int64_t)v * h, h, dv);
+      load_heads(p.c + (int64_t)v * h, h, cv);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        if (k < h) {
+          const float zz = alv[k] + arv[k];
+          const float a = dv[k] > 0.f ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
+          const float ga = lrelu_grad(zz, slope) * a;
+          sm.t0[lane * TS + k] = a;
+          sm.t1[lane * TS + k] = ga;
+          T[k] = fmaf(ga, cv[k], T[k]);
+        }
+      }
+    }
+    __syncwarp();
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> gv[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const float* row = p.dOut + (int64_t)sm.nb[j + t] * hf;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          if (okv[i]) gv[t][i] = ldg_vec<VW>(row + colv[i]);
+          else
+#pragma unroll
+            for (int q = 0; q < VW; ++q) gv[t][i].x[q] = 0.f;
+        }
+      }
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[(j + t) * TS + hdv[i]], ga = sm.t1[(j + t) * TS + hdv[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            acc[i].x[q] = fmaf(a, gv[t][i].x[q], acc[i].x[q]);
+            wv[i].x[q] = fmaf(ga, gv[t][i].x[q], wv[i].x[q]);
+          }
+        }
+    }
+    for (; j < n; ++j) {
+      const float* row = p.dOut + (int64_t)sm.nb[j] * hf;
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        if (okv[i]) {
+          const Vec<VW> gv = ldg_vec<VW>(row + colv[i]);
+          const float a = sm.t0[j * TS + hdv[i]], ga = sm.t1[j * TS + hdv[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            acc[i].x[q] = fmaf(a, gv.x[q], acc[i].x[q]);
+            wv[i].x[q] = fmaf(ga, gv.x[q], wv[i].x[q]);
+          }
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k)
+    if (k < h) T[k] = warp_sum(T[k]);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) s = fmaf(x[i].x[q], wv[i].x[q], s);
+    sm.t0[i * 32 + lane] = s;
+  }
+  __syncwarp();
+  if (lane < h) {
+    float tk = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k)
+      if (k == lane) tk = T[k];
+    const float dal = head_sum<VW>(sm.t0, lane, f) - tk;
+    sm.stat[0][lane] = dal;
+    const bool local = u >= p.row_base && u < p.row_base + p.num_local;
+    sm.stat[1][lane] = local ? p.dAr[(u - p.row_base) * h + lane] : 0.f;
+  }
+  __syncwarp();
+  if (!it.split) {
+    if (lane < h) p.dAl[u * h + lane] = sm.stat[0][lane];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (okv[i]) {
+        const float dal = sm.stat[0][hdv[i]], dar = sm.stat[1][hdv[i]];
+        const Vec<VW> al = ldg_vec<VW>(p.a_l + colv[i]);
+        const Vec<VW> ar = ldg_vec<VW>(p.a_r + colv[i]);
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] + dal * al.x[q] + dar * ar.x[q];
+        st_vec<VW>(p.dHt + u * hf + colv[i], o);
+      }
+    }
+  } else {
+    float* part = p.part + wi * (int64_t)(hf + h);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (okv[i]) st_vec<VW>(part + colv[i], acc[i]);
+    if (lane < h) part[hf + lane] = sm.stat[0][lane];
+  }
+}
+
+__global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
+                                         const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
+  __shared__ float st[WARPS][2][MAXH];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
+  if (sr >= num_split_rows) return;
+  const int h = p.h, f = p.f, hf = h * f;
+  const int64_t stride = hf + h;
+  const int64_t u = split_rows[sr];
+  const int64_t i0 = split_first[sr], i1 = split_first[sr + 1];
+  if (lane < h) {
+    float dal = 0.f;
+    for (int64_t it = i0; it < i1; ++it) dal += p.part[it * stride + hf + lane];
+    st[w][0][lane] = dal;
+    const bool local = u >= p.row_base && u < p.row_base + p.num_local;
+    st[w][1][lane] = local ? p.dAr[(u - p.row_base) * h + lane] : 0.f;
+    p.dAl[u * h + lane] = dal;
+  }
+  __syncwarp();
+  for (int c = lane; c < hf; c += 32) {
+    const int hd = c / f;
+    float s = 0.f;
+    for (int64_t it = i0; it < i1; ++it) s += p.part[it * stride + c];
+    p.dHt[u * hf + c] = s + st[w][0][hd] * p.a_l[c] + st[w][1][hd] * p.a_r[c];
+  }
+}
+
+// ---------------------------------------------------------------------------
+// Reorganized LPs and their parameter gradients.
+// ---------------------------------------------------------------------------
+__global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __restrict__ Ht,
+                                 const float* __restrict__ a_l, const float* __restrict__ a_r, float* __restrict__ Al,
+                                 float* __restrict__ Ar) {
+  const int64_t n = rows * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / h;
+    const int k = (int)(i % h);
+    const float* x = Ht + v * h * f + (int64_t)k * f;
+    float sl = 0.f, sr = 0.f;
+    for (int j = 0; j < f; ++j) {
+      const float xv = __ldg(x + j);
+      sl = fmaf(xv, __ldg(a_l + k * f + j), sl);
+      sr = fmaf(xv, __ldg(a_r + k * f + j), sr);
+    }
+    Al[i] = sl;
+    Ar[i] = sr;
+  }
+}
+
+constexpr int kGradBlocks = 296;
+
+__global__ void attn_grad_partial_kernel(int64_t rows, int h, int f, const float* __restrict__ Ht,
+                                         const float* __restrict__ dAl, const float* __restrict__ dAr,
+                                         float* __restrict__ part) {
+  const int hf = h * f;
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= hf) return;
+  const int k = c / f;
+  const int64_t per = ceil_div(rows, (int64_t)gridDim.x);
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float sl = 0.f, sr = 0.f;
+  for (int64_t v = r0; v < r1; ++v) {
+    const float x = __ldg(Ht + v * hf + c);
+    sl = fmaf(__ldg(dAl + v * h + k), x, sl);
+    sr = fmaf(__ldg(dAr + v * h + k), x, sr);
+  }
+  part[(int64_t)blockIdx.x * 2 * hf + c] = sl;
+  part[(int64_t)blockIdx.x * 2 * hf + hf + c] = sr;
+}
+
+__global__ void attn_grad_reduce_kernel(int nb, int hf, const float* __restrict__ part, float* __restrict__ da_l,
+                                        float* __restrict__ da_r) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= 2 * hf) return;
+  float s = 0.f;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * 2 * hf + c];
+  if (c < hf) da_l[c] = s; else da_r[c - hf] = s;
+}
+
+// ---------------------------------------------------------------------------
+// Dispatch over the compiled (VW, NV) variants.
+// ---------------------------------------------------------------------------
+enum class Kind { Fwd, BwdDst, BwdSrc };
+
+template <int VW, int NV>
+void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
+  switch (kind) {
+    case Kind::Fwd: gat_fwd_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
+  }
+}
+
+template <int VW>
+int launch_nv(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
+  const int hf = p.h * p.f;
+  const int nvec = (int)ceil_div(hf / VW, 32);
+  if (nvec <= 1) launch_variant<VW, 1>(kind, p, grid, s);
+  else if (nvec <= 2) launch_variant<VW, 2>(kind, p, grid, s);
+  else if (nvec <= 4) launch_variant<VW, 4>(kind, p, grid, s);
+  else if (nvec <= 8) launch_variant<VW, 8>(kind, p, grid, s);
+  else return fail(GNNCG_ERR_UNSUPPORTED, "gat: h*f = %d exceeds the compiled limit %d", hf, 256 * VW);
+  return GNNCG_OK;
+}
+
+int dispatch(Kind kind, const GatParams& p, cudaStream_t s) {
+  if (p.num_items == 0) return GNNCG_OK;
+  dim3 grid((unsigned)ceil_div(p.num_items, WARPS));
+  int rc;
+  if (p.f % 4 == 0) rc = launch_nv<4>(kind, p, grid, s);
+  else if (p.f % 2 == 0) rc = launch_nv<2>(kind, p, grid, s);
+  else rc = launch_nv<1>(kind, p, grid, s);
+  if (rc != GNNCG_OK) return rc;
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+int check_common(const gnncg_index_t* idx, const gnncg_sched_t* sched, int h, int f) {
+  GNNCG_REQUIRE(idx && sched, GNNCG_ERR_ARG, "gat: null index or schedule");
+  GNNCG_REQUIRE(h >= 1 && h <= MAXH, GNNCG_ERR_UNSUPPORTED, "gat: heads=%d outside [1,%d]", h, MAXH);
+  GNNCG_REQUIRE(f >= 1, GNNCG_ERR_SHAPE, "gat: f must be >= 1");
+  GNNCG_REQUIRE(idx->num_rows >= 0 && (idx->num_rows == 0 || idx->off), GNNCG_ERR_ARG, "gat: bad index");
+  GNNCG_REQUIRE(sched->num_items == 0 || sched->items, GNNCG_ERR_ARG, "gat: bad schedule");
+  GNNCG_REQUIRE(sched->chunk >= 32, GNNCG_ERR_ARG, "gat: schedule chunk < 32");
+  return GNNCG_OK;
+}
+
+size_t fwd_part_bytes(const gnncg_sched_t* s, int h, int f) {
+  return s ? (size_t)s->num_split_items * (size_t)(h * f + 2 * h) * sizeof(float) : 0;
+}
+size_t dst_part_bytes(const gnncg_sched_t* s, int h) {
+  return s ? (size_t)s->num_split_items * (size_t)(3 * h) * sizeof(float) : 0;
+}
+size_t src_part_bytes(const gnncg_sched_t* s, int h, int f) {
+  return s ? (size_t)s->num_split_items * (size_t)(h * f + h) * sizeof(float) : 0;
+}
+
+}  // namespace
+}  // namespace gnncg_b200
+
+using namespace gnncg_b200;
+
+extern "C" {
+
+int gnncg_gat_attn_dots(int64_t rows, int h, int f, const float* Ht, const float* a_l, const float* a_r, float* Al,
+                        float* Ar, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(rows >= 0 && h >= 1 && f >= 1, GNNCG_ERR_SHAPE, "attn_dots: bad shape");
+  if (rows == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(Ht && a_l && a_r && Al && Ar, GNNCG_ERR_ARG, "attn_dots: null pointer");
+  const int64_t n = rows * h;
+  const int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 32);
+  attn_dots_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, Ht, a_l, a_r, Al, Ar);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* src_sched, int h, int f) {
+  size_t b = fwd_part_bytes(dst_sched, h, f);
+  b = std::max(b, dst_part_bytes(dst_sched, h));
+  b = std::max(b, src_part_bytes(src_sched, h, f));
+  return align_up(b);
+}
+
+int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+                  const float* Ht, const float* Al, const float* Ar, float* out, float* m, float* d, void* ws,
+                  size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  int rc = check_common(csr_dst, sched, h, f);
+  if (rc) return rc;
+  if (sched->num_items == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(Ht && Al && Ar && out && m && d && csr_dst->nbr, GNNCG_ERR_ARG, "gat_fwd: null pointer");
+  const size_t need = fwd_part_bytes(sched, h, f);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
+                ws_bytes, need);
+  GatParams p{};
+  p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
+  p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
+  p.h = h; p.f = f; p.slope = slope;
+  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
+  cudaStream_t s = as_stream(stream);
+  rc = dispatch(Kind::Fwd, p, s);
+  if (rc) return rc;
+  if (sched->num_split_rows > 0) {
+    gat_fwd_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
+        p, sched->split_rows, sched->split_first, sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+                      const float* Ht, const float* Al, const float* Ar, const float* m, const float* d,
+                      const float* dOut, float* c, float* dAr, void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  int rc = check_common(csr_dst, sched, h, f);
+  if (rc) return rc;
+  if (sched->num_items == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(Ht && Al && Ar && m && d && dOut && c && dAr && csr_dst->nbr, GNNCG_ERR_ARG,
+                "gat_bwd_dst: null pointer");
+  const size_t need = dst_part_bytes(sched, h);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_dst: workspace %zu < %zu",
+                ws_bytes, need);
+  GatParams p{};
+  p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
+  p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
+  p.h = h; p.f = f; p.slope = slope;
+  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.m = m; p.d = d; p.dOut = dOut; p.co = c; p.dAro = dAr;
+  p.part = static_cast<float*>(ws);
+  cudaStream_t s = as_stream(stream);
+  rc = dispatch(Kind::BwdDst, p, s);
+  if (rc) return rc;
+  if (sched->num_split_rows > 0) {
+    const int64_t n = sched->num_split_rows * h;
+    gat_bwd_dst_merge_kernel<<<(unsigned)ceil_div(n, 256), 256, 0, s>>>(p, sched->split_rows, sched->split_first,
+                                                                        sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
+                      int64_t row_base, int64_t num_local, const float* Ht, const float* Al, const float* Ar,
+                      const float* m, const float* d, const float* c, const float* dOut, const float* dAr,
+                      const float* a_l, const float* a_r, float* dHt, float* dAl, void* ws, size_t ws_bytes,
+                      void* stream) {
+  GNNCG_DEVICE_GUARD();
+  int rc = check_common(csc_src, sched, h, f);
+  if (rc) return rc;
+  if (sched->num_items == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(Ht && Al && Ar && m && d && c && dOut && dAr && a_l && a_r && dHt && dAl, GNNCG_ERR_ARG,
+                "gat_bwd_src: null pointer");
+  GNNCG_REQUIRE(row_base >= 0 && num_local >= 0, GNNCG_ERR_ARG, "gat_bwd_src: bad row block");
+  const size_t need = src_part_bytes(sched, h, f);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_src: workspace %zu < %zu",
+                ws_bytes, need);
+  GatParams p{};
+  p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
+  p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
+  p.h = h; p.f = f; p.slope = slope;
+  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.m = m; p.d = d; p.c = c; p.dOut = dOut; p.dAr = dAr;
+  p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
+  p.part = static_cast<float*>(ws);
+  cudaStream_t s = as_stream(stream);
+  rc = dispatch(Kind::BwdSrc, p, s);
+  if (rc) return rc;
+  if (sched->num_split_rows > 0) {
+    gat_bwd_src_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
+        p, sched->split_rows, sched->split_first, sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+size_t gnncg_gat_attn_grad_workspace(int64_t rows, int h, int f) {
+  (void)rows;
+  return align_up((size_t)kGradBlocks * 2 * h * f * sizeof(float));
+}
+
+int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float* dAl, const float* dAr,
+                        float* da_l, float* da_r, void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(rows >= 0 && h >= 1 && f >= 1, GNNCG_ERR_SHAPE, "attn_grad: bad shape");
+  GNNCG_REQUIRE(da_l && da_r && (rows == 0 || (Ht && dAl && dAr)), GNNCG_ERR_ARG, "attn_grad: null pointer");
+  const size_t need = gnncg_gat_attn_grad_workspace(rows, h, f);
+  GNNCG_REQUIRE(ws_bytes >= need && ws, GNNCG_ERR_WORKSPACE, "attn_grad: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  const int hf = h * f;
+  float* part = static_cast<float*>(ws);
+  dim3 g1(kGradBlocks, (unsigned)ceil_div(hf, 256));
+  attn_grad_partial_kernel<<<g1, 256, 0, s>>>(rows, h, f, Ht, dAl, dAr, part);
+  GNNCG_LAUNCH_CHECK();
+  attn_grad_reduce_kernel<<<(unsigned)ceil_div(2 * hf, 256), 256, 0, s>>>(kGradBlocks, hf, part, da_l, da_r);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+}  // extern "C"

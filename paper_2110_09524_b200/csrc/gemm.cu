@@ -1,0 +1,207 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Dense transforms (K1 / K5): ApplyVertex(W) and its two backward Applies.
+// Replaces matmul / matmul_nt / matmul_tn (proj/src/tensor.cpp:8-60).
+//
+// fp32 in, fp32 accumulate (the reference computes these in T = float/double;
+// SPEC.md:139).  This translation unit is the CUDA-core SIMT path: 128x128x16
+// CTA tiles, 8x8 register micro-tiles, double-buffered shared memory, and a
+// deterministic split-K (fixed-order partial reduction) for the tall-skinny
+// Hᵀ·dH̃ weight gradient (K = |V|).  The GEMMs are <= ~6% of the GAT layer step
+// (SURVEY §7 "Hard parts"), the fused gather kernels dominate.
+#include "common.cuh"
+
+namespace gnncg_b200 {
+namespace {
+
+constexpr int BM = 128, BN = 128, BK = 16, NT = 256;
+
+template <bool TA, bool TB>
+__global__ void __launch_bounds__(NT, 2)
+    sgemm_kernel(int64_t M, int64_t N, int64_t K, const float* __restrict__ A, int64_t lda,
+                 const float* __restrict__ B, int64_t ldb, float* __restrict__ C, int64_t ldc, int64_t kchunk,
+                 int64_t split_stride) {
+  __shared__ __align__(16) float As[2][BK][BM];
+  __shared__ __align__(16) float Bs[2][BK][BN];
+  const int t = threadIdx.x;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb = (int64_t)blockIdx.z * kchunk;
+  const int64_t ke = min(K, kb + kchunk);
+  float* Cz = C + (int64_t)blockIdx.z * split_stride;
+
+  float ra[8], rb[8];
+  auto load_tile = [&](int64_t k0) {
+    if (!TA) {  // A[m*lda + k]
+      const int ml = t >> 1, kl = (t & 1) * 8;
+      const int64_t m = m0 + ml;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t k = k0 + kl + i;
+        ra[i] = (m < M && k < ke) ? __ldg(A + m * lda + k) : 0.f;
+      }
+    } else {  // A[k*lda + m]
+      const int kl = t >> 4, ml = (t & 15) * 8;
+      const int64_t k = k0 + kl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t m = m0 + ml + i;
+        ra[i] = (m < M && k < ke) ? __ldg(A + k * lda + m) : 0.f;
+      }
+    }
+    if (!TB) {  // B[k*ldb + n]
+      const int kl = t >> 4, nl = (t & 15) * 8;
+      const int64_t k = k0 + kl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t n = n0 + nl + i;
+        rb[i] = (n < N && k < ke) ? __ldg(B + k * ldb + n) : 0.f;
+      }
+    } else {  // B[n*ldb + k]
+      const int nl = t >> 1, kl = (t & 1) * 8;
+      const int64_t n = n0 + nl;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) {
+        const int64_t k = k0 + kl + i;
+        rb[i] = (n < N && k < ke) ? __ldg(B + n * ldb + k) : 0.f;
+      }
+    }
+  };
+  auto store_tile = [&](int buf) {
+    if (!TA) {
+      const int ml = t >> 1, kl = (t & 1) * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) As[buf][kl + i][ml] = ra[i];
+    } else {
+      const int kl = t >> 4, ml = (t & 15) * 8;
+      *reinterpret_cast<float4*>(&As[buf][kl][ml]) = make_float4(ra[0], ra[1], ra[2], ra[3]);
+      *reinterpret_cast<float4*>(&As[buf][kl][ml + 4]) = make_float4(ra[4], ra[5], ra[6], ra[7]);
+    }
+    if (!TB) {
+      const int kl = t >> 4, nl = (t & 15) * 8;
+      *reinterpret_cast<float4*>(&Bs[buf][kl][nl]) = make_float4(rb[0], rb[1], rb[2], rb[3]);
+      *reinterpret_cast<float4*>(&Bs[buf][kl][nl + 4]) = make_float4(rb[4], rb[5], rb[6], rb[7]);
+    } else {
+      const int nl = t >> 1, kl = (t & 1) * 8;
+#pragma unroll
+      for (int i = 0; i < 8; ++i) Bs[buf][kl + i][nl] = rb[i];
+    }
+  };
+
+  float acc[8][8];
+#pragma unroll
+  for (int i = 0; i < 8; ++i)
+#pragma unroll
+    for (int j = 0; j < 8; ++j) acc[i][j] = 0.f;
+
+  const int tx = t & 15, ty = t >> 4;
+  int buf = 0;
+  if (kb < ke) {
+    load_tile(kb);
+    store_tile(0);
+    __syncthreads();
+  }
+  for (int64_t k0 = kb; k0 < ke; k0 += BK) {
+    const bool more = k0 + BK < ke;
+    if (more) load_tile(k0 + BK);
+#pragma unroll
+    for (int k = 0; k < BK; ++k) {
+      const float4 a0 = *reinterpret_cast<const float4*>(&As[buf][k][ty * 4]);
+      const float4 a1 = *reinterpret_cast<const float4*>(&As[buf][k][64 + ty * 4]);
+      const float4 b0 = *reinterpret_cast<const float4*>(&Bs[buf][k][tx * 4]);
+      const float4 b1 = *reinterpret_cast<const float4*>(&Bs[buf][k][64 + tx * 4]);
+      const float a[8] = {a0.x, a0.y, a0.z, a0.w, a1.x, a1.y, a1.z, a1.w};
+      const float b[8] = {b0.x, b0.y, b0.z, b0.w, b1.x, b1.y, b1.z, b1.w};
+#pragma unroll
+      for (int i = 0; i < 8; ++i)
+#pragma unroll
+        for (int j = 0; j < 8; ++j) acc[i][j] = fmaf(a[i], b[j], acc[i][j]);
+    }
+    if (more) {
+      store_tile(buf ^ 1);
+      __syncthreads();
+      buf ^= 1;
+    }
+  }
+#pragma unroll
+  for (int i = 0; i < 8; ++i) {
+    const int64_t m = m0 + (i < 4 ? ty * 4 + i : 64 + ty * 4 + (i - 4));
+    if (m >= M) continue;
+#pragma unroll
+    for (int j = 0; j < 8; ++j) {
+      const int64_t n = n0 + (j < 4 ? tx * 4 + j : 64 + tx * 4 + (j - 4));
+      if (n < N) Cz[m * ldc + n] = acc[i][j];
+    }
+  }
+}
+
+// C[m,n] = sum_z P[z][m][n] in ascending z (deterministic split-K merge).
+__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float* __restrict__ P, float* __restrict__ C,
+                                     int64_t ldc) {
+  const int64_t total = M * N;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+    float s = 0.f;
+    for (int z = 0; z < splits; ++z) s += P[(int64_t)z * total + i];
+    C[(i / N) * ldc + (i % N)] = s;
+  }
+}
+
+int choose_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
+  if (tiles >= 2 * 148 || K < 4 * 256) return 1;
+  int64_t s = ceil_div(2 * 148, tiles);
+  s = std::min<int64_t>(s, K / 256);
+  s = std::min<int64_t>(s, 64);
+  return (int)std::max<int64_t>(s, 1);
+}
+
+}  // namespace
+}  // namespace gnncg_b200
+
+using namespace gnncg_b200;
+
+extern "C" {
+
+size_t gnncg_gemm_workspace(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K) {
+  (void)trans_a;
+  (void)trans_b;
+  const int s = choose_splits(M, N, K);
+  return s > 1 ? align_up((size_t)s * M * N * sizeof(float)) : 0;
+}
+
+int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+               const float* B, int64_t ldb, float* C, int64_t ldc, void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(M >= 0 && N >= 0 && K >= 0, GNNCG_ERR_SHAPE, "gemm: negative dimension");
+  GNNCG_REQUIRE(!(trans_a && trans_b), GNNCG_ERR_UNSUPPORTED, "gemm: A^T B^T not supported");
+  GNNCG_REQUIRE(lda >= (trans_a ? M : K) && ldb >= (trans_b ? K : N) && ldc >= N, GNNCG_ERR_SHAPE,
+                "gemm: leading dimension too small");
+  if (M == 0 || N == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(A && B && C, GNNCG_ERR_ARG, "gemm: null pointer");
+  cudaStream_t s = as_stream(stream);
+  const int splits = choose_splits(M, N, K);
+  const size_t need = gnncg_gemm_workspace(trans_a, trans_b, M, N, K);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gemm: workspace %zu < %zu", ws_bytes,
+                need);
+  const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), BK) * BK : std::max<int64_t>(K, 1);
+  const int real_splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)real_splits);
+  float* out = splits > 1 ? static_cast<float*>(ws) : C;
+  const int64_t ldo = splits > 1 ? N : ldc;
+  const int64_t stride = splits > 1 ? M * N : 0;
+  if (!trans_a && !trans_b)
+    sgemm_kernel<false, false><<<grid, NT, 0, s>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, stride);
+  else if (!trans_a && trans_b)
+    sgemm_kernel<false, true><<<grid, NT, 0, s>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, stride);
+  else
+    sgemm_kernel<true, false><<<grid, NT, 0, s>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, stride);
+  GNNCG_LAUNCH_CHECK();
+  if (splits > 1) {
+    const int64_t total = M * N;
+    const int g = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+    splitk_reduce_kernel<<<g, 256, 0, s>>>(M, N, real_splits, out, C, ldc);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+}  // extern "C"

@@ -1,0 +1,338 @@
+"""Operator API of the fused GNN layer path -- the Python mirror of the C++ layer in
+include/gnncg/ops.hpp, both sitting on the C ABI of include/gnncg_b200.h.
+
+Names, argument meaning and error behaviour follow the reference's data model
+(gnncg::Graph / gnncg::Tensor, head-major multi-head layout, LeakyReLU slope 0.2,
+TensorError on shape mismatch, GraphError on bad endpoints) and the operator
+contracts of its specified executor:
+
+  gat_forward / gat_backward           GAT layer (App. B)
+  edgeconv_forward / edgeconv_backward EdgeConv layer
+  gmm_forward / gmm_backward           GMMConv layer
+  matmul / matmul_nt / matmul_tn       dense transforms (tensor.cpp:8-60)
+
+All tensors are fp32 CUDA tensors; every FLOP runs in libgnncg_b200.so.  torch
+provides device memory and the current stream only.
+"""
+from __future__ import annotations
+
+from dataclasses import dataclass
+
+import torch
+
+from . import _lib
+from ._lib import TensorError, call
+from .graph import DeviceGraph, _ptr, _stream
+
+DEFAULT_SLOPE = 0.2  # tensor.hpp:93 
+
+
+class KernelProbe:
+    """Optional per-call CUDA-event timing on the launching stream (bench.py roofline).
+    Disabled by default; enabling it records two events around each fused / GEMM call."""
+
+    def __init__(self):
+        self.enabled = False
+        self.pending = []  # (name, start, end)
+        self.totals: dict[str, list] = {}
+
+    def __call__(self, name):
+        probe = self
+
+        class _Scope:
+            def __enter__(self):
+                if probe.enabled:
+                    self.s = torch.cuda.Event(enable_timing=True)
+                    self.e = torch.cuda.Event(enable_timing=True)
+                    self.s.record()
+                return self
+
+            def __exit__(self, *exc):
+                if probe.enabled:
+                    self.e.record()
+                    probe.pending.append((name, self.s, self.e))
+                return False
+
+        return _Scope()
+
+    def collect(self):
+        """Synchronise and fold pending events into totals[name] = [ms_sum, count]."""
+        torch.cuda.synchronize()
+        for name, s, e in self.pending:
+            t = self.totals.setdefault(name, [0.0, 0])
+            t[0] += s.elapsed_time(e)
+            t[1] += 1
+        self.pending.clear()
+        return self.totals
+
+    def reset(self):
+        self.pending.clear()
+        self.totals.clear()
+
+
+PROBE = KernelProbe()
+
+
+def _f32(t: torch.Tensor, name: str) -> torch.Tensor:
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda:
+        raise TensorError(f"{name}: expected a float32 CUDA tensor")
+    return t.contiguous()
+
+
+def _shape(t: torch.Tensor, shape, name: str):
+    if tuple(t.shape) != tuple(shape):
+        raise TensorError(f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
+
+
+# ---------------------------------------------------------------------------
+# Dense transforms (K1 / K5)
+# ---------------------------------------------------------------------------
+def gemm(A: torch.Tensor, B: torch.Tensor, trans_a=False, trans_b=False, out: torch.Tensor | None = None,
+         ws=None) -> torch.Tensor:
+    """C = op(A) op(B) in fp32 on the device (deterministic)."""
+    A = _f32(A, "gemm A")
+    B = _f32(B, "gemm B")
+    M, K = (A.shape[1], A.shape[0]) if trans_a else (A.shape[0], A.shape[1])
+    Kb, N = (B.shape[1], B.shape[0]) if trans_b else (B.shape[0], B.shape[1])
+    if K != Kb:
+        raise TensorError("matmul: inner dimension mismatch")  # tensor.cpp:10
+    if out is None:
+        out = torch.empty(M, N, dtype=torch.float32, device=A.device)
+    need = _lib.lib().gnncg_gemm_workspace(int(trans_a), int(trans_b), M, N, K)
+    if ws is None:
+        buf = torch.empty(max(need, 1), dtype=torch.uint8, device=A.device)
+        wp, wn = buf.data_ptr(), buf.numel()
+    else:
+        wp, wn = ws.get(need)
+    with PROBE(f"gemm_{'t' if trans_a else 'n'}{'t' if trans_b else 'n'}"):
+        call("gnncg_gemm", int(trans_a), int(trans_b), M, N, K, _ptr(A), A.stride(0), _ptr(B), B.stride(0),
+             _ptr(out), out.stride(0), wp, wn, _stream())
+    return out
+
+
+def matmul(a, b, ws=None):
+    """C = A B (tensor.cpp:8-24)."""
+    return gemm(a, b, ws=ws)
+
+
+def matmul_nt(a, b, ws=None):
+    """C = A B^T (tensor.cpp:26-42)."""
+    return gemm(a, b, trans_b=True, ws=ws)
+
+
+def matmul_tn(a, b, ws=None):
+    """C = A^T B (tensor.cpp:44-60)."""
+    return gemm(a, b, trans_a=True, ws=ws)
+
+
+# ---------------------------------------------------------------------------
+# GAT
+# ---------------------------------------------------------------------------
+@dataclass
+class GatParams:
+    heads: int
+    f: int
+    slope: float = DEFAULT_SLOPE
+
+
+@dataclass
+class GatStash:
+    """What the forward keeps for the backward: vertex tensors only (O(|V|)).
+    Ht / Al / Ar are the reorganized ApplyVertex outputs; m / d the edge-softmax statistics."""
+
+    Ht: torch.Tensor
+    Al: torch.Tensor
+    Ar: torch.Tensor
+    m: torch.Tensor
+    d: torch.Tensor
+
+
+@dataclass
+class GatGrads:
+    dH: torch.Tensor | None
+    dW: torch.Tensor
+    da_l: torch.Tensor
+    da_r: torch.Tensor
+
+
+def gat_region_forward(g: DeviceGraph, Ht, Al, Ar, p: GatParams, out=None, m=None, d=None, chunk=None):
+    """K2 alone: the fused region given the reorganized vertex tensors."""
+    V, h, f = g.num_vertices, p.heads, p.f
+    Ht, Al, Ar = _f32(Ht, "Ht"), _f32(Al, "A_l"), _f32(Ar, "A_r")
+    _shape(Ht, (V, h * f), "Ht")
+    _shape(Al, (V, h), "A_l")
+    _shape(Ar, (V, h), "A_r")
+    dev = Ht.device
+    out = torch.empty(V, h * f, device=dev) if out is None else out
+    m = torch.empty(V, h, device=dev) if m is None else m
+    d = torch.empty(V, h, device=dev) if d is None else d
+    idx = g.csr_dst
+    sched = idx.sched(chunk) if chunk else idx.sched()
+    need = _lib.lib().gnncg_gat_workspace(sched.struct(), None, h, f)
+    wp, wn = g.ws.get(need)
+    with PROBE("gat_fwd"):
+        call("gnncg_gat_fwd", idx.struct(), sched.struct(), h, f, p.slope, _ptr(Ht), _ptr(Al), _ptr(Ar), _ptr(out),
+             _ptr(m), _ptr(d), wp, wn, _stream())
+    return out, m, d
+
+
+def attn_dots(Ht, a_l, a_r, heads, f, Al=None, Ar=None):
+    V = Ht.shape[0]
+    Al = torch.empty(V, heads, device=Ht.device) if Al is None else Al
+    Ar = torch.empty(V, heads, device=Ht.device) if Ar is None else Ar
+    with PROBE("attn_dots"):
+        call("gnncg_gat_attn_dots", V, heads, f, _ptr(Ht), _ptr(_f32(a_l, "a_l")), _ptr(_f32(a_r, "a_r")),
+             _ptr(Al), _ptr(Ar), _stream())
+    return Al, Ar
+
+
+def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
+    """One GAT layer forward, reorganized:
+    Ht = H W (K1), A_l = Ht . a_l, A_r = Ht . a_r, then the fused region (K2).
+    Returns (out, GatStash)."""
+    h, f = p.heads, p.f
+    H, W = _f32(H, "H"), _f32(W, "W")
+    if H.shape[0] != g.num_vertices:
+        raise TensorError("gat_forward: H rows != num_vertices")
+    if W.shape != (H.shape[1], h * f):
+        raise TensorError(f"gat_forward: W shape {tuple(W.shape)} != ({H.shape[1]}, {h * f})")
+    _shape(a_l, (h, f), "a_l")
+    _shape(a_r, (h, f), "a_r")
+    Ht = gemm(H, W, ws=g.ws)
+    Al, Ar = attn_dots(Ht, a_l, a_r, h, f)
+    out, m, d = gat_region_forward(g, Ht, Al, Ar, p, chunk=chunk)
+    return out, GatStash(Ht, Al, Ar, m, d)
+
+
+def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatParams, chunk=None):
+    """K3 + K4 + LP grads: returns (dHt, dAl, dAr, da_l, da_r, c)."""
+    V, h, f = g.num_vertices, p.heads, p.f
+    dOut = _f32(dOut, "dOut")
+    _shape(dOut, (V, h * f), "dOut")
+    a_l, a_r = _f32(a_l, "a_l"), _f32(a_r, "a_r")
+    dev = dOut.device
+    c = torch.empty(V, h, device=dev)
+    dAr = torch.empty(V, h, device=dev)
+    dAl = torch.empty(V, h, device=dev)
+    dHt = torch.empty(V, h * f, device=dev)
+    sd = g.csr_dst.sched(chunk) if chunk else g.csr_dst.sched()
+    ss = g.csc_src.sched(chunk) if chunk else g.csc_src.sched()
+    L = _lib.lib()
+    need = max(L.gnncg_gat_workspace(sd.struct(), ss.struct(), h, f), L.gnncg_gat_attn_grad_workspace(V, h, f))
+    wp, wn = g.ws.get(need)
+    s = _stream()
+    with PROBE("gat_bwd_dst"):
+        call("gnncg_gat_bwd_dst", g.csr_dst.struct(), sd.struct(), h, f, p.slope, _ptr(stash.Ht), _ptr(stash.Al),
+             _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(dOut), _ptr(c), _ptr(dAr), wp, wn, s)
+    with PROBE("gat_bwd_src"):
+        call("gnncg_gat_bwd_src", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
+             _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(c), _ptr(dOut), _ptr(dAr),
+             _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), wp, wn, s)
+    da_l = torch.empty(h, f, device=dev)
+    da_r = torch.empty(h, f, device=dev)
+    with PROBE("attn_grad"):
+        call("gnncg_gat_attn_grad", V, h, f, _ptr(stash.Ht), _ptr(dAl), _ptr(dAr), _ptr(da_l), _ptr(da_r), wp, wn,
+             s)
+    return dHt, dAl, dAr, da_l, da_r, c
+
+
+def gat_backward(g: DeviceGraph, H, W, a_l, a_r, stash: GatStash, dOut, p: GatParams, need_dH=True, chunk=None):
+    """GAT layer backward with recomputation:
+    K3 (csr_dst) -> K4 (csc_src) -> LP grads -> dW = H^T dHt (K5), dH = dHt W^T (K5)."""
+    H, W = _f32(H, "H"), _f32(W, "W")
+    dHt, _, _, da_l, da_r, _ = gat_region_backward(g, stash, a_l, a_r, dOut, p, chunk=chunk)
+    dW = gemm(H, dHt, trans_a=True, ws=g.ws)
+    dH = gemm(dHt, W, trans_b=True, ws=g.ws) if need_dH else None
+    return GatGrads(dH, dW, da_l, da_r)
+
+
+# ---------------------------------------------------------------------------
+# EdgeConv
+# ---------------------------------------------------------------------------
+NO_EDGE = 0xFFFFFFFF
+
+
+@dataclass
+class EdgeConvStash:
+    Y: torch.Tensor  # [Th | Ph], V x 2C
+    argmax: torch.Tensor  # int32 holding u32 edge ids (0xFFFFFFFF = empty row)
+
+
+def edgeconv_region_forward(g: DeviceGraph, Th, Ph):
+    """K6 alone: out, argmax (int32 view of u32 edge ids)."""
+    V, C_ = Th.shape
+    out = torch.empty(V, C_, device=Th.device)
+    amax = torch.empty(V, C_, dtype=torch.int32, device=Th.device)
+    call("gnncg_edgeconv_fwd", g.csr_dst.struct(), C_, 0, _ptr(Th), Th.stride(0), _ptr(Ph), Ph.stride(0), _ptr(out),
+         _ptr(amax), _stream())
+    return out, amax
+
+
+def edgeconv_forward(g: DeviceGraph, H, Theta, Phi):
+    """EdgeConv layer forward, reorganized: Y = H [Theta | Phi] (one GEMM),
+    then the fused max region."""
+    H, Theta, Phi = _f32(H, "H"), _f32(Theta, "Theta"), _f32(Phi, "Phi")
+    if Theta.shape != Phi.shape or Theta.shape[0] != H.shape[1]:
+        raise TensorError("edgeconv_forward: Theta/Phi must both be (F_in, C)")
+    C_ = Theta.shape[1]
+    Y = gemm(H, torch.cat([Theta, Phi], dim=1), ws=g.ws)
+    out, amax = edgeconv_region_forward(g, Y[:, :C_], Y[:, C_:])
+    return out, EdgeConvStash(Y, amax)
+
+
+def edgeconv_backward(g: DeviceGraph, H, Theta, Phi, stash: EdgeConvStash, dOut, need_dH=True):
+    """Argmax routing (K7) then dY -> d[Theta|Phi] = H^T dY, dH = dY [Theta|Phi]^T."""
+    H = _f32(H, "H")
+    C_ = Theta.shape[1]
+    dOut = _f32(dOut, "dOut")
+    V = g.num_vertices
+    dY = torch.empty(V, 2 * C_, device=H.device)
+    call("gnncg_edgeconv_bwd", g.csc_src.struct(), g.csr_dst.struct(), C_, _ptr(stash.argmax), _ptr(dOut),
+         _ptr(dY), dY.stride(0), _ptr(dY) + 4 * C_, dY.stride(0), _stream())
+    dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
+    dH = gemm(dY, torch.cat([Theta, Phi], dim=1), trans_b=True, ws=g.ws) if need_dH else None
+    return dH, dWcat[:, :C_].contiguous(), dWcat[:, C_:].contiguous()
+
+
+# ---------------------------------------------------------------------------
+# GMMConv
+# ---------------------------------------------------------------------------
+@dataclass
+class GmmStash:
+    Y: torch.Tensor  # [hW | pl | pr], V x (K f + 2 r)
+
+
+def gmm_forward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K: int, r: int, f: int):
+    """GMMConv layer forward: Y = H [W | P_l | P_r], then the fused
+    Gaussian-weighted aggregation (K8)."""
+    H = _f32(H, "H")
+    Fin = H.shape[1]
+    _shape(W, (Fin, K * f), "W")
+    _shape(P_l, (Fin, r), "P_l")
+    _shape(P_r, (Fin, r), "P_r")
+    _shape(mu, (K, r), "mu")
+    _shape(sinv, (K, r), "sinv")
+    Y = gemm(H, torch.cat([_f32(W, "W"), _f32(P_l, "P_l"), _f32(P_r, "P_r")], dim=1), ws=g.ws)
+    out = torch.empty(g.num_vertices, f, device=H.device)
+    call("gnncg_gmm_fwd", g.csr_dst.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(_f32(mu, "mu")),
+         _ptr(_f32(sinv, "sinv")), _ptr(out), _stream())
+    return out, GmmStash(Y)
+
+
+def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmStash, dOut, need_dH=True):
+    """Returns (dH, dW, dP_l, dP_r, dmu, dsinv)."""
+    H = _f32(H, "H")
+    dOut = _f32(dOut, "dOut")
+    V = g.num_vertices
+    Y = stash.Y
+    dY = torch.empty_like(Y)
+    dmu = torch.empty(K, r, device=H.device)
+    dsinv = torch.empty(K, r, device=H.device)
+    need = _lib.lib().gnncg_gmm_bwd_workspace(g.csr_dst.struct(), K, r)
+    wp, wn = g.ws.get(need)
+    call("gnncg_gmm_bwd", g.csr_dst.struct(), g.csc_src.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(mu),
+         _ptr(sinv), _ptr(dOut), _ptr(dY), _ptr(dmu), _ptr(dsinv), wp, wn, _stream())
+    dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
+    dH = gemm(dY, torch.cat([W, P_l, P_r], dim=1), trans_b=True, ws=g.ws) if need_dH else None
+    Kf = K * f
+    return dH, dWcat[:, :Kf].contiguous(), dWcat[:, Kf:Kf + r].contiguous(), dWcat[:, Kf + r:].contiguous(), dmu, dsinv

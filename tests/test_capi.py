@@ -1,0 +1,98 @@
+"""CPU: the C-ABI library loads, exports every symbol include/gnncg_b200.h declares,
+refuses to compute without a B200 (no CPU fallback), and its host-only entry points
+(schedule builder, partitioner) satisfy their contracts."""
+import ctypes as C
+import os
+import re
+
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2110_09524_b200 import _lib
+from paper_2110_09524_b200.graph import DeviceSched, partition_rows
+from tests.conftest import ROOT
+
+
+def header_functions():
+    src = open(os.path.join(ROOT, "include", "gnncg_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    return sorted(set(re.findall(r"\b(gnncg_[a-z0-9_]+)\s*\(", src)))
+
+
+def test_header_symbols_exported():
+    L = _lib.lib()
+    names = header_functions()
+    assert len(names) >= 25
+    for n in names:
+        assert hasattr(L, n), f"{n} declared in gnncg_b200.h but not exported"
+    # every binding the Python layer declares is a header function
+    assert set(_lib.EXPORTED) <= set(names)
+    assert set(names) <= set(_lib.EXPORTED), set(names) - set(_lib.EXPORTED)
+
+
+def test_version():
+    assert b"sm_100a" in _lib.lib().gnncg_version()
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_no_cpu_fallback():
+    L = _lib.lib()
+    assert L.gnncg_device_check() == 3  # GNNCG_ERR_NO_DEVICE
+    with pytest.raises(_lib.DeviceError):
+        _lib.require_device()
+    # a compute entry point refuses too
+    rc = L.gnncg_gemm(0, 0, 4, 4, 4, None, 4, None, 4, None, 4, None, 0, None)
+    assert rc == 3
+    assert "no CPU fallback" in _lib.last_error() or "CUDA" in _lib.last_error()
+
+
+def _sched_reference(off, chunk):
+    """Restatement of the schedule contract (runtime.cu:gnncg_sched_build_host)."""
+    deg = np.diff(off.astype(np.int64))
+    split = [r for r in range(len(deg)) if deg[r] > chunk]
+    items = []
+    for r in split:
+        items += [(r, c) for c in range(-(-deg[r] // chunk))]
+    n_split_items = len(items)
+    rest = [r for r in range(len(deg)) if deg[r] <= chunk]
+    rest.sort(key=lambda r: (-int(np.floor(np.log2(deg[r] + 1))), r))
+    items += [(r, 0) for r in rest]
+    return items, n_split_items, split
+
+
+@pytest.mark.parametrize("chunk", [32, 64, 2048])
+def test_schedule_builder_contract(chunk):
+    rng = np.random.default_rng(chunk)
+    deg = np.concatenate([rng.integers(0, 40, 500), [0, 0, 1000, 33, 64, 65, 4097]])
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    n, ns, nr, items, split_rows, split_first = DeviceSched.host_arrays(off, chunk)
+    ref_items, ref_ns, ref_split = _sched_reference(off, chunk)
+    assert n == len(ref_items) and ns == ref_ns and nr == len(ref_split)
+    assert [tuple(x) for x in items[:2 * n].reshape(-1, 2)] == ref_items
+    assert list(split_rows[:nr]) == ref_split
+    # every edge covered exactly once by the items' [e0, e1) ranges
+    cover = np.zeros(int(off[-1]), np.int32)
+    for r, c in ref_items:
+        e0 = int(off[r]) + c * chunk
+        e1 = min(int(off[r + 1]), e0 + chunk)
+        cover[e0:e1] += 1
+    assert np.all(cover == 1)
+    # split_first delimits each split row's items
+    for i, r in enumerate(split_rows[:nr]):
+        its = items[2 * split_first[i]:2 * split_first[i + 1]].reshape(-1, 2)
+        assert set(its[:, 0]) == {r} and list(its[:, 1]) == list(range(len(its)))
+
+
+def test_partitioner_matches_oracle():
+    rng = np.random.default_rng(1)
+    off = np.concatenate([[0], np.cumsum(rng.integers(0, 100, 5000))]).astype(np.uint64)
+    for P in (1, 2, 4, 7, 8):
+        np.testing.assert_array_equal(partition_rows(off, P), O.partition_rows(off, P))
+
+
+def test_errors_map_to_reference_exceptions():
+    assert issubclass(_lib.GraphError, RuntimeError) and issubclass(_lib.TensorError, RuntimeError)
+    with pytest.raises(_lib.ArgumentError):
+        _lib.call("gnncg_partition_rows", 10, None, 2, None)

@@ -1,0 +1,100 @@
+"""GPU parity of EdgeConv (bit-exact argmax) and GMMConv against the oracle."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2110_09524_b200 import DeviceGraph, edgeconv_backward, edgeconv_forward, gmm_backward, gmm_forward
+from paper_2110_09524_b200.graph import knn_edges
+from paper_2110_09524_b200.ops import edgeconv_region_forward
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def t32(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+
+
+def np64(t):
+    return t.detach().cpu().double().numpy()
+
+
+@pytest.mark.parametrize("clouds,points,k,C", [(2, 256, 20, 64), (4, 1024, 40, 64), (1, 64, 8, 33)])
+def test_edgeconv_region_argmax_bit_exact(cuda, clouds, points, k, C):
+    src, dst = knn_edges(clouds, points, k, seed=0)
+    V = clouds * points
+    hg = O.host_graph(V, src, dst)
+    g = DeviceGraph.from_edges(V, src, dst, device=cuda)
+    rng = np.random.default_rng(C)
+    # quantized values create exact ties, exercising the lowest-edge-id rule
+    Th = (rng.integers(-8, 8, (V, C)) / 4.0).astype(np.float32)
+    Ph = rng.uniform(-1, 1, (V, C)).astype(np.float32)
+    ref_out, ref_amax = O.edgeconv_fwd(hg, Th, Ph, np.float32)
+    out, amax = edgeconv_region_forward(g, t32(Th, cuda), t32(Ph, cuda))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(amax.cpu().numpy().view(np.uint32), ref_amax)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref_out)  # same fp32 RN expression -> bitwise
+
+
+def test_edgeconv_empty_rows_and_ties(cuda):
+    src, dst = [1, 2, 3, 1, 2, 3], [0, 0, 0, 0, 0, 0]
+    g = DeviceGraph.from_edges(4, src, dst, device=cuda)
+    Th = t32([[0.0], [5.0], [5.0], [1.0]], cuda)
+    out, amax = edgeconv_region_forward(g, Th, t32(np.zeros((4, 1)), cuda))
+    a = amax.cpu().numpy().view(np.uint32)
+    assert a[0, 0] == 0 and out[0, 0].item() == 5.0
+    assert all(a[v, 0] == 0xFFFFFFFF and out[v, 0].item() == 0.0 for v in (1, 2, 3))
+
+
+@pytest.mark.parametrize("k", [20, 40])
+def test_edgeconv_layer_vs_oracle(cuda, k):
+    src, dst = knn_edges(2, 512, k, seed=1)
+    V = 1024
+    hg = O.host_graph(V, src, dst)
+    g = DeviceGraph.from_edges(V, src, dst, device=cuda)
+    rng = np.random.default_rng(k)
+    Fin, C = 64, 64
+    H = rng.uniform(-1, 1, (V, Fin))
+    Theta, Phi = rng.uniform(-0.125, 0.125, (Fin, C)), rng.uniform(-0.125, 0.125, (Fin, C))
+    dOut = rng.uniform(-1, 1, (V, C))
+    tH, tT, tP = t32(H, cuda), t32(Theta, cuda), t32(Phi, cuda)
+    out, st = edgeconv_forward(g, tH, tT, tP)
+    # argmax parity is defined on identical Th/Ph: feed the device GEMM output to the f32 oracle
+    Y = st.Y.cpu().numpy()
+    ref_out, ref_amax = O.edgeconv_fwd(hg, Y[:, :C], Y[:, C:], np.float32)
+    np.testing.assert_array_equal(st.argmax.cpu().numpy().view(np.uint32), ref_amax)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref_out)
+    fw = O.edgeconv_layer_fwd_f64(hg, H, Theta, Phi)
+    assert O.max_rel_err(np64(out), fw["out"]) < TOL
+    dH, dTheta, dPhi = edgeconv_backward(g, tH, tT, tP, st, t32(dOut, cuda))
+    torch.cuda.synchronize()
+    bw = O.edgeconv_layer_bwd_f64(hg, H, Theta, Phi, ref_amax, dOut)  # route with the shared argmax
+    for name, got in (("dH", dH), ("dTheta", dTheta), ("dPhi", dPhi)):
+        scale = max(1.0, np.abs(bw[name]).max())
+        assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name
+
+
+@pytest.mark.parametrize("V,E,Fin,K,r,f", [(200, 1500, 20, 3, 2, 16), (19717, 88648, 500, 3, 3, 16),
+                                           (500, 4000, 8, 2, 1, 16), (300, 2000, 10, 8, 4, 32)])
+def test_gmm_layer_vs_oracle(cuda, V, E, Fin, K, r, f):
+    rng = np.random.default_rng(V)
+    src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    hg = O.host_graph(V, src, dst)
+    g = DeviceGraph.from_edges(V, src, dst, device=cuda)
+    s = 1 / np.sqrt(Fin)
+    H = rng.uniform(-1, 1, (V, Fin))
+    W = rng.uniform(-s, s, (Fin, K * f))
+    Pl, Pr = rng.uniform(-s, s, (Fin, r)), rng.uniform(-s, s, (Fin, r))
+    mu, sinv = rng.uniform(-0.5, 0.5, (K, r)), rng.uniform(0.5, 1.5, (K, r))
+    dOut = rng.uniform(-1, 1, (V, f))
+    fw = O.gmm_layer_fwd_f64(hg, H, W, Pl, Pr, mu, sinv, K, r, f)
+    bw = O.gmm_layer_bwd_f64(hg, H, W, Pl, Pr, mu, sinv, K, r, f, fw, dOut)
+    args = [t32(x, cuda) for x in (H, W, Pl, Pr, mu, sinv)]
+    out, st = gmm_forward(g, *args, K, r, f)
+    grads = gmm_backward(g, *args, K, r, f, st, t32(dOut, cuda))
+    torch.cuda.synchronize()
+    assert O.max_rel_err(np64(out), fw["out"]) < TOL
+    for name, got in zip(("dH", "dW", "dPl", "dPr", "dmu", "dsinv"), grads):
+        scale = max(1.0, np.abs(bw[name]).max())
+        assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name

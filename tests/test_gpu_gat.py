@@ -1,0 +1,177 @@
+"""GPU parity of the fused GAT path (K2 forward, K3/K4 recompute backward, K1/K5 GEMMs)
+against the f64 oracle.  Tolerance: 1e-4 relative with the reference's comparator
+|a-b| / max(1,|a|,|b|) (tensor.hpp:153-156; north_star fp32 bound)."""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from paper_2110_09524_b200 import DeviceGraph, GatParams, gat_backward, gat_forward, gemm
+from paper_2110_09524_b200.models import GAT
+from paper_2110_09524_b200.ops import GatStash, gat_region_backward, gat_region_forward
+
+pytestmark = pytest.mark.gpu
+TOL = 1e-4
+
+
+def t32(x, dev):
+    return torch.from_numpy(np.ascontiguousarray(x, dtype=np.float32)).to(dev)
+
+
+def np64(t):
+    return t.detach().cpu().double().numpy()
+
+
+def make_graph(kind, dev, seed=0):
+    rng = np.random.default_rng(seed)
+    if kind == "G3":
+        V, src, dst = 3, np.array([0, 1, 0]), np.array([2, 2, 1])
+    elif kind == "ER16":
+        V = 16
+        src, dst = np.nonzero(np.random.default_rng(7).random((16, 16)) < 0.3)
+    elif kind == "cora":
+        V, E = 2708, 10556
+        src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    elif kind == "star":  # one hub with 5000 in-edges + a hub source with many out-edges + empty rows
+        V = 6000
+        src = np.concatenate([np.arange(1, 5001), np.full(3000, 7), rng.integers(0, V, 2000)])
+        dst = np.concatenate([np.zeros(5000, np.int64), rng.integers(0, V, 3000), rng.integers(0, 100, 2000)])
+    elif kind == "powerlaw":
+        V, E = 3000, 200000
+        w = 1.0 / (np.arange(V) + 30.0)
+        w /= w.sum()
+        src, dst = rng.choice(V, E, p=w), rng.choice(V, E, p=w)
+    else:
+        raise ValueError(kind)
+    hg = O.host_graph(V, src, dst)
+    return hg, DeviceGraph.from_edges(V, src, dst, device=dev)
+
+
+CASES = [("G3", 1, 2), ("ER16", 2, 3), ("ER16", 3, 5), ("cora", 8, 8), ("star", 8, 32), ("powerlaw", 8, 32),
+         ("powerlaw", 1, 128), ("powerlaw", 4, 64), ("cora", 8, 16), ("star", 2, 1), ("cora", 4, 256)]
+
+
+@pytest.mark.parametrize("kind,h,f", CASES)
+@pytest.mark.parametrize("chunk", [32, 2048])
+def test_region_forward_and_backward(cuda, kind, h, f, chunk):
+    hg, g = make_graph(kind, cuda)
+    V = hg.V
+    rng = np.random.default_rng(h * 100 + f)
+    Ht = rng.uniform(-1, 1, (V, h * f))
+    Al, Ar = rng.uniform(-1, 1, (V, h)), rng.uniform(-1, 1, (V, h))
+    al, ar = rng.uniform(-1, 1, (h, f)), rng.uniform(-1, 1, (h, f))
+    dOut = rng.uniform(-1, 1, (V, h * f))
+    p = GatParams(h, f)
+    ref = O.gat_region_fwd_f64(hg, Ht, Al, Ar, h, f)
+    tHt, tAl, tAr = t32(Ht, cuda), t32(Al, cuda), t32(Ar, cuda)
+    out, m, d = gat_region_forward(g, tHt, tAl, tAr, p, chunk=chunk)
+    torch.cuda.synchronize()
+    assert O.max_rel_err(np64(out), ref["out"]) < TOL
+    assert O.max_rel_err(np64(m), ref["m"]) < TOL
+    assert O.max_rel_err(np64(d), ref["d"]) < TOL
+    rb = O.gat_region_bwd_f64(hg, Ht, Al, Ar, al, ar, h, f, dOut)
+    st = GatStash(tHt, tAl, tAr, m, d)
+    dHt, dAl, dAr, da_l, da_r, c = gat_region_backward(g, st, t32(al, cuda), t32(ar, cuda), t32(dOut, cuda), p,
+                                                       chunk=chunk)
+    torch.cuda.synchronize()
+    for name, got in (("dHt", dHt), ("dAl", dAl), ("dAr", dAr), ("dal", da_l), ("dar", da_r)):
+        scale = max(1.0, np.abs(rb[name]).max()) if name in ("dal", "dar") else 1.0
+        err = O.max_rel_err(np64(got) / scale, rb[name] / scale)
+        assert err < TOL, (name, err)
+
+
+def test_chunking_is_consistent(cuda):
+    hg, g = make_graph("star", cuda)
+    V, h, f = hg.V, 8, 32
+    rng = np.random.default_rng(0)
+    Ht, Al, Ar = (t32(rng.uniform(-1, 1, s), cuda) for s in ((V, h * f), (V, h), (V, h)))
+    p = GatParams(h, f)
+    a = gat_region_forward(g, Ht, Al, Ar, p, chunk=32)
+    b = gat_region_forward(g, Ht, Al, Ar, p, chunk=1 << 20)
+    for x, y in zip(a, b):
+        assert torch.allclose(x, y, rtol=1e-5, atol=1e-5)
+
+
+def test_deterministic_runs(cuda):
+    hg, g = make_graph("powerlaw", cuda)
+    V, h, f = hg.V, 8, 32
+    rng = np.random.default_rng(1)
+    H, W = t32(rng.uniform(-0.1, 0.1, (V, 64)), cuda), t32(rng.uniform(-0.1, 0.1, (64, h * f)), cuda)
+    al, ar = t32(rng.uniform(-1, 1, (h, f)), cuda), t32(rng.uniform(-1, 1, (h, f)), cuda)
+    dOut = t32(rng.uniform(-1, 1, (V, h * f)), cuda)
+    p = GatParams(h, f)
+    res = []
+    for _ in range(2):
+        out, st = gat_forward(g, H, W, al, ar, p)
+        gr = gat_backward(g, H, W, al, ar, st, dOut, p)
+        res.append([out, gr.dH, gr.dW, gr.da_l, gr.da_r])
+    for x, y in zip(*res):
+        assert torch.equal(x, y)  # fixed-order reductions: bitwise reproducible
+
+
+@pytest.mark.parametrize("kind,Fin,h,f", [("G3", 2, 1, 2), ("ER16", 3, 2, 2), ("cora", 1433, 8, 8),
+                                          ("powerlaw", 602, 8, 32)])
+def test_layer_vs_oracle(cuda, kind, Fin, h, f):
+    hg, g = make_graph(kind, cuda)
+    V = hg.V
+    rng = np.random.default_rng(5)
+    s = lambda n: 1 / np.sqrt(n)  # noqa: E731  init_seeded scale (tensor.hpp:55)
+    H = rng.uniform(-1, 1, (V, Fin))
+    W = rng.uniform(-s(h * f), s(h * f), (Fin, h * f))
+    al, ar = rng.uniform(-s(f), s(f), (h, f)), rng.uniform(-s(f), s(f), (h, f))
+    dOut = rng.uniform(-1, 1, (V, h * f))
+    fw = O.gat_layer_fwd_f64(hg, H, W, al, ar, h, f)
+    bw = O.gat_layer_bwd_f64(hg, H, W, al, ar, h, f, fw, dOut)
+    p = GatParams(h, f)
+    tH, tW, tal, tar = (t32(x, cuda) for x in (H, W, al, ar))
+    out, st = gat_forward(g, tH, tW, tal, tar, p)
+    gr = gat_backward(g, tH, tW, tal, tar, st, t32(dOut, cuda), p, need_dH=True)
+    torch.cuda.synchronize()
+    assert O.max_rel_err(np64(st.Ht), fw["Ht"]) < TOL
+    assert O.max_rel_err(np64(out), fw["out"]) < TOL
+    for name, got in (("dH", gr.dH), ("dW", gr.dW), ("dal", gr.da_l), ("dar", gr.da_r)):
+        scale = max(1.0, np.abs(bw[name]).max())  # reductions over V: compare relative to the magnitude
+        err = O.max_rel_err(np64(got) / scale, bw[name] / scale)
+        assert err < TOL, (name, err)
+
+
+def test_two_layer_model_step(cuda):
+    hg, g = make_graph("cora", cuda)
+    V, Fin = hg.V, 100
+    dims = [(Fin, 8, 8), (64, 8, 8)]
+    model = GAT(g, dims, seed=3)
+    rng = np.random.default_rng(2)
+    H = rng.uniform(-1, 1, (V, Fin))
+    tH = t32(H, cuda)
+    Ws = [(np64(L.W), np64(L.a_l), np64(L.a_r)) for L in model.layers]
+    loss, grads = model.train_step(tH, lr=0.0)
+    torch.cuda.synchronize()
+    # oracle chain: identity between layers, loss = sum(out), dOut = ones
+    f1 = O.gat_layer_fwd_f64(hg, H, *Ws[0], 8, 8)
+    f2 = O.gat_layer_fwd_f64(hg, f1["out"], *Ws[1], 8, 8)
+    assert abs(float(loss.item()) - f2["out"].sum()) / max(1.0, abs(f2["out"].sum())) < TOL
+    b2 = O.gat_layer_bwd_f64(hg, f1["out"], *Ws[1], 8, 8, f2, np.ones((V, 64)))
+    b1 = O.gat_layer_bwd_f64(hg, H, *Ws[0], 8, 8, f1, b2["dH"], need_dH=False)
+    for gr, b in ((grads[1], b2), (grads[0], b1)):
+        for name, got in (("dW", gr.dW), ("dal", gr.da_l), ("dar", gr.da_r)):
+            scale = max(1.0, np.abs(b[name]).max())
+            assert O.max_rel_err(np64(got) / scale, b[name] / scale) < TOL, name
+    # SGD: lr = 0 leaves params bitwise unchanged
+    for L, (W, al, ar) in zip(model.layers, Ws):
+        assert np.array_equal(np64(L.W), W)
+    loss2, _ = model.train_step(tH, lr=1e-3)
+    torch.cuda.synchronize()
+    assert not np.array_equal(np64(model.layers[0].W), Ws[0][0])
+
+
+@pytest.mark.parametrize("ta,tb,M,N,K", [(0, 0, 300, 257, 129), (0, 1, 1000, 602, 256), (1, 0, 602, 256, 20000),
+                                         (0, 0, 5, 3, 0), (1, 0, 33, 17, 5)])
+def test_gemm_vs_reference_matmul(cuda, ta, tb, M, N, K):
+    rng = np.random.default_rng(M + N + K)
+    A = rng.uniform(-1, 1, (K, M) if ta else (M, K)).astype(np.float32)
+    B = rng.uniform(-1, 1, (N, K) if tb else (K, N)).astype(np.float32)
+    ref = (A.T.astype(np.float64) if ta else A.astype(np.float64)) @ (B.T.astype(np.float64) if tb else B.astype(np.float64))
+    got = gemm(t32(A, cuda), t32(B, cuda), trans_a=bool(ta), trans_b=bool(tb))
+    torch.cuda.synchronize()
+    scale = max(1.0, np.abs(ref).max())
+    assert O.max_rel_err(np64(got) / scale, ref / scale) < 1e-5

@@ -1,0 +1,307 @@
+"""CPU: pin the oracle (test infrastructure) to the reference before trusting it.
+
+  * restated build_index == the reference's own Graph ctor on every committed golden
+    graph (bit-exact) and on fresh random edge lists via oracle/_ref when present;
+  * SPEC known-answer examples;
+  * GAT / EdgeConv / GMMConv f64 layers == torch autograd (f64) and central finite
+    differences (h = 1e-4, 1e-4 relative);
+  * the f32 OpenMP baseline == the f64 oracle within 1e-4 (SPEC.md:139 tolerance).
+"""
+import numpy as np
+import pytest
+import torch
+
+from oracle import oracle as O
+from tests.conftest import golden_graphs
+
+
+def G3():
+    return O.host_graph(3, [0, 1, 0], [2, 2, 1])
+
+
+# ---------------------------------------------------------------- graph store
+def test_build_index_matches_reference_goldens(golden):
+    for name, d in golden_graphs(golden):
+        g = O.host_graph(d["V"], d["src"], d["dst"])
+        for fld in ("dst_off", "dst_src", "dst_eid", "src_off", "src_dst", "src_eid"):
+            np.testing.assert_array_equal(getattr(g, fld), d[fld], err_msg=f"{name}:{fld}")
+
+
+def test_degree_stats_goldens(golden):
+    for name, d in golden_graphs(golden):
+        off_in, off_out = d["dst_off"].astype(np.int64), d["src_off"].astype(np.int64)
+        V = d["V"]
+        mi = int(np.diff(off_in).max()) if V else 0
+        mo = int(np.diff(off_out).max()) if V else 0
+        mean = 0.0 if V == 0 else len(d["src"]) / V
+        assert (mi, mean, mo) == tuple([d["stats"][0], d["stats"][1], d["stats"][2]]), name
+
+
+def test_spec_graph_known_answers(golden):
+    names = {n: d for n, d in golden_graphs(golden)}
+    # G3: in-edges of v2 = {e0, e1}, of v1 = {e2}, of v0 = none
+    g3 = names["G3"]
+    assert list(g3["dst_off"]) == [0, 0, 1, 3] and list(g3["dst_eid"]) == [2, 0, 1]
+    # star(4): max_in = 3, mean_in = 0.75
+    s4 = names["star:4@0"]["stats"]
+    assert s4[0] == 3 and s4[1] == 0.75
+    # k_regular_in(5,2,42): every in-degree 2, E = 10
+    k = names["k_regular_in:5:2@42"]
+    assert len(k["src"]) == 10 and set(np.diff(k["dst_off"].astype(np.int64))) == {2}
+    # empty graph: all zeros, mean defined as 0
+    assert tuple(names["empty"]["stats"]) == (0.0, 0.0, 0.0)
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_build_index_matches_reference_random():
+    rng = np.random.default_rng(5)
+    for V, E in ((1, 5), (17, 0), (64, 3000), (4000, 50000)):
+        src = rng.integers(0, V, E)
+        dst = rng.integers(0, V, E)
+        r = O.RefGraph.from_edges(V, src, dst).to_host()
+        g = O.host_graph(V, src, dst)
+        for fld in ("dst_off", "dst_src", "dst_eid", "src_off", "src_dst", "src_eid"):
+            np.testing.assert_array_equal(getattr(g, fld), getattr(r, fld))
+
+
+@pytest.mark.skipif(not O.ref_available(), reason="oracle/_ref not built")
+def test_reference_rejects_out_of_range():
+    with pytest.raises(ValueError, match="out of range"):
+        O.RefGraph.from_edges(2, [0, 2], [1, 1])
+
+
+def test_init_seeded_goldens(golden):
+    # SURVEY Appendix A probe: init_seeded<double>(2,3,42)
+    np.testing.assert_array_equal(golden["init_f64_2x3_42"].ravel(), np.array(
+        [0.29462823127305104, 0.16053962533563693, 0.29115219905349077, -0.41999612803286523, 0.46565489264649285,
+         -0.46872953895265052]))
+    assert golden["init_f64_ones"][0, 0] == 1.0
+
+
+def test_oracle_matmul_matches_reference_goldens(golden):
+    A, B, Bt, At = golden["mm_A"], golden["mm_B"], golden["mm_Bt"], golden["mm_At"]
+    C = np.zeros((A.shape[0], B.shape[1]), np.float32)
+    O.lib().orc_mm_nn_f32(O.u64(A.shape[0]), O.u64(A.shape[1]), O.u64(B.shape[1]), O._p(A), O._p(B), O._p(C))
+    np.testing.assert_array_equal(C, golden["mm_nn"])  # same loop order => bitwise
+    C2 = np.zeros((A.shape[0], Bt.shape[0]), np.float32)
+    O.lib().orc_mm_nt_f32(O.u64(A.shape[0]), O.u64(A.shape[1]), O.u64(Bt.shape[0]), O._p(A), O._p(Bt), O._p(C2))
+    np.testing.assert_array_equal(C2, golden["mm_nt"])
+    C3 = np.zeros((At.shape[1], B.shape[1]), np.float32)
+    O.lib().orc_mm_tn_f32(O.u64(At.shape[0]), O.u64(At.shape[1]), O.u64(B.shape[1]), O._p(At), O._p(B), O._p(C3))
+    np.testing.assert_array_equal(C3, golden["mm_tn"])
+
+
+def test_partition_rows_contract():
+    rng = np.random.default_rng(0)
+    off = np.concatenate([[0], np.cumsum(rng.integers(0, 50, 1000))]).astype(np.uint64)
+    for P in (1, 2, 3, 8):
+        b = O.partition_rows(off, P)
+        E = int(off[-1])
+        assert b[0] == 0 and b[-1] == 1000 and np.all(np.diff(b.astype(np.int64)) >= 0)
+        for p in range(1, P):
+            target = -(-p * E // P)
+            assert b[p] == np.searchsorted(off, target, side="left")
+
+
+# ---------------------------------------------------------------- SPEC known answers
+def test_gather_sum_g3():
+    # Gather(sum) on G3, m = [1,2,3] -> h = [0, 3, 3]
+    g = G3()
+    m = np.array([1.0, 2.0, 3.0])
+    h = np.zeros(3)
+    for v in range(3):
+        for i in range(g.dst_off[v], g.dst_off[v + 1]):
+            h[v] += m[g.dst_eid[i]]
+    assert list(h) == [0, 3, 3]
+
+
+def test_dense_aggregate_g3():
+    # fused copy_u x w sum with H = [[1],[2],[4]] -> [0, 1, 3] = A^T H
+    out = O.dense_aggregate_f64(3, [0, 1, 0], [2, 2, 1], np.array([[1.0], [2.0], [4.0]]))
+    assert list(out[:, 0]) == [0, 1, 3]
+
+
+def test_gather_and_scatter_backward_g3():
+    g = G3()
+    hbar = np.array([1.0, 10.0, 100.0])  # Gather(sum) bwd: edge e gets its destination's grad
+    mbar = np.zeros(3)
+    for v in range(3):
+        for i in range(g.dst_off[v], g.dst_off[v + 1]):
+            mbar[g.dst_eid[i]] = hbar[v]
+    assert list(mbar) == [100, 100, 10]
+    ebar = np.array([1.0, 2.0, 3.0])  # Scatter(copy_u) bwd: per-source sums over out-edges
+    vbar = np.zeros(3)
+    for u in range(3):
+        for i in range(g.src_off[u], g.src_off[u + 1]):
+            vbar[u] += ebar[g.src_eid[i]]
+    assert list(vbar) == [4, 2, 0]
+
+
+def test_cost_formulas_g3():
+    c = O.cost_counts(3, 3, 1, 2)
+    assert (c["flops_naive"], c["flops_reorg"], c["io_unfused"], c["io_fused"]) == (39, 30, 45, 33)
+
+
+def test_gat_on_g3_by_hand():
+    # f=1, h=1: v2 averages Ht[0], Ht[1] by softmax weights; v1 copies Ht[0]; v0 empty.
+    g = G3()
+    Ht = np.array([[1.0], [3.0], [5.0]])
+    Al = np.array([[0.5], [-1.0], [0.0]])
+    Ar = np.array([[0.0], [0.2], [0.1]])
+    r = O.gat_region_fwd_f64(g, Ht, Al, Ar, 1, 1)
+    lr = lambda z: z if z > 0 else 0.2 * z  # noqa: E731
+    s0, s1 = lr(0.5 + 0.1), lr(-1.0 + 0.1)
+    a0 = np.exp(s0) / (np.exp(s0) + np.exp(s1))
+    assert r["out"][0, 0] == 0 and r["m"][0, 0] == 0 and r["d"][0, 0] == 0
+    assert abs(r["out"][1, 0] - 1.0) < 1e-15
+    assert abs(r["out"][2, 0] - (a0 * 1 + (1 - a0) * 3)) < 1e-14
+    assert abs(r["m"][2, 0] - max(s0, s1)) == 0
+
+
+def test_leaky_relu_definition():
+    g = O.host_graph(2, [0], [1])
+    Ht = np.array([[2.0], [0.0]])
+    # single edge: softmax weight 1 => out = Ht[0] regardless; m = LReLU(A_l+A_r)
+    for z, expect in ((-1.0, -0.2), (2.0, 2.0)):
+        r = O.gat_region_fwd_f64(g, Ht, np.array([[z], [0.0]]), np.zeros((2, 1)), 1, 1)
+        assert abs(r["m"][1, 0] - expect) < 1e-15 and r["d"][1, 0] == 1.0
+
+
+# ---------------------------------------------------------------- autograd / finite differences
+def _torch_gat(src, dst, V, H, W, al, ar, h, f):
+    Ht = H @ W
+    Ht3 = Ht.view(V, h, f)
+    Al = (Ht3 * al).sum(-1)
+    Ar = (Ht3 * ar).sum(-1)
+    s = torch.nn.functional.leaky_relu(Al[src] + Ar[dst], 0.2)
+    E = src.shape[0]
+    mx = torch.full((V, h), -float("inf"), dtype=H.dtype).scatter_reduce(0, dst[:, None].expand(E, h), s, "amax")
+    p = torch.exp(s - mx[dst])
+    den = torch.zeros(V, h, dtype=H.dtype).index_add(0, dst, p)
+    a = p / den[dst]
+    return torch.zeros(V, h, f, dtype=H.dtype).index_add(0, dst, a[:, :, None] * Ht3[src]).view(V, h * f)
+
+
+@pytest.mark.parametrize("V,E,Fin,h,f,seed", [(3, 3, 2, 1, 2, 0), (20, 90, 5, 3, 4, 1), (40, 300, 7, 2, 3, 2)])
+def test_gat_oracle_vs_autograd(V, E, Fin, h, f, seed):
+    rng = np.random.default_rng(seed)
+    if V == 3:
+        src, dst = np.array([0, 1, 0]), np.array([2, 2, 1])
+    else:
+        src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    g = O.host_graph(V, src, dst)
+    H, W = rng.standard_normal((V, Fin)), rng.standard_normal((Fin, h * f))
+    al, ar, dOut = rng.standard_normal((h, f)), rng.standard_normal((h, f)), rng.standard_normal((V, h * f))
+    fw = O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)
+    bw = O.gat_layer_bwd_f64(g, H, W, al, ar, h, f, fw, dOut)
+    t = [torch.tensor(x, requires_grad=True) for x in (H, W, al, ar)]
+    out = _torch_gat(torch.tensor(src), torch.tensor(dst), V, *t, h, f)
+    (out * torch.tensor(dOut)).sum().backward()
+    assert np.abs(out.detach().numpy() - fw["out"]).max() < 1e-12
+    for name, tt in zip(("dH", "dW", "dal", "dar"), t):
+        assert np.abs(tt.grad.numpy() - bw[name]).max() < 1e-11, name
+
+
+def _fd_check(loss_fn, params, grads, step=1e-4, tol=1e-4, max_entries=40, seed=0):
+    rng = np.random.default_rng(seed)
+    for P, G in zip(params, grads):
+        flat = P.reshape(-1)
+        idx = rng.choice(flat.size, size=min(max_entries, flat.size), replace=False)
+        for i in idx:
+            old = flat[i]
+            flat[i] = old + step
+            lp = loss_fn()
+            flat[i] = old - step
+            lm = loss_fn()
+            flat[i] = old
+            fd = (lp - lm) / (2 * step)
+            assert O.rel_err(fd, G.reshape(-1)[i]) < tol, (fd, G.reshape(-1)[i])
+
+
+@pytest.mark.parametrize("graph", ["G3", "ER16"])
+def test_gat_finite_differences(graph):
+    # analytic vs central differences, f64, step 1e-4, 1e-4 relative
+    if graph == "G3":
+        V, src, dst = 3, [0, 1, 0], [2, 2, 1]
+    else:
+        V, src, dst = 16, *np.nonzero(np.random.default_rng(7).random((16, 16)) < 0.3)
+    g = O.host_graph(V, src, dst)
+    rng = np.random.default_rng(42)
+    h, f, Fin = 2, 2, 3
+    H, W = rng.standard_normal((V, Fin)), rng.standard_normal((Fin, h * f)) * 0.5
+    al, ar = rng.standard_normal((h, f)), rng.standard_normal((h, f))
+    ones = np.ones((V, h * f))
+    fw = O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)
+    bw = O.gat_layer_bwd_f64(g, H, W, al, ar, h, f, fw, ones)
+    loss = lambda: O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)["out"].sum()  # noqa: E731
+    _fd_check(loss, [W, al, ar, H], [bw["dW"], bw["dal"], bw["dar"], bw["dH"]])
+
+
+def test_edgeconv_finite_differences():
+    rng = np.random.default_rng(3)
+    V = 16
+    src, dst = np.nonzero(rng.random((V, V)) < 0.3)
+    g = O.host_graph(V, src, dst)
+    Fin, C_ = 3, 4
+    H = rng.standard_normal((V, Fin))
+    Th, Ph = rng.standard_normal((Fin, C_)), rng.standard_normal((Fin, C_))
+    fw = O.edgeconv_layer_fwd_f64(g, H, Th, Ph)
+    bw = O.edgeconv_layer_bwd_f64(g, H, Th, Ph, fw["amax"], np.ones((V, C_)))
+    loss = lambda: O.edgeconv_layer_fwd_f64(g, H, Th, Ph)["out"].sum()  # noqa: E731
+    _fd_check(loss, [Th, Ph, H], [bw["dTheta"], bw["dPhi"], bw["dH"]])
+
+
+def test_edgeconv_argmax_lowest_edge_id_and_empty_rows():
+    # star(4, mult 2): two parallel edges per spoke tie exactly -> lowest eid wins
+    src = [1, 2, 3, 1, 2, 3]
+    dst = [0, 0, 0, 0, 0, 0]
+    g = O.host_graph(4, src, dst)
+    Th = np.array([[0.0], [5.0], [5.0], [1.0]], np.float32)
+    Ph = np.zeros((4, 1), np.float32)
+    out, amax = O.edgeconv_fwd(g, Th, Ph)
+    assert out[0, 0] == 5.0 and amax[0, 0] == 0  # e0 (1->0) and e1 (2->0), e3, e4 tie at 5
+    assert all(amax[v, 0] == O.NO_EDGE and out[v, 0] == 0 for v in (1, 2, 3))
+    dTh, dPh = O.edgeconv_bwd(g, amax, np.ones((4, 1)))
+    assert dTh[1, 0] == 1 and dTh[2, 0] == 0 and dTh[0, 0] == -1 and dPh[0, 0] == 1 and dPh[1, 0] == 0
+
+
+def test_gmm_oracle_vs_autograd_and_fd():
+    rng = np.random.default_rng(11)
+    V, E, Fin, K, r, f = 18, 70, 5, 3, 2, 4
+    src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    g = O.host_graph(V, src, dst)
+    H, W = rng.standard_normal((V, Fin)), rng.standard_normal((Fin, K * f))
+    Pl, Pr = rng.standard_normal((Fin, r)) * 0.3, rng.standard_normal((Fin, r)) * 0.3
+    mu, sinv = rng.standard_normal((K, r)) * 0.5, 0.5 + rng.random((K, r))
+    dOut = rng.standard_normal((V, f))
+    fw = O.gmm_layer_fwd_f64(g, H, W, Pl, Pr, mu, sinv, K, r, f)
+    bw = O.gmm_layer_bwd_f64(g, H, W, Pl, Pr, mu, sinv, K, r, f, fw, dOut)
+    t = [torch.tensor(x, requires_grad=True) for x in (H, W, Pl, Pr, mu, sinv)]
+    tH, tW, tPl, tPr, tmu, tsi = t
+    hW = (tH @ tW).view(V, K, f)
+    m = (tH @ tPl)[src] + (tH @ tPr)[dst]  # E x r
+    w = torch.exp(-0.5 * (((m[:, None, :] - tmu[None]) ** 2) * tsi[None] ** 2).sum(-1))  # E x K
+    msg = (w[:, :, None] * hW[src]).sum(1) / K
+    out = torch.zeros(V, f, dtype=torch.float64).index_add(0, torch.tensor(dst), msg)
+    (out * torch.tensor(dOut)).sum().backward()
+    assert np.abs(out.detach().numpy() - fw["out"]).max() < 1e-12
+    for name, tt in zip(("dH", "dW", "dPl", "dPr", "dmu", "dsinv"), t):
+        assert np.abs(tt.grad.numpy() - bw[name]).max() < 1e-10, name
+    loss = lambda: (O.gmm_layer_fwd_f64(g, H, W, Pl, Pr, mu, sinv, K, r, f)["out"] * dOut).sum()  # noqa: E731
+    _fd_check(loss, [mu, sinv, Pl], [bw["dmu"], bw["dsinv"], bw["dPl"]])
+
+
+def test_f32_baseline_matches_f64_oracle():
+    rng = np.random.default_rng(9)
+    V, E, Fin, h, f = 400, 6000, 24, 8, 8
+    g = O.host_graph(V, rng.integers(0, V, E), rng.integers(0, V, E))
+    H = O.ref_init_seeded(V, Fin, 1) if O.ref_available() else rng.uniform(-0.2, 0.2, (V, Fin))
+    W, al, ar = rng.uniform(-0.2, 0.2, (Fin, h * f)), rng.uniform(-0.3, 0.3, (h, f)), rng.uniform(-0.3, 0.3, (h, f))
+    dOut = rng.uniform(-1, 1, (V, h * f))
+    fw = O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)
+    bw = O.gat_layer_bwd_f64(g, H, W, al, ar, h, f, fw, dOut)
+    f32f = O.gat_layer_fwd_f32_omp(g, H, W, al, ar, h, f)
+    f32b = O.gat_layer_bwd_f32_omp(g, H, W, al, ar, h, f, f32f, dOut)
+    assert O.max_rel_err(f32f["out"], fw["out"]) < 1e-4
+    for k in ("dH", "dW", "dal", "dar"):
+        assert O.max_rel_err(f32b[k], bw[k]) < 1e-4, k
