@@ -1,0 +1,299 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// gnncg_b200/ops.hpp -- header-only C++ operator API of the B200 fused GNN layer path,
+// written against the reference's own types (gnncg::Graph, graph.hpp:34-65;
+// gnncg::Tensor<float>, tensor.hpp:20-35) and error classes (GraphError,
+// TensorError).  It is what a reference executor (run_forward /
+// run_backward / train_step) calls in place of its CPU fused regions:
+//
+//   b200::DeviceGraph dg(graph);                          // upload + device CSR/CSC (bit-exact)
+//   b200::GatStash st;
+//   Tensor<float> out = b200::gat_forward(dg, H, W, a_l, a_r, {8, 32}, &st);
+//   b200::GatGrads gr = b200::gat_backward(dg, H, W, a_l, a_r, st, dOut, {8, 32}, true);
+//
+// Host tensors in, host tensors out (copies on the graph's stream); the device
+// stash stays resident between forward and backward.  Every FLOP runs in
+// libgnncg_b200.so through the C ABI of gnncg_b200.h; there is no CPU fallback.
+// Include after <gnncg/graph.hpp> and <gnncg/tensor.hpp>.
+#pragma once
+
+#include <cuda_runtime.h>
+
+#include <algorithm>  // tensor.hpp uses std::max(initializer_list) without including these
+#include <cstdint>
+#include <limits>
+#include <memory>
+#include <stdexcept>
+#include <string>
+#include <utility>
+#include <vector>
+
+#include "gnncg/graph.hpp"
+#include "gnncg/tensor.hpp"
+#include "gnncg_b200.h"
+
+namespace gnncg {
+namespace b200 {
+
+// Map a C-ABI status to the reference's exception types.
+inline void check(int rc, const char* what) {
+  if (rc == GNNCG_OK) return;
+  const std::string msg = std::string(what) + ": " + gnncg_last_error();
+  if (rc == GNNCG_ERR_SHAPE) throw TensorError(msg);
+  if (rc == GNNCG_ERR_RANGE) throw GraphError(msg);
+  throw std::runtime_error(msg);
+}
+
+inline void cuda_check(cudaError_t e, const char* what) {
+  if (e != cudaSuccess) throw std::runtime_error(std::string(what) + ": " + cudaGetErrorString(e));
+}
+
+// Owning device allocation.
+class DeviceBuffer {
+ public:
+  DeviceBuffer() = default;
+  explicit DeviceBuffer(size_t bytes) : bytes_(bytes) {
+    if (bytes) cuda_check(cudaMalloc(&ptr_, bytes), "cudaMalloc");
+  }
+  DeviceBuffer(DeviceBuffer&& o) noexcept : ptr_(o.ptr_), bytes_(o.bytes_) { o.ptr_ = nullptr; o.bytes_ = 0; }
+  DeviceBuffer& operator=(DeviceBuffer&& o) noexcept {
+    std::swap(ptr_, o.ptr_);
+    std::swap(bytes_, o.bytes_);
+    return *this;
+  }
+  DeviceBuffer(const DeviceBuffer&) = delete;
+  DeviceBuffer& operator=(const DeviceBuffer&) = delete;
+  ~DeviceBuffer() { if (ptr_) cudaFree(ptr_); }
+  template <typename T = void>
+  T* get() const { return static_cast<T*>(ptr_); }
+  size_t bytes() const { return bytes_; }
+  void ensure(size_t bytes) { if (bytes > bytes_) *this = DeviceBuffer(bytes); }
+
+ private:
+  void* ptr_ = nullptr;
+  size_t bytes_ = 0;
+};
+
+template <typename T>
+DeviceBuffer upload(const T* host, size_t n, cudaStream_t s) {
+  DeviceBuffer b(n * sizeof(T));
+  if (n) cuda_check(cudaMemcpyAsync(b.get(), host, n * sizeof(T), cudaMemcpyHostToDevice, s), "upload");
+  return b;
+}
+
+inline DeviceBuffer upload(const Tensor<float>& t, cudaStream_t s) { return upload(t.data.data(), t.size(), s); }
+
+inline Tensor<float> download(const DeviceBuffer& b, std::uint64_t rows, std::uint64_t cols, cudaStream_t s) {
+  Tensor<float> t(rows, cols);
+  if (t.size()) {
+    cuda_check(cudaMemcpyAsync(t.data.data(), b.get(), t.size() * sizeof(float), cudaMemcpyDeviceToHost, s),
+               "download");
+    cuda_check(cudaStreamSynchronize(s), "sync");
+  }
+  return t;
+}
+
+// One adjacency index in HBM plus its edge-balance schedule.
+struct DeviceIndex {
+  std::int64_t rows = 0, edges = 0;
+  DeviceBuffer off, nbr, eid;
+  DeviceBuffer items, split_rows, split_first;
+  gnncg_sched_t sched{};
+
+  gnncg_index_t view() const {
+    return gnncg_index_t{rows, edges, off.get<std::uint64_t>(), nbr.get<std::uint32_t>(), eid.get<std::uint32_t>()};
+  }
+};
+
+// gnncg::Graph resident in HBM: both indexes rebuilt on the device by the
+// bit-exact counting sort (gnncg_csr_build == build_index, graph.cpp:14-28).
+class DeviceGraph {
+ public:
+  explicit DeviceGraph(const Graph& g, std::int32_t chunk = 2048, cudaStream_t stream = nullptr)
+      : V_(static_cast<std::int64_t>(g.num_vertices())), E_(static_cast<std::int64_t>(g.num_edges())), s_(stream) {
+    check(gnncg_device_check(), "gnncg_device_check");
+    std::vector<std::uint32_t> src(E_), dst(E_);
+    for (std::int64_t e = 0; e < E_; ++e) {
+      src[e] = g.edge_src(static_cast<EdgeId>(e));
+      dst[e] = g.edge_dst(static_cast<EdgeId>(e));
+    }
+    edge_src_ = upload(src.data(), src.size(), s_);
+    edge_dst_ = upload(dst.data(), dst.size(), s_);
+    DeviceBuffer ws(gnncg_csr_build_workspace(V_, E_));
+    build(dst_, edge_dst_, edge_src_, ws, chunk);
+    build(src_, edge_src_, edge_dst_, ws, chunk);
+  }
+
+  std::int64_t num_vertices() const { return V_; }
+  std::int64_t num_edges() const { return E_; }
+  const DeviceIndex& csr_dst() const { return dst_; }
+  const DeviceIndex& csc_src() const { return src_; }
+  cudaStream_t stream() const { return s_; }
+  DeviceBuffer& workspace(size_t bytes) const {
+    ws_.ensure(bytes);
+    return ws_;
+  }
+
+ private:
+  void build(DeviceIndex& idx, const DeviceBuffer& key, const DeviceBuffer& other, DeviceBuffer& ws,
+             std::int32_t chunk) {
+    idx.rows = V_;
+    idx.edges = E_;
+    idx.off = DeviceBuffer((V_ + 1) * sizeof(std::uint64_t));
+    idx.nbr = DeviceBuffer(E_ * sizeof(std::uint32_t));
+    idx.eid = DeviceBuffer(E_ * sizeof(std::uint32_t));
+    check(gnncg_csr_build(V_, E_, key.get<std::uint32_t>(), other.get<std::uint32_t>(), idx.off.get<std::uint64_t>(),
+                          idx.nbr.get<std::uint32_t>(), idx.eid.get<std::uint32_t>(), ws.get(), ws.bytes(), s_),
+          "gnncg_csr_build");
+    std::vector<std::uint64_t> off(V_ + 1);
+    cuda_check(cudaMemcpyAsync(off.data(), idx.off.get(), off.size() * 8, cudaMemcpyDeviceToHost, s_), "offsets");
+    cuda_check(cudaStreamSynchronize(s_), "sync");
+    std::int64_t n = 0, ns = 0, nr = 0;
+    check(gnncg_sched_build_host(V_, off.data(), chunk, &n, &ns, &nr, nullptr, nullptr, nullptr), "sched");
+    std::vector<std::uint32_t> items(2 * n + 2), rows(nr + 1), first(nr + 1);
+    check(gnncg_sched_build_host(V_, off.data(), chunk, &n, &ns, &nr, items.data(), rows.data(), first.data()),
+          "sched");
+    idx.items = upload(items.data(), items.size(), s_);
+    idx.split_rows = upload(rows.data(), rows.size(), s_);
+    idx.split_first = upload(first.data(), first.size(), s_);
+    idx.sched = gnncg_sched_t{n, ns, nr, chunk, 0, idx.items.get<std::uint32_t>(), idx.split_rows.get<std::uint32_t>(),
+                              idx.split_first.get<std::uint32_t>()};
+  }
+
+  std::int64_t V_, E_;
+  cudaStream_t s_;
+  DeviceBuffer edge_src_, edge_dst_;
+  DeviceIndex dst_, src_;
+  mutable DeviceBuffer ws_;
+};
+
+struct GatParams {
+  int heads;
+  int f;
+  float slope = 0.2f;  // tensor.hpp:93
+};
+
+// O(|V|) forward state kept for the backward.
+struct GatStash {
+  DeviceBuffer Ht, Al, Ar, m, d;
+};
+
+struct GatGrads {
+  Tensor<float> dH, dW, da_l, da_r;
+};
+
+namespace detail {
+inline void require_shape(const Tensor<float>& t, std::uint64_t r, std::uint64_t c, const char* name) {
+  if (t.rows != r || t.cols != c)
+    throw TensorError(std::string(name) + ": shape mismatch (" + std::to_string(t.rows) + "x" +
+                      std::to_string(t.cols) + " vs " + std::to_string(r) + "x" + std::to_string(c) + ")");
+}
+
+inline void gemm(const DeviceGraph& g, int ta, int tb, std::int64_t M, std::int64_t N, std::int64_t K, const float* A,
+                 std::int64_t lda, const float* B, std::int64_t ldb, float* C, std::int64_t ldc) {
+  DeviceBuffer& ws = g.workspace(gnncg_gemm_workspace(ta, tb, M, N, K));
+  check(gnncg_gemm(ta, tb, M, N, K, A, lda, B, ldb, C, ldc, ws.get(), ws.bytes(), g.stream()), "gnncg_gemm");
+}
+}  // namespace detail
+
+// GAT layer forward, reorganized and fused.
+inline Tensor<float> gat_forward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
+                                 const Tensor<float>& a_l, const Tensor<float>& a_r, const GatParams& p,
+                                 GatStash* stash) {
+  const std::int64_t V = g.num_vertices(), h = p.heads, f = p.f, hf = h * f;
+  detail::require_shape(H, V, H.cols, "gat_forward H");
+  detail::require_shape(W, H.cols, hf, "gat_forward W");
+  detail::require_shape(a_l, h, f, "gat_forward a_l");
+  detail::require_shape(a_r, h, f, "gat_forward a_r");
+  cudaStream_t s = g.stream();
+  GatStash local;
+  GatStash& st = stash ? *stash : local;
+  DeviceBuffer dH = upload(H, s), dW = upload(W, s), dal = upload(a_l, s), dar = upload(a_r, s);
+  st.Ht = DeviceBuffer(V * hf * 4);
+  st.Al = DeviceBuffer(V * h * 4);
+  st.Ar = DeviceBuffer(V * h * 4);
+  st.m = DeviceBuffer(V * h * 4);
+  st.d = DeviceBuffer(V * h * 4);
+  detail::gemm(g, 0, 0, V, hf, H.cols, dH.get<float>(), H.cols, dW.get<float>(), hf, st.Ht.get<float>(), hf);
+  check(gnncg_gat_attn_dots(V, h, f, st.Ht.get<float>(), dal.get<float>(), dar.get<float>(), st.Al.get<float>(),
+                            st.Ar.get<float>(), s),
+        "gnncg_gat_attn_dots");
+  DeviceBuffer out(V * hf * 4);
+  const gnncg_index_t idx = g.csr_dst().view();
+  DeviceBuffer& ws = g.workspace(gnncg_gat_workspace(&g.csr_dst().sched, nullptr, h, f));
+  check(gnncg_gat_fwd(&idx, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
+                      st.Ar.get<float>(), out.get<float>(), st.m.get<float>(), st.d.get<float>(), ws.get(),
+                      ws.bytes(), s),
+        "gnncg_gat_fwd");
+  return download(out, V, hf, s);
+}
+
+// GAT layer backward with recomputation.
+inline GatGrads gat_backward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
+                             const Tensor<float>& a_l, const Tensor<float>& a_r, const GatStash& st,
+                             const Tensor<float>& dOut, const GatParams& p, bool need_dH) {
+  const std::int64_t V = g.num_vertices(), h = p.heads, f = p.f, hf = h * f, Fin = H.cols;
+  detail::require_shape(dOut, V, hf, "gat_backward dOut");
+  detail::require_shape(W, Fin, hf, "gat_backward W");
+  cudaStream_t s = g.stream();
+  DeviceBuffer dH_in = upload(H, s), dW_in = upload(W, s), dal_in = upload(a_l, s), dar_in = upload(a_r, s);
+  DeviceBuffer g_out = upload(dOut, s);
+  DeviceBuffer c(V * h * 4), dAr(V * h * 4), dAl(V * h * 4), dHt(V * hf * 4), da_l(hf * 4), da_r(hf * 4);
+  const gnncg_index_t csr = g.csr_dst().view(), csc = g.csc_src().view();
+  size_t need = gnncg_gat_workspace(&g.csr_dst().sched, &g.csc_src().sched, h, f);
+  need = std::max(need, gnncg_gat_attn_grad_workspace(V, h, f));
+  DeviceBuffer& ws = g.workspace(need);
+  check(gnncg_gat_bwd_dst(&csr, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
+                          st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), g_out.get<float>(), c.get<float>(),
+                          dAr.get<float>(), ws.get(), ws.bytes(), s),
+        "gnncg_gat_bwd_dst");
+  check(gnncg_gat_bwd_src(&csc, &g.csc_src().sched, h, f, p.slope, 0, V, st.Ht.get<float>(), st.Al.get<float>(),
+                          st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), c.get<float>(), g_out.get<float>(),
+                          dAr.get<float>(), dal_in.get<float>(), dar_in.get<float>(), dHt.get<float>(),
+                          dAl.get<float>(), ws.get(), ws.bytes(), s),
+        "gnncg_gat_bwd_src");
+  check(gnncg_gat_attn_grad(V, h, f, st.Ht.get<float>(), dAl.get<float>(), dAr.get<float>(), da_l.get<float>(),
+                            da_r.get<float>(), ws.get(), ws.bytes(), s),
+        "gnncg_gat_attn_grad");
+  GatGrads out;
+  DeviceBuffer dW(Fin * hf * 4);
+  detail::gemm(g, 1, 0, Fin, hf, V, dH_in.get<float>(), Fin, dHt.get<float>(), hf, dW.get<float>(), hf);
+  out.dW = download(dW, Fin, hf, s);
+  out.da_l = download(da_l, h, f, s);
+  out.da_r = download(da_r, h, f, s);
+  if (need_dH) {
+    DeviceBuffer dHb(V * Fin * 4);
+    detail::gemm(g, 0, 1, V, Fin, hf, dHt.get<float>(), hf, dW_in.get<float>(), hf, dHb.get<float>(), Fin);
+    out.dH = download(dHb, V, Fin, s);
+  }
+  return out;
+}
+
+// EdgeConv layer forward: returns out; argmax (edge ids) via *argmax.
+inline Tensor<float> edgeconv_forward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& Theta,
+                                      const Tensor<float>& Phi, std::vector<std::uint32_t>* argmax) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, C = Theta.cols;
+  detail::require_shape(Theta, Fin, C, "edgeconv Theta");
+  detail::require_shape(Phi, Fin, C, "edgeconv Phi");
+  cudaStream_t s = g.stream();
+  Tensor<float> Wc(Fin, 2 * C);
+  for (std::int64_t i = 0; i < Fin; ++i)
+    for (std::int64_t c = 0; c < C; ++c) {
+      Wc.at(i, c) = Theta.at(i, c);
+      Wc.at(i, C + c) = Phi.at(i, c);
+    }
+  DeviceBuffer dH = upload(H, s), dWc = upload(Wc, s), Y(V * 2 * C * 4), out(V * C * 4), am(V * C * 4);
+  detail::gemm(g, 0, 0, V, 2 * C, Fin, dH.get<float>(), Fin, dWc.get<float>(), 2 * C, Y.get<float>(), 2 * C);
+  const gnncg_index_t csr = g.csr_dst().view();
+  check(gnncg_edgeconv_fwd(&csr, (int)C, 0, Y.get<float>(), 2 * C, Y.get<float>() + C, 2 * C, out.get<float>(),
+                           am.get<std::uint32_t>(), s),
+        "gnncg_edgeconv_fwd");
+  if (argmax) {
+    argmax->resize(V * C);
+    cuda_check(cudaMemcpyAsync(argmax->data(), am.get(), V * C * 4, cudaMemcpyDeviceToHost, s), "argmax");
+  }
+  return download(out, V, C, s);
+}
+
+}  // namespace b200
+}  // namespace gnncg

@@ -37,9 +37,14 @@ struct WarpSmem {
   uint32_t nb[kWarp];
   float t0[kWarp * TS];
   float t1[kWarp * TS];
+  float t2[kWarp * TS];
   float red[8 * kWarp];
   float stat[4][MAXH];
 };
+
+// Split-row partial records are padded to 16 bytes (vector stores).
+__host__ __device__ __forceinline__ int64_t fwd_stride(int h, int f) { return (h * f + 2 * h + 3) / 4 * 4; }
+__host__ __device__ __forceinline__ int64_t src_stride(int h, int f) { return (h * f + h + 3) / 4 * 4; }
 
 struct Item {
   uint32_t row;
@@ -100,10 +105,64 @@ struct GatParams {
 };
 
 // ---------------------------------------------------------------------------
-// K2: forward.
+// Shared pieces of the three fused kernels.
+//
+// Per work item the warp walks its edges in 32-edge blocks.  Latency hiding:
+//   * neighbour ids are prefetched two blocks ahead and the per-edge logits one
+//     block ahead, so the dependent id -> logit loads overlap the previous
+//     block's gathers;
+//   * the column phase gathers U rows per step (U * NV * VW floats per lane in
+//     flight) before consuming any of them.
+// ---------------------------------------------------------------------------
+template <int NV>
+struct GatherDepth {
+  static constexpr int U = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);
+};
+
+template <int VW, int NV>
+struct Cols {
+  int col[NV], hd[NV];
+  bool ok[NV];
+  __device__ __forceinline__ Cols(int lane, int hf, int f) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      col[i] = (i * 32 + lane) * VW;
+      ok[i] = col[i] < hf;
+      hd[i] = ok[i] ? col[i] / f : 0;
+    }
+  }
+};
+
+template <int VW, int NV>
+__device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) v[i].x[q] = 0.f;
+}
+
+// Gather row `r` of a row-major [*, hf] matrix at this lane's columns.
+template <int VW, int NV>
+__device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
+                                           Vec<VW> (&x)[NV]) {
+  const float* row = base + r * hf;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
+    else
+#pragma unroll
+      for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K2: forward, single pass with a block-online softmax (RS1/RS2 folded into the
+// Aggregate): per 32-edge block the running max per head is updated once, the
+// accumulators rescaled by exp(m_old - m_new), and the block's unnormalised
+// weights exp(s - m_new) written to the per-warp table.
 // ---------------------------------------------------------------------------
 template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS) gat_fwd_kernel(GatParams p) {
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatParams p) {
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
@@ -112,119 +171,97 @@ __global__ void __launch_bounds__(THREADS) gat_fwd_kernel(GatParams p) {
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
+  constexpr int U = GatherDepth<NV>::U;
 
-  float arv[MAXH];
-  load_heads(p.Ar + (int64_t)it.row * h, h, arv);
-
-  // RS1/RS2 over the item's edges, lanes over edges (online max/sum, merged once).
-  float M[MAXH], S[MAXH];
+  if (lane < h) sm.stat[3][lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);  // A_r[v], read per edge from smem
+  float M[MAXH], Sl[MAXH];
 #pragma unroll
-  for (int k = 0; k < MAXH; ++k) { M[k] = -FLT_MAX; S[k] = 0.f; }
-  for (uint64_t e = it.e0 + lane; e < it.e1; e += 32) {
-    const uint32_t u = __ldg(p.nbr + e);
-    float al[MAXH];
-    load_heads(p.Al + (int64_t)u * h, h, al);
+  for (int k = 0; k < MAXH; ++k) { M[k] = -FLT_MAX; Sl[k] = 0.f; }
+  const Cols<VW, NV> cols(lane, hf, f);
+  Vec<VW> acc[NV];
+  zero(acc);
+
+  const uint64_t e0 = it.e0, e1 = it.e1;
+  uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+  uint32_t u_nxt = e0 + 32 + lane < e1 ? __ldg(p.nbr + e0 + 32 + lane) : 0u;
+  float al[MAXH];
+  load_heads(p.Al + (int64_t)u_cur * h, h, al);  // u_cur = 0 for idle lanes: a valid row, value unused
+  __syncwarp();
+
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min((uint64_t)32, e1 - base);
+    const bool valid = lane < n;
 #pragma unroll
     for (int k = 0; k < MAXH; ++k) {
       if (k < h) {
-        const float s = lrelu(al[k] + arv[k], slope);
-        if (s > M[k]) { S[k] = S[k] * __expf(M[k] - s) + 1.f; M[k] = s; }
-        else S[k] += __expf(s - M[k]);
+        const float s = valid ? lrelu(al[k] + sm.stat[3][k], slope) : -FLT_MAX;
+        const float mnew = fmaxf(M[k], warp_max(s));
+        const float sc = __expf(M[k] - mnew);
+        const float pk = valid ? __expf(s - mnew) : 0.f;
+        M[k] = mnew;
+        Sl[k] = fmaf(Sl[k], sc, pk);
+        sm.t0[lane * TS + k] = pk;
+        if (lane == 0) sm.stat[2][k] = sc;
       }
     }
-  }
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k) {
-    if (k < h) {
-      const float mk = warp_max(M[k]);
-      S[k] = warp_sum(S[k] * __expf(M[k] - mk));
-      M[k] = mk;
-    }
-  }
-
-  // Aggregate: column mapping over 32-edge blocks.
-  int colv[NV], hdv[NV];
-  bool okv[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    colv[i] = (i * 32 + lane) * VW;
-    okv[i] = colv[i] < hf;
-    hdv[i] = okv[i] ? colv[i] / f : 0;
-  }
-  Vec<VW> acc[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-#pragma unroll
-    for (int q = 0; q < VW; ++q) acc[i].x[q] = 0.f;
-
-  constexpr int U = NV >= 4 ? 2 : 4;
-  for (uint64_t base = it.e0; base < it.e1; base += 32) {
-    const int n = (int)min((uint64_t)32, it.e1 - base);
-    if (lane < n) {
-      const uint32_t u = __ldg(p.nbr + base + lane);
-      sm.nb[lane] = u;
-      float al[MAXH];
-      load_heads(p.Al + (int64_t)u * h, h, al);
-#pragma unroll
-      for (int k = 0; k < MAXH; ++k)
-        if (k < h) sm.t0[lane * TS + k] = __expf(lrelu(al[k] + arv[k], slope) - M[k]);
-    }
+    sm.nb[lane] = u_cur;
     __syncwarp();
+    // prefetch: logits of the next block, ids of the block after
+    u_cur = u_nxt;
+    if (base + 32 + lane < e1) load_heads(p.Al + (int64_t)u_cur * h, h, al);
+    u_nxt = base + 64 + lane < e1 ? __ldg(p.nbr + base + 64 + lane) : 0u;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float sc = sm.stat[2][cols.hd[i]];
+#pragma unroll
+      for (int q = 0; q < VW; ++q) acc[i].x[q] *= sc;
+    }
     int j = 0;
     for (; j + U <= n; j += U) {
       Vec<VW> x[U][NV];
-      float a[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const float* row = p.Ht + (int64_t)sm.nb[j + t] * hf;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          if (okv[i]) x[t][i] = ldg_vec<VW>(row + colv[i]);
-          else
-#pragma unroll
-            for (int q = 0; q < VW; ++q) x[t][i].x[q] = 0.f;
-          a[t][i] = sm.t0[(j + t) * TS + hdv[i]];
-        }
-      }
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[j + t], hf, cols, x[t]);
 #pragma unroll
       for (int t = 0; t < U; ++t)
 #pragma unroll
-        for (int i = 0; i < NV; ++i)
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[(j + t) * TS + cols.hd[i]];
 #pragma unroll
-          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a[t][i], x[t][i].x[q], acc[i].x[q]);
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
+        }
     }
     for (; j < n; ++j) {
-      const float* row = p.Ht + (int64_t)sm.nb[j] * hf;
+      Vec<VW> x[NV];
+      gather_row<VW, NV>(p.Ht, sm.nb[j], hf, cols, x);
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
-        if (okv[i]) {
-          const Vec<VW> x = ldg_vec<VW>(row + colv[i]);
-          const float a = sm.t0[j * TS + hdv[i]];
+        const float a = sm.t0[j * TS + cols.hd[i]];
 #pragma unroll
-          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x.x[q], acc[i].x[q]);
-        }
+        for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[i].x[q], acc[i].x[q]);
       }
     }
     __syncwarp();
   }
 
-  const bool empty = it.e0 == it.e1;
-  if (lane == 0) {
+  const bool empty = e0 == e1;
 #pragma unroll
-    for (int k = 0; k < MAXH; ++k)
-      if (k < h) { sm.stat[0][k] = empty ? 0.f : M[k]; sm.stat[1][k] = S[k]; }
+  for (int k = 0; k < MAXH; ++k) {
+    if (k < h) {
+      const float S = warp_sum(Sl[k]);
+      if (lane == 0) { sm.stat[0][k] = empty ? 0.f : M[k]; sm.stat[1][k] = S; }
+    }
   }
   __syncwarp();
   if (!it.split) {
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
-      if (okv[i]) {
-        const float den = sm.stat[1][hdv[i]];
+      if (cols.ok[i]) {
+        const float den = sm.stat[1][cols.hd[i]];
         const float inv = den > 0.f ? 1.f / den : 0.f;
         Vec<VW> o;
 #pragma unroll
         for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
-        st_vec<VW>(p.out + (int64_t)it.row * hf + colv[i], o);
+        st_vec<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
       }
     }
     if (lane < h) {
@@ -232,14 +269,270 @@ __global__ void __launch_bounds__(THREADS) gat_fwd_kernel(GatParams p) {
       p.dd[(int64_t)it.row * h + lane] = sm.stat[1][lane];
     }
   } else {
-    float* part = p.part + wi * (int64_t)(hf + 2 * h);
+    float* part = p.part + wi * fwd_stride(h, f);
 #pragma unroll
     for (int i = 0; i < NV; ++i)
-      if (okv[i]) st_vec<VW>(part + colv[i], acc[i]);
+      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
     if (lane < h) {
       part[hf + lane] = sm.stat[0][lane];
       part[hf + h + lane] = sm.stat[1][lane];
     }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K3: backward pass 1 over csr_dst.  Per destination v, alpha recomputed from the
+// stash (m, d):  c = <g, sum alpha x_u>,  P = <g, sum gate*alpha x_u>,
+// Q = sum gate*alpha,  dA_r = P - c Q  (g = dOut[v]; the softmax weights of a
+// row sum to one, so no large cancellation).
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_dst_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+  constexpr int U = GatherDepth<NV>::U;
+
+  if (lane < h) {
+    const int64_t r = (int64_t)it.row * h + lane;
+    const float dv = __ldg(p.d + r);
+    sm.stat[0][lane] = __ldg(p.Ar + r);
+    sm.stat[1][lane] = __ldg(p.m + r);
+    sm.stat[2][lane] = dv > 0.f ? 1.f / dv : 0.f;
+  }
+  float Q[MAXH];
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) Q[k] = 0.f;
+  const Cols<VW, NV> cols(lane, hf, f);
+  Vec<VW> g[NV], y[NV], z[NV];
+  gather_row<VW, NV>(p.dOut, it.row, hf, cols, g);
+  zero(y);
+  zero(z);
+
+  const uint64_t e0 = it.e0, e1 = it.e1;
+  uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+  uint32_t u_nxt = e0 + 32 + lane < e1 ? __ldg(p.nbr + e0 + 32 + lane) : 0u;
+  float al[MAXH];
+  load_heads(p.Al + (int64_t)u_cur * h, h, al);
+  __syncwarp();
+
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min((uint64_t)32, e1 - base);
+    if (lane < n) {
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        if (k < h) {
+          const float zz = al[k] + sm.stat[0][k];
+          const float a = __expf(lrelu(zz, slope) - sm.stat[1][k]) * sm.stat[2][k];
+          const float ga = lrelu_grad(zz, slope) * a;
+          sm.t0[lane * TS + k] = a;
+          sm.t1[lane * TS + k] = ga;
+          Q[k] += ga;
+        }
+      }
+    }
+    sm.nb[lane] = u_cur;
+    __syncwarp();
+    u_cur = u_nxt;
+    if (base + 32 + lane < e1) load_heads(p.Al + (int64_t)u_cur * h, h, al);
+    u_nxt = base + 64 + lane < e1 ? __ldg(p.nbr + base + 64 + lane) : 0u;
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> x[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[j + t], hf, cols, x[t]);
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[(j + t) * TS + cols.hd[i]], ga = sm.t1[(j + t) * TS + cols.hd[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            y[i].x[q] = fmaf(a, x[t][i].x[q], y[i].x[q]);
+            z[i].x[q] = fmaf(ga, x[t][i].x[q], z[i].x[q]);
+          }
+        }
+    }
+    for (; j < n; ++j) {
+      Vec<VW> x[NV];
+      gather_row<VW, NV>(p.Ht, sm.nb[j], hf, cols, x);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float a = sm.t0[j * TS + cols.hd[i]], ga = sm.t1[j * TS + cols.hd[i]];
+#pragma unroll
+        for (int q = 0; q < VW; ++q) {
+          y[i].x[q] = fmaf(a, x[i].x[q], y[i].x[q]);
+          z[i].x[q] = fmaf(ga, x[i].x[q], z[i].x[q]);
+        }
+      }
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k)
+    if (k < h) Q[k] = warp_sum(Q[k]);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    float cp = 0.f, pp = 0.f;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) { cp = fmaf(g[i].x[q], y[i].x[q], cp); pp = fmaf(g[i].x[q], z[i].x[q], pp); }
+    sm.t0[i * 32 + lane] = cp;  // tables are free now; reuse as reduction scratch
+    sm.t1[i * 32 + lane] = pp;
+  }
+  __syncwarp();
+  if (lane < h) {
+    const float ck = head_sum<VW>(sm.t0, lane, f), pk = head_sum<VW>(sm.t1, lane, f);
+    float qk = 0.f;
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k)
+      if (k == lane) qk = Q[k];
+    if (!it.split) {
+      p.co[(int64_t)it.row * h + lane] = ck;
+      p.dAro[(int64_t)it.row * h + lane] = pk - ck * qk;
+    } else {
+      float* part = p.part + wi * (int64_t)(3 * h);
+      part[lane] = ck;
+      part[h + lane] = pk;
+      part[2 * h + lane] = qk;
+    }
+  }
+}
+
+// ---------------------------------------------------------------------------
+// K4: backward pass 2 over csc_src.  Per source u (global), over out-edges to
+// local destinations v, alpha and the gate recomputed:
+//   dHt[u]  = sum alpha dOut[v]                      (Aggregate backward)
+//   dA_l[u] = sum gate*alpha (dalpha - c[v]),  dalpha = <dOut[v], x_u>
+// evaluated per 32-edge block as <x_u, sum_b gate*alpha dOut[v]> - sum_b gate*alpha c[v]
+// (out-edge sums are NOT normalised, so the difference is taken block by block to
+// avoid cancellation on hub sources), then the LP epilogue
+// dHt[u] += dA_l[u] (x) a_l + dA_r[u] (x) a_r.
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+  const int64_t u = it.row;
+  constexpr int U = GatherDepth<NV>::U;
+
+  if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
+  float dal_acc = 0.f;  // lane k < h: dA_l[u, k]
+  const Cols<VW, NV> cols(lane, hf, f);
+  Vec<VW> x[NV], acc[NV], wv[NV];
+  gather_row<VW, NV>(p.Ht, u, hf, cols, x);
+  zero(acc);
+  zero(wv);
+
+  const uint64_t e0 = it.e0, e1 = it.e1;
+  uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+  __syncwarp();
+
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min((uint64_t)32, e1 - base);
+    if (lane < n) {
+      float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
+      load_heads(p.Ar + (int64_t)v_cur * h, h, arv);
+      load_heads(p.m + (int64_t)v_cur * h, h, mv);
+      load_heads(p.d + (int64_t)v_cur * h, h, dv);
+      load_heads(p.c + (int64_t)v_cur * h, h, cv);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        if (k < h) {
+          const float zz = sm.stat[3][k] + arv[k];
+          const float a = dv[k] > 0.f ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
+          const float ga = lrelu_grad(zz, slope) * a;
+          sm.t0[lane * TS + k] = a;
+          sm.t1[lane * TS + k] = ga;
+          sm.t2[lane * TS + k] = ga * cv[k];
+        }
+      }
+    }
+    sm.nb[lane] = v_cur;
+    __syncwarp();
+    v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> gv[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[j + t], hf, cols, gv[t]);
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[(j + t) * TS + cols.hd[i]], ga = sm.t1[(j + t) * TS + cols.hd[i]];
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            acc[i].x[q] = fmaf(a, gv[t][i].x[q], acc[i].x[q]);
+            wv[i].x[q] = fmaf(ga, gv[t][i].x[q], wv[i].x[q]);
+          }
+        }
+    }
+    for (; j < n; ++j) {
+      Vec<VW> gv[NV];
+      gather_row<VW, NV>(p.dOut, sm.nb[j], hf, cols, gv);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float a = sm.t0[j * TS + cols.hd[i]], ga = sm.t1[j * TS + cols.hd[i]];
+#pragma unroll
+        for (int q = 0; q < VW; ++q) {
+          acc[i].x[q] = fmaf(a, gv[i].x[q], acc[i].x[q]);
+          wv[i].x[q] = fmaf(ga, gv[i].x[q], wv[i].x[q]);
+        }
+      }
+    }
+    // block-level dA_l contribution
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      float s = 0.f;
+#pragma unroll
+      for (int q = 0; q < VW; ++q) { s = fmaf(x[i].x[q], wv[i].x[q], s); wv[i].x[q] = 0.f; }
+      sm.red[i * 32 + lane] = s;
+    }
+    __syncwarp();
+    if (lane < h) {
+      float r = head_sum<VW>(sm.red, lane, f);
+      for (int jj = 0; jj < n; ++jj) r -= sm.t2[jj * TS + lane];
+      dal_acc += r;
+    }
+    __syncwarp();
+  }
+  if (lane < h) {
+    sm.stat[0][lane] = dal_acc;
+    const bool local = u >= p.row_base && u < p.row_base + p.num_local;
+    sm.stat[1][lane] = local ? __ldg(p.dAr + (u - p.row_base) * h + lane) : 0.f;
+  }
+  __syncwarp();
+  if (!it.split) {
+    if (lane < h) p.dAl[u * h + lane] = sm.stat[0][lane];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (cols.ok[i]) {
+        const float dal = sm.stat[0][cols.hd[i]], dar = sm.stat[1][cols.hd[i]];
+        const Vec<VW> al = ldg_vec<VW>(p.a_l + cols.col[i]);
+        const Vec<VW> ar = ldg_vec<VW>(p.a_r + cols.col[i]);
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] + dal * al.x[q] + dar * ar.x[q];
+        st_vec<VW>(p.dHt + u * hf + cols.col[i], o);
+      }
+    }
+  } else {
+    float* part = p.part + wi * src_stride(h, f);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
+    if (lane < h) part[hf + lane] = sm.stat[0][lane];
   }
 }
 
@@ -251,7 +544,7 @@ __global__ void gat_fwd_merge_kernel(GatParams p, const uint32_t* __restrict__ s
   const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
   if (sr >= num_split_rows) return;
   const int h = p.h, f = p.f, hf = h * f;
-  const int64_t stride = hf + 2 * h;
+  const int64_t stride = fwd_stride(h, f);
   const uint32_t row = split_rows[sr];
   const int64_t i0 = split_first[sr], i1 = split_first[sr + 1];
   if (lane < h) {
@@ -275,144 +568,6 @@ __global__ void gat_fwd_merge_kernel(GatParams p, const uint32_t* __restrict__ s
   }
 }
 
-// ---------------------------------------------------------------------------
-// K3: backward pass 1 over csr_dst.  Per destination v, with alpha recomputed:
-//   c = sum alpha <g, x_u> = <g, sum alpha x_u>,   P = <g, sum LReLU'(z) alpha x_u>,
-//   Q = sum LReLU'(z) alpha,   dA_r = P - c Q
-// (the column phase only accumulates sum alpha x_u and sum gate*alpha x_u; the
-// dot with g = dOut[v] happens once per row, not per edge).
-// ---------------------------------------------------------------------------
-template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS) gat_bwd_dst_kernel(GatParams p) {
-  __shared__ WarpSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WarpSmem& sm = smem[w];
-  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
-  if (wi >= p.num_items) return;
-  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
-  const int h = p.h, f = p.f, hf = h * f;
-  const float slope = p.slope;
-
-  float arv[MAXH], mv[MAXH], invd[MAXH], Q[MAXH];
-  load_heads(p.Ar + (int64_t)it.row * h, h, arv);
-  load_heads(p.m + (int64_t)it.row * h, h, mv);
-  load_heads(p.d + (int64_t)it.row * h, h, invd);
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k) { invd[k] = invd[k] > 0.f ? 1.f / invd[k] : 0.f; Q[k] = 0.f; }
-
-  int colv[NV], hdv[NV];
-  bool okv[NV];
-  Vec<VW> g[NV], y[NV], z[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    colv[i] = (i * 32 + lane) * VW;
-    okv[i] = colv[i] < hf;
-    hdv[i] = okv[i] ? colv[i] / f : 0;
-    if (okv[i]) g[i] = ldg_vec<VW>(p.dOut + (int64_t)it.row * hf + colv[i]);
-#pragma unroll
-    for (int q = 0; q < VW; ++q) {
-      if (!okv[i]) g[i].x[q] = 0.f;
-      y[i].x[q] = 0.f;
-      z[i].x[q] = 0.f;
-    }
-  }
-
-  constexpr int U = NV >= 4 ? 2 : 4;
-  for (uint64_t base = it.e0; base < it.e1; base += 32) {
-    const int n = (int)min((uint64_t)32, it.e1 - base);
-    if (lane < n) {
-      const uint32_t u = __ldg(p.nbr + base + lane);
-      sm.nb[lane] = u;
-      float al[MAXH];
-      load_heads(p.Al + (int64_t)u * h, h, al);
-#pragma unroll
-      for (int k = 0; k < MAXH; ++k) {
-        if (k < h) {
-          const float zz = al[k] + arv[k];
-          const float a = __expf(lrelu(zz, slope) - mv[k]) * invd[k];
-          const float ga = lrelu_grad(zz, slope) * a;
-          sm.t0[lane * TS + k] = a;
-          sm.t1[lane * TS + k] = ga;
-          Q[k] += ga;
-        }
-      }
-    }
-    __syncwarp();
-    int j = 0;
-    for (; j + U <= n; j += U) {
-      Vec<VW> x[U][NV];
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const float* row = p.Ht + (int64_t)sm.nb[j + t] * hf;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          if (okv[i]) x[t][i] = ldg_vec<VW>(row + colv[i]);
-          else
-#pragma unroll
-            for (int q = 0; q < VW; ++q) x[t][i].x[q] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < U; ++t)
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const float a = sm.t0[(j + t) * TS + hdv[i]], ga = sm.t1[(j + t) * TS + hdv[i]];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) {
-            y[i].x[q] = fmaf(a, x[t][i].x[q], y[i].x[q]);
-            z[i].x[q] = fmaf(ga, x[t][i].x[q], z[i].x[q]);
-          }
-        }
-    }
-    for (; j < n; ++j) {
-      const float* row = p.Ht + (int64_t)sm.nb[j] * hf;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        if (okv[i]) {
-          const Vec<VW> x = ldg_vec<VW>(row + colv[i]);
-          const float a = sm.t0[j * TS + hdv[i]], ga = sm.t1[j * TS + hdv[i]];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) {
-            y[i].x[q] = fmaf(a, x.x[q], y[i].x[q]);
-            z[i].x[q] = fmaf(ga, x.x[q], z[i].x[q]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k)
-    if (k < h) Q[k] = warp_sum(Q[k]);
-
-  // c and P per head: per-lane partial dots -> shared -> head sums.
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    float cp = 0.f, pp = 0.f;
-#pragma unroll
-    for (int q = 0; q < VW; ++q) { cp = fmaf(g[i].x[q], y[i].x[q], cp); pp = fmaf(g[i].x[q], z[i].x[q], pp); }
-    sm.t0[i * 32 + lane] = cp;   // tables are free now; reuse as reduction scratch
-    sm.t1[i * 32 + lane] = pp;
-  }
-  __syncwarp();
-  if (lane < h) {
-    const float ck = head_sum<VW>(sm.t0, lane, f), pk = head_sum<VW>(sm.t1, lane, f);
-    float qk = 0.f;
-#pragma unroll
-    for (int k = 0; k < MAXH; ++k)
-      if (k == lane) qk = Q[k];
-    if (!it.split) {
-      p.co[(int64_t)it.row * h + lane] = ck;
-      p.dAro[(int64_t)it.row * h + lane] = pk - ck * qk;
-    } else {
-      float* part = p.part + wi * (int64_t)(3 * h);
-      part[lane] = ck;
-      part[h + lane] = pk;
-      part[2 * h + lane] = qk;
-    }
-  }
-}
-
 __global__ void gat_bwd_dst_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
                                          const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
   const int64_t sr = (int64_t)blockIdx.x * blockDim.x + threadIdx.x;
@@ -431,159 +586,6 @@ __global__ void gat_bwd_dst_merge_kernel(GatParams p, const uint32_t* __restrict
   p.dAro[(int64_t)row * h + k] = P - c * Q;
 }
 
-// ---------------------------------------------------------------------------
-// K4: backward pass 2 over csc_src.  Per source u (global), over out-edges to
-// local destinations v, alpha and the gate recomputed:
-//   dHt[u] = sum alpha dOut[v]                      (Aggregate backward)
-//   dA_l[u] = <x_u, sum gate*alpha dOut[v]> - sum gate*alpha c[v]
-// then the LP epilogue dHt[u] += dA_l[u] (x) a_l + dA_r[u] (x) a_r.
-// ---------------------------------------------------------------------------
-template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS) gat_bwd_src_kernel(GatParams p) {
-  __shared__ WarpSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WarpSmem& sm = smem[w];
-  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
-  if (wi >= p.num_items) return;
-  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
-  const int h = p.h, f = p.f, hf = h * f;
-  const float slope = p.slope;
-  const int64_t u = it.row;
-
-  float alv[MAXH], T[MAXH];
-  load_heads(p.Al + u * h, h, alv);
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k) T[k] = 0.f;
-
-  int colv[NV], hdv[NV];
-  bool okv[NV];
-  Vec<VW> x[NV], acc[NV], wv[NV];
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    colv[i] = (i * 32 + lane) * VW;
-    okv[i] = colv[i] < hf;
-    hdv[i] = okv[i] ? colv[i] / f : 0;
-    if (okv[i]) x[i] = ldg_vec<VW>(p.Ht + u * hf + colv[i]);
-#pragma unroll
-    for (int q = 0; q < VW; ++q) {
-      if (!okv[i]) x[i].x[q] = 0.f;
-      acc[i].x[q] = 0.f;
-      wv[i].x[q] = 0.f;
-    }
-  }
-
-  constexpr int U = NV >= 4 ? 2 : 4;
-  for (uint64_t base = it.e0; base < it.e1; base += 32) {
-    const int n = (int)min((uint64_t)32, it.e1 - base);
-    if (lane < n) {
-      const uint32_t v = __ldg(p.nbr + base + lane);
-      sm.nb[lane] = v;
-      float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
-      load_heads(p.Ar + (int64_t)v * h, h, arv);
-      load_heads(p.m + (int64_t)v * h, h, mv);
-      load_heads(p.d + (int64_t)v * h, h, dv);
-      load_heads(p.c + (int64_t)v * h, h, cv);
-#pragma unroll
-      for (int k = 0; k < MAXH; ++k) {
-        if (k < h) {
-          const float zz = alv[k] + arv[k];
-          const float a = dv[k] > 0.f ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
-          const float ga = lrelu_grad(zz, slope) * a;
-          sm.t0[lane * TS + k] = a;
-          sm.t1[lane * TS + k] = ga;
-          T[k] = fmaf(ga, cv[k], T[k]);
-        }
-      }
-    }
-    __syncwarp();
-    int j = 0;
-    for (; j + U <= n; j += U) {
-      Vec<VW> gv[U][NV];
-#pragma unroll
-      for (int t = 0; t < U; ++t) {
-        const float* row = p.dOut + (int64_t)sm.nb[j + t] * hf;
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          if (okv[i]) gv[t][i] = ldg_vec<VW>(row + colv[i]);
-          else
-#pragma unroll
-            for (int q = 0; q < VW; ++q) gv[t][i].x[q] = 0.f;
-        }
-      }
-#pragma unroll
-      for (int t = 0; t < U; ++t)
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const float a = sm.t0[(j + t) * TS + hdv[i]], ga = sm.t1[(j + t) * TS + hdv[i]];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) {
-            acc[i].x[q] = fmaf(a, gv[t][i].x[q], acc[i].x[q]);
-            wv[i].x[q] = fmaf(ga, gv[t][i].x[q], wv[i].x[q]);
-          }
-        }
-    }
-    for (; j < n; ++j) {
-      const float* row = p.dOut + (int64_t)sm.nb[j] * hf;
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        if (okv[i]) {
-          const Vec<VW> gv = ldg_vec<VW>(row + colv[i]);
-          const float a = sm.t0[j * TS + hdv[i]], ga = sm.t1[j * TS + hdv[i]];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) {
-            acc[i].x[q] = fmaf(a, gv.x[q], acc[i].x[q]);
-            wv[i].x[q] = fmaf(ga, gv.x[q], wv[i].x[q]);
-          }
-        }
-      }
-    }
-    __syncwarp();
-  }
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k)
-    if (k < h) T[k] = warp_sum(T[k]);
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    float s = 0.f;
-#pragma unroll
-    for (int q = 0; q < VW; ++q) s = fmaf(x[i].x[q], wv[i].x[q], s);
-    sm.t0[i * 32 + lane] = s;
-  }
-  __syncwarp();
-  if (lane < h) {
-    float tk = 0.f;
-#pragma unroll
-    for (int k = 0; k < MAXH; ++k)
-      if (k == lane) tk = T[k];
-    const float dal = head_sum<VW>(sm.t0, lane, f) - tk;
-    sm.stat[0][lane] = dal;
-    const bool local = u >= p.row_base && u < p.row_base + p.num_local;
-    sm.stat[1][lane] = local ? p.dAr[(u - p.row_base) * h + lane] : 0.f;
-  }
-  __syncwarp();
-  if (!it.split) {
-    if (lane < h) p.dAl[u * h + lane] = sm.stat[0][lane];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      if (okv[i]) {
-        const float dal = sm.stat[0][hdv[i]], dar = sm.stat[1][hdv[i]];
-        const Vec<VW> al = ldg_vec<VW>(p.a_l + colv[i]);
-        const Vec<VW> ar = ldg_vec<VW>(p.a_r + colv[i]);
-        Vec<VW> o;
-#pragma unroll
-        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] + dal * al.x[q] + dar * ar.x[q];
-        st_vec<VW>(p.dHt + u * hf + colv[i], o);
-      }
-    }
-  } else {
-    float* part = p.part + wi * (int64_t)(hf + h);
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-      if (okv[i]) st_vec<VW>(part + colv[i], acc[i]);
-    if (lane < h) part[hf + lane] = sm.stat[0][lane];
-  }
-}
-
 __global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
                                          const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
   __shared__ float st[WARPS][2][MAXH];
@@ -591,7 +593,7 @@ __global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict
   const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
   if (sr >= num_split_rows) return;
   const int h = p.h, f = p.f, hf = h * f;
-  const int64_t stride = hf + h;
+  const int64_t stride = src_stride(h, f);
   const int64_t u = split_rows[sr];
   const int64_t i0 = split_first[sr], i1 = split_first[sr + 1];
   if (lane < h) {
@@ -712,13 +714,13 @@ int check_common(const gnncg_index_t* idx, const gnncg_sched_t* sched, int h, in
 }
 
 size_t fwd_part_bytes(const gnncg_sched_t* s, int h, int f) {
-  return s ? (size_t)s->num_split_items * (size_t)(h * f + 2 * h) * sizeof(float) : 0;
+  return s ? (size_t)s->num_split_items * (size_t)fwd_stride(h, f) * sizeof(float) : 0;
 }
 size_t dst_part_bytes(const gnncg_sched_t* s, int h) {
   return s ? (size_t)s->num_split_items * (size_t)(3 * h) * sizeof(float) : 0;
 }
 size_t src_part_bytes(const gnncg_sched_t* s, int h, int f) {
-  return s ? (size_t)s->num_split_items * (size_t)(h * f + h) * sizeof(float) : 0;
+  return s ? (size_t)s->num_split_items * (size_t)src_stride(h, f) * sizeof(float) : 0;
 }
 
 }  // namespace

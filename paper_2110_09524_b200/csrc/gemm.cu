@@ -173,9 +173,15 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
   GNNCG_DEVICE_GUARD();
   GNNCG_REQUIRE(M >= 0 && N >= 0 && K >= 0, GNNCG_ERR_SHAPE, "gemm: negative dimension");
   GNNCG_REQUIRE(!(trans_a && trans_b), GNNCG_ERR_UNSUPPORTED, "gemm: A^T B^T not supported");
-  GNNCG_REQUIRE(lda >= (trans_a ? M : K) && ldb >= (trans_b ? K : N) && ldc >= N, GNNCG_ERR_SHAPE,
-                "gemm: leading dimension too small");
+  GNNCG_REQUIRE(ldc >= N, GNNCG_ERR_SHAPE, "gemm: ldc < N");
   if (M == 0 || N == 0) return GNNCG_OK;
+  if (K == 0) {  // empty contraction: C = 0
+    GNNCG_REQUIRE(C, GNNCG_ERR_ARG, "gemm: null C");
+    GNNCG_CUDA_TRY(cudaMemset2DAsync(C, ldc * sizeof(float), 0, N * sizeof(float), M, as_stream(stream)));
+    return GNNCG_OK;
+  }
+  GNNCG_REQUIRE(lda >= (trans_a ? M : K) && ldb >= (trans_b ? K : N), GNNCG_ERR_SHAPE,
+                "gemm: leading dimension too small");
   GNNCG_REQUIRE(A && B && C, GNNCG_ERR_ARG, "gemm: null pointer");
   cudaStream_t s = as_stream(stream);
   const int splits = choose_splits(M, N, K);

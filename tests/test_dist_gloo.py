@@ -1,0 +1,147 @@
+"""CPU, world_size 2 and 3 over gloo: the multi-GPU orchestration of dist.py (row
+partition, padded all-gather of Ht, K4 partials reduce-scattered, dW / da all-reduced,
+SGD in lock-step) reproduces the single-process f64 oracle.
+
+The product engine (CudaEngine) cannot run here; the same PartitionedGAT schedule is
+driven by an oracle-backed engine (test infrastructure) whose region backward is an
+independent per-edge numpy restatement of K3/K4 on the rank-local indexes."""
+import os
+import socket
+
+import numpy as np
+import pytest
+import torch
+import torch.distributed as dist
+import torch.multiprocessing as mp
+
+from oracle import oracle as O
+
+
+class OracleEngine:
+    device = torch.device("cpu")
+
+    def build_index(self, rows, key, other):
+        off, nbr, eid = O.build_index(rows, key.numpy().astype(np.uint32), other.numpy().astype(np.uint32))
+        return dict(off=off, nbr=nbr, eid=eid, rows=rows)
+
+    def zeros(self, *s):
+        return torch.zeros(*s, dtype=torch.float64)
+
+    def empty(self, *s):
+        return torch.zeros(*s, dtype=torch.float64)
+
+    def gemm(self, A, B, ta=False, tb=False):
+        return (A.T if ta else A) @ (B.T if tb else B)
+
+    def attn_dots(self, Ht, a_l, a_r, p):
+        H3 = Ht.view(Ht.shape[0], p.heads, p.f)
+        return (H3 * a_l).sum(-1), (H3 * a_r).sum(-1)
+
+    def region_fwd(self, lg, Ht, Al, Ar_local, p):
+        c = lg.csr
+        g = O.HostGraph(c["rows"], None, None, c["off"], c["nbr"], c["eid"], None, None, None)
+        r = O.gat_region_fwd_f64(g, Ht.numpy(), Al.numpy(), Ar_local.numpy(), p.heads, p.f, p.slope)
+        return torch.from_numpy(r["out"]), torch.from_numpy(r["m"]), torch.from_numpy(r["d"])
+
+    def region_bwd(self, lg, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p):
+        h, f, n, base = p.heads, p.f, lg.num_local, lg.row_base
+        c = lg.csr
+        v = np.repeat(np.arange(n), np.diff(c["off"].astype(np.int64)))
+        u = c["nbr"].astype(np.int64)
+        Ht3, dO3 = Ht.numpy().reshape(-1, h, f), dOut.numpy().reshape(n, h, f)
+        Ar = Ar_full.numpy()[base:base + n]
+        z = Al.numpy()[u] + Ar[v]
+        s = np.where(z > 0, z, p.slope * z)
+        a = np.exp(s - m.numpy()[v]) / d.numpy()[v]
+        da = (dO3[v] * Ht3[u]).sum(-1)
+        cc = np.zeros((n, h))
+        np.add.at(cc, v, a * da)
+        dz = np.where(z > 0, 1.0, p.slope) * a * (da - cc[v])
+        Vp = lg.plan.padded_V
+        dAl, dAr, dHt = np.zeros((Vp, h)), np.zeros((n, h)), np.zeros((Vp, h, f))
+        np.add.at(dAl, u, dz)
+        np.add.at(dAr, v, dz)
+        np.add.at(dHt, u, a[:, :, None] * dO3[v])
+        dHt += dAl[:, :, None] * a_l.numpy()[None]
+        dHt[base:base + n] += dAr[:, :, None] * a_r.numpy()[None]
+        return torch.from_numpy(dHt.reshape(Vp, h * f)), torch.from_numpy(dAl), torch.from_numpy(dAr)
+
+    def attn_grad(self, Ht, dAl, dAr, p):
+        H3 = Ht.view(-1, p.heads, p.f)
+        return (dAl[:, :, None] * H3).sum(0), (dAr[:, :, None] * H3).sum(0)
+
+    def sgd(self, param, grad, lr):
+        param -= lr * grad
+
+    def fill_ones(self, like):
+        return torch.ones_like(like)
+
+    def total(self, x, out):
+        out[0] = x.sum()
+
+
+def _free_port():
+    with socket.socket() as s:
+        s.bind(("127.0.0.1", 0))
+        return s.getsockname()[1]
+
+
+def _worker(rank, world, port, case, q):
+    os.environ.update(MASTER_ADDR="127.0.0.1", MASTER_PORT=str(port))
+    dist.init_process_group("gloo", rank=rank, world_size=world)
+    try:
+        from paper_2110_09524_b200.dist import PartitionedGAT, PartitionPlan, build_local
+
+        V, src, dst, H, params, dims = case
+        eng = OracleEngine()
+        plan = PartitionPlan.from_dst(V, torch.from_numpy(dst.astype(np.int64)), world)
+        lg = build_local(plan, rank, torch.from_numpy(src.astype(np.int64)), torch.from_numpy(dst.astype(np.int64)),
+                         eng)
+        r0, r1 = int(plan.bounds[rank]), int(plan.bounds[rank + 1])
+        tparams = [tuple(torch.from_numpy(x.copy()) for x in p) for p in params]
+        model = PartitionedGAT(lg, dims, engine=eng, params=tparams)
+        xs, stashes = model.forward(torch.from_numpy(H[r0:r1].copy()))
+        loss = xs[-1].sum().clone()
+        dist.all_reduce(loss)
+        grads = model.backward(xs, stashes, torch.ones_like(xs[-1]))
+        q.put((rank, r0, r1, xs[-1].numpy(), float(loss), [tuple(g[j].numpy() for j in range(3)) for g in grads]))
+    finally:
+        dist.destroy_process_group()
+
+
+@pytest.mark.parametrize("world", [2, 3])
+def test_partitioned_gat_matches_single_process_oracle(world):
+    rng = np.random.default_rng(world)
+    V, E = 120, 1500
+    w = 1.0 / (np.arange(V) + 5.0)
+    w /= w.sum()
+    src, dst = rng.choice(V, E, p=w), rng.choice(V, E, p=w)
+    dims = [(12, 2, 4), (8, 2, 4)]
+    H = rng.uniform(-1, 1, (V, 12))
+    params = [(rng.uniform(-0.5, 0.5, (fin, h * f)), rng.uniform(-0.5, 0.5, (h, f)), rng.uniform(-0.5, 0.5, (h, f)))
+              for fin, h, f in dims]
+    ctx = mp.get_context("spawn")
+    q = ctx.Queue()
+    port = _free_port()
+    procs = [ctx.Process(target=_worker, args=(r, world, port, (V, src, dst, H, params, dims), q)) for r in range(world)]
+    for p in procs:
+        p.start()
+    res = sorted(q.get(timeout=300) for _ in range(world))
+    for p in procs:
+        p.join(timeout=60)
+        assert p.exitcode == 0
+    hg = O.host_graph(V, src, dst)
+    f1 = O.gat_layer_fwd_f64(hg, H, *params[0], 2, 4)
+    f2 = O.gat_layer_fwd_f64(hg, f1["out"], *params[1], 2, 4)
+    b2 = O.gat_layer_bwd_f64(hg, f1["out"], *params[1], 2, 4, f2, np.ones((V, 8)))
+    b1 = O.gat_layer_bwd_f64(hg, H, *params[0], 2, 4, f1, b2["dH"], need_dH=False)
+    out = np.zeros((V, 8))
+    for rank, r0, r1, o, loss, grads in res:
+        out[r0:r1] = o
+        assert abs(loss - f2["out"].sum()) < 1e-9
+        for (dW, dal, dar), b in zip(grads, (b1, b2)):
+            np.testing.assert_allclose(dW, b["dW"], atol=1e-10)
+            np.testing.assert_allclose(dal, b["dal"], atol=1e-10)
+            np.testing.assert_allclose(dar, b["dar"], atol=1e-10)
+    np.testing.assert_allclose(out, f2["out"], atol=1e-12)
+    assert sorted((r0, r1) for _, r0, r1, *_ in res)[-1][1] == V
