@@ -102,6 +102,7 @@ struct GatParams {
   float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
   float* part;  // split-row partials
   int64_t row_base, num_local;
+  int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
 };
 
 // ---------------------------------------------------------------------------
@@ -536,6 +537,152 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_kernel(G
   }
 }
 
+// ---------------------------------------------------------------------------
+// K4 "fast" (SPEC.md:378 fast mode): backward pass 2 with pass 1 folded in.
+// With c[v] = <dOut[v], out[v]> per head (= sum_e alpha_e dalpha_e, the softmax
+// backward identity; gat_rowdot_kernel), a single pass over csc_src computes per
+// edge dalpha_e = <dOut[v], x_u> (a per-edge head reduction across the lanes of
+// the head) and dz_e = gate*alpha (dalpha_e - c[v]); dA_l[u] sums dz_e in the warp,
+// dA_r[v] receives dz_e by a global red (order-nondeterministic, tolerance-tested).
+// Removes the whole csr_dst gather pass of K3.  Requires f/VW to be a power of
+// two <= 32 (each head's columns inside one lane group).
+// ---------------------------------------------------------------------------
+template <int VW, int NV>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_kernel(GatParams p) {
+  __shared__ WarpSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  WarpSmem& sm = smem[w];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+  const int64_t u = it.row;
+  const int per = f / VW;  // lanes per head
+  const bool leader = (lane & (per - 1)) == 0;
+  constexpr int U = GatherDepth<NV>::U;
+
+  if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
+  const Cols<VW, NV> cols(lane, hf, f);
+  Vec<VW> x[NV], acc[NV];
+  float dal[NV];
+  gather_row<VW, NV>(p.Ht, u, hf, cols, x);
+  zero(acc);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) dal[i] = 0.f;
+
+  const uint64_t e0 = it.e0, e1 = it.e1;
+  uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+  __syncwarp();
+
+  auto edge = [&](int j, const Vec<VW>(&gv)[NV]) {
+    const int64_t v = sm.nb[j];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float a = sm.t0[j * TS + cols.hd[i]];
+      float pd = 0.f;
+#pragma unroll
+      for (int q = 0; q < VW; ++q) {
+        acc[i].x[q] = fmaf(a, gv[i].x[q], acc[i].x[q]);
+        pd = fmaf(x[i].x[q], gv[i].x[q], pd);
+      }
+      for (int o = 1; o < per; o <<= 1) pd += __shfl_xor_sync(0xffffffffu, pd, o);
+      if (cols.ok[i]) {
+        const float dz = sm.t1[j * TS + cols.hd[i]] * (pd - sm.t2[j * TS + cols.hd[i]]);
+        dal[i] += dz;
+        if (leader) atomicAdd(p.dAro + v * h + cols.hd[i], dz);
+      }
+    }
+  };
+
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min((uint64_t)32, e1 - base);
+    if (lane < n) {
+      float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
+      load_heads(p.Ar + (int64_t)v_cur * h, h, arv);
+      load_heads(p.m + (int64_t)v_cur * h, h, mv);
+      load_heads(p.d + (int64_t)v_cur * h, h, dv);
+      load_heads(p.c + (int64_t)v_cur * h, h, cv);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        if (k < h) {
+          const float zz = sm.stat[3][k] + arv[k];
+          const float a = dv[k] > 0.f ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
+          sm.t0[lane * TS + k] = a;
+          sm.t1[lane * TS + k] = lrelu_grad(zz, slope) * a;
+          sm.t2[lane * TS + k] = cv[k];
+        }
+      }
+    }
+    sm.nb[lane] = v_cur;
+    __syncwarp();
+    v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> gv[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[j + t], hf, cols, gv[t]);
+#pragma unroll
+      for (int t = 0; t < U; ++t) edge(j + t, gv[t]);
+    }
+    for (; j < n; ++j) {
+      Vec<VW> gv[NV];
+      gather_row<VW, NV>(p.dOut, sm.nb[j], hf, cols, gv);
+      edge(j, gv);
+    }
+    __syncwarp();
+  }
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    if (cols.ok[i] && leader) sm.stat[0][cols.hd[i]] = dal[i];
+  __syncwarp();
+  if (!it.split) {
+    if (lane < h) p.dAl[u * h + lane] = sm.stat[0][lane];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (cols.ok[i]) {
+        const float dl = sm.stat[0][cols.hd[i]];
+        const Vec<VW> al = ldg_vec<VW>(p.a_l + cols.col[i]);
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = fmaf(dl, al.x[q], acc[i].x[q]);
+        st_vec<VW>(p.dHt + u * hf + cols.col[i], o);
+      }
+    }
+  } else {
+    float* part = p.part + wi * src_stride(h, f);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
+    if (lane < h) part[hf + lane] = sm.stat[0][lane];
+  }
+}
+
+// c[v,k] = <dOut[v,k,:], out[v,k,:]> (fast-mode input of K4).
+__global__ void gat_rowdot_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
+                                  const float* __restrict__ out, float* __restrict__ c) {
+  const int64_t n = rows * h;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const float* g = dOut + i * f;
+    const float* o = out + i * f;
+    float s = 0.f;
+    for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
+    c[i] = s;
+  }
+}
+
+// dHt[row_base + r, :] += dA_r[r] (x) a_r  for the local rows (fast-mode LP epilogue).
+__global__ void gat_lp_dar_kernel(int64_t rows, int64_t row_base, int h, int f, const float* __restrict__ dAr,
+                                  const float* __restrict__ a_r, float* __restrict__ dHt) {
+  const int hf = h * f;
+  const int64_t n = rows * hf;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / hf;
+    const int col = (int)(i % hf);
+    dHt[(row_base + r) * hf + col] += __ldg(dAr + r * h + col / f) * __ldg(a_r + col);
+  }
+}
+
 // Merge of split-row partials (forward): online-softmax combination in chunk order.
 __global__ void gat_fwd_merge_kernel(GatParams p, const uint32_t* __restrict__ split_rows,
                                      const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
@@ -601,7 +748,7 @@ __global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict
     for (int64_t it = i0; it < i1; ++it) dal += p.part[it * stride + hf + lane];
     st[w][0][lane] = dal;
     const bool local = u >= p.row_base && u < p.row_base + p.num_local;
-    st[w][1][lane] = local ? p.dAr[(u - p.row_base) * h + lane] : 0.f;
+    st[w][1][lane] = (local && !p.fast) ? p.dAr[(u - p.row_base) * h + lane] : 0.f;
     p.dAl[u * h + lane] = dal;
   }
   __syncwarp();
@@ -668,7 +815,7 @@ __global__ void attn_grad_reduce_kernel(int nb, int hf, const float* __restrict_
 // ---------------------------------------------------------------------------
 // Dispatch over the compiled (VW, NV) variants.
 // ---------------------------------------------------------------------------
-enum class Kind { Fwd, BwdDst, BwdSrc };
+enum class Kind { Fwd, BwdDst, BwdSrc, BwdSrcFast };
 
 template <int VW, int NV>
 void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
@@ -676,6 +823,7 @@ void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
     case Kind::Fwd: gat_fwd_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdSrcFast: gat_bwd_src_fast_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
   }
 }
 
@@ -835,6 +983,64 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
   if (sched->num_split_rows > 0) {
     gat_bwd_src_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
         p, sched->split_rows, sched->split_first, sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+int gnncg_gat_fast_supported(int h, int f) {
+  const int vw = f % 4 == 0 ? 4 : (f % 2 == 0 ? 2 : 1);
+  const int per = f / vw;
+  return h >= 1 && h <= MAXH && per >= 1 && per <= 32 && (per & (per - 1)) == 0 && h * f <= 256 * vw;
+}
+
+int gnncg_gat_rowdot(int64_t rows, int h, int f, const float* dOut, const float* out, float* c, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(rows >= 0 && h >= 1 && f >= 1, GNNCG_ERR_SHAPE, "gat_rowdot: bad shape");
+  if (rows == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(dOut && out && c, GNNCG_ERR_ARG, "gat_rowdot: null pointer");
+  const int g = (int)std::min<int64_t>(ceil_div(rows * h, 256), 148 * 32);
+  gat_rowdot_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, dOut, out, c);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
+                            int64_t row_base, int64_t num_local, const float* Ht, const float* Al, const float* Ar,
+                            const float* m, const float* d, const float* c, const float* dOut, const float* a_l,
+                            const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
+                            void* stream) {
+  GNNCG_DEVICE_GUARD();
+  int rc = check_common(csc_src, sched, h, f);
+  if (rc) return rc;
+  GNNCG_REQUIRE(gnncg_gat_fast_supported(h, f), GNNCG_ERR_UNSUPPORTED,
+                "gat_bwd_src_fused: f/VW must be a power of two <= 32 (use gnncg_gat_bwd_dst + gnncg_gat_bwd_src)");
+  GNNCG_REQUIRE(Ht && Al && Ar && m && d && c && dOut && a_l && a_r && dHt && dAl && dAr, GNNCG_ERR_ARG,
+                "gat_bwd_src_fused: null pointer");
+  GNNCG_REQUIRE(row_base >= 0 && num_local >= 0, GNNCG_ERR_ARG, "gat_bwd_src_fused: bad row block");
+  const size_t need = src_part_bytes(sched, h, f);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE,
+                "gat_bwd_src_fused: workspace %zu < %zu", ws_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  GNNCG_CUDA_TRY(cudaMemsetAsync(dAr, 0, sizeof(float) * (size_t)num_local * h, s));
+  GatParams p{};
+  p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
+  p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
+  p.h = h; p.f = f; p.slope = slope;
+  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.m = m; p.d = d; p.c = c; p.dOut = dOut; p.dAr = dAr; p.dAro = dAr;
+  p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
+  p.part = static_cast<float*>(ws);
+  p.fast = 1;
+  rc = dispatch(Kind::BwdSrcFast, p, s);
+  if (rc) return rc;
+  if (sched->num_split_rows > 0) {
+    gat_bwd_src_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
+        p, sched->split_rows, sched->split_first, sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  if (num_local > 0) {
+    const int g = (int)std::min<int64_t>(ceil_div(num_local * h * f, 256), 148 * 32);
+    gat_lp_dar_kernel<<<g, 256, 0, s>>>(num_local, row_base, h, f, dAr, a_r, dHt);
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;

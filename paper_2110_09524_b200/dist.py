@@ -107,10 +107,11 @@ def build_local(plan: PartitionPlan, rank: int, src: torch.Tensor, dst: torch.Te
 class CudaEngine:
     """The product engine: libgnncg_b200 kernels on the current CUDA device."""
 
-    def __init__(self, device, chunk=None):
+    def __init__(self, device, chunk=None, mode="auto"):
         self.device = device
         self.ws = Workspace(device)
         self.chunk = chunk
+        self.mode = mode
 
     def build_index(self, rows: int, key: torch.Tensor, other: torch.Tensor):
         from .graph import DeviceGraph
@@ -149,8 +150,8 @@ class CudaEngine:
                  _ptr(Ar_local), _ptr(out), _ptr(m), _ptr(d), wp, wn, _stream())
         return out, m, d
 
-    def region_bwd(self, lg: LocalGraph, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p: GatParams):
-        """K3 + K4 -> (dHt partial over padded sources, dAl partial, dAr local)."""
+    def region_bwd(self, lg: LocalGraph, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p: GatParams, out=None):
+        """K3 + K4 (or the fused fast pass) -> (dHt partial over padded sources, dAl partial, dAr local)."""
         n, h, f = lg.num_local, p.heads, p.f
         Ar_local = Ar_full[lg.row_base:lg.row_base + n]
         c, dAr = self.empty(n, h), self.empty(n, h)
@@ -159,6 +160,14 @@ class CudaEngine:
         dHt, dAl = self.empty(Vp, h * f), self.empty(Vp, h)
         wp, wn = self.ws.get(_lib.lib().gnncg_gat_workspace(sd.struct(), ss.struct(), h, f))
         st = _stream()
+        if out is not None and self.mode != "deterministic" and _lib.lib().gnncg_gat_fast_supported(h, f):
+            with PROBE("gat_rowdot"):
+                call("gnncg_gat_rowdot", n, h, f, _ptr(dOut), _ptr(out), _ptr(c), st)
+            with PROBE("gat_bwd_src_fused"):
+                call("gnncg_gat_bwd_src_fused", lg.csc.struct(), ss.struct(), h, f, p.slope, lg.row_base, n,
+                     _ptr(Ht), _ptr(Al), _ptr(Ar_local), _ptr(m), _ptr(d), _ptr(c), _ptr(dOut), _ptr(a_l),
+                     _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp, wn, st)
+            return dHt, dAl, dAr
         with PROBE("gat_bwd_dst"):
             call("gnncg_gat_bwd_dst", lg.csr.struct(), sd.struct(), h, f, p.slope, _ptr(Ht), _ptr(Al),
                  _ptr(Ar_local), _ptr(m), _ptr(d), _ptr(dOut), _ptr(c), _ptr(dAr), wp, wn, st)
@@ -261,7 +270,7 @@ class PartitionedGAT:
             Ar_local = Ar[lg.row_base:lg.row_base + lg.num_local]
             out, m, d = E.region_fwd(lg, Ht, Al, Ar_local, L.p)
             xs.append(out)
-            stashes.append((Ht, Al, Ar, m, d))
+            stashes.append((Ht, Al, Ar, m, d, out))
         return xs, stashes
 
     def backward(self, xs, stashes, dOut):
@@ -271,8 +280,8 @@ class PartitionedGAT:
         g = dOut
         for i in reversed(range(len(self.layers))):
             L = self.layers[i]
-            Ht, Al, Ar, m, d = stashes[i]
-            dHt_part, dAl_part, dAr = E.region_bwd(lg, Ht, Al, Ar, m, d, g, L.a_l, L.a_r, L.p)
+            Ht, Al, Ar, m, d, out = stashes[i]
+            dHt_part, dAl_part, dAr = E.region_bwd(lg, Ht, Al, Ar, m, d, g, L.a_l, L.a_r, L.p, out=out)
             dHt = self.comm.reduce_scatter_rows(dHt_part, mr, n)
             dAr_full = E.zeros(lg.plan.padded_V, L.p.heads)
             dAr_full[lg.row_base:lg.row_base + n] = dAr

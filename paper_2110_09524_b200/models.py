@@ -35,9 +35,11 @@ class GatLayerParams:
 class GAT:
     """A stack of GAT layers: dims = [(F_in, heads, f), ...]; layer l+1 has F_in = heads*f of layer l."""
 
-    def __init__(self, g: DeviceGraph, dims, seed: int = 0, slope: float = 0.2, chunk: int | None = None):
+    def __init__(self, g: DeviceGraph, dims, seed: int = 0, slope: float = 0.2, chunk: int | None = None,
+                 mode: str = "auto"):
         self.g = g
         self.chunk = chunk
+        self.mode = mode  # backward: "auto" (fast when supported) | "fast" | "deterministic"
         dev = g.device
         gen = torch.Generator(device=dev)
         gen.manual_seed(seed)
@@ -62,7 +64,8 @@ class GAT:
         g = dOut
         for i in reversed(range(len(self.layers))):
             L = self.layers[i]
-            gr = gat_backward(self.g, xs[i], L.W, L.a_l, L.a_r, stashes[i], g, L.p, need_dH=i > 0, chunk=self.chunk)
+            gr = gat_backward(self.g, xs[i], L.W, L.a_l, L.a_r, stashes[i], g, L.p, need_dH=i > 0, chunk=self.chunk,
+                              mode=self.mode)
             grads[i] = gr
             g = gr.dH
         return grads

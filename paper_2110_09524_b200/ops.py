@@ -145,6 +145,7 @@ class GatStash:
     Ar: torch.Tensor
     m: torch.Tensor
     d: torch.Tensor
+    out: torch.Tensor | None = None  # the layer output (kept anyway as the next layer's input)
 
 
 @dataclass
@@ -201,15 +202,26 @@ def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
     Ht = gemm(H, W, ws=g.ws)
     Al, Ar = attn_dots(Ht, a_l, a_r, h, f)
     out, m, d = gat_region_forward(g, Ht, Al, Ar, p, chunk=chunk)
-    return out, GatStash(Ht, Al, Ar, m, d)
+    return out, GatStash(Ht, Al, Ar, m, d, out)
 
 
-def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatParams, chunk=None):
-    """K3 + K4 + LP grads: returns (dHt, dAl, dAr, da_l, da_r, c)."""
+def fast_supported(p: GatParams) -> bool:
+    return bool(_lib.lib().gnncg_gat_fast_supported(p.heads, p.f))
+
+
+def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatParams, chunk=None, mode="auto"):
+    """Recompute backward of the fused region: returns (dHt, dAl, dAr, da_l, da_r, c).
+
+    mode "deterministic": K3 over csr_dst then K4 over csc_src, fixed-order sums (bitwise
+    reproducible).  mode "fast": the spec's lock-free fast mode -- c from the
+    row dot <dOut, out>, then one fused pass over csc_src with dA_r accumulated by global
+    reductions (no csr_dst gather pass).  "auto" = fast when supported and stash.out is present."""
     V, h, f = g.num_vertices, p.heads, p.f
     dOut = _f32(dOut, "dOut")
     _shape(dOut, (V, h * f), "dOut")
     a_l, a_r = _f32(a_l, "a_l"), _f32(a_r, "a_r")
+    if mode == "auto":
+        mode = "fast" if (stash.out is not None and fast_supported(p)) else "deterministic"
     dev = dOut.device
     c = torch.empty(V, h, device=dev)
     dAr = torch.empty(V, h, device=dev)
@@ -221,13 +233,26 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
     need = max(L.gnncg_gat_workspace(sd.struct(), ss.struct(), h, f), L.gnncg_gat_attn_grad_workspace(V, h, f))
     wp, wn = g.ws.get(need)
     s = _stream()
-    with PROBE("gat_bwd_dst"):
-        call("gnncg_gat_bwd_dst", g.csr_dst.struct(), sd.struct(), h, f, p.slope, _ptr(stash.Ht), _ptr(stash.Al),
-             _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(dOut), _ptr(c), _ptr(dAr), wp, wn, s)
-    with PROBE("gat_bwd_src"):
-        call("gnncg_gat_bwd_src", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
-             _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(c), _ptr(dOut), _ptr(dAr),
-             _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), wp, wn, s)
+    if mode == "fast":
+        if stash.out is None:
+            raise TensorError("gat_region_backward(fast): stash.out is required")
+        with PROBE("gat_rowdot"):
+            call("gnncg_gat_rowdot", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(c), s)
+        with PROBE("gat_bwd_src_fused"):
+            call("gnncg_gat_bwd_src_fused", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
+                 _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(c), _ptr(dOut), _ptr(a_l),
+                 _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp, wn, s)
+    elif mode == "deterministic":
+        with PROBE("gat_bwd_dst"):
+            call("gnncg_gat_bwd_dst", g.csr_dst.struct(), sd.struct(), h, f, p.slope, _ptr(stash.Ht),
+                 _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(dOut), _ptr(c), _ptr(dAr),
+                 wp, wn, s)
+        with PROBE("gat_bwd_src"):
+            call("gnncg_gat_bwd_src", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
+                 _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(c), _ptr(dOut), _ptr(dAr),
+                 _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), wp, wn, s)
+    else:
+        raise ValueError(f"unknown backward mode {mode!r}")
     da_l = torch.empty(h, f, device=dev)
     da_r = torch.empty(h, f, device=dev)
     with PROBE("attn_grad"):
@@ -236,11 +261,13 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
     return dHt, dAl, dAr, da_l, da_r, c
 
 
-def gat_backward(g: DeviceGraph, H, W, a_l, a_r, stash: GatStash, dOut, p: GatParams, need_dH=True, chunk=None):
+def gat_backward(g: DeviceGraph, H, W, a_l, a_r, stash: GatStash, dOut, p: GatParams, need_dH=True, chunk=None,
+                 mode="auto"):
     """GAT layer backward with recomputation:
-    K3 (csr_dst) -> K4 (csc_src) -> LP grads -> dW = H^T dHt (K5), dH = dHt W^T (K5)."""
+    region backward (K3+K4, or the fused fast pass) -> LP grads -> dW = H^T dHt (K5),
+    dH = dHt W^T (K5)."""
     H, W = _f32(H, "H"), _f32(W, "W")
-    dHt, _, _, da_l, da_r, _ = gat_region_backward(g, stash, a_l, a_r, dOut, p, chunk=chunk)
+    dHt, _, _, da_l, da_r, _ = gat_region_backward(g, stash, a_l, a_r, dOut, p, chunk=chunk, mode=mode)
     dW = gemm(H, dHt, trans_a=True, ws=g.ws)
     dH = gemm(dHt, W, trans_b=True, ws=g.ws) if need_dH else None
     return GatGrads(dH, dW, da_l, da_r)

@@ -43,7 +43,7 @@ class OracleEngine:
         r = O.gat_region_fwd_f64(g, Ht.numpy(), Al.numpy(), Ar_local.numpy(), p.heads, p.f, p.slope)
         return torch.from_numpy(r["out"]), torch.from_numpy(r["m"]), torch.from_numpy(r["d"])
 
-    def region_bwd(self, lg, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p):
+    def region_bwd(self, lg, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p, out=None):
         h, f, n, base = p.heads, p.f, lg.num_local, lg.row_base
         c = lg.csr
         v = np.repeat(np.arange(n), np.diff(c["off"].astype(np.int64)))

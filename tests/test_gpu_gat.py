@@ -8,7 +8,7 @@ import torch
 from oracle import oracle as O
 from paper_2110_09524_b200 import DeviceGraph, GatParams, gat_backward, gat_forward, gemm
 from paper_2110_09524_b200.models import GAT
-from paper_2110_09524_b200.ops import GatStash, gat_region_backward, gat_region_forward
+from paper_2110_09524_b200.ops import GatStash, fast_supported, gat_region_backward, gat_region_forward
 
 pytestmark = pytest.mark.gpu
 TOL = 1e-4
@@ -53,7 +53,8 @@ CASES = [("G3", 1, 2), ("ER16", 2, 3), ("ER16", 3, 5), ("cora", 8, 8), ("star", 
 
 @pytest.mark.parametrize("kind,h,f", CASES)
 @pytest.mark.parametrize("chunk", [32, 2048])
-def test_region_forward_and_backward(cuda, kind, h, f, chunk):
+@pytest.mark.parametrize("mode", ["deterministic", "fast"])
+def test_region_forward_and_backward(cuda, kind, h, f, chunk, mode):
     hg, g = make_graph(kind, cuda)
     V = hg.V
     rng = np.random.default_rng(h * 100 + f)
@@ -70,9 +71,11 @@ def test_region_forward_and_backward(cuda, kind, h, f, chunk):
     assert O.max_rel_err(np64(m), ref["m"]) < TOL
     assert O.max_rel_err(np64(d), ref["d"]) < TOL
     rb = O.gat_region_bwd_f64(hg, Ht, Al, Ar, al, ar, h, f, dOut)
-    st = GatStash(tHt, tAl, tAr, m, d)
+    st = GatStash(tHt, tAl, tAr, m, d, out)
+    if mode == "fast" and not fast_supported(p):
+        pytest.skip("fast mode needs f/VW to be a power of two")
     dHt, dAl, dAr, da_l, da_r, c = gat_region_backward(g, st, t32(al, cuda), t32(ar, cuda), t32(dOut, cuda), p,
-                                                       chunk=chunk)
+                                                       chunk=chunk, mode=mode)
     torch.cuda.synchronize()
     for name, got in (("dHt", dHt), ("dAl", dAl), ("dAr", dAr), ("dal", da_l), ("dar", da_r)):
         scale = max(1.0, np.abs(rb[name]).max()) if name in ("dal", "dar") else 1.0
@@ -103,7 +106,7 @@ def test_deterministic_runs(cuda):
     res = []
     for _ in range(2):
         out, st = gat_forward(g, H, W, al, ar, p)
-        gr = gat_backward(g, H, W, al, ar, st, dOut, p)
+        gr = gat_backward(g, H, W, al, ar, st, dOut, p, mode="deterministic")
         res.append([out, gr.dH, gr.dW, gr.da_l, gr.da_r])
     for x, y in zip(*res):
         assert torch.equal(x, y)  # fixed-order reductions: bitwise reproducible
@@ -111,7 +114,8 @@ def test_deterministic_runs(cuda):
 
 @pytest.mark.parametrize("kind,Fin,h,f", [("G3", 2, 1, 2), ("ER16", 3, 2, 2), ("cora", 1433, 8, 8),
                                           ("powerlaw", 602, 8, 32)])
-def test_layer_vs_oracle(cuda, kind, Fin, h, f):
+@pytest.mark.parametrize("mode", ["deterministic", "auto"])
+def test_layer_vs_oracle(cuda, kind, Fin, h, f, mode):
     hg, g = make_graph(kind, cuda)
     V = hg.V
     rng = np.random.default_rng(5)
@@ -125,7 +129,7 @@ def test_layer_vs_oracle(cuda, kind, Fin, h, f):
     p = GatParams(h, f)
     tH, tW, tal, tar = (t32(x, cuda) for x in (H, W, al, ar))
     out, st = gat_forward(g, tH, tW, tal, tar, p)
-    gr = gat_backward(g, tH, tW, tal, tar, st, t32(dOut, cuda), p, need_dH=True)
+    gr = gat_backward(g, tH, tW, tal, tar, st, t32(dOut, cuda), p, need_dH=True, mode=mode)
     torch.cuda.synchronize()
     assert O.max_rel_err(np64(st.Ht), fw["Ht"]) < TOL
     assert O.max_rel_err(np64(out), fw["out"]) < TOL
