@@ -541,14 +541,35 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_kernel(G
 // K4 "fast" (SPEC.md:378 fast mode): backward pass 2 with pass 1 folded in.
 // With c[v] = <dOut[v], out[v]> per head (= sum_e alpha_e dalpha_e, the softmax
 // backward identity; gat_rowdot_kernel), a single pass over csc_src computes per
-// edge dalpha_e = <dOut[v], x_u> (a per-edge head reduction across the lanes of
-// the head) and dz_e = gate*alpha (dalpha_e - c[v]); dA_l[u] sums dz_e in the warp,
-// dA_r[v] receives dz_e by a global red (order-nondeterministic, tolerance-tested).
-// Removes the whole csr_dst gather pass of K3.  Requires f/VW to be a power of
-// two <= 32 (each head's columns inside one lane group).
+// edge dalpha_e = <dOut[v], x_u> and dz_e = gate*alpha (dalpha_e - c[v]); dA_l[u]
+// sums dz_e in the warp, dA_r[v] receives dz_e by a global red (order-
+// nondeterministic, tolerance-tested).  Removes K3's whole csr_dst gather pass.
+//
+// Per-edge head dots without per-edge shuffles: for a group of U gathered edges
+// each lane holds U*NV partial dots; a butterfly transpose-reduction over the
+// PER lanes that share a head (log2(PER) steps, halving the values each step)
+// leaves lane r of every PER-group with the complete dots of (edge, vector)
+// pairs [r*NOUT, r*NOUT+NOUT) -- U*NV*(1-1/PER) shuffles instead of U*NV*log2(PER).
 // ---------------------------------------------------------------------------
-template <int VW, int NV>
+template <int CNT, int OFF>
+__device__ __forceinline__ void butterfly(float* v, int lane) {
+  if constexpr (OFF >= 1) {
+    const bool up = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < CNT / 2; ++j) {
+      const float send = up ? v[j] : v[j + CNT / 2];
+      const float keep = up ? v[j + CNT / 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+    }
+    butterfly<CNT / 2, OFF / 2>(v, lane);
+  }
+}
+
+template <int VW, int NV, int PER>
 __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_kernel(GatParams p) {
+  constexpr int U = GatherDepth<NV>::U;
+  constexpr int NVAL = U * NV, NOUT = NVAL / PER;
+  static_assert(NVAL % PER == 0, "fast K4 needs U*NV to be a multiple of the lanes per head");
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
@@ -558,9 +579,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_ker
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
   const int64_t u = it.row;
-  const int per = f / VW;  // lanes per head
-  const bool leader = (lane & (per - 1)) == 0;
-  constexpr int U = GatherDepth<NV>::U;
+  const int r = lane & (PER - 1);  // rank inside the head's lane group
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
   const Cols<VW, NV> cols(lane, hf, f);
@@ -575,29 +594,10 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_ker
   uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
   __syncwarp();
 
-  auto edge = [&](int j, const Vec<VW>(&gv)[NV]) {
-    const int64_t v = sm.nb[j];
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const float a = sm.t0[j * TS + cols.hd[i]];
-      float pd = 0.f;
-#pragma unroll
-      for (int q = 0; q < VW; ++q) {
-        acc[i].x[q] = fmaf(a, gv[i].x[q], acc[i].x[q]);
-        pd = fmaf(x[i].x[q], gv[i].x[q], pd);
-      }
-      for (int o = 1; o < per; o <<= 1) pd += __shfl_xor_sync(0xffffffffu, pd, o);
-      if (cols.ok[i]) {
-        const float dz = sm.t1[j * TS + cols.hd[i]] * (pd - sm.t2[j * TS + cols.hd[i]]);
-        dal[i] += dz;
-        if (leader) atomicAdd(p.dAro + v * h + cols.hd[i], dz);
-      }
-    }
-  };
-
   for (uint64_t base = e0; base < e1; base += 32) {
     const int n = (int)min((uint64_t)32, e1 - base);
-    if (lane < n) {
+    {
+      const bool valid = lane < n;
       float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
       load_heads(p.Ar + (int64_t)v_cur * h, h, arv);
       load_heads(p.m + (int64_t)v_cur * h, h, mv);
@@ -607,34 +607,63 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_ker
       for (int k = 0; k < MAXH; ++k) {
         if (k < h) {
           const float zz = sm.stat[3][k] + arv[k];
-          const float a = dv[k] > 0.f ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
+          const float a = (valid && dv[k] > 0.f) ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
           sm.t0[lane * TS + k] = a;
           sm.t1[lane * TS + k] = lrelu_grad(zz, slope) * a;
           sm.t2[lane * TS + k] = cv[k];
         }
       }
     }
-    sm.nb[lane] = v_cur;
+    sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
     __syncwarp();
     v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
-    int j = 0;
-    for (; j + U <= n; j += U) {
+    for (int j = 0; j < n; j += U) {
       Vec<VW> gv[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[j + t], hf, cols, gv[t]);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[(j + t) & 31], hf, cols, gv[t]);
+      float pd[NVAL];
 #pragma unroll
-      for (int t = 0; t < U; ++t) edge(j + t, gv[t]);
-    }
-    for (; j < n; ++j) {
-      Vec<VW> gv[NV];
-      gather_row<VW, NV>(p.dOut, sm.nb[j], hf, cols, gv);
-      edge(j, gv);
+      for (int t = 0; t < U; ++t) {
+        const int e = (j + t) & 31;
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.t0[e * TS + cols.hd[i]];
+          float s = 0.f;
+#pragma unroll
+          for (int q = 0; q < VW; ++q) {
+            acc[i].x[q] = fmaf(a, gv[t][i].x[q], acc[i].x[q]);
+            s = fmaf(x[i].x[q], gv[t][i].x[q], s);
+          }
+          pd[t * NV + i] = s;
+        }
+      }
+      butterfly<NVAL, PER / 2>(pd, lane);
+#pragma unroll
+      for (int q = 0; q < NOUT; ++q) {
+        const int idx = r * NOUT + q;
+        const int t = idx / NV, i = idx % NV;
+        int hd = cols.hd[0];
+        bool ok = cols.ok[0];
+#pragma unroll
+        for (int ii = 1; ii < NV; ++ii)
+          if (i == ii) { hd = cols.hd[ii]; ok = cols.ok[ii]; }
+        const int e = j + t;
+        const bool valid = ok && e < n;
+        const float dz = valid ? sm.t1[e * TS + hd] * (pd[q] - sm.t2[e * TS + hd]) : 0.f;
+#pragma unroll
+        for (int ii = 0; ii < NV; ++ii)
+          if (i == ii) dal[ii] += dz;
+        if (valid) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
+      }
     }
     __syncwarp();
   }
 #pragma unroll
-  for (int i = 0; i < NV; ++i)
-    if (cols.ok[i] && leader) sm.stat[0][cols.hd[i]] = dal[i];
+  for (int i = 0; i < NV; ++i) {
+#pragma unroll
+    for (int o = 1; o < PER; o <<= 1) dal[i] += __shfl_xor_sync(0xffffffffu, dal[i], o);
+    if (cols.ok[i] && r == 0) sm.stat[0][cols.hd[i]] = dal[i];
+  }
   __syncwarp();
   if (!it.split) {
     if (lane < h) p.dAl[u * h + lane] = sm.stat[0][lane];
@@ -818,12 +847,25 @@ __global__ void attn_grad_reduce_kernel(int nb, int hf, const float* __restrict_
 enum class Kind { Fwd, BwdDst, BwdSrc, BwdSrcFast };
 
 template <int VW, int NV>
+void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
+  constexpr int NVAL = GatherDepth<NV>::U * NV;
+  switch (p.f / VW) {
+    case 1: gat_bwd_src_fast_kernel<VW, NV, 1><<<grid, THREADS, 0, s>>>(p); break;
+    case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2><<<grid, THREADS, 0, s>>>(p); break;
+    case 4: if constexpr (NVAL % 4 == 0) gat_bwd_src_fast_kernel<VW, NV, 4><<<grid, THREADS, 0, s>>>(p); break;
+    case 8: if constexpr (NVAL % 8 == 0) gat_bwd_src_fast_kernel<VW, NV, 8><<<grid, THREADS, 0, s>>>(p); break;
+    case 16: if constexpr (NVAL % 16 == 0) gat_bwd_src_fast_kernel<VW, NV, 16><<<grid, THREADS, 0, s>>>(p); break;
+    default: break;  // excluded by gnncg_gat_fast_supported
+  }
+}
+
+template <int VW, int NV>
 void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
   switch (kind) {
     case Kind::Fwd: gat_fwd_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
-    case Kind::BwdSrcFast: gat_bwd_src_fast_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdSrcFast: launch_fast<VW, NV>(p, grid, s); break;
   }
 }
 
@@ -991,7 +1033,11 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
 int gnncg_gat_fast_supported(int h, int f) {
   const int vw = f % 4 == 0 ? 4 : (f % 2 == 0 ? 2 : 1);
   const int per = f / vw;
-  return h >= 1 && h <= MAXH && per >= 1 && per <= 32 && (per & (per - 1)) == 0 && h * f <= 256 * vw;
+  if (h < 1 || h > MAXH || per < 1 || per > 16 || (per & (per - 1)) != 0 || h * f > 256 * vw) return 0;
+  const int nvec = (int)ceil_div(h * f / vw, 32);
+  const int nv = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : 8;
+  const int u = nv <= 2 ? 8 : (nv == 4 ? 4 : 2);
+  return (u * nv) % per == 0;
 }
 
 int gnncg_gat_rowdot(int64_t rows, int h, int f, const float* dOut, const float* out, float* c, void* stream) {

@@ -155,6 +155,31 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 }
 
 }  // namespace
+
+// Tensor-core path (gemm_tc.cu).
+bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb);
+int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s);
+
+namespace {
+// GNNCG_GEMM=simt forces the CUDA-core kernel (A/B comparisons); default: tensor cores when eligible.
+bool tc_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GEMM");
+    v = (e && strcmp(e, "simt") == 0) ? 0 : 1;
+  }
+  return v == 1;
+}
+
+int tc_splits(int64_t M, int64_t N, int64_t K) {
+  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, N > 128 ? 256 : 128);
+  if (tiles >= 148 || K < 8 * 1024) return 1;
+  int64_t s = std::min<int64_t>(ceil_div(148, tiles), K / 2048);
+  return (int)std::max<int64_t>(std::min<int64_t>(s, 64), 1);
+}
+}  // namespace
 }  // namespace gnncg_b200
 
 using namespace gnncg_b200;
@@ -164,7 +189,7 @@ extern "C" {
 size_t gnncg_gemm_workspace(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K) {
   (void)trans_a;
   (void)trans_b;
-  const int s = choose_splits(M, N, K);
+  const int s = std::max(choose_splits(M, N, K), tc_splits(M, N, K));
   return s > 1 ? align_up((size_t)s * M * N * sizeof(float)) : 0;
 }
 
@@ -184,10 +209,24 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
                 "gemm: leading dimension too small");
   GNNCG_REQUIRE(A && B && C, GNNCG_ERR_ARG, "gemm: null pointer");
   cudaStream_t s = as_stream(stream);
-  const int splits = choose_splits(M, N, K);
   const size_t need = gnncg_gemm_workspace(trans_a, trans_b, M, N, K);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gemm: workspace %zu < %zu", ws_bytes,
                 need);
+  if (tc_enabled() && tc_gemm_eligible(trans_a, trans_b, M, N, K, A, lda, B, ldb)) {
+    int splits = tc_splits(M, N, K);
+    const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), 32) * 32 : K;
+    splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;  // every split gets >= 1 k-block
+    int rc = tc_gemm(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, splits, kchunk, static_cast<float*>(ws), s);
+    if (rc != GNNCG_OK) return rc;
+    if (splits > 1) {
+      const int64_t total = M * N;
+      const int g = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
+      splitk_reduce_kernel<<<g, 256, 0, s>>>(M, N, splits, static_cast<float*>(ws), C, ldc);
+      GNNCG_LAUNCH_CHECK();
+    }
+    return GNNCG_OK;
+  }
+  const int splits = choose_splits(M, N, K);
   const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), BK) * BK : std::max<int64_t>(K, 1);
   const int real_splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)real_splits);

@@ -1,0 +1,378 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Dense transforms on the 5th-gen tensor cores (K1 / K5 on sm_100a):
+//   C[M,N] = op(A)[M,K] op(B)[K,N], fp32 in / fp32 out, fp32-accurate via a 3xTF32
+//   split: x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x - hi
+//   exactly), C = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.
+// Replaces matmul / matmul_nt / matmul_tn (proj/src/tensor.cpp:8-60) for the
+// reorganized ApplyVertex(W) of the GNN layers and its two backward Applies.
+//
+// Structure (one 128 x BN output tile per CTA, K split across gridDim.z):
+//   warp 0      TMA producer: cp.async.bulk.tensor 2D boxes (SWIZZLE_128B) of A and B
+//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32)
+//   warps 2..5  split warps: hi/lo of each landed stage in shared memory, then the
+//               epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
+// mbarrier pipeline: full (TMA bytes) -> split (128 threads) -> MMA -> empty
+// (tcgen05.commit) ; accum (tcgen05.commit after the last k-block) -> epilogue.
+// Operands may be K-major or MN-major (transposed), both through SW128 smem
+// descriptors: K-major rows of 32 fp32 (128 B), MN-major 32-element x 32-k boxes.
+#include <cuda.h>
+#include <cudaTypedefs.h>
+
+#include <cstring>
+#include <mutex>
+
+#include "common.cuh"
+
+namespace gnncg_b200 {
+namespace tc {
+
+constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one SW128 row
+constexpr int THREADS = 192;
+
+template <int BN>
+struct Cfg {
+  static constexpr int A_BYTES = BM * BK * 4;
+  static constexpr int B_BYTES = BN * BK * 4;
+  static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw->hi and lo of A and B
+  static constexpr int STAGES = BN >= 256 ? 2 : 3;
+  static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
+};
+
+__device__ __forceinline__ uint32_t smem_u32(const void* p) {
+  return static_cast<uint32_t>(__cvta_generic_to_shared(p));
+}
+
+__device__ __forceinline__ void mbar_init(uint64_t* bar, uint32_t count) {
+  asm volatile("mbarrier.init.shared::cta.b64 [%0], %1;" ::"r"(smem_u32(bar)), "r"(count));
+}
+__device__ __forceinline__ void mbar_expect_tx(uint64_t* bar, uint32_t bytes) {
+  asm volatile("mbarrier.arrive.expect_tx.shared::cta.b64 _, [%0], %1;" ::"r"(smem_u32(bar)), "r"(bytes) : "memory");
+}
+__device__ __forceinline__ void mbar_arrive(uint64_t* bar) {
+  asm volatile("mbarrier.arrive.shared::cta.b64 _, [%0];" ::"r"(smem_u32(bar)) : "memory");
+}
+__device__ __forceinline__ void mbar_wait(uint64_t* bar, uint32_t parity) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "WAIT_%=:\n\t"
+      "mbarrier.try_wait.parity.shared::cta.b64 p, [%0], %1;\n\t"
+      "@!p bra WAIT_%=;\n\t}" ::"r"(smem_u32(bar)),
+      "r"(parity)
+      : "memory");
+}
+
+__device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, int c0, int c1, uint64_t* bar) {
+  asm volatile(
+      "cp.async.bulk.tensor.2d.shared::cluster.global.mbarrier::complete_tx::bytes [%0], [%1, {%2, %3}], [%4];" ::"r"(
+          smem_u32(dst)),
+      "l"(map), "r"(c0), "r"(c1), "r"(smem_u32(bar))
+      : "memory");
+}
+
+// SM100 shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1.
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+  uint64_t d = 0;
+  d |= (uint64_t)((addr >> 4) & 0x3FFF);
+  d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
+  d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
+  d |= (uint64_t)1 << 46;  // version (sm100)
+  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  return d;
+}
+
+// Instruction descriptor: kind::tf32, fp32 accumulate, M = 128, N = BN.
+__host__ __device__ constexpr uint32_t instr_desc(int N, bool a_mn, bool b_mn) {
+  return (1u << 4)                   // c_format = F32
+         | (2u << 7)                 // a_format = TF32
+         | (2u << 10)                // b_format = TF32
+         | ((a_mn ? 1u : 0u) << 15)  // a_major
+         | ((b_mn ? 1u : 0u) << 16)  // b_major
+         | ((uint32_t)(N >> 3) << 17) | ((uint32_t)(BM >> 4) << 24);
+}
+
+__device__ __forceinline__ void mma_tf32(uint32_t tmem_c, uint64_t da, uint64_t db, uint32_t idesc, uint32_t acc) {
+  asm volatile(
+      "{\n\t.reg .pred p;\n\t"
+      "setp.ne.b32 p, %4, 0;\n\t"
+      "tcgen05.mma.cta_group::1.kind::tf32 [%0], %1, %2, %3, p;\n\t}" ::"r"(tmem_c),
+      "l"(da), "l"(db), "r"(idesc), "r"(acc));
+}
+
+__device__ __forceinline__ void mma_commit(uint64_t* bar) {
+  asm volatile("tcgen05.commit.cta_group::1.mbarrier::arrive::one.shared::cluster.b64 [%0];" ::"r"(smem_u32(bar))
+               : "memory");
+}
+
+__device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
+  asm volatile(
+      "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
+      "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
+        "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
+        "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
+        "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
+      : "r"(taddr));
+  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+}
+
+// Split a landed stage buffer in place: buf holds raw fp32; write hi (in place) and lo.
+__device__ __forceinline__ void split_hi_lo(float* raw, float* lo, int bytes, int tid, int nthr) {
+  float4* r4 = reinterpret_cast<float4*>(raw);
+  float4* l4 = reinterpret_cast<float4*>(lo);
+  const int n = bytes / 16;
+  for (int i = tid; i < n; i += nthr) {
+    float4 v = r4[i];
+    float4 h;
+    h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
+    h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
+    h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
+    h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
+    r4[i] = h;
+    l4[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
+  }
+}
+
+// A_MN: A stored K x M (M contiguous); else M x K.  B_MN: B stored K x N (N contiguous); else N x K.
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(THREADS, 1)
+    gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                       float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk,
+                       int64_t split_stride) {
+  using CF = Cfg<BN>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* split = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* accum = bars + 3 * S;
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
+
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t kb0 = (int64_t)blockIdx.z * kchunk;
+  const int64_t kb1 = min(K, kb0 + kchunk);
+  const int nk = (int)((kb1 - kb0 + BK - 1) / BK);
+  float* Cz = C + (int64_t)blockIdx.z * split_stride;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 128);
+      mbar_init(&empty[s], 1);
+    }
+    mbar_init(accum, 1);
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  auto a_hi = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES); };
+  auto a_lo = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + CF::A_BYTES); };
+  auto b_hi = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES); };
+  auto b_lo = [&](int s) {
+    return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES + CF::B_BYTES);
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        const uint32_t ph = (uint32_t)(i / S) & 1u;
+        mbar_wait(&empty[s], ph ^ 1u);
+        mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+        const int k = (int)(kb0 + (int64_t)i * BK);
+        if (!A_MN) {
+          tma_load_2d(a_hi(s), &map_a, k, (int)m0, &full[s]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BM / 32; ++j)
+            tma_load_2d(reinterpret_cast<uint8_t*>(a_hi(s)) + j * 4096, &map_a, (int)m0 + 32 * j, k, &full[s]);
+        }
+        if (!B_MN) {
+          tma_load_2d(b_hi(s), &map_b, k, (int)n0, &full[s]);
+        } else {
+#pragma unroll
+          for (int j = 0; j < BN / 32; ++j)
+            tma_load_2d(reinterpret_cast<uint8_t*>(b_hi(s)) + j * 4096, &map_b, (int)n0 + 32 * j, k, &full[s]);
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+      // K-major: rows of 128 B, 8-row atoms 1024 B apart (SBO), k-step = +32 B.
+      // MN-major: 32-element x 32-k boxes (4 KB) along MN (LBO), 8-k groups 1024 B apart (SBO), k-step = +1024 B.
+      const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = 1024u, a_step = A_MN ? 1024u : 32u;
+      const uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = 1024u, b_step = B_MN ? 1024u : 32u;
+      for (int i = 0; i < nk; ++i) {
+        const int s = i % S;
+        const uint32_t ph = (uint32_t)(i / S) & 1u;
+        mbar_wait(&split[s], ph);
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t ah = smem_u32(a_hi(s)), al = smem_u32(a_lo(s));
+        const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+#pragma unroll
+        for (int k = 0; k < BK / 8; ++k) {
+          const uint64_t dah = smem_desc(ah + k * a_step, a_lbo, a_sbo);
+          const uint64_t dal = smem_desc(al + k * a_step, a_lbo, a_sbo);
+          const uint64_t dbh = smem_desc(bh + k * b_step, b_lbo, b_sbo);
+          const uint64_t dbl = smem_desc(bl + k * b_step, b_lbo, b_sbo);
+          mma_tf32(tmem, dah, dbh, idesc, (i > 0 || k > 0) ? 1u : 0u);
+          mma_tf32(tmem, dah, dbl, idesc, 1u);
+          mma_tf32(tmem, dal, dbh, idesc, 1u);
+        }
+        mma_commit(&empty[s]);
+      }
+      mma_commit(accum);
+    }
+  } else {
+    // ---- split warps (2..5), then epilogue
+    const int tid = threadIdx.x - 64;
+    for (int i = 0; i < nk; ++i) {
+      const int s = i % S;
+      const uint32_t ph = (uint32_t)(i / S) & 1u;
+      mbar_wait(&full[s], ph);
+      split_hi_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 128);
+      split_hi_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 128);
+      asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+      mbar_arrive(&split[s]);
+    }
+    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int64_t row = m0 + q * 32 + lane;
+    if (nk > 0) {
+      mbar_wait(accum, 0);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+    }
+#pragma unroll 1
+    for (int c = 0; c < BN / 32; ++c) {
+      uint32_t r[32];
+      if (nk > 0) {
+        tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+      } else {
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = 0u;
+      }
+      const int64_t col = n0 + c * 32;
+      if (row < M) {
+        float* dst = Cz + row * ldc + col;
+        if (col + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+          for (int j = 0; j < 32; j += 4)
+            *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                              __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+        } else {
+#pragma unroll
+          for (int j = 0; j < 32; ++j)
+            if (col + j < N) dst[j] = __uint_as_float(r[j]);
+        }
+      }
+    }
+    asm volatile("tcgen05.fence::before_thread_sync;");
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(BN));
+  }
+}
+
+// ---------------------------------------------------------------------------------- host
+PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
+  static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
+  static std::once_flag once;
+  std::call_once(once, [] {
+    void* p = nullptr;
+    cudaDriverEntryPointQueryResult q;
+    if (cudaGetDriverEntryPoint("cuTensorMapEncodeTiled", &p, cudaEnableDefault, &q) == cudaSuccess &&
+        q == cudaDriverEntryPointSuccess)
+      fn = reinterpret_cast<PFN_cuTensorMapEncodeTiled_v12000>(p);
+  });
+  return fn;
+}
+
+// 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride `ld` elements.
+bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
+              int box_outer) {
+  auto fn = encode_fn();
+  if (!fn) return false;
+  cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
+  cuuint64_t strides[1] = {(cuuint64_t)ld * 4};
+  cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
+  cuuint32_t estr[2] = {1, 1};
+  CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
+  return r == CUDA_SUCCESS;
+}
+
+template <int BN, bool A_MN, bool B_MN>
+int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
+           int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s) {
+  using CF = Cfg<BN>;
+  CUtensorMap ma, mb;
+  bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK) : make_map(&ma, A, K, M, lda, BK, BM);
+  ok = ok && (B_MN ? make_map(&mb, B, N, K, ldb, 32, BK) : make_map(&mb, B, K, N, ldb, BK, BN));
+  if (!ok) return fail(GNNCG_ERR_CUDA, "gemm_tc: cuTensorMapEncodeTiled failed");
+  auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN>;
+  static bool attr_set = false;
+  if (!attr_set) {
+    GNNCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+    attr_set = true;
+  }
+  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
+  kern<<<grid, THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+}  // namespace tc
+
+// Entry used by gnncg_gemm (gemm.cu).  trans_a: A stored K x M ; trans_b: B stored N x K.
+// In the tensor-core kernel's terms A is MN-major iff trans_a, B is MN-major iff !trans_b.
+bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
+                      const float* B, int64_t ldb) {
+  if (!tc::encode_fn()) return false;
+  if (M <= 0 || N <= 0 || K <= 0) return false;
+  if (((uintptr_t)A & 15) || ((uintptr_t)B & 15) || (lda % 4) || (ldb % 4)) return false;
+  if (M >= (1ll << 31) || N >= (1ll << 31) || K >= (1ll << 31)) return false;
+  (void)trans_a;
+  (void)trans_b;
+  return true;
+}
+
+int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
+            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s) {
+  float* out = splits > 1 ? partial : C;
+  const int64_t ldo = splits > 1 ? N : ldc;
+  const int64_t stride = splits > 1 ? M * N : 0;
+  const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
+  const bool wide = N > 128;
+#define GNNCG_TC(BN, AM, BMN) return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s)
+  if (wide) {
+    if (!a_mn && !b_mn) GNNCG_TC(256, false, false);
+    if (!a_mn && b_mn) GNNCG_TC(256, false, true);
+    if (a_mn && !b_mn) GNNCG_TC(256, true, false);
+    GNNCG_TC(256, true, true);
+  } else {
+    if (!a_mn && !b_mn) GNNCG_TC(128, false, false);
+    if (!a_mn && b_mn) GNNCG_TC(128, false, true);
+    if (a_mn && !b_mn) GNNCG_TC(128, true, false);
+    GNNCG_TC(128, true, true);
+  }
+#undef GNNCG_TC
+}
+
+}  // namespace gnncg_b200

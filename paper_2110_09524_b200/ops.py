@@ -79,6 +79,16 @@ def _f32(t: torch.Tensor, name: str) -> torch.Tensor:
     return t.contiguous()
 
 
+def _f32_rows(t: torch.Tensor, name: str) -> torch.Tensor:
+    """fp32 CUDA matrix with unit column stride; a padded row stride (e.g. 16-byte aligned, which
+    the TMA tensor-core GEMM needs) is kept as is."""
+    if not isinstance(t, torch.Tensor) or t.dtype != torch.float32 or not t.is_cuda or t.dim() != 2:
+        raise TensorError(f"{name}: expected a 2-D float32 CUDA tensor")
+    if t.stride(1) != 1 or t.stride(0) < t.shape[1]:
+        t = t.contiguous()
+    return t
+
+
 def _shape(t: torch.Tensor, shape, name: str):
     if tuple(t.shape) != tuple(shape):
         raise TensorError(f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
@@ -90,8 +100,8 @@ def _shape(t: torch.Tensor, shape, name: str):
 def gemm(A: torch.Tensor, B: torch.Tensor, trans_a=False, trans_b=False, out: torch.Tensor | None = None,
          ws=None) -> torch.Tensor:
     """C = op(A) op(B) in fp32 on the device (deterministic)."""
-    A = _f32(A, "gemm A")
-    B = _f32(B, "gemm B")
+    A = _f32_rows(A, "gemm A")
+    B = _f32_rows(B, "gemm B")
     M, K = (A.shape[1], A.shape[0]) if trans_a else (A.shape[0], A.shape[1])
     Kb, N = (B.shape[1], B.shape[0]) if trans_b else (B.shape[0], B.shape[1])
     if K != Kb:
@@ -192,7 +202,7 @@ def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
     Ht = H W (K1), A_l = Ht . a_l, A_r = Ht . a_r, then the fused region (K2).
     Returns (out, GatStash)."""
     h, f = p.heads, p.f
-    H, W = _f32(H, "H"), _f32(W, "W")
+    H, W = _f32_rows(H, "H"), _f32(W, "W")
     if H.shape[0] != g.num_vertices:
         raise TensorError("gat_forward: H rows != num_vertices")
     if W.shape != (H.shape[1], h * f):
@@ -266,7 +276,7 @@ def gat_backward(g: DeviceGraph, H, W, a_l, a_r, stash: GatStash, dOut, p: GatPa
     """GAT layer backward with recomputation:
     region backward (K3+K4, or the fused fast pass) -> LP grads -> dW = H^T dHt (K5),
     dH = dHt W^T (K5)."""
-    H, W = _f32(H, "H"), _f32(W, "W")
+    H, W = _f32_rows(H, "H"), _f32(W, "W")
     dHt, _, _, da_l, da_r, _ = gat_region_backward(g, stash, a_l, a_r, dOut, p, chunk=chunk, mode=mode)
     dW = gemm(H, dHt, trans_a=True, ws=g.ws)
     dH = gemm(dHt, W, trans_b=True, ws=g.ws) if need_dH else None
