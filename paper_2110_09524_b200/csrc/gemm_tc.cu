@@ -19,6 +19,7 @@
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <cstdlib>
 #include <cstring>
 #include <mutex>
 
@@ -70,14 +71,17 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// SM100 shared-memory matrix descriptor, SWIZZLE_128B (layout type 2), version 1.
-__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes) {
+// SM100 shared-memory matrix descriptor, version 1.  layout: 2 = SWIZZLE_128B (K-major
+// operands), 1 = SWIZZLE_128B_BASE32B (the only layout for MN-major 32-bit operands:
+// Swizzle<2,5,2>, atoms of 32 elements x 4 k-rows).
+__device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
+                                              uint32_t layout) {
   uint64_t d = 0;
   d |= (uint64_t)((addr >> 4) & 0x3FFF);
   d |= (uint64_t)((lbo_bytes >> 4) & 0x3FFF) << 16;
   d |= (uint64_t)((sbo_bytes >> 4) & 0x3FFF) << 32;
   d |= (uint64_t)1 << 46;  // version (sm100)
-  d |= (uint64_t)2 << 61;  // SWIZZLE_128B
+  d |= (uint64_t)layout << 61;
   return d;
 }
 
@@ -104,17 +108,20 @@ __device__ __forceinline__ void mma_commit(uint64_t* bar) {
                : "memory");
 }
 
+// Load + wait in ONE asm statement: the destination registers are undefined until
+// tcgen05.wait::ld, so the compiler must not see them as defined in between.
 __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
   asm volatile(
       "tcgen05.ld.sync.aligned.32x32b.x32.b32 "
       "{%0,%1,%2,%3,%4,%5,%6,%7,%8,%9,%10,%11,%12,%13,%14,%15,"
-      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];"
+      "%16,%17,%18,%19,%20,%21,%22,%23,%24,%25,%26,%27,%28,%29,%30,%31}, [%32];\n\t"
+      "tcgen05.wait::ld.sync.aligned;"
       : "=r"(r[0]), "=r"(r[1]), "=r"(r[2]), "=r"(r[3]), "=r"(r[4]), "=r"(r[5]), "=r"(r[6]), "=r"(r[7]), "=r"(r[8]),
         "=r"(r[9]), "=r"(r[10]), "=r"(r[11]), "=r"(r[12]), "=r"(r[13]), "=r"(r[14]), "=r"(r[15]), "=r"(r[16]),
         "=r"(r[17]), "=r"(r[18]), "=r"(r[19]), "=r"(r[20]), "=r"(r[21]), "=r"(r[22]), "=r"(r[23]), "=r"(r[24]),
         "=r"(r[25]), "=r"(r[26]), "=r"(r[27]), "=r"(r[28]), "=r"(r[29]), "=r"(r[30]), "=r"(r[31])
-      : "r"(taddr));
-  asm volatile("tcgen05.wait::ld.sync.aligned;" ::: "memory");
+      : "r"(taddr)
+      : "memory");
 }
 
 // Split a landed stage buffer in place: buf holds raw fp32; write hi (in place) and lo.
@@ -139,7 +146,7 @@ template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk,
-                       int64_t split_stride) {
+                       int64_t split_stride, int dbg) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -213,10 +220,12 @@ __global__ void __launch_bounds__(THREADS, 1)
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
-      // K-major: rows of 128 B, 8-row atoms 1024 B apart (SBO), k-step = +32 B.
-      // MN-major: 32-element x 32-k boxes (4 KB) along MN (LBO), 8-k groups 1024 B apart (SBO), k-step = +1024 B.
-      const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = 1024u, a_step = A_MN ? 1024u : 32u;
-      const uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = 1024u, b_step = B_MN ? 1024u : 32u;
+      // K-major (SW128): rows of 128 B, 8-row atoms 1024 B apart (SBO), k-step = +32 B.
+      // MN-major (SW128_32B): 32-element x 32-k boxes (4 KB) along MN (LBO), 4-k-row atoms
+      // 512 B apart (SBO), k-step (8 rows) = +1024 B.
+      const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u, a_step = A_MN ? 1024u : 32u;
+      const uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
+      const uint32_t a_lay = A_MN ? 1u : 2u, b_lay = B_MN ? 1u : 2u;
       for (int i = 0; i < nk; ++i) {
         const int s = i % S;
         const uint32_t ph = (uint32_t)(i / S) & 1u;
@@ -226,10 +235,10 @@ __global__ void __launch_bounds__(THREADS, 1)
         const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
 #pragma unroll
         for (int k = 0; k < BK / 8; ++k) {
-          const uint64_t dah = smem_desc(ah + k * a_step, a_lbo, a_sbo);
-          const uint64_t dal = smem_desc(al + k * a_step, a_lbo, a_sbo);
-          const uint64_t dbh = smem_desc(bh + k * b_step, b_lbo, b_sbo);
-          const uint64_t dbl = smem_desc(bl + k * b_step, b_lbo, b_sbo);
+          const uint64_t dah = smem_desc(ah + k * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dal = smem_desc(al + k * a_step, a_lbo, a_sbo, a_lay);
+          const uint64_t dbh = smem_desc(bh + k * b_step, b_lbo, b_sbo, b_lay);
+          const uint64_t dbl = smem_desc(bl + k * b_step, b_lbo, b_sbo, b_lay);
           mma_tf32(tmem, dah, dbh, idesc, (i > 0 || k > 0) ? 1u : 0u);
           mma_tf32(tmem, dah, dbl, idesc, 1u);
           mma_tf32(tmem, dal, dbh, idesc, 1u);
@@ -259,7 +268,13 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t r[32];
-      if (nk > 0) {
+      if (dbg == 1) {  // debug: bypass TMEM, write a coordinate pattern
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = __float_as_uint((float)(row * 1000 + c * 32 + j));
+      } else if (dbg == 2) {  // debug: first raw smem words of stage 0 (A hi)
+#pragma unroll
+        for (int j = 0; j < 32; ++j) r[j] = reinterpret_cast<const uint32_t*>(smem)[(lane * 32 + j) & 4095];
+      } else if (nk > 0) {
         tmem_ld32(tmem + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
       } else {
 #pragma unroll
@@ -305,7 +320,7 @@ PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
 
 // 2-D fp32 tensor map: inner dim `inner` (contiguous), outer dim `outer`, row stride `ld` elements.
 bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, int64_t ld, int box_inner,
-              int box_outer) {
+              int box_outer, bool mn_major) {
   auto fn = encode_fn();
   if (!fn) return false;
   cuuint64_t dims[2] = {(cuuint64_t)inner, (cuuint64_t)outer};
@@ -313,7 +328,9 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, 
   cuuint32_t box[2] = {(cuuint32_t)box_inner, (cuuint32_t)box_outer};
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
-                  CU_TENSOR_MAP_INTERLEAVE_NONE, CU_TENSOR_MAP_SWIZZLE_128B, CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
+                  CU_TENSOR_MAP_INTERLEAVE_NONE,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
 }
@@ -323,8 +340,8 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
            int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s) {
   using CF = Cfg<BN>;
   CUtensorMap ma, mb;
-  bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK) : make_map(&ma, A, K, M, lda, BK, BM);
-  ok = ok && (B_MN ? make_map(&mb, B, N, K, ldb, 32, BK) : make_map(&mb, B, K, N, ldb, BK, BN));
+  bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
+  ok = ok && (B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true) : make_map(&mb, B, K, N, ldb, BK, BN, false));
   if (!ok) return fail(GNNCG_ERR_CUDA, "gemm_tc: cuTensorMapEncodeTiled failed");
   auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
@@ -333,7 +350,12 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
     attr_set = true;
   }
   dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
-  kern<<<grid, THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride);
+  static int dbg = -1;
+  if (dbg < 0) {
+    const char* e = getenv("GNNCG_TC_DEBUG");
+    dbg = e ? atoi(e) : 0;
+  }
+  kern<<<grid, THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride, dbg);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }

@@ -57,7 +57,7 @@ def launch_summary(path):
         if len(r) <= mv:
             continue
         v = float(r[mv].replace(",", ""))
-        v = v / 1e6 if r[un] == "nsecond" else (v / 1e3 if r[un] == "usecond" else v)  # -> ms
+        v = v / 1e6 if r[un] in ("ns", "nsecond") else (v / 1e3 if r[un] in ("us", "usecond") else v)  # -> ms
         k = short(r[kn])
         tot[k] += v
         cnt[k] += 1
