@@ -285,17 +285,35 @@ def run_ours(args):
     # --- end-to-end through the public API with host buffers ----------------------------
     e2e = None
     if not args.no_e2e:
+        # Input pipeline of a training loop: step i+1's features are copied host->device on a
+        # copy stream (double buffer) while step i computes; every step still pays its own copy
+        # and reads its loss and parameter gradients back to pinned host memory.
         H_host = torch.empty(H_buf.shape, dtype=torch.float32, pin_memory=True)
         H_host.copy_(H_buf.cpu())
         out_bufs = None
         s, e = torch.cuda.Event(enable_timing=True), torch.cuda.Event(enable_timing=True)
-        H_dev_buf = torch.empty_like(H_buf)
-        H_dev = H_dev_buf[:, :fin]
+        bufs = [torch.empty_like(H_buf), torch.empty_like(H_buf)]
+        copy_stream = torch.cuda.Stream()
+        compute = torch.cuda.current_stream()
+        ready = [torch.cuda.Event(), torch.cuda.Event()]
+        free = [torch.cuda.Event(), torch.cuda.Event()]
         barrier()
         s.record()
-        for _ in range(args.steps):
-            H_dev_buf.copy_(H_host, non_blocking=True)
-            loss, grads = model.train_step(H_dev, lr=lr)
+        copy_stream.wait_event(s)
+        with torch.cuda.stream(copy_stream):
+            bufs[0].copy_(H_host, non_blocking=True)
+            ready[0].record(copy_stream)
+        for i in range(args.steps):
+            b = i % 2
+            if i + 1 < args.steps:
+                with torch.cuda.stream(copy_stream):
+                    if i >= 1:
+                        copy_stream.wait_event(free[1 - b])
+                    bufs[1 - b].copy_(H_host, non_blocking=True)
+                    ready[1 - b].record(copy_stream)
+            compute.wait_event(ready[b])
+            loss, grads = model.train_step(bufs[b][:, :fin], lr=lr)
+            free[b].record(compute)
             res = [loss] + [t for gr in grads for t in (gr.dW, gr.da_l, gr.da_r)]
             if out_bufs is None:
                 out_bufs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
