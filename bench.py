@@ -73,6 +73,8 @@ def gat_kernel_bytes(V: int, E: int, h: int, f: int) -> dict:
         "gat_bwd_dst": E * (4 + 4 * h + 4 * hf) + V * (16 + 12 * h + 4 * hf + 8 * h),
         # K4: nbr, A_r/m/d/c[v], dOut[v] per edge; item, off, A_l/Ht/dA_r in, dHt/dAl out per row
         "gat_bwd_src": E * (4 + 16 * h + 4 * hf) + V * (16 + 8 * h + 8 * hf + 4 * h),
+        # fused fast K4: K4's reads + the dA_r[v] reduction per edge; c from the row dot instead of K3
+        "gat_bwd_src_fused": E * (4 + 16 * h + 4 * hf + 4 * h) + V * (16 + 8 * h + 8 * hf),
     }
 
 
