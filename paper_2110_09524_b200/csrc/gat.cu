@@ -24,137 +24,12 @@
 #include <cfloat>
 
 #include "common.cuh"
+#include "gat_common.cuh"
 
 namespace gnncg_b200 {
 namespace {
 
-constexpr int MAXH = 8;          // compiled head limit
-constexpr int TS = MAXH + 1;     // padded row of the per-warp edge tables (bank-conflict free)
-constexpr int WARPS = 8;         // warps per CTA
-constexpr int THREADS = WARPS * kWarp;
-
-struct WarpSmem {
-  uint32_t nb[kWarp];
-  float t0[kWarp * TS];
-  float t1[kWarp * TS];
-  float t2[kWarp * TS];
-  float red[8 * kWarp];
-  float stat[4][MAXH];
-};
-
-// Split-row partial records are padded to 16 bytes (vector stores).
-__host__ __device__ __forceinline__ int64_t fwd_stride(int h, int f) { return (h * f + 2 * h + 3) / 4 * 4; }
-__host__ __device__ __forceinline__ int64_t src_stride(int h, int f) { return (h * f + h + 3) / 4 * 4; }
-
-struct Item {
-  uint32_t row;
-  uint64_t e0, e1;
-  bool split;
-};
-
-__device__ __forceinline__ Item decode_item(const uint32_t* __restrict__ items, const uint64_t* __restrict__ off,
-                                            int64_t wi, int64_t num_split_items, int chunk) {
-  Item it;
-  it.row = __ldg(items + 2 * wi);
-  const uint32_t ch = __ldg(items + 2 * wi + 1);
-  const uint64_t rb = __ldg(off + it.row), re = __ldg(off + it.row + 1);
-  it.e0 = rb + (uint64_t)ch * (uint64_t)chunk;
-  it.e1 = min(re, it.e0 + (uint64_t)chunk);
-  it.split = wi < num_split_items;
-  return it;
-}
-
-// h per-vertex values p[0..h) into registers (vectorised when possible).
-__device__ __forceinline__ void load_heads(const float* __restrict__ p, int h, float (&v)[MAXH]) {
-  if (h == 8) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
-  } else if (h == 4) {
-    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
-    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
-#pragma unroll
-    for (int k = 4; k < MAXH; ++k) v[k] = 0.f;
-  } else {
-#pragma unroll
-    for (int k = 0; k < MAXH; ++k) v[k] = k < h ? __ldg(p + k) : 0.f;
-  }
-}
-
-// Sum, for head `k`, of red[] entries belonging to that head (vector index
-// range [k*f/VW, (k+1)*f/VW) of the flattened lane-vector numbering).
-template <int VW>
-__device__ __forceinline__ float head_sum(const float* red, int k, int f) {
-  const int per = f / VW;
-  float s = 0.f;
-  for (int q = k * per; q < (k + 1) * per; ++q) s += red[q];
-  return s;
-}
-
-struct GatParams {
-  const uint64_t* off;
-  const uint32_t* nbr;
-  const uint32_t* items;
-  int64_t num_items, num_split_items;
-  int chunk, h, f;
-  float slope;
-  const float *Ht, *Al, *Ar, *m, *d, *c, *dOut, *dAr, *a_l, *a_r;
-  float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
-  float* part;  // split-row partials
-  int64_t row_base, num_local;
-  int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
-};
-
-// ---------------------------------------------------------------------------
-// Shared pieces of the three fused kernels.
-//
-// Per work item the warp walks its edges in 32-edge blocks.  Latency hiding:
-//   * neighbour ids are prefetched two blocks ahead and the per-edge logits one
-//     block ahead, so the dependent id -> logit loads overlap the previous
-//     block's gathers;
-//   * the column phase gathers U rows per step (U * NV * VW floats per lane in
-//     flight) before consuming any of them.
-// ---------------------------------------------------------------------------
-template <int NV>
-struct GatherDepth {
-  static constexpr int U = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);
-};
-
-template <int VW, int NV>
-struct Cols {
-  int col[NV], hd[NV];
-  bool ok[NV];
-  __device__ __forceinline__ Cols(int lane, int hf, int f) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      col[i] = (i * 32 + lane) * VW;
-      ok[i] = col[i] < hf;
-      hd[i] = ok[i] ? col[i] / f : 0;
-    }
-  }
-};
-
-template <int VW, int NV>
-__device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
-#pragma unroll
-  for (int i = 0; i < NV; ++i)
-#pragma unroll
-    for (int q = 0; q < VW; ++q) v[i].x[q] = 0.f;
-}
-
-// Gather row `r` of a row-major [*, hf] matrix at this lane's columns.
-template <int VW, int NV>
-__device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
-                                           Vec<VW> (&x)[NV]) {
-  const float* row = base + r * hf;
-#pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
-    else
-#pragma unroll
-      for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;
-  }
-}
+using namespace gat;
 
 // ---------------------------------------------------------------------------
 // K2: forward, single pass with a block-online softmax (RS1/RS2 folded into the
@@ -893,6 +768,16 @@ int dispatch(Kind kind, const GatParams& p, cudaStream_t s) {
   return GNNCG_OK;
 }
 
+// GNNCG_GAT_TMA=0 selects the register-fed kernels (A/B comparisons); default: TMA-fed when supported.
+bool tma_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_TMA");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 int check_common(const gnncg_index_t* idx, const gnncg_sched_t* sched, int h, int f) {
   GNNCG_REQUIRE(idx && sched, GNNCG_ERR_ARG, "gat: null index or schedule");
   GNNCG_REQUIRE(h >= 1 && h <= MAXH, GNNCG_ERR_UNSUPPORTED, "gat: heads=%d outside [1,%d]", h, MAXH);
@@ -937,7 +822,7 @@ size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* 
   size_t b = fwd_part_bytes(dst_sched, h, f);
   b = std::max(b, dst_part_bytes(dst_sched, h));
   b = std::max(b, src_part_bytes(src_sched, h, f));
-  return align_up(b);
+  return align_up(b) + 256;  // + the work counter of the persistent TMA-fed kernels
 }
 
 int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
@@ -957,7 +842,13 @@ int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int 
   p.h = h; p.f = f; p.slope = slope;
   p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
-  rc = dispatch(Kind::Fwd, p, s);
+  if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
+    int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
+    GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
+    rc = launch_fwd_tma(p, counter, s);
+  } else {
+    rc = dispatch(Kind::Fwd, p, s);
+  }
   if (rc) return rc;
   if (sched->num_split_rows > 0) {
     gat_fwd_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(

@@ -1,0 +1,150 @@
+// SPDX-License-Identifier: Apache-2.0
+// Device-side pieces shared by the fused GAT kernels (gat.cu, gat_tma.cu): work-item
+// decoding, per-warp tables, lane/column mapping, split-row partial strides.
+#pragma once
+
+#include <cfloat>
+
+#include "common.cuh"
+
+namespace gnncg_b200 {
+namespace gat {
+
+constexpr int MAXH = 8;          // compiled head limit
+constexpr int TS = MAXH + 1;     // padded row of the per-warp edge tables (bank-conflict free)
+constexpr int WARPS = 8;         // warps per CTA
+constexpr int THREADS = WARPS * kWarp;
+
+struct WarpSmem {
+  uint32_t nb[kWarp];
+  float t0[kWarp * TS];
+  float t1[kWarp * TS];
+  float t2[kWarp * TS];
+  float red[8 * kWarp];
+  float stat[4][MAXH];
+};
+
+// Split-row partial records are padded to 16 bytes (vector stores).
+__host__ __device__ __forceinline__ int64_t fwd_stride(int h, int f) { return (h * f + 2 * h + 3) / 4 * 4; }
+__host__ __device__ __forceinline__ int64_t src_stride(int h, int f) { return (h * f + h + 3) / 4 * 4; }
+
+struct Item {
+  uint32_t row;
+  uint64_t e0, e1;
+  bool split;
+};
+
+__device__ __forceinline__ Item decode_item(const uint32_t* __restrict__ items, const uint64_t* __restrict__ off,
+                                            int64_t wi, int64_t num_split_items, int chunk) {
+  Item it;
+  it.row = __ldg(items + 2 * wi);
+  const uint32_t ch = __ldg(items + 2 * wi + 1);
+  const uint64_t rb = __ldg(off + it.row), re = __ldg(off + it.row + 1);
+  it.e0 = rb + (uint64_t)ch * (uint64_t)chunk;
+  it.e1 = min(re, it.e0 + (uint64_t)chunk);
+  it.split = wi < num_split_items;
+  return it;
+}
+
+// h per-vertex values p[0..h) into registers (vectorised when possible).
+__device__ __forceinline__ void load_heads(const float* __restrict__ p, int h, float (&v)[MAXH]) {
+  if (h == 8) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 b = __ldg(reinterpret_cast<const float4*>(p + 4));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w; v[4] = b.x; v[5] = b.y; v[6] = b.z; v[7] = b.w;
+  } else if (h == 4) {
+    const float4 a = __ldg(reinterpret_cast<const float4*>(p));
+    v[0] = a.x; v[1] = a.y; v[2] = a.z; v[3] = a.w;
+#pragma unroll
+    for (int k = 4; k < MAXH; ++k) v[k] = 0.f;
+  } else {
+#pragma unroll
+    for (int k = 0; k < MAXH; ++k) v[k] = k < h ? __ldg(p + k) : 0.f;
+  }
+}
+
+// Sum, for head `k`, of red[] entries belonging to that head (vector index
+// range [k*f/VW, (k+1)*f/VW) of the flattened lane-vector numbering).
+template <int VW>
+__device__ __forceinline__ float head_sum(const float* red, int k, int f) {
+  const int per = f / VW;
+  float s = 0.f;
+  for (int q = k * per; q < (k + 1) * per; ++q) s += red[q];
+  return s;
+}
+
+struct GatParams {
+  const uint64_t* off;
+  const uint32_t* nbr;
+  const uint32_t* items;
+  int64_t num_items, num_split_items;
+  int chunk, h, f;
+  float slope;
+  const float *Ht, *Al, *Ar, *m, *d, *c, *dOut, *dAr, *a_l, *a_r;
+  float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
+  float* part;  // split-row partials
+  int64_t row_base, num_local;
+  int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
+};
+
+// ---------------------------------------------------------------------------
+// Shared pieces of the three fused kernels.
+//
+// Per work item the warp walks its edges in 32-edge blocks.  Latency hiding:
+//   * neighbour ids are prefetched two blocks ahead and the per-edge logits one
+//     block ahead, so the dependent id -> logit loads overlap the previous
+//     block's gathers;
+//   * the column phase gathers U rows per step (U * NV * VW floats per lane in
+//     flight) before consuming any of them.
+// ---------------------------------------------------------------------------
+template <int NV>
+struct GatherDepth {
+  static constexpr int U = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);
+};
+
+template <int VW, int NV>
+struct Cols {
+  int col[NV], hd[NV];
+  bool ok[NV];
+  __device__ __forceinline__ Cols(int lane, int hf, int f) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      col[i] = (i * 32 + lane) * VW;
+      ok[i] = col[i] < hf;
+      hd[i] = ok[i] ? col[i] / f : 0;
+    }
+  }
+};
+
+template <int VW, int NV>
+__device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+#pragma unroll
+    for (int q = 0; q < VW; ++q) v[i].x[q] = 0.f;
+}
+
+// Gather row `r` of a row-major [*, hf] matrix at this lane's columns.
+template <int VW, int NV>
+__device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
+                                           Vec<VW> (&x)[NV]) {
+  const float* row = base + r * hf;
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
+    else
+#pragma unroll
+      for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;
+  }
+}
+
+
+}  // namespace gat
+
+// TMA-fed kernels (gat_tma.cu)
+namespace gat {
+bool tma_fwd_supported(int h, int f);
+size_t tma_smem_bytes(int h, int f);
+int launch_fwd_tma(const GatParams& p, int* counter, cudaStream_t s);
+}  // namespace gat
+}  // namespace gnncg_b200
