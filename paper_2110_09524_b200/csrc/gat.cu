@@ -37,8 +37,8 @@ using namespace gat;
 // accumulators rescaled by exp(m_old - m_new), and the block's unnormalised
 // weights exp(s - m_new) written to the per-warp table.
 // ---------------------------------------------------------------------------
-template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatParams p) {
+template <int VW, int NV, int OCC>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(GatParams p) {
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
@@ -47,12 +47,16 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatPa
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
-  constexpr int U = GatherDepth<NV>::U;
+  constexpr int U = GatherDepth<NV, OCC>::U;
 
-  if (lane < h) sm.stat[3][lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);  // A_r[v], read per edge from smem
-  float M[MAXH], Sl[MAXH];
+  // Per-warp shared state (keeps registers for the gathers): stat[3] = A_r[v], stat[0] = running
+  // max per head (warp-uniform), t1[lane][k] = this lane's running exp-sum partial.
+  if (lane < h) {
+    sm.stat[3][lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);
+    sm.stat[0][lane] = -FLT_MAX;
+  }
 #pragma unroll
-  for (int k = 0; k < MAXH; ++k) { M[k] = -FLT_MAX; Sl[k] = 0.f; }
+  for (int k = 0; k < MAXH; ++k) sm.t1[lane * TS + k] = 0.f;
   const Cols<VW, NV> cols(lane, hf, f);
   Vec<VW> acc[NV];
   zero(acc);
@@ -67,17 +71,19 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatPa
   for (uint64_t base = e0; base < e1; base += 32) {
     const int n = (int)min((uint64_t)32, e1 - base);
     const bool valid = lane < n;
+    __syncwarp();
 #pragma unroll
     for (int k = 0; k < MAXH; ++k) {
       if (k < h) {
         const float s = valid ? lrelu(al[k] + sm.stat[3][k], slope) : -FLT_MAX;
-        const float mnew = fmaxf(M[k], warp_max(s));
-        const float sc = __expf(M[k] - mnew);
+        const float mold = sm.stat[0][k];
+        const float mnew = fmaxf(mold, warp_max(s));
+        const float sc = __expf(mold - mnew);
         const float pk = valid ? __expf(s - mnew) : 0.f;
-        M[k] = mnew;
-        Sl[k] = fmaf(Sl[k], sc, pk);
+        sm.t1[lane * TS + k] = fmaf(sm.t1[lane * TS + k], sc, pk);
         sm.t0[lane * TS + k] = pk;
-        if (lane == 0) sm.stat[2][k] = sc;
+        __syncwarp();
+        if (lane == 0) { sm.stat[2][k] = sc; sm.stat[0][k] = mnew; }
       }
     }
     sm.nb[lane] = u_cur;
@@ -120,11 +126,15 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatPa
   }
 
   const bool empty = e0 == e1;
+  __syncwarp();
 #pragma unroll
   for (int k = 0; k < MAXH; ++k) {
     if (k < h) {
-      const float S = warp_sum(Sl[k]);
-      if (lane == 0) { sm.stat[0][k] = empty ? 0.f : M[k]; sm.stat[1][k] = S; }
+      const float S = warp_sum(sm.t1[lane * TS + k]);
+      if (lane == 0) {
+        if (empty) sm.stat[0][k] = 0.f;
+        sm.stat[1][k] = S;
+      }
     }
   }
   __syncwarp();
@@ -162,8 +172,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_fwd_kernel(GatPa
 // Q = sum gate*alpha,  dA_r = P - c Q  (g = dOut[v]; the softmax weights of a
 // row sum to one, so no large cancellation).
 // ---------------------------------------------------------------------------
-template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_dst_kernel(GatParams p) {
+template <int VW, int NV, int OCC>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_dst_kernel(GatParams p) {
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
@@ -172,7 +182,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_dst_kernel(G
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
-  constexpr int U = GatherDepth<NV>::U;
+  constexpr int U = GatherDepth<NV, OCC>::U;
 
   if (lane < h) {
     const int64_t r = (int64_t)it.row * h + lane;
@@ -289,8 +299,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_dst_kernel(G
 // avoid cancellation on hub sources), then the LP epilogue
 // dHt[u] += dA_l[u] (x) a_l + dA_r[u] (x) a_r.
 // ---------------------------------------------------------------------------
-template <int VW, int NV>
-__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_kernel(GatParams p) {
+template <int VW, int NV, int OCC>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_kernel(GatParams p) {
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
@@ -300,7 +310,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_kernel(G
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
   const int64_t u = it.row;
-  constexpr int U = GatherDepth<NV>::U;
+  constexpr int U = GatherDepth<NV, OCC>::U;
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
   float dal_acc = 0.f;  // lane k < h: dA_l[u, k]
@@ -440,9 +450,9 @@ __device__ __forceinline__ void butterfly(float* v, int lane) {
   }
 }
 
-template <int VW, int NV, int PER>
-__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : 2) gat_bwd_src_fast_kernel(GatParams p) {
-  constexpr int U = GatherDepth<NV>::U;
+template <int VW, int NV, int PER, int OCC>
+__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_kernel(GatParams p) {
+  constexpr int U = GatherDepth<NV, OCC>::U;
   constexpr int NVAL = U * NV, NOUT = NVAL / PER;
   static_assert(NVAL % PER == 0, "fast K4 needs U*NV to be a multiple of the lanes per head");
   __shared__ WarpSmem smem[WARPS];
@@ -721,27 +731,33 @@ __global__ void attn_grad_reduce_kernel(int nb, int hf, const float* __restrict_
 // ---------------------------------------------------------------------------
 enum class Kind { Fwd, BwdDst, BwdSrc, BwdSrcFast };
 
-template <int VW, int NV>
+template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
-  constexpr int NVAL = GatherDepth<NV>::U * NV;
+  constexpr int NVAL = GatherDepth<NV, OCC>::U * NV;
   switch (p.f / VW) {
-    case 1: gat_bwd_src_fast_kernel<VW, NV, 1><<<grid, THREADS, 0, s>>>(p); break;
-    case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2><<<grid, THREADS, 0, s>>>(p); break;
-    case 4: if constexpr (NVAL % 4 == 0) gat_bwd_src_fast_kernel<VW, NV, 4><<<grid, THREADS, 0, s>>>(p); break;
-    case 8: if constexpr (NVAL % 8 == 0) gat_bwd_src_fast_kernel<VW, NV, 8><<<grid, THREADS, 0, s>>>(p); break;
-    case 16: if constexpr (NVAL % 16 == 0) gat_bwd_src_fast_kernel<VW, NV, 16><<<grid, THREADS, 0, s>>>(p); break;
+    case 1: gat_bwd_src_fast_kernel<VW, NV, 1, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case 4: if constexpr (NVAL % 4 == 0) gat_bwd_src_fast_kernel<VW, NV, 4, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case 8: if constexpr (NVAL % 8 == 0) gat_bwd_src_fast_kernel<VW, NV, 8, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case 16: if constexpr (NVAL % 16 == 0) gat_bwd_src_fast_kernel<VW, NV, 16, OCC><<<grid, THREADS, 0, s>>>(p); break;
     default: break;  // excluded by gnncg_gat_fast_supported
+  }
+}
+
+template <int VW, int NV, int OCC>
+void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
+  switch (kind) {
+    case Kind::Fwd: gat_fwd_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::BwdSrcFast: launch_fast<VW, NV, OCC>(p, grid, s); break;
   }
 }
 
 template <int VW, int NV>
 void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
-  switch (kind) {
-    case Kind::Fwd: gat_fwd_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
-    case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
-    case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV><<<grid, THREADS, 0, s>>>(p); break;
-    case Kind::BwdSrcFast: launch_fast<VW, NV>(p, grid, s); break;
-  }
+  if (gat_occupancy() >= 4) launch_occ<VW, NV, 4>(kind, p, grid, s);
+  else launch_occ<VW, NV, 2>(kind, p, grid, s);
 }
 
 template <int VW>
@@ -768,12 +784,27 @@ int dispatch(Kind kind, const GatParams& p, cudaStream_t s) {
   return GNNCG_OK;
 }
 
-// GNNCG_GAT_TMA=0 selects the register-fed kernels (A/B comparisons); default: TMA-fed when supported.
+}  // namespace
+
+int gat::gat_occupancy() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_OCC");
+    v = (e && atoi(e) == 2) ? 2 : 4;
+  }
+  return v;
+}
+
+namespace {
+
+// GNNCG_GAT_TMA=1 selects the TMA-fed forward (gat_tma.cu).  Default off: measured slower
+// (17.9 vs 9.5 ms at the Reddit shape) -- the 8 persistent warps per SM it can host next
+// to its shared-memory ring do not issue enough independent row requests.
 bool tma_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("GNNCG_GAT_TMA");
-    v = (e && e[0] == '0') ? 0 : 1;
+    v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
 }
@@ -927,7 +958,7 @@ int gnncg_gat_fast_supported(int h, int f) {
   if (h < 1 || h > MAXH || per < 1 || per > 16 || (per & (per - 1)) != 0 || h * f > 256 * vw) return 0;
   const int nvec = (int)ceil_div(h * f / vw, 32);
   const int nv = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : 8;
-  const int u = nv <= 2 ? 8 : (nv == 4 ? 4 : 2);
+  const int u = gat_occupancy() >= 4 ? (nv <= 2 ? 4 : (nv == 4 ? 2 : 1)) : (nv <= 2 ? 8 : (nv == 4 ? 4 : 2));
   return (u * nv) % per == 0;
 }
 

@@ -97,10 +97,17 @@ struct GatParams {
 //   * the column phase gathers U rows per step (U * NV * VW floats per lane in
 //     flight) before consuming any of them.
 // ---------------------------------------------------------------------------
-template <int NV>
+// OCC = CTAs per SM the kernel is built for (launch bound): 2 -> 16 warps/SM with deep
+// per-warp gathers; 4 -> 32 warps/SM (<= 64 registers) with shallower ones.  More warps
+// win for Zipf-distributed gathers (scripts/gather_bench.cu: 9 -> 16 TB/s from 16 to 32
+// warps/SM at equal bytes in flight).
+template <int NV, int OCC = 2>
 struct GatherDepth {
-  static constexpr int U = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);
+  static constexpr int U = OCC >= 4 ? (NV <= 2 ? 4 : (NV == 4 ? 2 : 1)) : (NV <= 2 ? 8 : (NV == 4 ? 4 : 2));
 };
+
+// Runtime choice of OCC (GNNCG_GAT_OCC=2|4, default 4).
+int gat_occupancy();
 
 template <int VW, int NV>
 struct Cols {
