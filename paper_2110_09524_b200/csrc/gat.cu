@@ -790,7 +790,7 @@ int gat::gat_occupancy() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("GNNCG_GAT_OCC");
-    v = (e && atoi(e) == 2) ? 2 : 4;
+    v = (e && atoi(e) == 4) ? 4 : 2;
   }
   return v;
 }

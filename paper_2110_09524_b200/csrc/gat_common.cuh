@@ -106,7 +106,7 @@ struct GatherDepth {
   static constexpr int U = OCC >= 4 ? (NV <= 2 ? 4 : (NV == 4 ? 2 : 1)) : (NV <= 2 ? 8 : (NV == 4 ? 4 : 2));
 };
 
-// Runtime choice of OCC (GNNCG_GAT_OCC=2|4, default 4).
+// Runtime choice of OCC (GNNCG_GAT_OCC=2|4, default 2: measured faster at the Reddit shape).
 int gat_occupancy();
 
 template <int VW, int NV>
