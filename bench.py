@@ -49,6 +49,8 @@ def parse():
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk", type=int, default=None)
     ap.add_argument("--scale", type=float, default=1.0, help="shrink V and E (debug only)")
+    ap.add_argument("--config", default="reddit", choices=["reddit", "cora", "edgeconv20", "edgeconv40", "monet", "c5"],
+                    help="reddit = the headline (BASELINE configs[1]); the others are configs[0,2,3,4]")
     return ap.parse_args()
 
 
@@ -76,6 +78,108 @@ def gat_kernel_bytes(V: int, E: int, h: int, f: int) -> dict:
         # fused fast K4: K4's reads + the dA_r[v] reduction per edge; c from the row dot instead of K3
         "gat_bwd_src_fused": E * (4 + 16 * h + 4 * hf + 4 * h) + V * (16 + 8 * h + 8 * hf),
     }
+
+
+def edgeconv_kernel_bytes(V: int, E: int, C: int) -> dict:
+    """K6: nbr + eid + Th[u] row per edge; offsets, Th[v], Ph[v], out, argmax per row.
+    K7 (inverse argmax over csc_src): nbr + eid + argmax[v] + g[v] rows per edge; g[u], dTh, dPh per row."""
+    return {"edgeconv_fwd": E * (8 + 4 * C) + V * (8 + 16 * C),
+            "edgeconv_bwd": E * (8 + 8 * C) + V * (16 + 12 * C)}
+
+
+def gmm_kernel_bytes(V: int, E: int, K: int, r: int, f: int) -> dict:
+    """K8 forward: nbr + Y[u] (hW, pl) per edge; pr[v] in, out per row.  Backward: both passes
+    (csr_dst: nbr + Y[u]; csc_src: nbr + pr[v] + dOut[v]) plus the dY writes."""
+    return {"gmm_fwd": E * (4 + 4 * (K * f + r)) + V * (8 + 4 * r + 4 * f),
+            "gmm_bwd": E * (8 + 4 * (K * f + r) + 4 * (r + f)) + V * (16 + 8 * (K * f + 2 * r) + 4 * f)}
+
+
+def build_workload(args, dev, world: int, rank: int) -> dict:
+    """Graph + model + input features of the selected config, built on the device."""
+    import numpy as np
+    import torch
+
+    from paper_2110_09524_b200.graph import DeviceGraph, knn_edges, uniform_edges
+    from paper_2110_09524_b200.models import GAT, EdgeConvNet, MoNet
+
+    t0 = time.perf_counter()
+    cfg = args.config
+    if world > 1 and cfg not in ("reddit", "c5"):
+        raise SystemExit(f"--config {cfg} is single-GPU only")
+    gen = torch.Generator(device=dev)
+    gen.manual_seed(1234 + rank)
+
+    def features(rows, fin):
+        ld = (fin + 3) // 4 * 4  # 16-byte aligned rows: the TMA tensor-core GEMM needs them
+        return torch.rand(rows, ld, generator=gen, device=dev).mul_(2).sub_(1)
+
+    if cfg in ("reddit", "c5"):
+        if cfg == "reddit":
+            V, E, offset, dims = REDDIT["V"], REDDIT["E"], REDDIT["offset"], REDDIT["dims"]
+            desc = "GAT 2-layer fwd+bwd+SGD, Reddit-shaped (BASELINE configs[1])"
+        else:
+            V, E, offset, dims = 10_000_000, 1_000_000_000, 10_000, [(128, 8, 16)] * 3
+            desc = "GAT 3-layer fwd+bwd+SGD, power-law 10M nodes / 1B edges, 128-dim (BASELINE configs[4])"
+        V, E, offset = int(V * args.scale), int(E * args.scale), max(1, int(offset * args.scale))
+        if world > 1:
+            from paper_2110_09524_b200.dist import PartitionedGAT, partitioned_chung_lu
+
+            lg = partitioned_chung_lu(V * world, E * world, offset=offset * world, seed=0, rank=rank, world=world,
+                                      device=dev)
+            model = PartitionedGAT(lg, dims, seed=1, chunk=args.chunk)
+            V_loc, E_loc = lg.num_local, int(lg.csr.num_edges)
+        else:
+            g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
+            model = GAT(g, dims, seed=1, chunk=args.chunk)
+            V_loc, E_loc = V, E
+        h, f = dims[0][1], dims[0][2]
+        wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E * world,
+                  layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f),
+                  config={"workload": desc, "V": V * world, "E": E * world, "layers": len(dims),
+                          "dims": ", ".join(f"{a}->{b}x{c}" for a, b, c in dims),
+                          "graph": f"Chung-Lu w_i=2^40/(i+{offset * world}), seed 0",
+                          "l2": "inputs larger than L2 (features and index exceed 126 MB)"})
+    elif cfg == "cora":
+        V, E, dims = 2708, 10556, [(1433, 8, 8)]
+        src, dst = uniform_edges(V, E, seed=0)
+        g = DeviceGraph.from_edges(V, src, dst, device=dev)
+        wl = dict(model=GAT(g, dims, seed=1, chunk=args.chunk), H_buf=features(V, 1433), fin=1433, E_total=E,
+                  layers=1, bytes=gat_kernel_bytes(V, E, 8, 8),
+                  config={"workload": "GAT 1-layer fwd+bwd+SGD, Cora-shaped (BASELINE configs[0])", "V": V, "E": E,
+                          "layers": 1, "dims": "1433->8x8", "graph": "uniform random, seed 0",
+                          "l2": "working set fits L2 (latency-bound; no flush)"})
+    elif cfg.startswith("edgeconv"):
+        k = int(cfg[len("edgeconv"):])
+        clouds, points = 32, 1024
+        src, dst = knn_edges(clouds, points, k, seed=0)
+        V, E = clouds * points, int(src.size)
+        dims = [64, 64, 64, 128, 256]  # the paper's DGCNN stack (PAPER.md:409) on 64-dim inputs
+        g = DeviceGraph.from_edges(V, src, dst, device=dev)
+        per = [edgeconv_kernel_bytes(V, E, c) for c in dims[1:]]
+        byts = {n: sum(p[n] for p in per) / len(per) for n in per[0]}
+        wl = dict(model=EdgeConvNet(g, dims, seed=1), H_buf=features(V, 64), fin=64, E_total=E,
+                  layers=len(dims) - 1, bytes=byts,
+                  config={"workload": f"EdgeConv 4-layer fwd+bwd+SGD, ModelNet40-shaped kNN batch 32x1024, k={k} "
+                                      "(BASELINE configs[2])", "V": V, "E": E, "layers": len(dims) - 1,
+                          "dims": "64->64->64->128->256", "graph": f"kNN k={k} of 32 uniform clouds, seed 0",
+                          "l2": "working set fits L2 (no flush)"})
+    elif cfg == "monet":
+        V, E, K, r = 19717, 88648, 3, 3
+        src, dst = uniform_edges(V, E, seed=0)
+        g = DeviceGraph.from_edges(V, src, dst, device=dev)
+        dims = [500, 16, 16]
+        wl = dict(model=MoNet(g, dims, K, r, seed=1), H_buf=features(V, 500), fin=500, E_total=E,
+                  layers=len(dims) - 1, bytes=gmm_kernel_bytes(V, E, K, r, 16),
+                  config={"workload": "MoNet/GMMConv 2-layer fwd+bwd+SGD, Pubmed-shaped, K=3, r=3 "
+                                      "(BASELINE configs[3])", "V": V, "E": E, "layers": 2,
+                          "dims": "500->16->16", "graph": "uniform random, seed 0",
+                          "l2": "working set fits L2 (latency-bound; no flush)"})
+    else:
+        raise SystemExit(f"unknown config {cfg}")
+    torch.cuda.synchronize()
+    wl["build_s"] = time.perf_counter() - t0
+    _ = np
+    return wl
 
 
 # ----------------------------------------------------------------------------- clocks
@@ -200,35 +304,10 @@ def run_ours(args):
     dev = torch.device("cuda", local)
     if world > 1:
         dist.init_process_group("nccl", device_id=dev)
-    V = int(REDDIT["V"] * args.scale)
-    E = int(REDDIT["E"] * args.scale)
-    offset = max(1, int(REDDIT["offset"] * args.scale))
-    dims = REDDIT["dims"]
-    layers = len(dims)
-
-    t_build = time.perf_counter()
-    if world > 1:
-        from paper_2110_09524_b200.dist import PartitionedGAT, partitioned_chung_lu
-
-        pg = partitioned_chung_lu(V * world, E * world, offset=offset * world, seed=0, rank=rank, world=world,
-                                  device=dev)
-        model = PartitionedGAT(pg, dims, seed=1, chunk=args.chunk)
-        E_total = E * world
-        V_local = pg.num_local
-    else:
-        g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
-        model = GAT(g, dims, seed=1, chunk=args.chunk)
-        E_total = E
-        V_local = V
-    gen = torch.Generator(device=dev)
-    gen.manual_seed(1234 + rank)
-    # features stored with a 16-byte aligned row stride (602 -> 604): the TMA tensor-core GEMM needs it
-    fin = dims[0][0]
-    ld = (fin + 3) // 4 * 4
-    H_buf = torch.rand(V_local, ld, generator=gen, device=dev).mul_(2).sub_(1)
+    wl = build_workload(args, dev, world, rank)
+    model, H_buf, fin, E_total, layers = wl["model"], wl["H_buf"], wl["fin"], wl["E_total"], wl["layers"]
     H = H_buf[:, :fin]
-    torch.cuda.synchronize()
-    build_s = time.perf_counter() - t_build
+    build_s = wl["build_s"]
 
     def barrier():
         if world > 1:
@@ -265,8 +344,7 @@ def run_ours(args):
 
     # --- per-kernel roofline (rank 0's graph; bytes summed over the layers) -----------
     peak, peak_src = measured_peaks()
-    h, f = dims[0][1], dims[0][2]
-    per_launch = gat_kernel_bytes(V_local if world > 1 else V, E, h, f)
+    per_launch = wl["bytes"]
     kernels = {}
     for name, (tot_ms, cnt) in sorted(totals.items()):
         k = {"ms_per_launch": tot_ms / max(cnt, 1), "launches": cnt, "share_of_step": tot_ms / ms}
@@ -333,7 +411,7 @@ def run_ours(args):
                "ms_per_step": ems / args.steps}
 
     cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline:
+    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "reddit":
         gteps, dt, info = cpu_sample_step()
         cpu = {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port", "sample": info["sample"],
                "s_per_step": dt}
@@ -343,11 +421,7 @@ def run_ours(args):
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
                 "vs_baseline": None, "dtype": "f32", "data": "synthetic (Chung-Lu graph, uniform features, "
                 "random-init weights)",
-                "config": {"workload": "GAT 2-layer fwd+bwd+SGD, Reddit-shaped (BASELINE configs[1])",
-                           "V": V * world, "E": E_total, "layers": layers, "dims": "602->8x32, 256->8x32",
-                           "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0", "parallelism":
-                           f"row-partition x{world}" if world > 1 else "single GPU",
-                           "l2": "inputs larger than L2 (H 561 MB, index 912 MB per direction)",
+                "config": {**wl["config"], "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "gpu_launches": launches, "clocks": clk}

@@ -92,3 +92,84 @@ class GAT:
         grads = self.backward(xs, stashes, self.seed_grad(out) if dOut is None else dOut)
         self.sgd(grads, lr)
         return self.loss[:1], grads
+
+
+class EdgeConvNet:
+    """EdgeConv stack (the paper's DGCNN setting uses layers {64,64,128,256},
+    PAPER.md:409): dims = [F0, F1, ...]; layer l maps F_l -> F_{l+1}; identity between layers,
+    loss = sum of exits, SGD."""
+
+    def __init__(self, g: DeviceGraph, dims, seed: int = 0):
+        from .ops import edgeconv_backward, edgeconv_forward  # noqa: F401
+
+        self.g = g
+        dev = g.device
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.layers = [(init_uniform(a, b, gen, dev), init_uniform(a, b, gen, dev)) for a, b in zip(dims[:-1], dims[1:])]
+        self.loss = torch.zeros(4, device=dev)
+        self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
+
+    def train_step(self, H: torch.Tensor, lr: float = 0.0):
+        from .ops import edgeconv_backward, edgeconv_forward
+
+        xs, stashes = [H], []
+        for Th, Ph in self.layers:
+            out, st = edgeconv_forward(self.g, xs[-1], Th, Ph)
+            xs.append(out)
+            stashes.append(st)
+        out = xs[-1]
+        call("gnncg_sum", out.numel(), _ptr(out), _ptr(self.loss), _ptr(self._sum_ws), self._sum_ws.numel(), _stream())
+        g = torch.empty_like(out)
+        call("gnncg_fill", g.numel(), 1.0, _ptr(g), _stream())
+        grads = [None] * len(self.layers)
+        for i in reversed(range(len(self.layers))):
+            Th, Ph = self.layers[i]
+            dH, dTh, dPh = edgeconv_backward(self.g, xs[i], Th, Ph, stashes[i], g, need_dH=i > 0)
+            grads[i] = (dTh, dPh)
+            g = dH
+        for (Th, Ph), (dTh, dPh) in zip(self.layers, grads):
+            call("gnncg_sgd_update", Th.numel(), lr, _ptr(dTh), _ptr(Th), _stream())
+            call("gnncg_sgd_update", Ph.numel(), lr, _ptr(dPh), _ptr(Ph), _stream())
+        return self.loss[:1], grads
+
+
+class MoNet:
+    """GMMConv stack: dims = [F0, F1, ...] with K kernels and r pseudo-coordinate
+    dimensions per layer; identity between layers, loss = sum of exits, SGD on W, P_l, P_r, mu, sinv."""
+
+    def __init__(self, g: DeviceGraph, dims, K: int, r: int, seed: int = 0):
+        self.g, self.K, self.r = g, K, r
+        dev = g.device
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.layers = []
+        for a, b in zip(dims[:-1], dims[1:]):
+            sinv = torch.rand(K, r, generator=gen, device=dev).add_(0.5)
+            self.layers.append([init_uniform(a, K * b, gen, dev), init_uniform(a, r, gen, dev),
+                                init_uniform(a, r, gen, dev), init_uniform(K, r, gen, dev), sinv, b])
+        self.loss = torch.zeros(4, device=dev)
+        self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
+
+    def train_step(self, H: torch.Tensor, lr: float = 0.0):
+        from .ops import gmm_backward, gmm_forward
+
+        xs, stashes = [H], []
+        for W, Pl, Pr, mu, sinv, f in self.layers:
+            out, st = gmm_forward(self.g, xs[-1], W, Pl, Pr, mu, sinv, self.K, self.r, f)
+            xs.append(out)
+            stashes.append(st)
+        out = xs[-1]
+        call("gnncg_sum", out.numel(), _ptr(out), _ptr(self.loss), _ptr(self._sum_ws), self._sum_ws.numel(), _stream())
+        g = torch.empty_like(out)
+        call("gnncg_fill", g.numel(), 1.0, _ptr(g), _stream())
+        grads = [None] * len(self.layers)
+        for i in reversed(range(len(self.layers))):
+            W, Pl, Pr, mu, sinv, f = self.layers[i]
+            res = gmm_backward(self.g, xs[i], W, Pl, Pr, mu, sinv, self.K, self.r, f, stashes[i], g, need_dH=i > 0)
+            grads[i] = res[1:]
+            g = res[0]
+        for L, gr in zip(self.layers, grads):
+            for p, dp in zip(L[:5], gr):
+                call("gnncg_sgd_update", p.numel(), lr, _ptr(dp.contiguous()), _ptr(p), _stream())
+        return self.loss[:1], grads

@@ -300,8 +300,9 @@ def edgeconv_region_forward(g: DeviceGraph, Th, Ph):
     V, C_ = Th.shape
     out = torch.empty(V, C_, device=Th.device)
     amax = torch.empty(V, C_, dtype=torch.int32, device=Th.device)
-    call("gnncg_edgeconv_fwd", g.csr_dst.struct(), C_, 0, _ptr(Th), Th.stride(0), _ptr(Ph), Ph.stride(0), _ptr(out),
-         _ptr(amax), _stream())
+    with PROBE("edgeconv_fwd"):
+        call("gnncg_edgeconv_fwd", g.csr_dst.struct(), C_, 0, _ptr(Th), Th.stride(0), _ptr(Ph), Ph.stride(0), _ptr(out),
+             _ptr(amax), _stream())
     return out, amax
 
 
@@ -324,8 +325,9 @@ def edgeconv_backward(g: DeviceGraph, H, Theta, Phi, stash: EdgeConvStash, dOut,
     dOut = _f32(dOut, "dOut")
     V = g.num_vertices
     dY = torch.empty(V, 2 * C_, device=H.device)
-    call("gnncg_edgeconv_bwd", g.csc_src.struct(), g.csr_dst.struct(), C_, _ptr(stash.argmax), _ptr(dOut),
-         _ptr(dY), dY.stride(0), _ptr(dY) + 4 * C_, dY.stride(0), _stream())
+    with PROBE("edgeconv_bwd"):
+        call("gnncg_edgeconv_bwd", g.csc_src.struct(), g.csr_dst.struct(), C_, _ptr(stash.argmax), _ptr(dOut),
+             _ptr(dY), dY.stride(0), _ptr(dY) + 4 * C_, dY.stride(0), _stream())
     dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
     dH = gemm(dY, torch.cat([Theta, Phi], dim=1), trans_b=True, ws=g.ws) if need_dH else None
     return dH, dWcat[:, :C_].contiguous(), dWcat[:, C_:].contiguous()
@@ -351,8 +353,9 @@ def gmm_forward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K: int, r: int, f: int
     _shape(sinv, (K, r), "sinv")
     Y = gemm(H, torch.cat([_f32(W, "W"), _f32(P_l, "P_l"), _f32(P_r, "P_r")], dim=1), ws=g.ws)
     out = torch.empty(g.num_vertices, f, device=H.device)
-    call("gnncg_gmm_fwd", g.csr_dst.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(_f32(mu, "mu")),
-         _ptr(_f32(sinv, "sinv")), _ptr(out), _stream())
+    with PROBE("gmm_fwd"):
+        call("gnncg_gmm_fwd", g.csr_dst.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(_f32(mu, "mu")),
+             _ptr(_f32(sinv, "sinv")), _ptr(out), _stream())
     return out, GmmStash(Y)
 
 
@@ -367,8 +370,9 @@ def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmSt
     dsinv = torch.empty(K, r, device=H.device)
     need = _lib.lib().gnncg_gmm_bwd_workspace(g.csr_dst.struct(), K, r)
     wp, wn = g.ws.get(need)
-    call("gnncg_gmm_bwd", g.csr_dst.struct(), g.csc_src.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(mu),
-         _ptr(sinv), _ptr(dOut), _ptr(dY), _ptr(dmu), _ptr(dsinv), wp, wn, _stream())
+    with PROBE("gmm_bwd"):
+        call("gnncg_gmm_bwd", g.csr_dst.struct(), g.csc_src.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(mu),
+             _ptr(sinv), _ptr(dOut), _ptr(dY), _ptr(dmu), _ptr(dsinv), wp, wn, _stream())
     dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
     dH = gemm(dY, torch.cat([W, P_l, P_r], dim=1), trans_b=True, ws=g.ws) if need_dH else None
     Kf = K * f
