@@ -24,7 +24,7 @@ __global__ void __launch_bounds__(NT, 2)
   __shared__ __align__(16) float As[2][BK][BM];
   __shared__ __align__(16) float Bs[2][BK][BN];
   const int t = threadIdx.x;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;  // M tiles on x: no 65535 limit
   const int64_t kb = (int64_t)blockIdx.z * kchunk;
   const int64_t ke = min(K, kb + kchunk);
   float* Cz = C + (int64_t)blockIdx.z * split_stride;
@@ -229,7 +229,7 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
   const int splits = choose_splits(M, N, K);
   const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), BK) * BK : std::max<int64_t>(K, 1);
   const int real_splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;
-  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)real_splits);
+  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)real_splits);
   float* out = splits > 1 ? static_cast<float*>(ws) : C;
   const int64_t ldo = splits > 1 ? N : ldc;
   const int64_t stride = splits > 1 ? M * N : 0;

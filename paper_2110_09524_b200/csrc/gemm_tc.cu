@@ -159,7 +159,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 1);
 
   const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
-  const int64_t m0 = (int64_t)blockIdx.y * BM, n0 = (int64_t)blockIdx.x * BN;
+  const int64_t m0 = (int64_t)blockIdx.x * BM, n0 = (int64_t)blockIdx.y * BN;  // M tiles on x: no 65535 limit
   const int64_t kb0 = (int64_t)blockIdx.z * kchunk;
   const int64_t kb1 = min(K, kb0 + kchunk);
   const int nk = (int)((kb1 - kb0 + BK - 1) / BK);
@@ -349,7 +349,7 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
     GNNCG_CUDA_TRY(cudaFuncSetAttribute(kern, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
     attr_set = true;
   }
-  dim3 grid((unsigned)ceil_div(N, BN), (unsigned)ceil_div(M, BM), (unsigned)splits);
+  dim3 grid((unsigned)ceil_div(M, BM), (unsigned)ceil_div(N, BN), (unsigned)splits);
   static int dbg = -1;
   if (dbg < 0) {
     const char* e = getenv("GNNCG_TC_DEBUG");

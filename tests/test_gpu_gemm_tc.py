@@ -58,3 +58,17 @@ def test_tc_and_simt_agree(cuda):
         subprocess.run([sys.executable, "-c", code, path], cwd=root, env=env, check=True, timeout=300)
         outs.append(np.load(path))
     assert np.abs(outs[0] - outs[1]).max() < 2e-5 * max(1.0, np.abs(outs[1]).max())
+
+
+@pytest.mark.parametrize("tc", ["tc", "simt"])
+def test_gemm_tall_m_beyond_grid_y(cuda, tc, monkeypatch):
+    """M > 65535 * 128 rows (C5: 10M vertices): M tiles are on gridDim.x."""
+    M, N, K = 9_000_000, 16, 16
+    if tc == "simt":
+        A = torch.ones(M, K + 1, device=cuda)[:, :K]  # unaligned ld -> CUDA-core path
+    else:
+        A = torch.ones(M, K, device=cuda)
+    B = torch.full((K, N), 0.5, device=cuda)
+    C = gemm(A, B)
+    torch.cuda.synchronize()
+    assert C.min().item() == 8.0 and C.max().item() == 8.0
