@@ -173,3 +173,29 @@ class MoNet:
             for p, dp in zip(L[:5], gr):
                 call("gnncg_sgd_update", p.numel(), lr, _ptr(dp.contiguous()), _ptr(p), _stream())
         return self.loss[:1], grads
+
+
+class GraphedStep:
+    """A training step captured once into a CUDA graph and replayed (launch-bound small graphs).
+
+    The model's train_step(H, lr) is recorded on a side stream with the input in a static buffer;
+    replay() re-runs every kernel of the step (forward, loss, backward, SGD) with one launch.
+    Device allocations made inside the step come from the graph's private memory pool."""
+
+    def __init__(self, model, H_static: torch.Tensor, lr: float, warmup: int = 2):
+        self.model, self.H, self.lr = model, H_static, lr
+        s = torch.cuda.Stream()
+        s.wait_stream(torch.cuda.current_stream())
+        with torch.cuda.stream(s):
+            for _ in range(warmup):
+                model.train_step(H_static, lr=lr)
+        torch.cuda.current_stream().wait_stream(s)
+        self.graph = torch.cuda.CUDAGraph()
+        n0 = _lib.lib().gnncg_launch_count()
+        with torch.cuda.graph(self.graph):
+            self.loss, self.grads = model.train_step(H_static, lr=lr)
+        self.kernels = int(_lib.lib().gnncg_launch_count() - n0)  # library kernels per replay
+
+    def replay(self):
+        self.graph.replay()
+        return self.loss, self.grads
