@@ -576,11 +576,20 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
 __global__ void gat_rowdot_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
                                   const float* __restrict__ out, float* __restrict__ c) {
   const int64_t n = rows * h;
+  const bool vec = (f % 4) == 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const float* g = dOut + i * f;
     const float* o = out + i * f;
     float s = 0.f;
-    for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
+    if (vec) {
+      for (int j = 0; j < f; j += 4) {
+        const float4 a = __ldg(reinterpret_cast<const float4*>(g + j));
+        const float4 b = __ldg(reinterpret_cast<const float4*>(o + j));
+        s = fmaf(a.x, b.x, s); s = fmaf(a.y, b.y, s); s = fmaf(a.z, b.z, s); s = fmaf(a.w, b.w, s);
+      }
+    } else {
+      for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
+    }
     c[i] = s;
   }
 }
@@ -681,49 +690,105 @@ __global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __rest
                                  const float* __restrict__ a_l, const float* __restrict__ a_r, float* __restrict__ Al,
                                  float* __restrict__ Ar) {
   const int64_t n = rows * h;
+  const bool vec = (f % 4) == 0;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t v = i / h;
     const int k = (int)(i % h);
     const float* x = Ht + v * h * f + (int64_t)k * f;
+    const float* pl = a_l + k * f;
+    const float* pr = a_r + k * f;
     float sl = 0.f, sr = 0.f;
-    for (int j = 0; j < f; ++j) {
-      const float xv = __ldg(x + j);
-      sl = fmaf(xv, __ldg(a_l + k * f + j), sl);
-      sr = fmaf(xv, __ldg(a_r + k * f + j), sr);
+    if (vec) {
+      for (int j = 0; j < f; j += 4) {
+        const float4 xv = __ldg(reinterpret_cast<const float4*>(x + j));
+        const float4 lv = __ldg(reinterpret_cast<const float4*>(pl + j));
+        const float4 rv = __ldg(reinterpret_cast<const float4*>(pr + j));
+        sl = fmaf(xv.x, lv.x, sl); sl = fmaf(xv.y, lv.y, sl); sl = fmaf(xv.z, lv.z, sl); sl = fmaf(xv.w, lv.w, sl);
+        sr = fmaf(xv.x, rv.x, sr); sr = fmaf(xv.y, rv.y, sr); sr = fmaf(xv.z, rv.z, sr); sr = fmaf(xv.w, rv.w, sr);
+      }
+    } else {
+      for (int j = 0; j < f; ++j) {
+        const float xv = __ldg(x + j);
+        sl = fmaf(xv, __ldg(pl + j), sl);
+        sr = fmaf(xv, __ldg(pr + j), sr);
+      }
     }
     Al[i] = sl;
     Ar[i] = sr;
   }
 }
 
-constexpr int kGradBlocks = 296;
+constexpr int kGradBlocks = 1184;  // 8 per SM: enough independent row streams (C5: V = 10M)
 
-__global__ void attn_grad_partial_kernel(int64_t rows, int h, int f, const float* __restrict__ Ht,
-                                         const float* __restrict__ dAl, const float* __restrict__ dAr,
-                                         float* __restrict__ part) {
+// Per-block partial of da_l / da_r: threads = (row group, column); each thread walks its
+// rows 4 at a time (independent loads in flight), then the row groups are combined in a
+// fixed order -> deterministic.
+__global__ void __launch_bounds__(256) attn_grad_partial_kernel(int64_t rows, int h, int f,
+                                                                const float* __restrict__ Ht,
+                                                                const float* __restrict__ dAl,
+                                                                const float* __restrict__ dAr,
+                                                                float* __restrict__ part) {
+  __shared__ float red[2][256];
   const int hf = h * f;
-  const int c = blockIdx.y * blockDim.x + threadIdx.x;
-  if (c >= hf) return;
+  const int cw = min(hf - (int)blockIdx.y * 256, 256);  // columns of this block
+  const int RG = 256 / cw;                               // row groups
+  const int t = threadIdx.x, grp = t / cw, cl = t % cw;
+  const int c = blockIdx.y * 256 + cl;
   const int k = c / f;
   const int64_t per = ceil_div(rows, (int64_t)gridDim.x);
   const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
   float sl = 0.f, sr = 0.f;
-  for (int64_t v = r0; v < r1; ++v) {
-    const float x = __ldg(Ht + v * hf + c);
-    sl = fmaf(__ldg(dAl + v * h + k), x, sl);
-    sr = fmaf(__ldg(dAr + v * h + k), x, sr);
+  if (grp < RG) {
+    int64_t v = r0 + grp;
+    for (; v + 3 * RG < r1; v += 4 * RG) {
+      float x[4], l[4], r[4];
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        const int64_t vv = v + q * RG;
+        x[q] = __ldg(Ht + vv * hf + c);
+        l[q] = __ldg(dAl + vv * h + k);
+        r[q] = __ldg(dAr + vv * h + k);
+      }
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sl = fmaf(l[q], x[q], sl);
+        sr = fmaf(r[q], x[q], sr);
+      }
+    }
+    for (; v < r1; v += RG) {
+      const float x = __ldg(Ht + v * hf + c);
+      sl = fmaf(__ldg(dAl + v * h + k), x, sl);
+      sr = fmaf(__ldg(dAr + v * h + k), x, sr);
+    }
   }
-  part[(int64_t)blockIdx.x * 2 * hf + c] = sl;
-  part[(int64_t)blockIdx.x * 2 * hf + hf + c] = sr;
+  red[0][t] = sl;
+  red[1][t] = sr;
+  __syncthreads();
+  if (grp == 0) {
+    for (int g = 1; g < RG; ++g) {
+      sl += red[0][g * cw + cl];
+      sr += red[1][g * cw + cl];
+    }
+    part[(int64_t)blockIdx.x * 2 * hf + c] = sl;
+    part[(int64_t)blockIdx.x * 2 * hf + hf + c] = sr;
+  }
 }
 
-__global__ void attn_grad_reduce_kernel(int nb, int hf, const float* __restrict__ part, float* __restrict__ da_l,
-                                        float* __restrict__ da_r) {
-  const int c = blockIdx.x * blockDim.x + threadIdx.x;
-  if (c >= 2 * hf) return;
+// Column c of the result = sum over blocks of the partials, one CTA per column (fixed order).
+__global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, const float* __restrict__ part,
+                                                               float* __restrict__ da_l, float* __restrict__ da_r) {
+  __shared__ float sh[8];
+  const int c = blockIdx.x;
   float s = 0.f;
-  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * 2 * hf + c];
-  if (c < hf) da_l[c] = s; else da_r[c - hf] = s;
+  for (int b = threadIdx.x; b < nb; b += blockDim.x) s += part[(int64_t)b * 2 * hf + c];
+  s = warp_sum(s);
+  if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    float t = 0.f;
+    for (int w = 0; w < 8; ++w) t += sh[w];
+    if (c < hf) da_l[c] = t; else da_r[c - hf] = t;
+  }
 }
 
 // ---------------------------------------------------------------------------
@@ -1032,7 +1097,7 @@ int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float
   dim3 g1(kGradBlocks, (unsigned)ceil_div(hf, 256));
   attn_grad_partial_kernel<<<g1, 256, 0, s>>>(rows, h, f, Ht, dAl, dAr, part);
   GNNCG_LAUNCH_CHECK();
-  attn_grad_reduce_kernel<<<(unsigned)ceil_div(2 * hf, 256), 256, 0, s>>>(kGradBlocks, hf, part, da_l, da_r);
+  attn_grad_reduce_kernel<<<(unsigned)(2 * hf), 256, 0, s>>>(kGradBlocks, hf, part, da_l, da_r);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }
