@@ -378,6 +378,13 @@ def run_ours(args):
             traffic = json.load(fh).get(dominant)
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": kernels[dominant]["GBps"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dominant]["frac"], "traffic": traffic, "peak_source": peak_src}
+    if traffic and args.config == "reddit" and world == 1:
+        # the algorithmic model counts every gathered row; hub rows are served from L2, so also
+        # report the DRAM bytes ncu measured for this kernel over its live launch time
+        dram = traffic / (kernels[dominant]["ms_per_launch"] / 1e3) / 1e9
+        roofline.update({"dram_achieved": dram, "dram_frac": dram / peak,
+                         "note": "achieved = algorithmic bytes (SURVEY §8d per-edge-gather model, DESIGN.md §4); "
+                                 "traffic = ncu dram__bytes per launch (profiles/ncu_traffic.json)"})
 
     # --- end-to-end through the public API with host buffers ----------------------------
     e2e = None
