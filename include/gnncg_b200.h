@@ -175,18 +175,21 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
                       size_t workspace_bytes, void* stream);
 
 /* Fast mode (lock-free atomic accumulation, tolerance-tested): K3 folded
- * into K4.  c must be the per-head row dot c[v,k] = <dOut[v,k,:], out[v,k,:]> (equal
- * to sum_e alpha_e dalpha_e, the softmax-backward identity), from gnncg_gat_rowdot.
- * One pass over csc_src then produces dHt (including both LP terms), dA_l, and dA_r
- * (zeroed and accumulated with global reductions: order-nondeterministic in the last
- * bits).  Supported when gnncg_gat_fast_supported(heads, f) != 0. */
+ * into K4.  gnncg_gat_bwd_prep builds, per destination row v and head k, the packed
+ * record {A_r[v,k] | lse[v,k] = m + log d | c[v,k] = <dOut[v,k,:], out[v,k,:]>}
+ * (row stride gnncg_gat_rec_stride(heads) floats; c = sum_e alpha_e dalpha_e by the
+ * softmax-backward identity, so no pass over csr_dst is needed).  One pass over
+ * csc_src then produces dHt (including both LP terms), dA_l, and dA_r (zeroed and
+ * accumulated with global reductions: order-nondeterministic in the last bits).
+ * Supported when gnncg_gat_fast_supported(heads, f) != 0. */
 int gnncg_gat_fast_supported(int heads, int f);
-int gnncg_gat_rowdot(int64_t num_rows, int heads, int f, const float* dOut, const float* out, float* c, void* stream);
+int gnncg_gat_rec_stride(int heads);
+int gnncg_gat_bwd_prep(int64_t num_rows, int heads, int f, const float* dOut, const float* out, const float* Ar,
+                       const float* m, const float* d, float* dst_rec, void* stream);
 int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int heads, int f, float slope,
                             int64_t row_base, int64_t num_local_rows, const float* Ht, const float* Al,
-                            const float* Ar, const float* m, const float* d, const float* c, const float* dOut,
-                            const float* a_l, const float* a_r, float* dHt, float* dAl, float* dAr, void* workspace,
-                            size_t workspace_bytes, void* stream);
+                            const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
+                            float* dAl, float* dAr, void* workspace, size_t workspace_bytes, void* stream);
 
 /* da_l[k,:] = sum_v dA_l[v,k] Ht[v,k,:] ; da_r likewise (LP parameter grads). */
 size_t gnncg_gat_attn_grad_workspace(int64_t num_rows, int heads, int f);

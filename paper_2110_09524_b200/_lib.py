@@ -93,9 +93,10 @@ _SIGS = {
     "gnncg_gat_bwd_src": ([P(Index), P(Sched), i32, i32, f32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                            vp, vp, sz, vp], i32),
     "gnncg_gat_fast_supported": ([i32, i32], i32),
-    "gnncg_gat_rowdot": ([i64, i32, i32, vp, vp, vp, vp], i32),
+    "gnncg_gat_rec_stride": ([i32], i32),
+    "gnncg_gat_bwd_prep": ([i64, i32, i32, vp, vp, vp, vp, vp, vp, vp], i32),
     "gnncg_gat_bwd_src_fused": ([P(Index), P(Sched), i32, i32, f32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
-                                 vp, vp, vp, vp, sz, vp], i32),
+                                 sz, vp], i32),
     "gnncg_gat_attn_grad_workspace": ([i64, i32, i32], sz),
     "gnncg_gat_attn_grad": ([i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_edgeconv_fwd": ([P(Index), i32, i64, vp, i64, vp, i64, vp, vp, vp], i32),

@@ -86,6 +86,23 @@ __device__ __forceinline__ Vec<VW> ldg_vec(const float* p) {
   return r;
 }
 
+// Streaming gather of neighbour rows: read-only path without L1 allocation, so the rows
+// (used once per edge) do not evict the reusable per-vertex data from L1.
+template <int VW>
+__device__ __forceinline__ Vec<VW> ldg_stream(const float* p) {
+  Vec<VW> r;
+  if constexpr (VW == 4) {
+    asm("ld.global.nc.L1::no_allocate.v4.f32 {%0, %1, %2, %3}, [%4];"
+                 : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
+                 : "l"(p));
+  } else if constexpr (VW == 2) {
+    asm("ld.global.nc.L1::no_allocate.v2.f32 {%0, %1}, [%2];" : "=f"(r.x[0]), "=f"(r.x[1]) : "l"(p));
+  } else {
+    asm("ld.global.nc.L1::no_allocate.f32 %0, [%1];" : "=f"(r.x[0]) : "l"(p));
+  }
+  return r;
+}
+
 template <int VW>
 __device__ __forceinline__ void st_vec(float* p, const Vec<VW>& v) {
   if constexpr (VW == 4) {

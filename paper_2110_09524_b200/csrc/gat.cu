@@ -483,16 +483,18 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
     const int n = (int)min((uint64_t)32, e1 - base);
     {
       const bool valid = lane < n;
-      float arv[MAXH], mv[MAXH], dv[MAXH], cv[MAXH];
-      load_heads(p.Ar + (int64_t)v_cur * h, h, arv);
-      load_heads(p.m + (int64_t)v_cur * h, h, mv);
-      load_heads(p.d + (int64_t)v_cur * h, h, dv);
-      load_heads(p.c + (int64_t)v_cur * h, h, cv);
+      // packed destination record {A_r | lse = m + log d | c} (gat_bwd_prep_kernel): one
+      // contiguous 3h-float read per edge, and alpha = exp(s - lse) needs no divide
+      const float* rec = p.rec + (int64_t)v_cur * rec_stride(h);
+      float arv[MAXH], lse[MAXH], cv[MAXH];
+      load_heads(rec, h, arv);
+      load_heads(rec + h, h, lse);
+      load_heads(rec + 2 * h, h, cv);
 #pragma unroll
       for (int k = 0; k < MAXH; ++k) {
         if (k < h) {
           const float zz = sm.stat[3][k] + arv[k];
-          const float a = (valid && dv[k] > 0.f) ? __expf(lrelu(zz, slope) - mv[k]) / dv[k] : 0.f;
+          const float a = valid ? __expf(lrelu(zz, slope) - lse[k]) : 0.f;
           sm.t0[lane * TS + k] = a;
           sm.t1[lane * TS + k] = lrelu_grad(zz, slope) * a;
           sm.t2[lane * TS + k] = cv[k];
@@ -572,12 +574,20 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   }
 }
 
-// c[v,k] = <dOut[v,k,:], out[v,k,:]> (fast-mode input of K4).
-__global__ void gat_rowdot_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
-                                  const float* __restrict__ out, float* __restrict__ c) {
+// Fast-mode input of K4f, per destination v and head k (row-local, vertex tensors only):
+//   rec[v] = { A_r[v,k] | lse[v,k] = m[v,k] + log d[v,k] | c[v,k] = <dOut[v,k,:], out[v,k,:]> }
+// c = sum_e alpha_e dalpha_e by the softmax-backward identity; lse folds the stashed
+// (m, d) so that alpha_e = exp(s_e - lse).  Empty rows (d = 0) get lse = 0 (never read).
+__global__ void gat_bwd_prep_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
+                                    const float* __restrict__ out, const float* __restrict__ Ar,
+                                    const float* __restrict__ m, const float* __restrict__ d,
+                                    float* __restrict__ rec) {
   const int64_t n = rows * h;
   const bool vec = (f % 4) == 0;
+  const int rs = rec_stride(h);
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / h;
+    const int k = (int)(i % h);
     const float* g = dOut + i * f;
     const float* o = out + i * f;
     float s = 0.f;
@@ -590,7 +600,11 @@ __global__ void gat_rowdot_kernel(int64_t rows, int h, int f, const float* __res
     } else {
       for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
     }
-    c[i] = s;
+    const float dv = __ldg(d + i);
+    float* r = rec + v * rs;
+    r[k] = __ldg(Ar + i);
+    r[h + k] = dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f;
+    r[2 * h + k] = s;
   }
 }
 
@@ -1027,28 +1041,30 @@ int gnncg_gat_fast_supported(int h, int f) {
   return (u * nv) % per == 0;
 }
 
-int gnncg_gat_rowdot(int64_t rows, int h, int f, const float* dOut, const float* out, float* c, void* stream) {
+int gnncg_gat_rec_stride(int h) { return rec_stride(h); }
+
+int gnncg_gat_bwd_prep(int64_t rows, int h, int f, const float* dOut, const float* out, const float* Ar,
+                       const float* m, const float* d, float* rec, void* stream) {
   GNNCG_DEVICE_GUARD();
-  GNNCG_REQUIRE(rows >= 0 && h >= 1 && f >= 1, GNNCG_ERR_SHAPE, "gat_rowdot: bad shape");
+  GNNCG_REQUIRE(rows >= 0 && h >= 1 && h <= MAXH && f >= 1, GNNCG_ERR_SHAPE, "gat_bwd_prep: bad shape");
   if (rows == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(dOut && out && c, GNNCG_ERR_ARG, "gat_rowdot: null pointer");
+  GNNCG_REQUIRE(dOut && out && Ar && m && d && rec, GNNCG_ERR_ARG, "gat_bwd_prep: null pointer");
   const int g = (int)std::min<int64_t>(ceil_div(rows * h, 256), 148 * 32);
-  gat_rowdot_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, dOut, out, c);
+  gat_bwd_prep_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, dOut, out, Ar, m, d, rec);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }
 
 int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
-                            int64_t row_base, int64_t num_local, const float* Ht, const float* Al, const float* Ar,
-                            const float* m, const float* d, const float* c, const float* dOut, const float* a_l,
-                            const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
-                            void* stream) {
+                            int64_t row_base, int64_t num_local, const float* Ht, const float* Al,
+                            const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
+                            float* dAl, float* dAr, void* ws, size_t ws_bytes, void* stream) {
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csc_src, sched, h, f);
   if (rc) return rc;
   GNNCG_REQUIRE(gnncg_gat_fast_supported(h, f), GNNCG_ERR_UNSUPPORTED,
                 "gat_bwd_src_fused: f/VW must be a power of two <= 32 (use gnncg_gat_bwd_dst + gnncg_gat_bwd_src)");
-  GNNCG_REQUIRE(Ht && Al && Ar && m && d && c && dOut && a_l && a_r && dHt && dAl && dAr, GNNCG_ERR_ARG,
+  GNNCG_REQUIRE(Ht && Al && dst_rec && dOut && a_l && a_r && dHt && dAl && dAr, GNNCG_ERR_ARG,
                 "gat_bwd_src_fused: null pointer");
   GNNCG_REQUIRE(row_base >= 0 && num_local >= 0, GNNCG_ERR_ARG, "gat_bwd_src_fused: bad row block");
   const size_t need = src_part_bytes(sched, h, f);
@@ -1060,7 +1076,7 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
-  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.m = m; p.d = d; p.c = c; p.dOut = dOut; p.dAr = dAr; p.dAro = dAr;
+  p.Ht = Ht; p.Al = Al; p.rec = dst_rec; p.dOut = dOut; p.dAr = dAr; p.dAro = dAr;
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;

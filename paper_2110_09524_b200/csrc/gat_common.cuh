@@ -28,6 +28,9 @@ struct WarpSmem {
 __host__ __device__ __forceinline__ int64_t fwd_stride(int h, int f) { return (h * f + 2 * h + 3) / 4 * 4; }
 __host__ __device__ __forceinline__ int64_t src_stride(int h, int f) { return (h * f + h + 3) / 4 * 4; }
 
+// Fast-mode destination record {A_r | lse | c}: 3h floats padded to 16 bytes.
+__host__ __device__ __forceinline__ int rec_stride(int h) { return (3 * h + 3) / 4 * 4; }
+
 struct Item {
   uint32_t row;
   uint64_t e0, e1;
@@ -84,6 +87,7 @@ struct GatParams {
   float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
   float* part;  // split-row partials
   int64_t row_base, num_local;
+  const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
 };
 
@@ -138,7 +142,7 @@ __device__ __forceinline__ void gather_row(const float* __restrict__ base, int64
   const float* row = base + r * hf;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
+    if (c.ok[i]) x[i] = ldg_stream<VW>(row + c.col[i]);
     else
 #pragma unroll
       for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;

@@ -161,12 +161,15 @@ class CudaEngine:
         wp, wn = self.ws.get(_lib.lib().gnncg_gat_workspace(sd.struct(), ss.struct(), h, f))
         st = _stream()
         if out is not None and self.mode != "deterministic" and _lib.lib().gnncg_gat_fast_supported(h, f):
-            with PROBE("gat_rowdot"):
-                call("gnncg_gat_rowdot", n, h, f, _ptr(dOut), _ptr(out), _ptr(c), st)
+            rec = self.empty(n, _lib.lib().gnncg_gat_rec_stride(h))
+            Ar_loc = Ar_local.contiguous()
+            with PROBE("gat_bwd_prep"):
+                call("gnncg_gat_bwd_prep", n, h, f, _ptr(dOut), _ptr(out), _ptr(Ar_loc), _ptr(m), _ptr(d), _ptr(rec),
+                     st)
             with PROBE("gat_bwd_src_fused"):
                 call("gnncg_gat_bwd_src_fused", lg.csc.struct(), ss.struct(), h, f, p.slope, lg.row_base, n,
-                     _ptr(Ht), _ptr(Al), _ptr(Ar_local), _ptr(m), _ptr(d), _ptr(c), _ptr(dOut), _ptr(a_l),
-                     _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp, wn, st)
+                     _ptr(Ht), _ptr(Al), _ptr(rec), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr),
+                     wp, wn, st)
             return dHt, dAl, dAr
         with PROBE("gat_bwd_dst"):
             call("gnncg_gat_bwd_dst", lg.csr.struct(), sd.struct(), h, f, p.slope, _ptr(Ht), _ptr(Al),

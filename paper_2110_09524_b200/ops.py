@@ -246,12 +246,15 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
     if mode == "fast":
         if stash.out is None:
             raise TensorError("gat_region_backward(fast): stash.out is required")
-        with PROBE("gat_rowdot"):
-            call("gnncg_gat_rowdot", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(c), s)
+        rec = torch.empty(V, L.gnncg_gat_rec_stride(h), device=dev)
+        with PROBE("gat_bwd_prep"):
+            call("gnncg_gat_bwd_prep", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(stash.Ar), _ptr(stash.m),
+                 _ptr(stash.d), _ptr(rec), s)
+        c = rec[:, 2 * h:3 * h]
         with PROBE("gat_bwd_src_fused"):
             call("gnncg_gat_bwd_src_fused", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
-                 _ptr(stash.Al), _ptr(stash.Ar), _ptr(stash.m), _ptr(stash.d), _ptr(c), _ptr(dOut), _ptr(a_l),
-                 _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp, wn, s)
+                 _ptr(stash.Al), _ptr(rec), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp,
+                 wn, s)
     elif mode == "deterministic":
         with PROBE("gat_bwd_dst"):
             call("gnncg_gat_bwd_dst", g.csr_dst.struct(), sd.struct(), h, f, p.slope, _ptr(stash.Ht),
