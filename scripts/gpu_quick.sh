@@ -3,5 +3,5 @@
 cd "$GRAFT_REPO_ROOT"; TAG=${1:-q}; mkdir -p gpurun_out
 timeout 600 python -m pytest tests/test_gpu_gat.py -q -x -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_$TAG.log
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$TAG.log 2>&1
-GNNCG_GAT_OCC=2 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline --no-e2e > gpurun_out/bench_${TAG}_occ2.log 2>&1
+timeout 600 python -m pytest tests/test_gpu_dist.py -q -p no:cacheprovider >> gpurun_out/pytest_$TAG.log 2>&1
 echo done

@@ -96,3 +96,14 @@ def test_errors_map_to_reference_exceptions():
     assert issubclass(_lib.GraphError, RuntimeError) and issubclass(_lib.TensorError, RuntimeError)
     with pytest.raises(_lib.ArgumentError):
         _lib.call("gnncg_partition_rows", 10, None, 2, None)
+
+
+def test_binding_arity_matches_header():
+    """Every ctypes signature declares exactly as many arguments as the C prototype."""
+    src = open(os.path.join(ROOT, "include", "gnncg_b200.h")).read()
+    src = re.sub(r"/\*.*?\*/", "", src, flags=re.S)
+    protos = dict(re.findall(r"\b(gnncg_[a-z0-9_]+)\s*\(([^)]*)\)\s*;", src))
+    for name, (args, _) in _lib._SIGS.items():
+        params = protos[name].strip()
+        n = 0 if params in ("", "void") else params.count(",") + 1
+        assert n == len(args), f"{name}: header has {n} parameters, binding declares {len(args)}"
