@@ -142,7 +142,7 @@ __device__ __forceinline__ void gather_row(const float* __restrict__ base, int64
   const float* row = base + r * hf;
 #pragma unroll
   for (int i = 0; i < NV; ++i) {
-    if (c.ok[i]) x[i] = ldg_stream<VW>(row + c.col[i]);
+    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
     else
 #pragma unroll
       for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;
