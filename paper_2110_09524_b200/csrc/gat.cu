@@ -77,7 +77,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(Gat
       if (k < h) {
         const float s = valid ? lrelu(al[k] + sm.stat[3][k], slope) : -FLT_MAX;
         const float mold = sm.stat[0][k];
-        const float mnew = fmaxf(mold, warp_max(s));
+        // the block max is only needed when some lane exceeds the running max
+        const float mnew = __any_sync(0xffffffffu, s > mold) ? fmaxf(mold, warp_max(s)) : mold;
         const float sc = __expf(mold - mnew);
         const float pk = valid ? __expf(s - mnew) : 0.f;
         sm.t1[lane * TS + k] = fmaf(sm.t1[lane * TS + k], sc, pk);

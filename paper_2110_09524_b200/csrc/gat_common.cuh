@@ -139,14 +139,11 @@ __device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
 template <int VW, int NV>
 __device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
                                            Vec<VW> (&x)[NV]) {
+  // Lanes past the last column load column 0 instead (branch-free); their accumulators are
+  // never stored and their partial dots only reach head groups that are masked by `ok`.
   const float* row = base + r * hf;
 #pragma unroll
-  for (int i = 0; i < NV; ++i) {
-    if (c.ok[i]) x[i] = ldg_vec<VW>(row + c.col[i]);
-    else
-#pragma unroll
-      for (int q = 0; q < VW; ++q) x[i].x[q] = 0.f;
-  }
+  for (int i = 0; i < NV; ++i) x[i] = ldg_vec<VW>(row + (c.ok[i] ? c.col[i] : 0));
 }
 
 

@@ -1,7 +1,7 @@
 #!/bin/bash
 # Quick pass: GAT GPU tests + bench (TMA-fed on, then off), no ncu.
 cd "$GRAFT_REPO_ROOT"; TAG=${1:-q}; mkdir -p gpurun_out
-timeout 600 python -m pytest tests/test_gpu_gat.py -q -x -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_$TAG.log
+timeout 600 python -m pytest tests/test_gpu_gat.py tests/test_gpu_edgeconv_gmm.py -q -x -p no:cacheprovider > gpurun_out/pytest_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/pytest_$TAG.log
 timeout 600 python bench.py --steps 10 --warmup 3 --no-cpu-baseline > gpurun_out/bench_$TAG.log 2>&1
 timeout 600 python -m pytest tests/test_gpu_dist.py -q -p no:cacheprovider >> gpurun_out/pytest_$TAG.log 2>&1
 echo done
