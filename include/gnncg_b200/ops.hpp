@@ -295,5 +295,140 @@ inline Tensor<float> edgeconv_forward(const DeviceGraph& g, const Tensor<float>&
   return download(out, V, C, s);
 }
 
+struct EdgeConvGrads {
+  Tensor<float> dH, dTheta, dPhi;
+};
+
+// EdgeConv backward: argmax routing then the two backward Applies.
+// `argmax` is the edge-id tensor returned by edgeconv_forward.
+inline EdgeConvGrads edgeconv_backward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& Theta,
+                                       const Tensor<float>& Phi, const std::vector<std::uint32_t>& argmax,
+                                       const Tensor<float>& dOut, bool need_dH) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, C = Theta.cols;
+  detail::require_shape(dOut, V, C, "edgeconv_backward dOut");
+  if ((std::int64_t)argmax.size() != V * C) throw TensorError("edgeconv_backward: argmax size != V*C");
+  cudaStream_t s = g.stream();
+  Tensor<float> Wc(Fin, 2 * C);
+  for (std::int64_t i = 0; i < Fin; ++i)
+    for (std::int64_t c = 0; c < C; ++c) {
+      Wc.at(i, c) = Theta.at(i, c);
+      Wc.at(i, C + c) = Phi.at(i, c);
+    }
+  DeviceBuffer dH = upload(H, s), dWc = upload(Wc, s), g_out = upload(dOut, s);
+  DeviceBuffer am = upload(argmax.data(), argmax.size(), s), dY(V * 2 * C * 4), dW(Fin * 2 * C * 4);
+  const gnncg_index_t csr = g.csr_dst().view(), csc = g.csc_src().view();
+  check(gnncg_edgeconv_bwd(&csc, &csr, (int)C, am.get<std::uint32_t>(), g_out.get<float>(), dY.get<float>(), 2 * C,
+                           dY.get<float>() + C, 2 * C, s),
+        "gnncg_edgeconv_bwd");
+  detail::gemm(g, 1, 0, Fin, 2 * C, V, dH.get<float>(), Fin, dY.get<float>(), 2 * C, dW.get<float>(), 2 * C);
+  EdgeConvGrads out;
+  const Tensor<float> dWh = download(dW, Fin, 2 * C, s);
+  out.dTheta = Tensor<float>(Fin, C);
+  out.dPhi = Tensor<float>(Fin, C);
+  for (std::int64_t i = 0; i < Fin; ++i)
+    for (std::int64_t c = 0; c < C; ++c) {
+      out.dTheta.at(i, c) = dWh.at(i, c);
+      out.dPhi.at(i, c) = dWh.at(i, C + c);
+    }
+  if (need_dH) {
+    DeviceBuffer dHb(V * Fin * 4);
+    detail::gemm(g, 0, 1, V, Fin, 2 * C, dY.get<float>(), 2 * C, dWc.get<float>(), 2 * C, dHb.get<float>(), Fin);
+    out.dH = download(dHb, V, Fin, s);
+  }
+  return out;
+}
+
+// GMMConv: parameters W (F_in x K*f), P_l, P_r (F_in x r), mu, sinv (K x r).
+struct GmmParams {
+  int K, r, f;
+};
+
+struct GmmStash {
+  DeviceBuffer Y;  // [hW | pl | pr], V x (K f + 2 r)
+  std::int64_t ldy = 0;
+};
+
+struct GmmGrads {
+  Tensor<float> dH, dW, dP_l, dP_r, dmu, dsinv;
+};
+
+namespace detail {
+inline Tensor<float> pack_cols(const std::vector<const Tensor<float>*>& parts) {
+  std::uint64_t cols = 0;
+  for (auto* p : parts) cols += p->cols;
+  Tensor<float> out(parts[0]->rows, cols);
+  std::uint64_t c0 = 0;
+  for (auto* p : parts) {
+    for (std::uint64_t i = 0; i < p->rows; ++i)
+      for (std::uint64_t c = 0; c < p->cols; ++c) out.at(i, c0 + c) = p->at(i, c);
+    c0 += p->cols;
+  }
+  return out;
+}
+}  // namespace detail
+
+inline Tensor<float> gmm_forward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
+                                 const Tensor<float>& P_l, const Tensor<float>& P_r, const Tensor<float>& mu,
+                                 const Tensor<float>& sinv, const GmmParams& p, GmmStash* stash) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, Kf = (std::int64_t)p.K * p.f, ldy = Kf + 2 * p.r;
+  detail::require_shape(W, Fin, Kf, "gmm W");
+  detail::require_shape(P_l, Fin, p.r, "gmm P_l");
+  detail::require_shape(P_r, Fin, p.r, "gmm P_r");
+  detail::require_shape(mu, p.K, p.r, "gmm mu");
+  detail::require_shape(sinv, p.K, p.r, "gmm sinv");
+  cudaStream_t s = g.stream();
+  GmmStash local;
+  GmmStash& st = stash ? *stash : local;
+  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}), s);
+  DeviceBuffer dmu = upload(mu, s), dsi = upload(sinv, s), out(V * p.f * 4);
+  st.Y = DeviceBuffer(V * ldy * 4);
+  st.ldy = ldy;
+  detail::gemm(g, 0, 0, V, ldy, Fin, dH.get<float>(), Fin, dWc.get<float>(), ldy, st.Y.get<float>(), ldy);
+  const gnncg_index_t csr = g.csr_dst().view();
+  check(gnncg_gmm_fwd(&csr, p.K, p.r, p.f, st.Y.get<float>(), ldy, dmu.get<float>(), dsi.get<float>(),
+                      out.get<float>(), s),
+        "gnncg_gmm_fwd");
+  return download(out, V, p.f, s);
+}
+
+inline GmmGrads gmm_backward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
+                             const Tensor<float>& P_l, const Tensor<float>& P_r, const Tensor<float>& mu,
+                             const Tensor<float>& sinv, const GmmParams& p, const GmmStash& st,
+                             const Tensor<float>& dOut, bool need_dH) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, Kf = (std::int64_t)p.K * p.f, ldy = st.ldy;
+  detail::require_shape(dOut, V, p.f, "gmm dOut");
+  cudaStream_t s = g.stream();
+  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}), s);
+  DeviceBuffer dmu_in = upload(mu, s), dsi_in = upload(sinv, s), g_out = upload(dOut, s);
+  DeviceBuffer dY(V * ldy * 4), dmu(p.K * p.r * 4), dsinv(p.K * p.r * 4), dW(Fin * ldy * 4);
+  const gnncg_index_t csr = g.csr_dst().view(), csc = g.csc_src().view();
+  DeviceBuffer& ws = g.workspace(gnncg_gmm_bwd_workspace(&csr, p.K, p.r));
+  check(gnncg_gmm_bwd(&csr, &csc, p.K, p.r, p.f, st.Y.get<float>(), ldy, dmu_in.get<float>(), dsi_in.get<float>(),
+                      g_out.get<float>(), dY.get<float>(), dmu.get<float>(), dsinv.get<float>(), ws.get(), ws.bytes(),
+                      s),
+        "gnncg_gmm_bwd");
+  detail::gemm(g, 1, 0, Fin, ldy, V, dH.get<float>(), Fin, dY.get<float>(), ldy, dW.get<float>(), ldy);
+  GmmGrads out;
+  const Tensor<float> dWh = download(dW, Fin, ldy, s);
+  out.dW = Tensor<float>(Fin, Kf);
+  out.dP_l = Tensor<float>(Fin, p.r);
+  out.dP_r = Tensor<float>(Fin, p.r);
+  for (std::int64_t i = 0; i < Fin; ++i) {
+    for (std::int64_t c = 0; c < Kf; ++c) out.dW.at(i, c) = dWh.at(i, c);
+    for (std::int64_t c = 0; c < p.r; ++c) {
+      out.dP_l.at(i, c) = dWh.at(i, Kf + c);
+      out.dP_r.at(i, c) = dWh.at(i, Kf + p.r + c);
+    }
+  }
+  out.dmu = download(dmu, p.K, p.r, s);
+  out.dsinv = download(dsinv, p.K, p.r, s);
+  if (need_dH) {
+    DeviceBuffer dHb(V * Fin * 4);
+    detail::gemm(g, 0, 1, V, Fin, ldy, dY.get<float>(), ldy, dWc.get<float>(), ldy, dHb.get<float>(), Fin);
+    out.dH = download(dHb, V, Fin, s);
+  }
+  return out;
+}
+
 }  // namespace b200
 }  // namespace gnncg

@@ -87,6 +87,52 @@ int main() {
       if (g.in_degree(v) == 0) ok = ok && e == 0xFFFFFFFFu && eo.at(v, c) == 0.f;
       else ok = ok && e < g.num_edges() && g.edge_dst(e) == v;
     }
+  // EdgeConv backward with loss = sum(out): dPh[v,c] = [in_degree(v) > 0], so dPhi = H^T M
+  TensorF ones_out(V, 16, 1.0f);
+  b200::EdgeConvGrads eg = b200::edgeconv_backward(dg, H, Th, Ph, amax, ones_out, true);
+  double worst_ec = 0.0;
+  for (int i = 0; i < Fin; ++i)
+    for (int c = 0; c < 16; ++c) {
+      double s = 0;
+      for (std::uint64_t v = 0; v < V; ++v)
+        if (g.in_degree(v) > 0) s += H.at(v, i);
+      worst_ec = std::max(worst_ec, rel_err(s, eg.dPhi.at(i, c)));
+    }
+  ok = ok && worst_ec < 1e-4 && eg.dH.rows == V && all_finite(eg.dTheta);
+  std::printf("edgeconv dPhi max rel_err = %.3e\n", worst_ec);
+
+  // GMMConv forward against a direct f64 evaluation
+  const b200::GmmParams gp{3, 2, 4};
+  const TensorF Wg = init_seeded<float>(Fin, gp.K * gp.f, 7), Pl = init_seeded<float>(Fin, gp.r, 8),
+                Pr = init_seeded<float>(Fin, gp.r, 9), mu = init_seeded<float>(gp.K, gp.r, 10);
+  TensorF sinv(gp.K, gp.r, 1.5f);
+  b200::GmmStash gst;
+  TensorF go = b200::gmm_forward(dg, H, Wg, Pl, Pr, mu, sinv, gp, &gst);
+  auto dotrow = [&](const TensorF& A, std::uint64_t v, const TensorF& B, int col) {
+    double s = 0;
+    for (int i = 0; i < Fin; ++i) s += (double)A.at(v, i) * B.at(i, col);
+    return s;
+  };
+  double worst_g = 0.0;
+  for (std::uint64_t v = 0; v < V; ++v)
+    for (int j = 0; j < gp.f; ++j) {
+      double o = 0;
+      for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i) {
+        const auto u = in.entries[i].vertex;
+        for (int k = 0; k < gp.K; ++k) {
+          double q = 0;
+          for (int t = 0; t < gp.r; ++t) {
+            const double m = dotrow(H, u, Pl, t) + dotrow(H, v, Pr, t) - mu.at(k, t);
+            q += m * m * sinv.at(k, t) * sinv.at(k, t);
+          }
+          o += std::exp(-0.5 * q) * dotrow(H, u, Wg, k * gp.f + j) / gp.K;
+        }
+      }
+      worst_g = std::max(worst_g, rel_err(o, go.at(v, j)));
+    }
+  b200::GmmGrads gg = b200::gmm_backward(dg, H, Wg, Pl, Pr, mu, sinv, gp, gst, TensorF(V, gp.f, 1.0f), true);
+  ok = ok && worst_g < 1e-4 && all_finite(gg.dW) && all_finite(gg.dmu) && all_finite(gg.dsinv) && gg.dH.rows == V;
+  std::printf("gmm forward max rel_err = %.3e\n", worst_g);
   std::printf("%s\n", ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
 }
