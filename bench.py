@@ -135,7 +135,10 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
             model = GAT(g, dims, seed=1, chunk=args.chunk)
             V_loc, E_loc = V, E
         h, f = dims[0][1], dims[0][2]
-        wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E * world,
+        from paper_2110_09524_b200.cost import gat_layer_report
+
+        wl_cost = {"per_layer": gat_layer_report(V * world, E * world, h, f), "source": "SPEC.md:282-289"}
+        wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E * world, cost=wl_cost,
                   layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f),
                   config={"workload": desc, "V": V * world, "E": E * world, "layers": len(dims),
                           "dims": ", ".join(f"{a}->{b}x{c}" for a, b, c in dims),
@@ -448,6 +451,7 @@ def run_ours(args):
                 "config": {**wl["config"], "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
+                "cost_model": wl.get("cost"),
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     if world > 1:

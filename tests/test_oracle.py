@@ -305,3 +305,16 @@ def test_f32_baseline_matches_f64_oracle():
     assert O.max_rel_err(f32f["out"], fw["out"]) < 1e-4
     for k in ("dH", "dW", "dal", "dar"):
         assert O.max_rel_err(f32b[k], bw[k]) < 1e-4, k
+
+
+def test_cost_module_matches_spec_and_oracle():
+    from paper_2110_09524_b200 import cost
+
+    assert cost.gat_attention_flops(3, 3, 2) == {"naive": 39, "reorganized": 30}
+    assert cost.gat_io_units(3, 3, 1, 2) == {"unfused": 45, "fused": 33}
+    for V, E, h, f in ((100, 495, 1, 2), (233000, 114000000, 8, 32)):
+        c = O.cost_counts(V, E, h, f)
+        assert cost.gat_io_units(V, E, h, f) == {"unfused": c["io_unfused"], "fused": c["io_fused"]}
+        assert cost.gat_attention_flops(V, E, f)["reorganized"] == c["flops_reorg"]
+    r = cost.gat_layer_report(233000, 114000000, 8, 32)
+    assert r["stash_bytes_saved"] > 7e9  # recompute drops the O(|E| h) stash: ~7.3 GB per Reddit layer
