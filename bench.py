@@ -51,7 +51,7 @@ def parse():
     ap.add_argument("--scale", type=float, default=1.0, help="shrink V and E (debug only)")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the step as a CUDA graph (auto: on for the small, launch-bound configs)")
-    ap.add_argument("--config", default="reddit", choices=["reddit", "cora", "edgeconv20", "edgeconv40", "monet", "c5"],
+    ap.add_argument("--config", default="reddit", choices=["reddit", "cora", "edgeconv20", "edgeconv40", "monet", "c5", "gcn"],
                     help="reddit = the headline (BASELINE configs[1]); the others are configs[0,2,3,4]")
     return ap.parse_args()
 
@@ -94,6 +94,20 @@ def gmm_kernel_bytes(V: int, E: int, K: int, r: int, f: int) -> dict:
     (csr_dst: nbr + Y[u]; csc_src: nbr + pr[v] + dOut[v]) plus the dY writes."""
     return {"gmm_fwd": E * (4 + 4 * (K * f + r)) + V * (8 + 4 * r + 4 * f),
             "gmm_bwd": E * (8 + 4 * (K * f + r) + 4 * (r + f)) + V * (16 + 8 * (K * f + 2 * r) + 4 * f)}
+
+
+def spmm_kernel_bytes(V: int, E: int, C: int) -> dict:
+    """GCN aggregate (csrc/spmm.cu): nbr + eid + w[eid] + the X[u] row per edge; item, offsets and
+    the output row per row.  The transposed pass (backward, over csc_src) moves the same bytes."""
+    b = E * (12 + 4 * C) + V * (16 + 4 * C)
+    return {"spmm": b, "spmm_t": b}
+
+
+def _grad_tensors(gr):
+    """Parameter-gradient tensors of one layer (GatGrads or a tuple), for the e2e read-back."""
+    if hasattr(gr, "dW"):
+        return (gr.dW, gr.da_l, gr.da_r)
+    return tuple(t for t in gr if t is not None)
 
 
 def build_workload(args, dev, world: int, rank: int) -> dict:
@@ -168,6 +182,18 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
                                       "(BASELINE configs[2])", "V": V, "E": E, "layers": len(dims) - 1,
                           "dims": "64->64->64->128->256", "graph": f"kNN k={k} of 32 uniform clouds, seed 0",
                           "l2": "working set fits L2 (no flush)"})
+    elif cfg == "gcn":
+        V, E, offset = int(REDDIT["V"] * args.scale), int(REDDIT["E"] * args.scale), REDDIT["offset"]
+        from paper_2110_09524_b200.models import GCN
+
+        g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
+        dims = [602, 256, 256]
+        per = [spmm_kernel_bytes(V, E, c) for c in dims[1:]]
+        wl = dict(model=GCN(g, dims, seed=1, chunk=args.chunk), H_buf=features(V, 602), fin=602, E_total=E,
+                  layers=len(dims) - 1, bytes={n: sum(p[n] for p in per) / len(per) for n in per[0]},
+                  config={"workload": "GCN 2-layer fwd+bwd+SGD, Reddit-shaped (SURVEY 8f rank 3)", "V": V, "E": E,
+                          "layers": 2, "dims": "602->256->256", "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0",
+                          "l2": "inputs larger than L2 (features and index exceed 126 MB)"})
     elif cfg == "monet":
         V, E, K, r = 19717, 88648, 3, 3
         src, dst = uniform_edges(V, E, seed=0)
@@ -421,7 +447,7 @@ def run_ours(args):
             compute.wait_event(ready[b])
             loss, grads = model.train_step(bufs[b][:, :fin], lr=lr)
             free[b].record(compute)
-            res = [loss] + [t for gr in grads for t in (gr.dW, gr.da_l, gr.da_r)]
+            res = [loss] + [t for gr in grads for t in _grad_tensors(gr)]
             if out_bufs is None:
                 out_bufs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
             for hb, t in zip(out_bufs, res):

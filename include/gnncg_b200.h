@@ -229,6 +229,27 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr_dst, const gnncg_index_t* csc_src, in
                   const float* Y, int64_t ldy, const float* mu, const float* sinv, const float* dOut, float* dY,
                   float* dmu, float* dsinv, void* workspace, size_t workspace_bytes, void* stream);
 
+/* ------------------------------------------------ GCN (weighted Aggregate)
+ * SURVEY §8f rank 3; the spec's gcn model:
+ *   [ApplyVertex(W), Scatter(copy_u), ApplyEdge(x e_uv), Gather(sum), ApplyVertex(+b, sigma)]
+ * One kernel over `idx` (csr_dst forward, csc_src for the transpose in backward):
+ *   Y[r,:] = act(bias + sum_{i in row r} w[eid_i] X[nbr_i,:])
+ * edge_w is indexed by edge id (NULL = all ones; non-NULL needs idx->eid); bias may be
+ * NULL; relu != 0 applies max(0,.).  Rows of idx are local (Y has idx->num_rows rows),
+ * neighbours global.  Deterministic (fixed-order split-row merge). */
+size_t gnncg_spmm_workspace(const gnncg_sched_t* sched, int cols);
+int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, const float* edge_w, const float* X,
+               const float* bias, int relu, float* Y, void* workspace, size_t workspace_bytes, void* stream);
+/* Backward of the epilogue: dZ = dOut * [out > 0] (relu) or dOut; dbias (if non-NULL) =
+ * column sums of dZ (fixed order). */
+size_t gnncg_relu_bwd_workspace(int cols);
+int gnncg_relu_bwd(int64_t rows, int cols, const float* dOut, const float* out, int relu, float* dZ, float* dbias,
+                   void* workspace, size_t workspace_bytes, void* stream);
+/* Symmetric GCN normalisation by edge id:
+ *   w[e] = 1 / sqrt(max(1, deg_in(dst e)) * max(1, deg_out(src e))) */
+int gnncg_gcn_norm(int64_t num_edges, const uint32_t* edge_src, const uint32_t* edge_dst,
+                   const gnncg_index_t* csr_dst, const gnncg_index_t* csc_src, float* w, void* stream);
+
 /* ------------------------------------------------- training-step helpers */
 /* params -= lr * grad  (train_step). */
 int gnncg_sgd_update(int64_t n, float lr, const float* grad, float* param, void* stream);

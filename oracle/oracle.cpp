@@ -615,6 +615,54 @@ void orc_gmm_layer_bwd_f64(u64 V, const u64* off, const u32* src, u64 Fin, const
 }
 
 // ---------------------------------------------------------------------------
+// GCN (PAPER.md:534-540 ): h'_v = sigma(b + sum_{(u,e,v)} w_e h_u W).
+// The weighted Aggregate over one index (csr_dst forward; csc_src = the transpose in
+// backward), edge weights looked up by edge id -- the same per-row sum as
+// dense_aggregate but walked in index order.
+// ---------------------------------------------------------------------------
+}  // extern "C"
+
+template <typename T>
+static void gcn_aggregate(u64 R, const u64* off, const u32* nbr, const u32* eid, const T* w, int F, const T* X,
+                          const T* bias, int relu, T* Y) {
+#pragma omp parallel for schedule(dynamic, 64) if (R > 4096)
+  for (long long r = 0; r < (long long)R; ++r) {
+    T* y = Y + (u64)r * F;
+    for (int j = 0; j < F; ++j) y[j] = 0;
+    for (u64 i = off[r]; i < off[r + 1]; ++i) {
+      const T a = w ? w[eid[i]] : T(1);
+      const T* x = X + (u64)nbr[i] * F;
+      for (int j = 0; j < F; ++j) y[j] += a * x[j];
+    }
+    for (int j = 0; j < F; ++j) {
+      const T z = y[j] + (bias ? bias[j] : T(0));
+      y[j] = (relu && !(z > 0)) ? T(0) : z;
+    }
+  }
+}
+
+extern "C" {
+
+void orc_gcn_aggregate_f64(u64 R, const u64* off, const u32* nbr, const u32* eid, const double* w, int F,
+                           const double* X, const double* bias, int relu, double* Y) {
+  gcn_aggregate(R, off, nbr, eid, w, F, X, bias, relu, Y);
+}
+void orc_gcn_aggregate_f32(u64 R, const u64* off, const u32* nbr, const u32* eid, const float* w, int F,
+                           const float* X, const float* bias, int relu, float* Y) {
+  gcn_aggregate(R, off, nbr, eid, w, F, X, bias, relu, Y);
+}
+
+// Symmetric normalisation w_e = 1/sqrt(max(1,deg_in(dst)) max(1,deg_out(src))).
+void orc_gcn_norm(u64 V, u64 E, const u32* src, const u32* dst, const u64* doff, const u64* soff, float* w) {
+  (void)V;
+  for (u64 e = 0; e < E; ++e) {
+    const double din = (double)std::max<u64>(1, doff[dst[e] + 1] - doff[dst[e]]);
+    const double dout = (double)std::max<u64>(1, soff[src[e] + 1] - soff[src[e]]);
+    w[e] = (float)(1.0 / std::sqrt(din * dout));
+  }
+}
+
+// ---------------------------------------------------------------------------
 // Cost-algebra closed forms (SPEC.md:282-289 ), element
 // counts.  Used as known-answer checks (G3: 39 -> 30 flops, 45 -> 33 IO units).
 // ---------------------------------------------------------------------------

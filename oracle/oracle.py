@@ -371,6 +371,39 @@ def gmm_layer_bwd_f64(g: HostGraph, H, W, Pl, Pr, mu, sinv, K, r, f, fwd, dOut, 
     return dict(dH=dH, dW=dW, dPl=dPl, dPr=dPr, dmu=dmu, dsinv=dsinv, dhW=dhW, dpl=dpl, dpr=dpr)
 
 
+# ----------------------------------------------------------------------------
+# GCN (PAPER.md:534-540 )
+# ----------------------------------------------------------------------------
+def gcn_aggregate(g: HostGraph, X, w=None, bias=None, relu=False, transpose=False, dtype=np.float64):
+    """Y = act(bias + A_w X) over csr_dst (A_w^T X over csc_src when transpose)."""
+    off, nbr, eid = (g.src_off, g.src_dst, g.src_eid) if transpose else (g.dst_off, g.dst_src, g.dst_eid)
+    X = _c(X, dtype)
+    F = X.shape[1]
+    Y = np.zeros((g.V, F), dtype)
+    fn = lib().orc_gcn_aggregate_f64 if dtype == np.float64 else lib().orc_gcn_aggregate_f32
+    fn(u64(g.V), _p(off), _p(nbr), _p(eid), _p(None if w is None else _c(w, dtype)), i32(F), _p(X),
+       _p(None if bias is None else _c(bias, dtype)), i32(int(relu)), _p(Y))
+    return Y
+
+
+def gcn_norm(g: HostGraph) -> np.ndarray:
+    w = np.zeros(g.E, np.float32)
+    lib().orc_gcn_norm(u64(g.V), u64(g.E), _p(g.src), _p(g.dst), _p(g.dst_off), _p(g.src_off), _p(w))
+    return w
+
+
+def gcn_layer_fwd_f64(g: HostGraph, H, W, b, w=None, relu=True):
+    Ht = _c(H, np.float64) @ _c(W, np.float64)
+    return dict(Ht=Ht, out=gcn_aggregate(g, Ht, w, b, relu))
+
+
+def gcn_layer_bwd_f64(g: HostGraph, H, W, fwd, dOut, w=None, relu=True):
+    dOut = _c(dOut, np.float64)
+    dZ = np.where(fwd["out"] > 0, dOut, 0.0) if relu else dOut
+    dHt = gcn_aggregate(g, dZ, w, transpose=True)
+    return dict(dH=dHt @ _c(W, np.float64).T, dW=_c(H, np.float64).T @ dHt, db=dZ.sum(axis=0), dHt=dHt)
+
+
 def dense_aggregate_f64(V, src, dst, H, w=None):
     src = _c(src, np.uint32); dst = _c(dst, np.uint32); H = _c(H, np.float64)
     F = H.shape[1]

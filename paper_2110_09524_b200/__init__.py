@@ -1,6 +1,6 @@
 """paper_2110_09524_b200 -- B200-native (sm_100a) fused GNN layer path of arXiv 2110.09524.
 
-Drop-in for the reference's fused GAT / EdgeConv / GMMConv layer path
+Drop-in for the reference's fused GAT / EdgeConv / GMMConv (+ GCN) layer path
 (SPEC.md:316-390 executor; proj/include/gnncg graph and tensor model).  All
 compute runs in the in-tree ``libgnncg_b200.so`` (C ABI: include/gnncg_b200.h);
 there is no CPU fallback.
@@ -9,7 +9,7 @@ from ._lib import (ArgumentError, CudaError, DeviceError, GnncgError, GraphError
                    UnsupportedError, WorkspaceError)
 from .graph import DeviceGraph, DeviceIndex, DeviceSched, chung_lu_cdf, knn_edges, partition_rows, uniform_edges  # noqa: F401
 from .ops import (GatGrads, GatParams, GatStash, edgeconv_backward, edgeconv_forward, gat_backward,  # noqa: F401
-                  gat_forward, gat_region_backward, gat_region_forward, gemm, gmm_backward, gmm_forward, matmul,
-                  matmul_nt, matmul_tn)
+                  gat_forward, gat_region_backward, gat_region_forward, gcn_backward, gcn_forward, gcn_norm, gemm,
+                  gmm_backward, gmm_forward, matmul, matmul_nt, matmul_tn, spmm)
 
 __version__ = "0.1.0"

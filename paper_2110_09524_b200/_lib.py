@@ -105,6 +105,11 @@ _SIGS = {
     "gnncg_gmm_fwd": ([P(Index), i32, i32, i32, vp, i64, vp, vp, vp, vp], i32),
     "gnncg_gmm_bwd_workspace": ([P(Index), i32, i32], sz),
     "gnncg_gmm_bwd": ([P(Index), P(Index), i32, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_spmm_workspace": ([P(Sched), i32], sz),
+    "gnncg_spmm": ([P(Index), P(Sched), i32, vp, vp, vp, i32, vp, vp, sz, vp], i32),
+    "gnncg_relu_bwd_workspace": ([i32], sz),
+    "gnncg_relu_bwd": ([i64, i32, vp, vp, i32, vp, vp, vp, sz, vp], i32),
+    "gnncg_gcn_norm": ([i64, vp, vp, P(Index), P(Index), vp, vp], i32),
     "gnncg_sgd_update": ([i64, f32, vp, vp, vp], i32),
     "gnncg_fill": ([i64, f32, vp, vp], i32),
     "gnncg_sum_workspace": ([], sz),

@@ -1,0 +1,261 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// Weighted Aggregate (GCN): the spec's GCN layer
+//   build_model(gcn) = [ApplyVertex(W), Scatter(copy_u), ApplyEdge(x e_uv), Gather(sum),
+//                       ApplyVertex(+b, sigma)]
+// with the graph part fused into one kernel over an index:
+//   Y[r, :] = act( b + sum_{i in row r} w[eid_i] * X[nbr_i, :] )
+// Forward: index = csr_dst, X = H W.  Backward: index = csc_src, X = dZ (= dOut masked by the
+// ReLU of the forward output), no bias/activation -- the transpose of the same aggregate.
+// Same unified thread mapping as the GAT kernels (gat.cu): one warp per work item, edge
+// weights staged per 32-edge block in shared memory, 16-byte column gathers, hub rows split
+// with fixed-order partial merges (deterministic).
+#include "common.cuh"
+#include "gat_common.cuh"
+
+#include <cstdlib>
+
+namespace gnncg_b200 {
+namespace {
+
+using namespace gat;
+
+struct SpmmParams {
+  const uint64_t* off;
+  const uint32_t* nbr;
+  const uint32_t* eid;
+  const uint32_t* items;
+  int64_t num_items, num_split_items;
+  int chunk, cols;
+  const float *w, *X, *bias;
+  float *Y, *part;
+  int relu;
+};
+
+struct SpmmSmem {
+  uint32_t nb[32];
+  float w[32];
+};
+
+template <int VW, int NV, int OCC>
+__global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
+  __shared__ SpmmSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
+  SpmmSmem& sm = smem[wp];
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + wp;
+  if (wi >= p.num_items) return;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int F = p.cols;
+  const Cols<VW, NV> cols(lane, F, F);  // one "head" spanning all columns
+  Vec<VW> acc[NV];
+  zero(acc);
+  constexpr int U = GatherDepth<NV, OCC>::U;
+  for (uint64_t base = it.e0; base < it.e1; base += 32) {
+    const int n = (int)min((uint64_t)32, it.e1 - base);
+    if (lane < n) {
+      sm.nb[lane] = __ldg(p.nbr + base + lane);
+      sm.w[lane] = p.w ? __ldg(p.w + __ldg(p.eid + base + lane)) : 1.f;
+    }
+    __syncwarp();
+    int j = 0;
+    for (; j + U <= n; j += U) {
+      Vec<VW> x[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t]);
+#pragma unroll
+      for (int t = 0; t < U; ++t) {
+        const float a = sm.w[j + t];
+#pragma unroll
+        for (int i = 0; i < NV; ++i)
+#pragma unroll
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
+      }
+    }
+    for (; j < n; ++j) {
+      Vec<VW> x[NV];
+      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x);
+      const float a = sm.w[j];
+#pragma unroll
+      for (int i = 0; i < NV; ++i)
+#pragma unroll
+        for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[i].x[q], acc[i].x[q]);
+    }
+    __syncwarp();
+  }
+  if (!it.split) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (cols.ok[i]) {
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) {
+          float z = acc[i].x[q] + (p.bias ? __ldg(p.bias + cols.col[i] + q) : 0.f);
+          o.x[q] = p.relu ? fmaxf(z, 0.f) : z;
+        }
+        st_vec<VW>(p.Y + (int64_t)it.row * F + cols.col[i], o);
+      }
+    }
+  } else {
+    float* part = p.part + wi * (int64_t)F;
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
+  }
+}
+
+__global__ void spmm_merge_kernel(SpmmParams p, const uint32_t* __restrict__ split_rows,
+                                  const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
+  const int64_t sr = blockIdx.x;
+  if (sr >= num_split_rows) return;
+  const int F = p.cols;
+  const uint32_t row = split_rows[sr];
+  for (int c = threadIdx.x; c < F; c += blockDim.x) {
+    float s = 0.f;
+    for (int64_t it = split_first[sr]; it < split_first[sr + 1]; ++it) s += p.part[it * F + c];
+    s += p.bias ? p.bias[c] : 0.f;
+    p.Y[(int64_t)row * F + c] = p.relu ? fmaxf(s, 0.f) : s;
+  }
+}
+
+// dZ = dOut * [out > 0] (ReLU backward from the stored output) ; db partials per block.
+constexpr int kColBlocks = 592;
+
+__global__ void relu_bwd_kernel(int64_t rows, int F, const float* __restrict__ dOut, const float* __restrict__ out,
+                                float* __restrict__ dZ, int relu) {
+  const int64_t n = rows * F;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dZ[i] = (!relu || out[i] > 0.f) ? dOut[i] : 0.f;
+}
+
+__global__ void colsum_partial_kernel(int64_t rows, int F, const float* __restrict__ X, float* __restrict__ part) {
+  const int c = blockIdx.y * blockDim.x + threadIdx.x;
+  if (c >= F) return;
+  const int64_t per = ceil_div(rows, (int64_t)gridDim.x);
+  const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
+  float s = 0.f;
+  for (int64_t r = r0; r < r1; ++r) s += __ldg(X + r * F + c);
+  part[(int64_t)blockIdx.x * F + c] = s;
+}
+
+__global__ void colsum_final_kernel(int nb, int F, const float* __restrict__ part, float* __restrict__ out) {
+  const int c = blockIdx.x * blockDim.x + threadIdx.x;
+  if (c >= F) return;
+  float s = 0.f;
+  for (int b = 0; b < nb; ++b) s += part[(int64_t)b * F + c];
+  out[c] = s;
+}
+
+// w[e] = 1 / sqrt(max(1, in_deg(dst e)) * max(1, out_deg(src e)))   (symmetric GCN normalisation)
+__global__ void gcn_norm_kernel(int64_t E, const uint32_t* __restrict__ src, const uint32_t* __restrict__ dst,
+                                const uint64_t* __restrict__ doff, const uint64_t* __restrict__ soff,
+                                float* __restrict__ w) {
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint32_t u = src[e], v = dst[e];
+    const double din = (double)max((uint64_t)1, doff[v + 1] - doff[v]);
+    const double dout = (double)max((uint64_t)1, soff[u + 1] - soff[u]);
+    w[e] = (float)(1.0 / sqrt(din * dout));
+  }
+}
+
+// CTAs per SM the gather kernel is built for (GNNCG_SPMM_OCC=2|4, default 4: the kernel is
+// a pure gather-FMA, so more resident warps buy more bytes in flight).
+int spmm_occupancy() {
+  static const int occ = [] {
+    const char* e = getenv("GNNCG_SPMM_OCC");
+    return (e && atoi(e) == 2) ? 2 : 4;
+  }();
+  return occ;
+}
+
+template <int VW, int OCC>
+int launch_spmm_occ(const SpmmParams& p, dim3 grid, cudaStream_t s) {
+  const int nvec = (int)ceil_div(p.cols / VW, 32);
+  if (nvec <= 1) spmm_kernel<VW, 1, OCC><<<grid, THREADS, 0, s>>>(p);
+  else if (nvec <= 2) spmm_kernel<VW, 2, OCC><<<grid, THREADS, 0, s>>>(p);
+  else if (nvec <= 4) spmm_kernel<VW, 4, OCC><<<grid, THREADS, 0, s>>>(p);
+  else if (nvec <= 8) spmm_kernel<VW, 8, OCC><<<grid, THREADS, 0, s>>>(p);
+  else return fail(GNNCG_ERR_UNSUPPORTED, "spmm: cols = %d exceeds the compiled limit %d", p.cols, 256 * VW);
+  return GNNCG_OK;
+}
+
+template <int VW>
+int launch_spmm(const SpmmParams& p, dim3 grid, cudaStream_t s) {
+  return spmm_occupancy() == 2 ? launch_spmm_occ<VW, 2>(p, grid, s) : launch_spmm_occ<VW, 4>(p, grid, s);
+}
+
+}  // namespace
+}  // namespace gnncg_b200
+
+using namespace gnncg_b200;
+
+extern "C" {
+
+size_t gnncg_spmm_workspace(const gnncg_sched_t* sched, int cols) {
+  return sched ? align_up((size_t)sched->num_split_items * cols * sizeof(float)) : 0;
+}
+
+int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, const float* edge_w, const float* X,
+               const float* bias, int relu, float* Y, void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(idx && sched && cols >= 1, GNNCG_ERR_ARG, "spmm: bad argument");
+  GNNCG_REQUIRE(sched->chunk >= 32, GNNCG_ERR_ARG, "spmm: schedule chunk < 32");
+  if (sched->num_items == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(idx->off && idx->nbr && X && Y && sched->items, GNNCG_ERR_ARG, "spmm: null pointer");
+  GNNCG_REQUIRE(!edge_w || idx->eid, GNNCG_ERR_ARG, "spmm: edge weights need the index's eid array");
+  const size_t need = gnncg_spmm_workspace(sched, cols);
+  GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "spmm: workspace %zu < %zu", ws_bytes,
+                need);
+  SpmmParams p{idx->off, idx->nbr, idx->eid, sched->items, sched->num_items, sched->num_split_items, sched->chunk,
+               cols, edge_w, X, bias, Y, static_cast<float*>(ws), relu};
+  cudaStream_t s = as_stream(stream);
+  dim3 grid((unsigned)ceil_div(sched->num_items, WARPS));
+  int rc = cols % 4 == 0 ? launch_spmm<4>(p, grid, s) : (cols % 2 == 0 ? launch_spmm<2>(p, grid, s)
+                                                                         : launch_spmm<1>(p, grid, s));
+  if (rc) return rc;
+  GNNCG_LAUNCH_CHECK();
+  if (sched->num_split_rows > 0) {
+    spmm_merge_kernel<<<(unsigned)sched->num_split_rows, 256, 0, s>>>(p, sched->split_rows, sched->split_first,
+                                                                    sched->num_split_rows);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+size_t gnncg_relu_bwd_workspace(int cols) { return align_up((size_t)kColBlocks * cols * sizeof(float)); }
+
+int gnncg_relu_bwd(int64_t rows, int cols, const float* dOut, const float* out, int relu, float* dZ, float* dbias,
+                   void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(rows >= 0 && cols >= 1, GNNCG_ERR_SHAPE, "relu_bwd: bad shape");
+  GNNCG_REQUIRE(dOut && dZ && (!relu || out), GNNCG_ERR_ARG, "relu_bwd: null pointer");
+  cudaStream_t s = as_stream(stream);
+  if (rows > 0) {
+    relu_bwd_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * cols, 256), 148 * 16), 256, 0, s>>>(
+        rows, cols, dOut, out, dZ, relu);
+    GNNCG_LAUNCH_CHECK();
+  }
+  if (dbias) {
+    GNNCG_REQUIRE(ws && ws_bytes >= gnncg_relu_bwd_workspace(cols), GNNCG_ERR_WORKSPACE, "relu_bwd: workspace");
+    float* part = static_cast<float*>(ws);
+    dim3 g1(kColBlocks, (unsigned)ceil_div(cols, 256));
+    colsum_partial_kernel<<<g1, 256, 0, s>>>(rows, cols, dZ, part);
+    GNNCG_LAUNCH_CHECK();
+    colsum_final_kernel<<<(unsigned)ceil_div(cols, 256), 256, 0, s>>>(kColBlocks, cols, part, dbias);
+    GNNCG_LAUNCH_CHECK();
+  }
+  return GNNCG_OK;
+}
+
+int gnncg_gcn_norm(int64_t num_edges, const uint32_t* edge_src, const uint32_t* edge_dst, const gnncg_index_t* csr_dst,
+                   const gnncg_index_t* csc_src, float* w, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(csr_dst && csc_src && (num_edges == 0 || (edge_src && edge_dst && w)), GNNCG_ERR_ARG,
+                "gcn_norm: null pointer");
+  if (num_edges == 0) return GNNCG_OK;
+  gcn_norm_kernel<<<(unsigned)std::min<int64_t>(ceil_div(num_edges, 256), 148 * 16), 256, 0, as_stream(stream)>>>(
+      num_edges, edge_src, edge_dst, csr_dst->off, csc_src->off, w);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+}  // extern "C"

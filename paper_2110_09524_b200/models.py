@@ -175,6 +175,47 @@ class MoNet:
         return self.loss[:1], grads
 
 
+class GCN:
+    """Vanilla GCN stack: h' = relu(b + sum_e w_e h_u W) per
+    layer with the symmetric edge normalisation, loss = sum of exits, SGD on W and b."""
+
+    def __init__(self, g: DeviceGraph, dims, seed: int = 0, chunk: int | None = None):
+        from .ops import gcn_norm
+
+        self.g, self.chunk = g, chunk
+        dev = g.device
+        gen = torch.Generator(device=dev)
+        gen.manual_seed(seed)
+        self.layers = [(init_uniform(a, b, gen, dev), init_uniform(1, b, gen, dev).view(b))
+                       for a, b in zip(dims[:-1], dims[1:])]
+        self.edge_w = gcn_norm(g)
+        self.loss = torch.zeros(4, device=dev)
+        self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
+
+    def train_step(self, H: torch.Tensor, lr: float = 0.0):
+        from .ops import gcn_backward, gcn_forward
+
+        xs, stashes = [H], []
+        for W, b in self.layers:
+            out, st = gcn_forward(self.g, xs[-1], W, b, self.edge_w, chunk=self.chunk)
+            xs.append(out)
+            stashes.append(st)
+        out = xs[-1]
+        call("gnncg_sum", out.numel(), _ptr(out), _ptr(self.loss), _ptr(self._sum_ws), self._sum_ws.numel(), _stream())
+        g = torch.empty_like(out)
+        call("gnncg_fill", g.numel(), 1.0, _ptr(g), _stream())
+        grads = [None] * len(self.layers)
+        for i in reversed(range(len(self.layers))):
+            W, b = self.layers[i]
+            dH, dW, db = gcn_backward(self.g, xs[i], W, stashes[i], g, self.edge_w, need_dH=i > 0, chunk=self.chunk)
+            grads[i] = (dW, db)
+            g = dH
+        for (W, b), (dW, db) in zip(self.layers, grads):
+            call("gnncg_sgd_update", W.numel(), lr, _ptr(dW), _ptr(W), _stream())
+            call("gnncg_sgd_update", b.numel(), lr, _ptr(db), _ptr(b), _stream())
+        return self.loss[:1], grads
+
+
 class GraphedStep:
     """A training step captured once into a CUDA graph and replayed (launch-bound small graphs).
 

@@ -9,6 +9,7 @@ contracts of its specified executor:
   gat_forward / gat_backward           GAT layer (App. B)
   edgeconv_forward / edgeconv_backward EdgeConv layer
   gmm_forward / gmm_backward           GMMConv layer
+  gcn_forward / gcn_backward / spmm    GCN layer, weighted Aggregate
   matmul / matmul_nt / matmul_tn       dense transforms (tensor.cpp:8-60)
 
 All tensors are fp32 CUDA tensors; every FLOP runs in libgnncg_b200.so.  torch
@@ -380,3 +381,73 @@ def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmSt
     dH = gemm(dY, torch.cat([W, P_l, P_r], dim=1), trans_b=True, ws=g.ws) if need_dH else None
     Kf = K * f
     return dH, dWcat[:, :Kf].contiguous(), dWcat[:, Kf:Kf + r].contiguous(), dWcat[:, Kf + r:].contiguous(), dmu, dsinv
+
+
+# ---------------------------------------------------------------------------
+# GCN (weighted Aggregate)
+# ---------------------------------------------------------------------------
+@dataclass
+class GcnStash:
+    Ht: torch.Tensor  # H W, V x F_out
+    out: torch.Tensor  # act(b + A_w Ht)
+
+
+def gcn_norm(g: DeviceGraph) -> torch.Tensor:
+    """Symmetric normalisation by edge id: w[e] = 1/sqrt(max(1,deg_in(dst)) max(1,deg_out(src)))."""
+    w = torch.empty(g.num_edges, dtype=torch.float32, device=g.device)
+    call("gnncg_gcn_norm", g.num_edges, _ptr(g.edge_src), _ptr(g.edge_dst), g.csr_dst.struct(), g.csc_src.struct(),
+         _ptr(w), _stream())
+    return w
+
+
+def spmm(g: DeviceGraph, X, edge_w=None, bias=None, relu=False, transpose=False, out=None, chunk=None):
+    """Y = act(bias + A_w X) with A_w[v,u] = sum of w[e] over edges u -> v (transpose: A_w^T X,
+    i.e. the sum runs over out-edges).  One fused kernel (csrc/spmm.cu)."""
+    X = _f32(X, "X")
+    idx = g.csc_src if transpose else g.csr_dst
+    V, C_ = g.num_vertices, X.shape[1]
+    _shape(X, (V, C_), "X")
+    if edge_w is not None:
+        edge_w = _f32(edge_w, "edge_w")
+        _shape(edge_w, (g.num_edges,), "edge_w")
+    if bias is not None:
+        bias = _f32(bias, "bias")
+        _shape(bias, (C_,), "bias")
+    out = torch.empty(V, C_, device=X.device) if out is None else out
+    sched = idx.sched(chunk) if chunk else idx.sched()
+    need = _lib.lib().gnncg_spmm_workspace(sched.struct(), C_)
+    wp, wn = g.ws.get(need)
+    with PROBE("spmm_t" if transpose else "spmm"):
+        call("gnncg_spmm", idx.struct(), sched.struct(), C_, _ptr(edge_w), _ptr(X), _ptr(bias), int(relu), _ptr(out),
+             wp, wn, _stream())
+    return out
+
+
+def gcn_forward(g: DeviceGraph, H, W, b, edge_w=None, relu=True, chunk=None):
+    """GCN layer forward: out = relu(b + A_w (H W))  (SPEC.md:184 gcn).
+    Transform first (F_out <= F_in on the benchmark shapes), then one fused aggregate kernel."""
+    H, W = _f32(H, "H"), _f32(W, "W")
+    if W.shape[0] != H.shape[1]:
+        raise TensorError("gcn_forward: W must be (F_in, F_out)")
+    Ht = gemm(H, W, ws=g.ws)
+    out = spmm(g, Ht, edge_w, b, relu, chunk=chunk)
+    return out, GcnStash(Ht, out)
+
+
+def gcn_backward(g: DeviceGraph, H, W, stash: GcnStash, dOut, edge_w=None, relu=True, need_dH=True, chunk=None):
+    """Returns (dH, dW, db): dZ = dOut * relu'(out), db = colsum dZ, dHt = A_w^T dZ (csc_src),
+    dW = H^T dHt, dH = dHt W^T."""
+    H = _f32(H, "H")
+    dOut = _f32(dOut, "dOut")
+    V, C_ = stash.out.shape
+    _shape(dOut, (V, C_), "dOut")
+    dZ = torch.empty(V, C_, device=H.device)
+    db = torch.empty(C_, device=H.device)
+    need = _lib.lib().gnncg_relu_bwd_workspace(C_)
+    wp, wn = g.ws.get(need)
+    with PROBE("relu_bwd"):
+        call("gnncg_relu_bwd", V, C_, _ptr(dOut), _ptr(stash.out), int(relu), _ptr(dZ), _ptr(db), wp, wn, _stream())
+    dHt = spmm(g, dZ, edge_w, transpose=True, chunk=chunk)
+    dW = gemm(H, dHt, trans_a=True, ws=g.ws)
+    dH = gemm(dHt, W, trans_b=True, ws=g.ws) if need_dH else None
+    return dH, dW, db

@@ -318,3 +318,49 @@ def test_cost_module_matches_spec_and_oracle():
         assert cost.gat_attention_flops(V, E, f)["reorganized"] == c["flops_reorg"]
     r = cost.gat_layer_report(233000, 114000000, 8, 32)
     assert r["stash_bytes_saved"] > 7e9  # recompute drops the O(|E| h) stash: ~7.3 GB per Reddit layer
+
+
+# ---------------------------------------------------------------- GCN (§8f rank 3)
+def test_gcn_aggregate_g3_and_dense_oracle():
+    # G3, w = 1, H = [[1],[2],[4]] -> [0, 1, 3]; the index-order walk agrees
+    # with the dense-adjacency oracle forward and transposed, weighted.
+    g = G3()
+    assert list(O.gcn_aggregate(g, np.array([[1.0], [2.0], [4.0]]))[:, 0]) == [0, 1, 3]
+    rng = np.random.default_rng(5)
+    V, E = 40, 300
+    src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
+    g = O.host_graph(V, src, dst)
+    X, w = rng.standard_normal((V, 6)), rng.standard_normal(E)
+    assert np.abs(O.gcn_aggregate(g, X, w) - O.dense_aggregate_f64(V, src, dst, X, w)).max() < 1e-12
+    assert np.abs(O.gcn_aggregate(g, X, w, transpose=True) - O.dense_aggregate_f64(V, dst, src, X, w)).max() < 1e-12
+    b = rng.standard_normal(6)
+    relu = O.gcn_aggregate(g, X, w, b, relu=True)
+    assert np.abs(relu - np.maximum(O.dense_aggregate_f64(V, src, dst, X, w) + b, 0.0)).max() < 1e-12
+
+
+def test_gcn_norm_definition():
+    g = O.host_graph(4, [0, 0, 1, 2, 2, 2], [1, 2, 2, 3, 3, 0])
+    w = O.gcn_norm(g)
+    din = np.diff(g.dst_off.astype(np.int64))
+    dout = np.diff(g.src_off.astype(np.int64))
+    ref = 1.0 / np.sqrt(np.maximum(din[g.dst], 1) * np.maximum(dout[g.src], 1))
+    assert np.array_equal(w, ref.astype(np.float32))
+
+
+@pytest.mark.parametrize("graph", ["G3", "ER16"])
+def test_gcn_finite_differences(graph):
+    # SPEC.md:484 acceptance 5 for GCN: analytic vs central differences (f64, 1e-4 step, 1e-4 rel)
+    if graph == "G3":
+        V, src, dst = 3, [0, 1, 0], [2, 2, 1]
+    else:
+        V, src, dst = 16, *np.nonzero(np.random.default_rng(7).random((16, 16)) < 0.3)
+    g = O.host_graph(V, src, dst)
+    rng = np.random.default_rng(42)
+    Fin, C_ = 3, 4
+    H, W, b = rng.standard_normal((V, Fin)), rng.standard_normal((Fin, C_)), rng.standard_normal(C_) + 0.5
+    w = O.gcn_norm(g).astype(np.float64)
+    ones = np.ones((V, C_))
+    fw = O.gcn_layer_fwd_f64(g, H, W, b, w)
+    bw = O.gcn_layer_bwd_f64(g, H, W, fw, ones, w)
+    loss = lambda: O.gcn_layer_fwd_f64(g, H, W, b, w)["out"].sum()  # noqa: E731
+    _fd_check(loss, [W, b, H], [bw["dW"], bw["db"], bw["dH"]])
