@@ -128,6 +128,8 @@ class DeviceGraph {
   std::int64_t num_edges() const { return E_; }
   const DeviceIndex& csr_dst() const { return dst_; }
   const DeviceIndex& csc_src() const { return src_; }
+  const std::uint32_t* edge_src() const { return edge_src_.get<std::uint32_t>(); }
+  const std::uint32_t* edge_dst() const { return edge_dst_.get<std::uint32_t>(); }
   cudaStream_t stream() const { return s_; }
   DeviceBuffer& workspace(size_t bytes) const {
     ws_.ensure(bytes);
@@ -425,6 +427,68 @@ inline GmmGrads gmm_backward(const DeviceGraph& g, const Tensor<float>& H, const
   if (need_dH) {
     DeviceBuffer dHb(V * Fin * 4);
     detail::gemm(g, 0, 1, V, Fin, ldy, dY.get<float>(), ldy, dWc.get<float>(), ldy, dHb.get<float>(), Fin);
+    out.dH = download(dHb, V, Fin, s);
+  }
+  return out;
+}
+
+// GCN: out = relu(b + sum_e w_e H[u] W) with the symmetric
+// normalisation w_e = 1/sqrt(max(1,deg_in(v)) max(1,deg_out(u))) computed on the device.
+struct GcnStash {
+  DeviceBuffer Ht, out, w;
+};
+
+struct GcnGrads {
+  Tensor<float> dH, dW, db;
+};
+
+inline Tensor<float> gcn_forward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
+                                 const Tensor<float>& b, GcnStash* stash) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, C = W.cols;
+  detail::require_shape(W, Fin, C, "gcn W");
+  detail::require_shape(b, 1, C, "gcn b");
+  cudaStream_t s = g.stream();
+  GcnStash local;
+  GcnStash& st = stash ? *stash : local;
+  DeviceBuffer dH = upload(H, s), dW = upload(W, s), db = upload(b, s);
+  st.Ht = DeviceBuffer(V * C * 4);
+  st.out = DeviceBuffer(V * C * 4);
+  st.w = DeviceBuffer(g.num_edges() * 4);
+  const gnncg_index_t csr = g.csr_dst().view(), csc = g.csc_src().view();
+  check(gnncg_gcn_norm(g.num_edges(), g.edge_src(), g.edge_dst(), &csr, &csc, st.w.get<float>(), s), "gnncg_gcn_norm");
+  detail::gemm(g, 0, 0, V, C, Fin, dH.get<float>(), Fin, dW.get<float>(), C, st.Ht.get<float>(), C);
+  DeviceBuffer& ws = g.workspace(gnncg_spmm_workspace(&g.csr_dst().sched, (int)C));
+  check(gnncg_spmm(&csr, &g.csr_dst().sched, (int)C, st.w.get<float>(), st.Ht.get<float>(), db.get<float>(), 1,
+                   st.out.get<float>(), ws.get(), ws.bytes(), s),
+        "gnncg_spmm");
+  return download(st.out, V, C, s);
+}
+
+inline GcnGrads gcn_backward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W, const GcnStash& st,
+                             const Tensor<float>& dOut, bool need_dH) {
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, C = W.cols;
+  detail::require_shape(dOut, V, C, "gcn dOut");
+  cudaStream_t s = g.stream();
+  DeviceBuffer dH = upload(H, s), dWin = upload(W, s), g_out = upload(dOut, s);
+  DeviceBuffer dZ(V * C * 4), db(C * 4), dHt(V * C * 4), dW(Fin * C * 4);
+  {
+    DeviceBuffer& ws = g.workspace(gnncg_relu_bwd_workspace((int)C));
+    check(gnncg_relu_bwd(V, (int)C, g_out.get<float>(), st.out.get<float>(), 1, dZ.get<float>(), db.get<float>(),
+                         ws.get(), ws.bytes(), s),
+          "gnncg_relu_bwd");
+  }
+  const gnncg_index_t csc = g.csc_src().view();
+  DeviceBuffer& ws = g.workspace(gnncg_spmm_workspace(&g.csc_src().sched, (int)C));
+  check(gnncg_spmm(&csc, &g.csc_src().sched, (int)C, st.w.get<float>(), dZ.get<float>(), nullptr, 0, dHt.get<float>(),
+                   ws.get(), ws.bytes(), s),
+        "gnncg_spmm");
+  detail::gemm(g, 1, 0, Fin, C, V, dH.get<float>(), Fin, dHt.get<float>(), C, dW.get<float>(), C);
+  GcnGrads out;
+  out.dW = download(dW, Fin, C, s);
+  out.db = download(db, 1, C, s);
+  if (need_dH) {
+    DeviceBuffer dHb(V * Fin * 4);
+    detail::gemm(g, 0, 1, V, Fin, C, dHt.get<float>(), C, dWin.get<float>(), C, dHb.get<float>(), Fin);
     out.dH = download(dHb, V, Fin, s);
   }
   return out;

@@ -133,6 +133,27 @@ int main() {
   b200::GmmGrads gg = b200::gmm_backward(dg, H, Wg, Pl, Pr, mu, sinv, gp, gst, TensorF(V, gp.f, 1.0f), true);
   ok = ok && worst_g < 1e-4 && all_finite(gg.dW) && all_finite(gg.dmu) && all_finite(gg.dsinv) && gg.dH.rows == V;
   std::printf("gmm forward max rel_err = %.3e\n", worst_g);
+
+  // GCN forward against a direct f64 evaluation over the reference's csr_dst
+  const TensorF Wc = init_seeded<float>(Fin, 12, 11), bc = init_seeded<float>(1, 12, 12);
+  b200::GcnStash cst;
+  TensorF co = b200::gcn_forward(dg, H, Wc, bc, &cst);
+  const AdjIndex& outx = g.csc_src();
+  auto deg_out = [&](std::uint64_t u) { return std::max<std::uint64_t>(1, outx.offsets[u + 1] - outx.offsets[u]); };
+  double worst_c = 0.0;
+  for (std::uint64_t v = 0; v < V; ++v)
+    for (int j = 0; j < 12; ++j) {
+      double z = bc.at(0, j);
+      const double din = (double)std::max<std::uint64_t>(1, in.offsets[v + 1] - in.offsets[v]);
+      for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i) {
+        const auto u = in.entries[i].vertex;
+        z += dotrow(H, u, Wc, j) / std::sqrt(din * (double)deg_out(u));
+      }
+      worst_c = std::max(worst_c, rel_err(z > 0 ? z : 0.0, co.at(v, j)));
+    }
+  b200::GcnGrads cg = b200::gcn_backward(dg, H, Wc, cst, TensorF(V, 12, 1.0f), true);
+  ok = ok && worst_c < 1e-4 && all_finite(cg.dW) && all_finite(cg.db) && cg.dH.rows == V;
+  std::printf("gcn forward max rel_err = %.3e\n", worst_c);
   std::printf("%s\n", ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
 }
