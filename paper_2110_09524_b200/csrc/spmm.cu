@@ -26,10 +26,11 @@ struct SpmmParams {
   const uint32_t* eid;
   const uint32_t* items;
   int64_t num_items, num_split_items;
-  int chunk, cols;
+  int chunk, cols, tile;  // tile = columns per blockIdx.y slice (multiple of VW)
   const float *w, *X, *bias;
   float *Y, *part;
   int relu;
+  int64_t hot_rows;
 };
 
 struct SpmmSmem {
@@ -46,10 +47,18 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
   if (wi >= p.num_items) return;
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int F = p.cols;
-  const Cols<VW, NV> cols(lane, F, F);  // one "head" spanning all columns
+  // column slice of this CTA row (wide feature matrices are split over blockIdx.y)
+  const int c0 = blockIdx.y * p.tile, c1 = min(F, c0 + p.tile);
+  Cols<VW, NV> cols(lane, F, F);
+#pragma unroll
+  for (int i = 0; i < NV; ++i) {
+    cols.col[i] += c0;
+    cols.ok[i] = cols.col[i] < c1;
+  }
   Vec<VW> acc[NV];
   zero(acc);
   constexpr int U = GatherDepth<NV, OCC>::U;
+  const L2Hint hint = make_l2_hint(p.hot_rows);
   for (uint64_t base = it.e0; base < it.e1; base += 32) {
     const int n = (int)min((uint64_t)32, it.e1 - base);
     if (lane < n) {
@@ -61,7 +70,7 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
     for (; j + U <= n; j += U) {
       Vec<VW> x[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t]);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t], hint);
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         const float a = sm.w[j + t];
@@ -73,7 +82,7 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
     }
     for (; j < n; ++j) {
       Vec<VW> x[NV];
-      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x);
+      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x, hint);
       const float a = sm.w[j];
 #pragma unroll
       for (int i = 0; i < NV; ++i)
@@ -168,18 +177,21 @@ int spmm_occupancy() {
 }
 
 template <int VW, int OCC>
-int launch_spmm_occ(const SpmmParams& p, dim3 grid, cudaStream_t s) {
-  const int nvec = (int)ceil_div(p.cols / VW, 32);
+int launch_spmm_occ(SpmmParams p, dim3 grid, cudaStream_t s) {
+  // split the columns into the fewest slices of <= 8 vectors per lane, evenly
+  const int vecs = p.cols / VW, slices = (int)ceil_div(vecs, 32 * 8), per = (int)ceil_div(vecs, slices);
+  p.tile = per * VW;
+  grid.y = (unsigned)slices;
+  const int nvec = (int)ceil_div(per, 32);
   if (nvec <= 1) spmm_kernel<VW, 1, OCC><<<grid, THREADS, 0, s>>>(p);
   else if (nvec <= 2) spmm_kernel<VW, 2, OCC><<<grid, THREADS, 0, s>>>(p);
   else if (nvec <= 4) spmm_kernel<VW, 4, OCC><<<grid, THREADS, 0, s>>>(p);
   else if (nvec <= 8) spmm_kernel<VW, 8, OCC><<<grid, THREADS, 0, s>>>(p);
-  else return fail(GNNCG_ERR_UNSUPPORTED, "spmm: cols = %d exceeds the compiled limit %d", p.cols, 256 * VW);
   return GNNCG_OK;
 }
 
 template <int VW>
-int launch_spmm(const SpmmParams& p, dim3 grid, cudaStream_t s) {
+int launch_spmm(const SpmmParams& p, dim3 grid, cudaStream_t s) {  // grid.y is set per column slicing
   return spmm_occupancy() == 2 ? launch_spmm_occ<VW, 2>(p, grid, s) : launch_spmm_occ<VW, 4>(p, grid, s);
 }
 
@@ -200,13 +212,15 @@ int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, c
   GNNCG_REQUIRE(idx && sched && cols >= 1, GNNCG_ERR_ARG, "spmm: bad argument");
   GNNCG_REQUIRE(sched->chunk >= 32, GNNCG_ERR_ARG, "spmm: schedule chunk < 32");
   if (sched->num_items == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(idx->off && idx->nbr && X && Y && sched->items, GNNCG_ERR_ARG, "spmm: null pointer");
-  GNNCG_REQUIRE(!edge_w || idx->eid, GNNCG_ERR_ARG, "spmm: edge weights need the index's eid array");
+  GNNCG_REQUIRE(idx->off && X && Y && sched->items && (idx->num_edges == 0 || idx->nbr), GNNCG_ERR_ARG,
+                "spmm: null pointer");
+  GNNCG_REQUIRE(!edge_w || idx->num_edges == 0 || idx->eid, GNNCG_ERR_ARG,
+                "spmm: edge weights need the index's eid array");
   const size_t need = gnncg_spmm_workspace(sched, cols);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "spmm: workspace %zu < %zu", ws_bytes,
                 need);
   SpmmParams p{idx->off, idx->nbr, idx->eid, sched->items, sched->num_items, sched->num_split_items, sched->chunk,
-               cols, edge_w, X, bias, Y, static_cast<float*>(ws), relu};
+               cols, 0, edge_w, X, bias, Y, static_cast<float*>(ws), relu, l2_hot_rows()};
   cudaStream_t s = as_stream(stream);
   dim3 grid((unsigned)ceil_div(sched->num_items, WARPS));
   int rc = cols % 4 == 0 ? launch_spmm<4>(p, grid, s) : (cols % 2 == 0 ? launch_spmm<2>(p, grid, s)

@@ -6,7 +6,7 @@ import pytest
 import torch
 
 from oracle import oracle as O
-from paper_2110_09524_b200 import DeviceGraph, UnsupportedError, gcn_backward, gcn_forward, gcn_norm, spmm
+from paper_2110_09524_b200 import DeviceGraph, gcn_backward, gcn_forward, gcn_norm, spmm
 from paper_2110_09524_b200.models import GCN
 from tests.test_gpu_gat import make_graph, np64, t32
 
@@ -15,7 +15,7 @@ TOL = 1e-4
 
 
 @pytest.mark.parametrize("kind", ["G3", "ER16", "cora", "star", "powerlaw"])
-@pytest.mark.parametrize("cols", [1, 3, 6, 64, 256, 602])
+@pytest.mark.parametrize("cols", [1, 3, 6, 64, 256, 602, 1030])
 @pytest.mark.parametrize("transpose", [False, True])
 def test_spmm_vs_oracle(cuda, kind, cols, transpose):
     hg, g = make_graph(kind, cuda)
@@ -39,8 +39,9 @@ def test_spmm_empty_graph_and_limits(cuda):
     out = spmm(g, X, bias=b, relu=True)
     assert torch.equal(out, b.expand(5, 8))  # empty rows: act(bias)
     hg, g = make_graph("ER16", cuda)
-    with pytest.raises(UnsupportedError):
-        spmm(g, torch.ones(16, 1025, device=cuda))
+    X = torch.rand(16, 2500, device=cuda)  # several column tiles
+    ref = O.gcn_aggregate(hg, X.cpu().numpy())
+    assert O.max_rel_err(np64(spmm(g, X)), ref) < TOL
 
 
 @pytest.mark.parametrize("kind", ["G3", "ER16", "star", "powerlaw"])
@@ -69,9 +70,9 @@ def test_gcn_layer_vs_oracle(cuda, kind, Fin, C):
     # the backward is checked given the forward's stash: the ReLU mask is the device output's
     # (a z within fp32 rounding of 0 may legitimately fall either side)
     bw = O.gcn_layer_bwd_f64(hg, H, W, {"out": np64(out)}, dOut, w.astype(np.float64))
-    assert O.max_rel_err(np64(dH), bw["dH"]) < TOL
-    assert O.max_rel_err(np64(dW), bw["dW"]) < TOL
-    assert O.max_rel_err(np64(db), bw["db"]) < TOL
+    for name, got in (("dH", dH), ("dW", dW), ("db", db)):
+        scale = max(1.0, np.abs(bw[name]).max())  # reductions over V: compare relative to the magnitude
+        assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name
 
 
 def test_gcn_training_loss_decreases(cuda):
