@@ -48,7 +48,6 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(Gat
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
   constexpr int U = GatherDepth<NV, OCC>::U;
-  const L2Hint hint = make_l2_hint(p.hot_rows);
 
   // Per-warp shared state (keeps registers for the gathers): stat[3] = A_r[v], stat[0] = running
   // max per head (warp-uniform), t1[lane][k] = this lane's running exp-sum partial.
@@ -104,7 +103,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(Gat
     for (; j + U <= n; j += U) {
       Vec<VW> x[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[j + t], hf, cols, x[t], hint);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[j + t], hf, cols, x[t]);
 #pragma unroll
       for (int t = 0; t < U; ++t)
 #pragma unroll
@@ -116,7 +115,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(Gat
     }
     for (; j < n; ++j) {
       Vec<VW> x[NV];
-      gather_row<VW, NV>(p.Ht, sm.nb[j], hf, cols, x, hint);
+      gather_row<VW, NV>(p.Ht, sm.nb[j], hf, cols, x);
 #pragma unroll
       for (int i = 0; i < NV; ++i) {
         const float a = sm.t0[j * TS + cols.hd[i]];
@@ -467,7 +466,6 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   const float slope = p.slope;
   const int64_t u = it.row;
   const int r = lane & (PER - 1);  // rank inside the head's lane group
-  const L2Hint hint = make_l2_hint(p.hot_rows);
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
   const Cols<VW, NV> cols(lane, hf, f);
@@ -510,7 +508,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
     for (int j = 0; j < n; j += U) {
       Vec<VW> gv[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[(j + t) & 31], hf, cols, gv[t], hint);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[(j + t) & 31], hf, cols, gv[t]);
       float pd[NVAL];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
@@ -877,14 +875,6 @@ int gat::gat_occupancy() {
   return v;
 }
 
-int64_t gat::l2_hot_rows() {
-  static const int64_t v = [] {
-    const char* e = getenv("GNNCG_L2_HOT_ROWS");
-    return e ? (int64_t)atoll(e) : (int64_t)-1;
-  }();
-  return v;
-}
-
 namespace {
 
 // GNNCG_GAT_TMA=1 selects the TMA-fed forward (gat_tma.cu).  Default off: measured slower
@@ -958,7 +948,6 @@ int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int 
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
-  p.hot_rows = l2_hot_rows();
   p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -993,7 +982,6 @@ int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, 
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_dst: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
-  p.hot_rows = l2_hot_rows();
   p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -1027,7 +1015,6 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_src: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
-  p.hot_rows = l2_hot_rows();
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -1087,7 +1074,6 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
   cudaStream_t s = as_stream(stream);
   GNNCG_CUDA_TRY(cudaMemsetAsync(dAr, 0, sizeof(float) * (size_t)num_local * h, s));
   GatParams p{};
-  p.hot_rows = l2_hot_rows();
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;

@@ -89,7 +89,6 @@ struct GatParams {
   int64_t row_base, num_local;
   const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
-  int64_t hot_rows;  // L2 hint for the neighbour-row gathers (L2Hint; < 0 = off)
 };
 
 // ---------------------------------------------------------------------------
@@ -146,51 +145,6 @@ __device__ __forceinline__ void gather_row(const float* __restrict__ base, int64
 #pragma unroll
   for (int i = 0; i < NV; ++i) x[i] = ldg_vec<VW>(row + (c.ok[i] ? c.col[i] : 0));
 }
-
-// L2 residency hint for the neighbour-row gathers: rows [0, rows) are "hot" and loaded with
-// an L2 evict_last policy, the rest with evict_first, so that misses on the long tail do not
-// displace the frequently gathered rows.  rows < 0 disables the hints (plain loads).
-struct L2Hint {
-  int64_t rows;
-};
-
-__device__ __forceinline__ L2Hint make_l2_hint(int64_t rows) { return L2Hint{rows}; }
-
-// The policy is created per gathered row (one ALU op) instead of being held in registers.
-__device__ __forceinline__ uint64_t l2_policy(bool hot) {
-  uint64_t pol;
-  if (hot) asm("createpolicy.fractional.L2::evict_last.b64 %0, 1.0;" : "=l"(pol));
-  else asm("createpolicy.fractional.L2::evict_first.b64 %0, 1.0;" : "=l"(pol));
-  return pol;
-}
-
-template <int VW>
-__device__ __forceinline__ Vec<VW> ldg_vec_pol(const float* p, uint64_t pol) {
-  Vec<VW> r;
-  if constexpr (VW == 4) {
-    asm("ld.global.nc.L2::cache_hint.v4.f32 {%0, %1, %2, %3}, [%4], %5;"
-                 : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3])
-                 : "l"(p), "l"(pol));
-  } else if constexpr (VW == 2) {
-    asm("ld.global.nc.L2::cache_hint.v2.f32 {%0, %1}, [%2], %3;" : "=f"(r.x[0]), "=f"(r.x[1]) : "l"(p), "l"(pol));
-  } else {
-    asm("ld.global.nc.L2::cache_hint.f32 %0, [%1], %2;" : "=f"(r.x[0]) : "l"(p), "l"(pol));
-  }
-  return r;
-}
-
-template <int VW, int NV>
-__device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
-                                           Vec<VW> (&x)[NV], const L2Hint& hint) {
-  if (hint.rows < 0) return gather_row<VW, NV>(base, r, hf, c, x);
-  const float* row = base + r * hf;
-  const uint64_t pol = l2_policy(r < hint.rows);
-#pragma unroll
-  for (int i = 0; i < NV; ++i) x[i] = ldg_vec_pol<VW>(row + (c.ok[i] ? c.col[i] : 0), pol);
-}
-
-// Host side: GNNCG_L2_HOT_ROWS (rows; unset = hints off).
-int64_t l2_hot_rows();
 
 
 }  // namespace gat

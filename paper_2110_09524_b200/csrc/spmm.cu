@@ -30,7 +30,6 @@ struct SpmmParams {
   const float *w, *X, *bias;
   float *Y, *part;
   int relu;
-  int64_t hot_rows;
 };
 
 struct SpmmSmem {
@@ -58,7 +57,6 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
   Vec<VW> acc[NV];
   zero(acc);
   constexpr int U = GatherDepth<NV, OCC>::U;
-  const L2Hint hint = make_l2_hint(p.hot_rows);
   for (uint64_t base = it.e0; base < it.e1; base += 32) {
     const int n = (int)min((uint64_t)32, it.e1 - base);
     if (lane < n) {
@@ -70,7 +68,7 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
     for (; j + U <= n; j += U) {
       Vec<VW> x[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t], hint);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t]);
 #pragma unroll
       for (int t = 0; t < U; ++t) {
         const float a = sm.w[j + t];
@@ -82,7 +80,7 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
     }
     for (; j < n; ++j) {
       Vec<VW> x[NV];
-      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x, hint);
+      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x);
       const float a = sm.w[j];
 #pragma unroll
       for (int i = 0; i < NV; ++i)
@@ -220,7 +218,7 @@ int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, c
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "spmm: workspace %zu < %zu", ws_bytes,
                 need);
   SpmmParams p{idx->off, idx->nbr, idx->eid, sched->items, sched->num_items, sched->num_split_items, sched->chunk,
-               cols, 0, edge_w, X, bias, Y, static_cast<float*>(ws), relu, l2_hot_rows()};
+               cols, 0, edge_w, X, bias, Y, static_cast<float*>(ws), relu};
   cudaStream_t s = as_stream(stream);
   dim3 grid((unsigned)ceil_div(sched->num_items, WARPS));
   int rc = cols % 4 == 0 ? launch_spmm<4>(p, grid, s) : (cols % 2 == 0 ? launch_spmm<2>(p, grid, s)
