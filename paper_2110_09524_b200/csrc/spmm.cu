@@ -7,9 +7,9 @@
 //   Y[r, :] = act( b + sum_{i in row r} w[eid_i] * X[nbr_i, :] )
 // Forward: index = csr_dst, X = H W.  Backward: index = csc_src, X = dZ (= dOut masked by the
 // ReLU of the forward output), no bias/activation -- the transpose of the same aggregate.
-// Same unified thread mapping as the GAT kernels (gat.cu): one warp per work item, edge
-// weights staged per 32-edge block in shared memory, 16-byte column gathers, hub rows split
-// with fixed-order partial merges (deterministic).
+// Same unified thread mapping as the GAT kernels (gat.cu): one warp per work item (and column
+// slice), the 32-edge block's ids and weights held one per lane and broadcast by shuffle,
+// 16-byte column gathers, hub rows split with fixed-order partial merges (deterministic).
 #include "common.cuh"
 #include "gat_common.cuh"
 
@@ -32,17 +32,18 @@ struct SpmmParams {
   int relu;
 };
 
-struct SpmmSmem {
-  uint32_t nb[32];
-  float w[32];
+// Rows gathered per step (U) for a given per-lane width NV and CTAs/SM OCC: the register
+// budget (255 / 128 / 64 / 32 for OCC 1 / 2 / 4 / 8) bounds U * NV float4s in flight.
+template <int NV, int OCC>
+struct SpmmDepth {
+  static constexpr int U = OCC >= 8 ? (NV == 1 ? 4 : (NV == 2 ? 2 : 1))
+                                    : GatherDepth<NV, OCC>::U;
 };
 
 template <int VW, int NV, int OCC>
 __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
-  __shared__ SpmmSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, wp = threadIdx.x >> 5;
-  SpmmSmem& sm = smem[wp];
-  const int64_t wi = (int64_t)blockIdx.x * WARPS + wp;
+  const int lane = threadIdx.x & 31;
+  const int64_t wi = (int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5);
   if (wi >= p.num_items) return;
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int F = p.cols;
@@ -56,38 +57,50 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
   }
   Vec<VW> acc[NV];
   zero(acc);
-  constexpr int U = GatherDepth<NV, OCC>::U;
+  constexpr int U = SpmmDepth<NV, OCC>::U;
+  // Lane j holds edge j of the current 32-edge block (neighbour id, weight) in registers and
+  // the warp reads them by shuffle.  The next block's ids are loaded before the current
+  // block's gathers; its weights (a dependent load through eid) after them.
+  uint32_t nb = 0;
+  float a = 0.f;
+  if (it.e0 + lane < it.e1) {
+    nb = __ldg(p.nbr + it.e0 + lane);
+    a = p.w ? __ldg(p.w + __ldg(p.eid + it.e0 + lane)) : 1.f;
+  }
   for (uint64_t base = it.e0; base < it.e1; base += 32) {
     const int n = (int)min((uint64_t)32, it.e1 - base);
-    if (lane < n) {
-      sm.nb[lane] = __ldg(p.nbr + base + lane);
-      sm.w[lane] = p.w ? __ldg(p.w + __ldg(p.eid + base + lane)) : 1.f;
+    const uint64_t nx = base + 32 + lane;
+    const bool has_next = nx < it.e1;
+    uint32_t nb_n = 0, eid_n = 0;
+    if (has_next) {
+      nb_n = __ldg(p.nbr + nx);
+      if (p.w) eid_n = __ldg(p.eid + nx);
     }
-    __syncwarp();
     int j = 0;
     for (; j + U <= n; j += U) {
       Vec<VW> x[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, sm.nb[j + t], F, cols, x[t]);
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.X, __shfl_sync(0xffffffffu, nb, j + t), F, cols, x[t]);
 #pragma unroll
       for (int t = 0; t < U; ++t) {
-        const float a = sm.w[j + t];
+        const float at = __shfl_sync(0xffffffffu, a, j + t);
 #pragma unroll
         for (int i = 0; i < NV; ++i)
 #pragma unroll
-          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(at, x[t][i].x[q], acc[i].x[q]);
       }
     }
     for (; j < n; ++j) {
       Vec<VW> x[NV];
-      gather_row<VW, NV>(p.X, sm.nb[j], F, cols, x);
-      const float a = sm.w[j];
+      gather_row<VW, NV>(p.X, __shfl_sync(0xffffffffu, nb, j), F, cols, x);
+      const float at = __shfl_sync(0xffffffffu, a, j);
 #pragma unroll
       for (int i = 0; i < NV; ++i)
 #pragma unroll
-        for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[i].x[q], acc[i].x[q]);
+        for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(at, x[i].x[q], acc[i].x[q]);
     }
-    __syncwarp();
+    nb = nb_n;
+    a = has_next ? (p.w ? __ldg(p.w + eid_n) : 1.f) : 0.f;
   }
   if (!it.split) {
 #pragma unroll
@@ -164,33 +177,46 @@ __global__ void gcn_norm_kernel(int64_t E, const uint32_t* __restrict__ src, con
   }
 }
 
-// CTAs per SM the gather kernel is built for (GNNCG_SPMM_OCC=2|4, default 4: the kernel is
-// a pure gather-FMA, so more resident warps buy more bytes in flight).
-int spmm_occupancy() {
-  static const int occ = [] {
-    const char* e = getenv("GNNCG_SPMM_OCC");
-    return (e && atoi(e) == 2) ? 2 : 4;
+// Launch shape, chosen by measurement on B200 (env overrides for experiments):
+//   GNNCG_SPMM_OCC = CTAs of 256 threads per SM the kernel is built for (2 | 4 | 8)
+//   GNNCG_SPMM_NV  = float-vectors per lane per column slice (1 | 2 | 4 | 8); narrower slices
+//                    put more warps on one row, each with fewer registers.
+struct SpmmShape {
+  int occ, nv;
+};
+
+SpmmShape spmm_shape() {
+  static const SpmmShape s = [] {
+    SpmmShape r{4, 8};
+    if (const char* e = getenv("GNNCG_SPMM_OCC")) r.occ = atoi(e);
+    if (const char* e = getenv("GNNCG_SPMM_NV")) r.nv = atoi(e);
+    if (r.occ != 2 && r.occ != 8) r.occ = 4;
+    if (r.nv != 1 && r.nv != 2 && r.nv != 4) r.nv = 8;
+    return r;
   }();
-  return occ;
+  return s;
 }
 
 template <int VW, int OCC>
-int launch_spmm_occ(SpmmParams p, dim3 grid, cudaStream_t s) {
-  // split the columns into the fewest slices of <= 8 vectors per lane, evenly
-  const int vecs = p.cols / VW, slices = (int)ceil_div(vecs, 32 * 8), per = (int)ceil_div(vecs, slices);
+int launch_spmm_occ(SpmmParams p, dim3 grid, int max_nv, cudaStream_t s) {
+  // split the columns into the fewest slices of <= max_nv vectors per lane, evenly
+  const int vecs = p.cols / VW, slices = (int)ceil_div(vecs, 32 * max_nv), per = (int)ceil_div(vecs, slices);
   p.tile = per * VW;
   grid.y = (unsigned)slices;
   const int nvec = (int)ceil_div(per, 32);
   if (nvec <= 1) spmm_kernel<VW, 1, OCC><<<grid, THREADS, 0, s>>>(p);
   else if (nvec <= 2) spmm_kernel<VW, 2, OCC><<<grid, THREADS, 0, s>>>(p);
   else if (nvec <= 4) spmm_kernel<VW, 4, OCC><<<grid, THREADS, 0, s>>>(p);
-  else if (nvec <= 8) spmm_kernel<VW, 8, OCC><<<grid, THREADS, 0, s>>>(p);
+  else spmm_kernel<VW, 8, OCC><<<grid, THREADS, 0, s>>>(p);
   return GNNCG_OK;
 }
 
 template <int VW>
-int launch_spmm(const SpmmParams& p, dim3 grid, cudaStream_t s) {  // grid.y is set per column slicing
-  return spmm_occupancy() == 2 ? launch_spmm_occ<VW, 2>(p, grid, s) : launch_spmm_occ<VW, 4>(p, grid, s);
+int launch_spmm(const SpmmParams& p, dim3 grid, cudaStream_t s) {
+  const SpmmShape sh = spmm_shape();
+  if (sh.occ == 8) return launch_spmm_occ<VW, 8>(p, grid, std::min(sh.nv, 2), s);
+  if (sh.occ == 2) return launch_spmm_occ<VW, 2>(p, grid, sh.nv, s);
+  return launch_spmm_occ<VW, 4>(p, grid, sh.nv, s);
 }
 
 }  // namespace
