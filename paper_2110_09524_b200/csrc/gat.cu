@@ -168,6 +168,202 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(Gat
 }
 
 // ---------------------------------------------------------------------------
+// K2 (overlapped edge phase): the block-synchronous forward with the edge phase moved
+// under the gathers.  At the start of every 32-edge block the warp first issues the loads of
+// the block's first U neighbour rows, and only then runs the edge phase (logits -> block
+// max -> exp weights); the block's logits were copied to shared memory by cp.async one
+// block earlier, so the edge phase waits on nothing but its own shuffles and exps, and those
+// overlap the row loads.  Same arithmetic as gat_fwd_kernel (bitwise identical results).
+// ---------------------------------------------------------------------------
+struct OvlSmem {
+  uint32_t nb[kWarp];
+  float w[kWarp * TS];    // unnormalised weights exp(s - m) of the current block
+  float sum[kWarp * TS];  // per-lane running exp-sum partials
+  float sc[MAXH];         // rescale factor exp(m_old - m_new) of the current block
+  float m[MAXH];          // running max
+  float mnext[MAXH];      // running max after the current edge phase
+  float ar[MAXH];         // A_r[v]
+  float al[kWarp * 12];   // logits A_l[u] of the next block's edges (cp.async), 48-byte lane stride
+};
+
+// Logits A_l[u] (h floats) of this lane's edge -> sm.al (asynchronous; waited for before the
+// edge phase that reads them).  Only the issuing lane reads its slot.
+__device__ __forceinline__ void ovl_issue_logits(OvlSmem& sm, const float* __restrict__ Al, uint32_t u, bool valid,
+                                                 int lane, int h) {
+  if (valid) {
+    const float* src = Al + (int64_t)u * h;
+    float* dst = sm.al + lane * 12;
+    if ((h & 3) == 0) {
+      for (int k = 0; k < h; k += 4) cp_async16(dst + k, src + k);
+    } else {
+      for (int k = 0; k < h; ++k) cp_async4(dst + k, src + k);
+    }
+  }
+  cp_async_commit();
+}
+
+// Edge phase of one 32-edge block: lane owns edge `lane` (valid if lane < n).  Heads are
+// processed together (one vote, interleaved shuffle trees) for instruction-level parallelism.
+__device__ __forceinline__ void ovl_edge_phase(OvlSmem& sm, int lane, int n, int h, float slope) {
+  constexpr int HB = 4;  // heads per pass (bounds the registers live next to the row loads)
+  const bool valid = lane < n;
+  const float* al = sm.al + lane * 12;  // idle lanes: stale, masked by `valid`
+#pragma unroll
+  for (int k0 = 0; k0 < MAXH; k0 += HB) {
+    if (k0 < h) {
+      float s[HB], mn[HB];
+      bool up = false;
+#pragma unroll
+      for (int k = 0; k < HB; ++k) {
+        s[k] = (valid && k0 + k < h) ? lrelu(al[k0 + k] + sm.ar[k0 + k], slope) : -FLT_MAX;
+        mn[k] = s[k];
+        up |= s[k] > sm.m[k0 + k];
+      }
+      // the block max is only needed when some lane exceeds a running max
+      if (__any_sync(0xffffffffu, up)) {
+#pragma unroll
+        for (int o = 16; o > 0; o >>= 1)
+#pragma unroll
+          for (int k = 0; k < HB; ++k) mn[k] = fmaxf(mn[k], __shfl_xor_sync(0xffffffffu, mn[k], o));
+#pragma unroll
+        for (int k = 0; k < HB; ++k) mn[k] = fmaxf(sm.m[k0 + k], mn[k]);
+      } else {
+#pragma unroll
+        for (int k = 0; k < HB; ++k) mn[k] = sm.m[k0 + k];
+      }
+#pragma unroll
+      for (int k = 0; k < HB; ++k) {
+        if (k0 + k < h) {
+          const int kk = k0 + k;
+          const float sc = __expf(sm.m[kk] - mn[k]);
+          const float pk = valid ? __expf(s[k] - mn[k]) : 0.f;
+          sm.sum[lane * TS + kk] = fmaf(sm.sum[lane * TS + kk], sc, pk);
+          sm.w[lane * TS + kk] = pk;
+          if (lane == 0) { sm.sc[kk] = sc; sm.mnext[kk] = mn[k]; }
+        }
+      }
+    }
+  }
+  __syncwarp();
+  if (lane < h) sm.m[lane] = sm.mnext[lane];
+  __syncwarp();
+}
+
+// U rows in flight per warp, CW warps per CTA, MINB CTAs per SM (register budget).
+template <int VW, int NV, int U, int CW, int MINB>
+__global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / (MINB * CW * kWarp)) / 8 * 8 > 255 ? 255 : (65536 / (MINB * CW * kWarp)) / 8 * 8) : 255) gat_fwd_ovl_kernel(GatParams p) {
+  static_assert(32 % U == 0, "U must divide the 32-edge block");
+  __shared__ OvlSmem smem[CW];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  OvlSmem& sm = smem[w];
+  const int h = p.h, f = p.f, hf = h * f;
+  const float slope = p.slope;
+  // persistent warps: a fixed stride over the work items (sorted by decreasing size), so no
+  // warp idles until the slowest warp of its CTA finishes
+  // (the loop is CTA-uniform -- the compiler keeps the memory descriptor in a uniform register
+  // -- but carries no barrier: warps advance independently)
+  for (int64_t g = blockIdx.x; g * CW < p.num_items; g += gridDim.x) {
+  const int64_t wi = g * CW + w;
+  if (wi >= p.num_items) continue;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+
+  if (lane < h) {
+    sm.ar[lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);
+    sm.m[lane] = -FLT_MAX;
+  }
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) sm.sum[lane * TS + k] = 0.f;
+  const Cols<VW, NV> cols(lane, hf, f);
+  Vec<VW> acc[NV];
+  zero(acc);
+
+  const uint64_t e0 = it.e0, e1 = it.e1;
+  uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+  uint32_t u_nxt = e0 + 32 + lane < e1 ? __ldg(p.nbr + e0 + 32 + lane) : 0u;
+  ovl_issue_logits(sm, p.Al, u_cur, e0 + lane < e1, lane, h);
+
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const int n = (int)min((uint64_t)32, e1 - base);
+    sm.nb[lane] = u_cur;
+    __syncwarp();
+    // the block's first U rows go out before the edge phase (rows past n repeat the last
+    // valid row; their weights are 0)
+    Vec<VW> x[U][NV];
+#pragma unroll
+    for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[min(t, n - 1)], hf, cols, x[t]);
+    cp_async_wait_all();
+    ovl_edge_phase(sm, lane, n, h, slope);
+    // next block: its logits (asynchronous) and the ids of the block after it
+    u_cur = u_nxt;
+    if (base + 32 < e1) ovl_issue_logits(sm, p.Al, u_cur, base + 32 + lane < e1, lane, h);
+    u_nxt = base + 64 + lane < e1 ? __ldg(p.nbr + base + 64 + lane) : 0u;
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const float sc = sm.sc[cols.hd[i]];
+#pragma unroll
+      for (int q = 0; q < VW; ++q) acc[i].x[q] *= sc;
+    }
+    int j = 0;
+    for (;;) {
+#pragma unroll
+      for (int t = 0; t < U; ++t)
+#pragma unroll
+        for (int i = 0; i < NV; ++i) {
+          const float a = sm.w[(j + t) * TS + cols.hd[i]];  // 0 past n (j + t < 32 always)
+#pragma unroll
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
+        }
+      j += U;
+      if (j >= n) break;
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[min(j + t, n - 1)], hf, cols, x[t]);
+    }
+    __syncwarp();
+  }
+
+  __syncwarp();
+  float S = 0.f;  // lane k < h: the exp-sum of head k
+#pragma unroll
+  for (int k = 0; k < MAXH; ++k) {
+    if (k < h) {
+      const float t = warp_sum(sm.sum[lane * TS + k]);
+      if (lane == k) S = t;
+    }
+  }
+  if (lane < h) sm.sc[lane] = S;
+  __syncwarp();
+  const float mk = e0 < e1 ? (lane < h ? sm.m[lane] : 0.f) : 0.f;
+  if (!it.split) {
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      if (cols.ok[i]) {
+        const float den = sm.sc[cols.hd[i]];
+        const float inv = den > 0.f ? 1.f / den : 0.f;
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
+        st_vec<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
+      }
+    }
+    if (lane < h) {
+      p.mo[(int64_t)it.row * h + lane] = mk;
+      p.dd[(int64_t)it.row * h + lane] = S;
+    }
+  } else {
+    float* part = p.part + wi * fwd_stride(h, f);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
+    if (lane < h) {
+      part[hf + lane] = mk;
+      part[hf + h + lane] = S;
+    }
+  }
+  }  // work items
+  __syncwarp();
+}
+
+// ---------------------------------------------------------------------------
 // K3: backward pass 1 over csr_dst.  Per destination v, alpha recomputed from the
 // stash (m, d):  c = <g, sum alpha x_u>,  P = <g, sum gate*alpha x_u>,
 // Q = sum gate*alpha,  dA_r = P - c Q  (g = dOut[v]; the softmax weights of a
@@ -809,7 +1005,8 @@ __global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, c
 // ---------------------------------------------------------------------------
 // Dispatch over the compiled (VW, NV) variants.
 // ---------------------------------------------------------------------------
-enum class Kind { Fwd, BwdDst, BwdSrc, BwdSrcFast };
+enum class Kind { Fwd, FwdRoll, BwdDst, BwdSrc, BwdSrcFast };
+int num_sms();
 
 template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
@@ -828,6 +1025,13 @@ template <int VW, int NV, int OCC>
 void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
   switch (kind) {
     case Kind::Fwd: gat_fwd_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case Kind::FwdRoll: {
+      constexpr int U = GatherDepth<NV, OCC>::U;
+      constexpr int MINB = NV >= 8 ? 1 : OCC;
+      const unsigned g = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * MINB);
+      gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB><<<g, THREADS, 0, s>>>(p);
+      break;
+    }
     case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdSrc: gat_bwd_src_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::BwdSrcFast: launch_fast<VW, NV, OCC>(p, grid, s); break;
@@ -887,6 +1091,27 @@ bool tma_enabled() {
     v = (e && e[0] == '1') ? 1 : 0;
   }
   return v == 1;
+}
+
+// GNNCG_GAT_ROLL=0 selects the block-synchronous forward (gat_fwd_kernel) instead of the
+// rolling-gather one.
+bool roll_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_ROLL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+int num_sms() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  }
+  return v;
 }
 
 int check_common(const gnncg_index_t* idx, const gnncg_sched_t* sched, int h, int f) {
@@ -958,7 +1183,7 @@ int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int 
     GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
     rc = launch_fwd_tma(p, counter, s);
   } else {
-    rc = dispatch(Kind::Fwd, p, s);
+    rc = dispatch(roll_enabled() ? Kind::FwdRoll : Kind::Fwd, p, s);
   }
   if (rc) return rc;
   if (sched->num_split_rows > 0) {

@@ -135,15 +135,18 @@ __device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
     for (int q = 0; q < VW; ++q) v[i].x[q] = 0.f;
 }
 
-// Gather row `r` of a row-major [*, hf] matrix at this lane's columns.
+// Gather row `r` of a row-major [*, hf] matrix at this lane's columns.  The address is
+// (base + column) + r * row_bytes with a 32 x 32 -> 64-bit multiply-add (one IMAD.WIDE.U32 per
+// vector; base + column is loop-invariant), which holds for tables of any size (C5: 5 GB).
 template <int VW, int NV>
-__device__ __forceinline__ void gather_row(const float* __restrict__ base, int64_t r, int hf, const Cols<VW, NV>& c,
+__device__ __forceinline__ void gather_row(const float* __restrict__ base, uint32_t r, int hf, const Cols<VW, NV>& c,
                                            Vec<VW> (&x)[NV]) {
   // Lanes past the last column load column 0 instead (branch-free); their accumulators are
   // never stored and their partial dots only reach head groups that are masked by `ok`.
-  const float* row = base + r * hf;
+  const uint64_t off = (uint64_t)r * (uint32_t)(hf * 4);
 #pragma unroll
-  for (int i = 0; i < NV; ++i) x[i] = ldg_vec<VW>(row + (c.ok[i] ? c.col[i] : 0));
+  for (int i = 0; i < NV; ++i)
+    x[i] = ldg_vec<VW>(reinterpret_cast<const float*>(reinterpret_cast<const char*>(base + (c.ok[i] ? c.col[i] : 0)) + off));
 }
 
 
