@@ -655,13 +655,15 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   __shared__ WarpSmem smem[WARPS];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   WarpSmem& sm = smem[w];
-  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
-  if (wi >= p.num_items) return;
-  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
-  const int64_t u = it.row;
   const int r = lane & (PER - 1);  // rank inside the head's lane group
+  // persistent CTA-uniform item loop (as in gat_fwd_ovl_kernel), no barrier inside
+  for (int64_t g = blockIdx.x; g * WARPS < p.num_items; g += gridDim.x) {
+  const int64_t wi = g * WARPS + w;
+  if (wi >= p.num_items) continue;
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const int64_t u = it.row;
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
   const Cols<VW, NV> cols(lane, hf, f);
@@ -769,6 +771,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
       if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
     if (lane < h) part[hf + lane] = sm.stat[0][lane];
   }
+  __syncwarp();
+  }  // work items
 }
 
 // Fast-mode input of K4f, per destination v and head k (row-local, vertex tensors only):
@@ -1007,10 +1011,12 @@ __global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, c
 // ---------------------------------------------------------------------------
 enum class Kind { Fwd, FwdRoll, BwdDst, BwdSrc, BwdSrcFast };
 int num_sms();
+bool roll_enabled();
 
 template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
   constexpr int NVAL = GatherDepth<NV, OCC>::U * NV;
+  grid.x = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * (NV >= 8 ? 1 : OCC));  // persistent
   switch (p.f / VW) {
     case 1: gat_bwd_src_fast_kernel<VW, NV, 1, OCC><<<grid, THREADS, 0, s>>>(p); break;
     case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2, OCC><<<grid, THREADS, 0, s>>>(p); break;
