@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--gather", choices=["fp32", "bf16"], default="fp32",
+                    help="GAT gather tables: fp32 (the 1e-4 contract, default) or bf16 (stated looser bound)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink V and E (debug only)")
     ap.add_argument("--graph", choices=["auto", "on", "off"], default="auto",
                     help="replay the step as a CUDA graph (auto: on for the small, launch-bound configs)")
@@ -66,19 +68,21 @@ def measured_peaks():
 
 
 # ----------------------------------------------------------------------------- bytes model
-def gat_kernel_bytes(V: int, E: int, h: int, f: int) -> dict:
+def gat_kernel_bytes(V: int, E: int, h: int, f: int, gather_bytes: int = 4) -> dict:
     """Algorithmic HBM bytes per launch (fp32), per-edge-gather model of SURVEY §8d / DESIGN.md §4.
-    The per-row terms include the 8 B work item and the 8 B offsets pair."""
+    The per-row terms include the 8 B work item and the 8 B offsets pair.  gather_bytes = 2 for
+    the bf16 gather tables (the gathered Ht / dOut rows of K2 / K4f)."""
     hf = h * f
+    gb = gather_bytes
     return {
         # K2: nbr, A_l[u], Ht[u] per edge; item, off, A_r[v] in; out, m, d out per row
-        "gat_fwd": E * (4 + 4 * h + 4 * hf) + V * (16 + 4 * h + 4 * hf + 8 * h),
+        "gat_fwd": E * (4 + 4 * h + gb * hf) + V * (16 + 4 * h + 4 * hf + 8 * h),
         # K3: nbr, A_l[u], Ht[u] per edge; item, off, A_r/m/d/dOut in, c/dA_r out per row
         "gat_bwd_dst": E * (4 + 4 * h + 4 * hf) + V * (16 + 12 * h + 4 * hf + 8 * h),
         # K4: nbr, A_r/m/d/c[v], dOut[v] per edge; item, off, A_l/Ht/dA_r in, dHt/dAl out per row
         "gat_bwd_src": E * (4 + 16 * h + 4 * hf) + V * (16 + 8 * h + 8 * hf + 4 * h),
         # fused fast K4: K4's reads + the dA_r[v] reduction per edge; c from the row dot instead of K3
-        "gat_bwd_src_fused": E * (4 + 16 * h + 4 * hf + 4 * h) + V * (16 + 8 * h + 8 * hf),
+        "gat_bwd_src_fused": E * (4 + 16 * h + gb * hf + 4 * h) + V * (16 + 8 * h + 8 * hf),
     }
 
 
@@ -122,6 +126,8 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
     cfg = args.config
     if world > 1 and cfg not in ("reddit", "c5"):
         raise SystemExit(f"--config {cfg} is single-GPU only")
+    if args.gather == "bf16" and (world > 1 or cfg not in ("reddit", "c5")):
+        raise SystemExit("--gather bf16 applies to the single-GPU GAT configs (reddit, c5)")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
 
@@ -146,15 +152,16 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
             V_loc, E_loc = lg.num_local, int(lg.csr.num_edges)
         else:
             g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
-            model = GAT(g, dims, seed=1, chunk=args.chunk)
+            model = GAT(g, dims, seed=1, chunk=args.chunk, gather=args.gather)
             V_loc, E_loc = V, E
         h, f = dims[0][1], dims[0][2]
         from paper_2110_09524_b200.cost import gat_layer_report
 
         wl_cost = {"per_layer": gat_layer_report(V * world, E * world, h, f), "source": "SPEC.md:282-289"}
         wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E * world, cost=wl_cost,
-                  layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f),
+                  layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f, 2 if args.gather == "bf16" else 4),
                   config={"workload": desc, "V": V * world, "E": E * world, "layers": len(dims),
+                          "gather": args.gather,
                           "dims": ", ".join(f"{a}->{b}x{c}" for a, b, c in dims),
                           "graph": f"Chung-Lu w_i=2^40/(i+{offset * world}), seed 0",
                           "l2": "inputs larger than L2 (features and index exceed 126 MB)"})
@@ -472,7 +479,8 @@ def run_ours(args):
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
                 "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
-                "vs_baseline": None, "dtype": "f32", "data": "synthetic (Chung-Lu graph, uniform features, "
+                "vs_baseline": None, "dtype": "f32" if args.gather == "fp32" else "f32 (bf16 gather tables)",
+                "data": "synthetic (Chung-Lu graph, uniform features, "
                 "random-init weights)",
                 "config": {**wl["config"], "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},

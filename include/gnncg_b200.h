@@ -191,6 +191,29 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
                             const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
                             float* dAl, float* dAr, void* workspace, size_t workspace_bytes, void* stream);
 
+/* bf16 gather tables (the north star's "bf16 features" option, with a stated looser bound):
+ * K2 gathers Ht[u] rows and K4f gathers dOut[v] rows from bf16 copies (round to nearest even);
+ * logits, records, every accumulation and every output stay fp32.  Half the gathered bytes
+ * per edge.  Consistency of the recompute backward: K4f takes the own row from the same bf16
+ * Ht the forward aggregated, and gnncg_gat_bwd_prep_bf16 forms c = <bf16(dOut), out> while it
+ * writes the bf16 dOut table, so sum_e alpha_e dalpha_e = c[v] holds as in fp32 mode.
+ * Same semantics and workspaces as gnncg_gat_fwd / gnncg_gat_bwd_prep /
+ * gnncg_gat_bwd_src_fused; supported when gnncg_gat_bf16_supported(heads, f) != 0
+ * (f % 4 == 0, heads * f <= 512).  Replaces the same spec ops. */
+int gnncg_gat_bf16_supported(int heads, int f);
+int gnncg_pack_bf16(int64_t n, const float* src, uint16_t* dst, void* stream);
+int gnncg_gat_fwd_bf16(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int heads, int f, float slope,
+                       const uint16_t* Ht_bf16, const float* Al, const float* Ar, float* out, float* m, float* d,
+                       void* workspace, size_t workspace_bytes, void* stream);
+int gnncg_gat_bwd_prep_bf16(int64_t num_rows, int heads, int f, const float* dOut, const float* out,
+                            const float* Ar, const float* m, const float* d, float* dst_rec, uint16_t* dOut_bf16,
+                            void* stream);
+int gnncg_gat_bwd_src_fused_bf16(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int heads, int f,
+                                 float slope, int64_t row_base, int64_t num_local_rows, const uint16_t* Ht_bf16,
+                                 const float* Al, const float* dst_rec, const uint16_t* dOut_bf16, const float* a_l,
+                                 const float* a_r, float* dHt, float* dAl, float* dAr, void* workspace,
+                                 size_t workspace_bytes, void* stream);
+
 /* da_l[k,:] = sum_v dA_l[v,k] Ht[v,k,:] ; da_r likewise (LP parameter grads). */
 size_t gnncg_gat_attn_grad_workspace(int64_t num_rows, int heads, int f);
 int gnncg_gat_attn_grad(int64_t num_rows, int heads, int f, const float* Ht, const float* dAl, const float* dAr,

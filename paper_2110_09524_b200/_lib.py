@@ -98,6 +98,13 @@ _SIGS = {
     # Ht, Al, dst_rec, dOut, a_l, a_r, dHt, dAl, dAr, workspace
     "gnncg_gat_bwd_src_fused": ([P(Index), P(Sched), i32, i32, f32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp, vp,
                                  vp, sz, vp], i32),
+    "gnncg_gat_bf16_supported": ([i32, i32], i32),
+    "gnncg_pack_bf16": ([i64, vp, vp, vp], i32),
+    "gnncg_gat_fwd_bf16": ([P(Index), P(Sched), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_gat_bwd_prep_bf16": ([i64, i32, i32, vp, vp, vp, vp, vp, vp, vp, vp], i32),
+    # Ht_bf16, Al, dst_rec, dOut_bf16, a_l, a_r, dHt, dAl, dAr, workspace
+    "gnncg_gat_bwd_src_fused_bf16": ([P(Index), P(Sched), i32, i32, f32, i64, i64, vp, vp, vp, vp, vp, vp, vp, vp,
+                                      vp, vp, sz, vp], i32),
     "gnncg_gat_attn_grad_workspace": ([i64, i32, i32], sz),
     "gnncg_gat_attn_grad": ([i64, i32, i32, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_edgeconv_fwd": ([P(Index), i32, i64, vp, i64, vp, i64, vp, vp, vp], i32),

@@ -74,7 +74,12 @@ struct Vec {
 template <int VW>
 __device__ __forceinline__ Vec<VW> ldg_vec(const float* p) {
   Vec<VW> r;
-  if constexpr (VW == 4) {
+  if constexpr (VW == 8) {
+    const float4 t = __ldg(reinterpret_cast<const float4*>(p));
+    const float4 u = __ldg(reinterpret_cast<const float4*>(p) + 1);
+    r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
+    r.x[4] = u.x; r.x[5] = u.y; r.x[6] = u.z; r.x[7] = u.w;
+  } else if constexpr (VW == 4) {
     const float4 t = __ldg(reinterpret_cast<const float4*>(p));
     r.x[0] = t.x; r.x[1] = t.y; r.x[2] = t.z; r.x[3] = t.w;
   } else if constexpr (VW == 2) {
@@ -105,7 +110,10 @@ __device__ __forceinline__ Vec<VW> ldg_stream(const float* p) {
 
 template <int VW>
 __device__ __forceinline__ void st_vec(float* p, const Vec<VW>& v) {
-  if constexpr (VW == 4) {
+  if constexpr (VW == 8) {
+    reinterpret_cast<float4*>(p)[0] = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
+    reinterpret_cast<float4*>(p)[1] = make_float4(v.x[4], v.x[5], v.x[6], v.x[7]);
+  } else if constexpr (VW == 4) {
     *reinterpret_cast<float4*>(p) = make_float4(v.x[0], v.x[1], v.x[2], v.x[3]);
   } else if constexpr (VW == 2) {
     *reinterpret_cast<float2*>(p) = make_float2(v.x[0], v.x[1]);

@@ -26,6 +26,8 @@
 #include "common.cuh"
 #include "gat_common.cuh"
 
+#include <cuda_bf16.h>
+
 namespace gnncg_b200 {
 namespace {
 
@@ -250,7 +252,7 @@ __device__ __forceinline__ void ovl_edge_phase(OvlSmem& sm, int lane, int n, int
 }
 
 // U rows in flight per warp, CW warps per CTA, MINB CTAs per SM (register budget).
-template <int VW, int NV, int U, int CW, int MINB>
+template <int VW, int NV, int U, int CW, int MINB, bool LP = false>
 __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / (MINB * CW * kWarp)) / 8 * 8 > 255 ? 255 : (65536 / (MINB * CW * kWarp)) / 8 * 8) : 255) gat_fwd_ovl_kernel(GatParams p) {
   static_assert(32 % U == 0, "U must divide the 32-edge block");
   __shared__ OvlSmem smem[CW];
@@ -288,9 +290,10 @@ __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / 
     __syncwarp();
     // the block's first U rows go out before the edge phase (rows past n repeat the last
     // valid row; their weights are 0)
-    Vec<VW> x[U][NV];
+    const void* tab = LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.Ht);
+    Row<VW, LP> x[U][NV];
 #pragma unroll
-    for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[min(t, n - 1)], hf, cols, x[t]);
+    for (int t = 0; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[min(t, n - 1)], hf, cols, x[t]);
     cp_async_wait_all();
     ovl_edge_phase(sm, lane, n, h, slope);
     // next block: its logits (asynchronous) and the ids of the block after it
@@ -311,12 +314,12 @@ __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / 
         for (int i = 0; i < NV; ++i) {
           const float a = sm.w[(j + t) * TS + cols.hd[i]];  // 0 past n (j + t < 32 always)
 #pragma unroll
-          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
+          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i][q], acc[i].x[q]);
         }
       j += U;
       if (j >= n) break;
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[min(j + t, n - 1)], hf, cols, x[t]);
+      for (int t = 0; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[min(j + t, n - 1)], hf, cols, x[t]);
     }
     __syncwarp();
   }
@@ -647,9 +650,9 @@ __device__ __forceinline__ void butterfly(float* v, int lane) {
   }
 }
 
-template <int VW, int NV, int PER, int OCC>
+template <int VW, int NV, int PER, int OCC, bool LP = false>
 __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_kernel(GatParams p) {
-  constexpr int U = GatherDepth<NV, OCC>::U;
+  constexpr int U = LP ? LpDepth<VW, NV>::U : GatherDepth<NV, OCC>::U;
   constexpr int NVAL = U * NV, NOUT = NVAL / PER;
   static_assert(NVAL % PER == 0, "fast K4 needs U*NV to be a multiple of the lanes per head");
   __shared__ WarpSmem smem[WARPS];
@@ -669,7 +672,18 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   const Cols<VW, NV> cols(lane, hf, f);
   Vec<VW> x[NV], acc[NV];
   float dal[NV];
-  gather_row<VW, NV>(p.Ht, u, hf, cols, x);
+  if constexpr (LP) {
+    // bf16 mode: the own row is the same rounded Ht[u] the forward aggregated, so that
+    // sum_e alpha_e dalpha_e = <dOut~[v], out[v]> = c[v] holds exactly as in fp32 mode
+    Row<VW, true> xr[NV];
+    gather_rows<VW, NV, true>(p.lp_x, (uint32_t)u, hf, cols, xr);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+#pragma unroll
+      for (int q = 0; q < VW; ++q) x[i].x[q] = xr[i][q];
+  } else {
+    gather_row<VW, NV>(p.Ht, u, hf, cols, x);
+  }
   zero(acc);
 #pragma unroll
   for (int i = 0; i < NV; ++i) dal[i] = 0.f;
@@ -703,10 +717,11 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
     sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
     __syncwarp();
     v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+    const void* tab = LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.dOut);
     for (int j = 0; j < n; j += U) {
-      Vec<VW> gv[U][NV];
+      Row<VW, LP> gv[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.dOut, sm.nb[(j + t) & 31], hf, cols, gv[t]);
+      for (int t = 0; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[(j + t) & 31], hf, cols, gv[t]);
       float pd[NVAL];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
@@ -717,8 +732,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
           float s = 0.f;
 #pragma unroll
           for (int q = 0; q < VW; ++q) {
-            acc[i].x[q] = fmaf(a, gv[t][i].x[q], acc[i].x[q]);
-            s = fmaf(x[i].x[q], gv[t][i].x[q], s);
+            acc[i].x[q] = fmaf(a, gv[t][i][q], acc[i].x[q]);
+            s = fmaf(x[i].x[q], gv[t][i][q], s);
           }
           pd[t * NV + i] = s;
         }
@@ -800,6 +815,39 @@ __global__ void gat_bwd_prep_kernel(int64_t rows, int h, int f, const float* __r
       }
     } else {
       for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
+    }
+    const float dv = __ldg(d + i);
+    float* r = rec + v * rs;
+    r[k] = __ldg(Ar + i);
+    r[h + k] = dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f;
+    r[2 * h + k] = s;
+  }
+}
+
+// bf16 mode of gat_bwd_prep_kernel: c = <dOut~, out> with dOut~ = bf16(dOut) (the rows K4f
+// gathers), and dOut~ written out as the gather table (f % 4 == 0).
+__global__ void gat_bwd_prep_bf16_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
+                                         const float* __restrict__ out, const float* __restrict__ Ar,
+                                         const float* __restrict__ m, const float* __restrict__ d,
+                                         float* __restrict__ rec, uint16_t* __restrict__ dOut_lp) {
+  const int64_t n = rows * h;
+  const int rs = rec_stride(h);
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t v = i / h;
+    const int k = (int)(i % h);
+    const float* g = dOut + i * f;
+    const float* o = out + i * f;
+    uint2* gl = reinterpret_cast<uint2*>(dOut_lp + i * f);
+    float s = 0.f;
+    for (int j = 0; j < f; j += 4) {
+      const float4 a = __ldg(reinterpret_cast<const float4*>(g + j));
+      const float4 b = __ldg(reinterpret_cast<const float4*>(o + j));
+      const __nv_bfloat16 ax = __float2bfloat16_rn(a.x), ay = __float2bfloat16_rn(a.y);
+      const __nv_bfloat16 az = __float2bfloat16_rn(a.z), aw = __float2bfloat16_rn(a.w);
+      s = fmaf(__bfloat162float(ax), b.x, s); s = fmaf(__bfloat162float(ay), b.y, s);
+      s = fmaf(__bfloat162float(az), b.z, s); s = fmaf(__bfloat162float(aw), b.w, s);
+      gl[j / 4] = make_uint2((uint32_t)__bfloat16_as_ushort(ax) | ((uint32_t)__bfloat16_as_ushort(ay) << 16),
+                             (uint32_t)__bfloat16_as_ushort(az) | ((uint32_t)__bfloat16_as_ushort(aw) << 16));
     }
     const float dv = __ldg(d + i);
     float* r = rec + v * rs;
@@ -1074,6 +1122,76 @@ int dispatch(Kind kind, const GatParams& p, cudaStream_t s) {
   return GNNCG_OK;
 }
 
+// bf16 gather table: lane width VW = 8 when the row fills whole 256-column warps, else 4.
+int lp_width(int h, int f) {
+  const int hf = h * f;
+  if (h < 1 || h > MAXH) return 0;
+  if (f % 8 == 0 && hf % 256 == 0 && hf <= 512) return 8;
+  if (f % 4 == 0 && hf <= 256) return 4;
+  return 0;
+}
+
+template <int VW, int NV>
+bool lp_fast_ok(int f) {
+  constexpr int NVAL = LpDepth<VW, NV>::U * NV;
+  const int per = f / VW;
+  return per >= 1 && per <= 16 && (per & (per - 1)) == 0 && NVAL % per == 0;
+}
+
+template <int VW, int NV, int PER>
+void launch_lp_fast_per(const GatParams& p, unsigned g, cudaStream_t s) {
+  constexpr int NVAL = LpDepth<VW, NV>::U * NV;
+  if constexpr (NVAL % PER == 0) gat_bwd_src_fast_kernel<VW, NV, PER, 2, true><<<g, THREADS, 0, s>>>(p);
+}
+
+template <int VW, int NV>
+void launch_lp(Kind kind, const GatParams& p, cudaStream_t s) {
+  const unsigned g = (unsigned)std::min<int64_t>(ceil_div(p.num_items, WARPS), (int64_t)num_sms() * 2);
+  if (kind == Kind::FwdRoll) {
+    gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true><<<g, THREADS, 0, s>>>(p);
+  } else {
+    switch (p.f / VW) {
+      case 1: launch_lp_fast_per<VW, NV, 1>(p, g, s); break;
+      case 2: launch_lp_fast_per<VW, NV, 2>(p, g, s); break;
+      case 4: launch_lp_fast_per<VW, NV, 4>(p, g, s); break;
+      case 8: launch_lp_fast_per<VW, NV, 8>(p, g, s); break;
+      case 16: launch_lp_fast_per<VW, NV, 16>(p, g, s); break;
+      default: break;  // excluded by gnncg_gat_bf16_supported
+    }
+  }
+}
+
+int dispatch_lp(Kind kind, const GatParams& p, cudaStream_t s) {
+  if (p.num_items == 0) return GNNCG_OK;
+  const int hf = p.h * p.f, vw = lp_width(p.h, p.f);
+  if (vw == 8) {
+    if (hf <= 256) launch_lp<8, 1>(kind, p, s);
+    else launch_lp<8, 2>(kind, p, s);
+  } else if (vw == 4) {
+    if (hf <= 128) launch_lp<4, 1>(kind, p, s);
+    else launch_lp<4, 2>(kind, p, s);
+  } else {
+    return fail(GNNCG_ERR_UNSUPPORTED, "gat bf16 gather: heads=%d f=%d unsupported", p.h, p.f);
+  }
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+// fp32 -> bf16, round to nearest even (the gather tables of the bf16 mode).
+__global__ void pack_bf16_kernel(int64_t n, const float* __restrict__ src, uint16_t* __restrict__ dst) {
+  const int64_t n4 = n / 4;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n4; i += (int64_t)gridDim.x * blockDim.x) {
+    const float4 v = __ldg(reinterpret_cast<const float4*>(src) + i);
+    const uint32_t lo = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v.x)) |
+                        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v.y)) << 16);
+    const uint32_t hi = (uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v.z)) |
+                        ((uint32_t)__bfloat16_as_ushort(__float2bfloat16_rn(v.w)) << 16);
+    reinterpret_cast<uint2*>(dst)[i] = make_uint2(lo, hi);
+  }
+  for (int64_t i = n4 * 4 + blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
+    dst[i] = __bfloat16_as_ushort(__float2bfloat16_rn(src[i]));
+}
+
 }  // namespace
 
 int gat::gat_occupancy() {
@@ -1167,14 +1285,14 @@ size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* 
   return align_up(b) + 256;  // + the work counter of the persistent TMA-fed kernels
 }
 
-int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
-                  const float* Ht, const float* Al, const float* Ar, float* out, float* m, float* d, void* ws,
-                  size_t ws_bytes, void* stream) {
+static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+                        const float* Ht, const uint16_t* Ht_lp, const float* Al, const float* Ar, float* out, float* m,
+                        float* d, void* ws, size_t ws_bytes, void* stream) {
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csr_dst, sched, h, f);
   if (rc) return rc;
   if (sched->num_items == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(Ht && Al && Ar && out && m && d && csr_dst->nbr, GNNCG_ERR_ARG, "gat_fwd: null pointer");
+  GNNCG_REQUIRE((Ht || Ht_lp) && Al && Ar && out && m && d && csr_dst->nbr, GNNCG_ERR_ARG, "gat_fwd: null pointer");
   const size_t need = fwd_part_bytes(sched, h, f);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
                 ws_bytes, need);
@@ -1182,9 +1300,11 @@ int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int 
   p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
-  p.Ht = Ht; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
+  p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
-  if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
+  if (Ht_lp) {
+    rc = dispatch_lp(Kind::FwdRoll, p, s);
+  } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
     int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
     GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
     rc = launch_fwd_tma(p, counter, s);
@@ -1198,6 +1318,41 @@ int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int 
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;
+}
+
+int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+                  const float* Ht, const float* Al, const float* Ar, float* out, float* m, float* d, void* ws,
+                  size_t ws_bytes, void* stream) {
+  GNNCG_REQUIRE(Ht, GNNCG_ERR_ARG, "gat_fwd: null Ht");
+  return gat_fwd_impl(csr_dst, sched, h, f, slope, Ht, nullptr, Al, Ar, out, m, d, ws, ws_bytes, stream);
+}
+
+int gnncg_gat_bf16_supported(int h, int f) {
+  const int vw = lp_width(h, f);
+  if (vw == 8) return h * f <= 256 ? lp_fast_ok<8, 1>(f) : lp_fast_ok<8, 2>(f);
+  if (vw == 4) return h * f <= 128 ? lp_fast_ok<4, 1>(f) : lp_fast_ok<4, 2>(f);
+  return 0;
+}
+
+int gnncg_pack_bf16(int64_t n, const float* src, uint16_t* dst, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(n >= 0, GNNCG_ERR_SHAPE, "pack_bf16: n < 0");
+  if (n == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(src && dst, GNNCG_ERR_ARG, "pack_bf16: null pointer");
+  GNNCG_REQUIRE(((uintptr_t)src & 15) == 0 && ((uintptr_t)dst & 7) == 0, GNNCG_ERR_ARG, "pack_bf16: misaligned");
+  const int g = (int)std::min<int64_t>(ceil_div(n / 4 + 1, 256), 148 * 16);
+  pack_bf16_kernel<<<g, 256, 0, as_stream(stream)>>>(n, src, dst);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+int gnncg_gat_fwd_bf16(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+                       const uint16_t* Ht_bf16, const float* Al, const float* Ar, float* out, float* m, float* d,
+                       void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_REQUIRE(Ht_bf16, GNNCG_ERR_ARG, "gat_fwd_bf16: null Ht_bf16");
+  GNNCG_REQUIRE(gnncg_gat_bf16_supported(h, f), GNNCG_ERR_UNSUPPORTED, "gat_fwd_bf16: heads=%d f=%d unsupported",
+                h, f);
+  return gat_fwd_impl(csr_dst, sched, h, f, slope, nullptr, Ht_bf16, Al, Ar, out, m, d, ws, ws_bytes, stream);
 }
 
 int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
@@ -1287,17 +1442,24 @@ int gnncg_gat_bwd_prep(int64_t rows, int h, int f, const float* dOut, const floa
   return GNNCG_OK;
 }
 
-int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
-                            int64_t row_base, int64_t num_local, const float* Ht, const float* Al,
-                            const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
-                            float* dAl, float* dAr, void* ws, size_t ws_bytes, void* stream) {
+static int gat_bwd_src_fused_impl(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f,
+                                  float slope, int64_t row_base, int64_t num_local, const float* Ht,
+                                  const uint16_t* Ht_lp, const float* Al,
+                                  const float* dst_rec, const float* dOut, const uint16_t* dOut_lp, const float* a_l,
+                                  const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
+                                  void* stream) {
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csc_src, sched, h, f);
   if (rc) return rc;
-  GNNCG_REQUIRE(gnncg_gat_fast_supported(h, f), GNNCG_ERR_UNSUPPORTED,
-                "gat_bwd_src_fused: f/VW must be a power of two <= 32 (use gnncg_gat_bwd_dst + gnncg_gat_bwd_src)");
-  GNNCG_REQUIRE(Ht && Al && dst_rec && dOut && a_l && a_r && dHt && dAl && dAr, GNNCG_ERR_ARG,
-                "gat_bwd_src_fused: null pointer");
+  if (dOut_lp) {
+    GNNCG_REQUIRE(gnncg_gat_bf16_supported(h, f), GNNCG_ERR_UNSUPPORTED,
+                  "gat_bwd_src_fused_bf16: heads=%d f=%d unsupported", h, f);
+  } else {
+    GNNCG_REQUIRE(gnncg_gat_fast_supported(h, f), GNNCG_ERR_UNSUPPORTED,
+                  "gat_bwd_src_fused: f/VW must be a power of two <= 32 (use gnncg_gat_bwd_dst + gnncg_gat_bwd_src)");
+  }
+  GNNCG_REQUIRE((dOut_lp ? (Ht_lp != nullptr) : (Ht && dOut)) && Al && dst_rec && a_l && a_r && dHt && dAl && dAr,
+                GNNCG_ERR_ARG, "gat_bwd_src_fused: null pointer");
   GNNCG_REQUIRE(row_base >= 0 && num_local >= 0, GNNCG_ERR_ARG, "gat_bwd_src_fused: bad row block");
   const size_t need = src_part_bytes(sched, h, f);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE,
@@ -1308,11 +1470,11 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
-  p.Ht = Ht; p.Al = Al; p.rec = dst_rec; p.dOut = dOut; p.dAr = dAr; p.dAro = dAr;
+  p.Ht = Ht; p.Al = Al; p.rec = dst_rec; p.dOut = dOut; p.lp = dOut_lp; p.lp_x = Ht_lp; p.dAr = dAr; p.dAro = dAr;
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;
-  rc = dispatch(Kind::BwdSrcFast, p, s);
+  rc = dOut_lp ? dispatch_lp(Kind::BwdSrcFast, p, s) : dispatch(Kind::BwdSrcFast, p, s);
   if (rc) return rc;
   if (sched->num_split_rows > 0) {
     gat_bwd_src_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
@@ -1325,6 +1487,38 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;
+}
+
+int gnncg_gat_bwd_prep_bf16(int64_t rows, int h, int f, const float* dOut, const float* out, const float* Ar,
+                            const float* m, const float* d, float* rec, uint16_t* dOut_bf16, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(rows >= 0 && h >= 1 && h <= MAXH && f >= 4 && f % 4 == 0, GNNCG_ERR_SHAPE,
+                "gat_bwd_prep_bf16: bad shape");
+  if (rows == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(dOut && out && Ar && m && d && rec && dOut_bf16, GNNCG_ERR_ARG, "gat_bwd_prep_bf16: null pointer");
+  const int g = (int)std::min<int64_t>(ceil_div(rows * h, 256), 148 * 32);
+  gat_bwd_prep_bf16_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, dOut, out, Ar, m, d, rec, dOut_bf16);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
+                            int64_t row_base, int64_t num_local, const float* Ht, const float* Al,
+                            const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
+                            float* dAl, float* dAr, void* ws, size_t ws_bytes, void* stream) {
+  GNNCG_REQUIRE(dOut, GNNCG_ERR_ARG, "gat_bwd_src_fused: null dOut");
+  return gat_bwd_src_fused_impl(csc_src, sched, h, f, slope, row_base, num_local, Ht, nullptr, Al, dst_rec, dOut,
+                                nullptr, a_l, a_r, dHt, dAl, dAr, ws, ws_bytes, stream);
+}
+
+int gnncg_gat_bwd_src_fused_bf16(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f,
+                                 float slope, int64_t row_base, int64_t num_local, const uint16_t* Ht_bf16,
+                                 const float* Al, const float* dst_rec, const uint16_t* dOut_bf16, const float* a_l,
+                                 const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
+                                 void* stream) {
+  GNNCG_REQUIRE(dOut_bf16 && Ht_bf16, GNNCG_ERR_ARG, "gat_bwd_src_fused_bf16: null bf16 table");
+  return gat_bwd_src_fused_impl(csc_src, sched, h, f, slope, row_base, num_local, nullptr, Ht_bf16, Al, dst_rec,
+                                nullptr, dOut_bf16, a_l, a_r, dHt, dAl, dAr, ws, ws_bytes, stream);
 }
 
 size_t gnncg_gat_attn_grad_workspace(int64_t rows, int h, int f) {

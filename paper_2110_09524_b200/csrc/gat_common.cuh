@@ -85,6 +85,8 @@ struct GatParams {
   float slope;
   const float *Ht, *Al, *Ar, *m, *d, *c, *dOut, *dAr, *a_l, *a_r;
   float *out, *mo, *dd, *co, *dAro, *dHt, *dAl;
+  const uint16_t* lp;    // bf16 copy of the gathered table (Ht for K2, dOut for K4f), or null
+  const uint16_t* lp_x;  // K4f bf16 mode: bf16 Ht (the own row, as the forward aggregated it)
   float* part;  // split-row partials
   int64_t row_base, num_local;
   const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
@@ -149,6 +151,61 @@ __device__ __forceinline__ void gather_row(const float* __restrict__ base, uint3
     x[i] = ldg_vec<VW>(reinterpret_cast<const float*>(reinterpret_cast<const char*>(base + (c.ok[i] ? c.col[i] : 0)) + off));
 }
 
+
+// Gathered-row storage of one lane vector (VW consecutive columns): fp32, or bf16 kept packed
+// in VW/2 registers until it is consumed (LP = the low-precision gather table of
+// gnncg_gat_fwd_bf16 / gnncg_gat_bwd_src_fused_bf16; all arithmetic stays fp32).
+template <int VW, bool LP>
+struct Row;
+template <int VW>
+struct Row<VW, false> {
+  Vec<VW> v;
+  __device__ __forceinline__ float operator[](int q) const { return v.x[q]; }
+};
+template <int VW>
+struct Row<VW, true> {
+  static_assert(VW % 2 == 0, "bf16 rows need an even lane width");
+  uint32_t w[VW / 2];
+  // little-endian pairs: element 2j in the low half-word, 2j+1 in the high one
+  __device__ __forceinline__ float operator[](int q) const {
+    return __uint_as_float((q & 1) ? (w[q >> 1] & 0xffff0000u) : (w[q >> 1] << 16));
+  }
+};
+
+// gather_row for either storage: `base` is the fp32 or the bf16 table (row stride hf elements).
+template <int VW, int NV, bool LP>
+__device__ __forceinline__ void gather_rows(const void* __restrict__ base, uint32_t r, int hf, const Cols<VW, NV>& c,
+                                            Row<VW, LP> (&x)[NV]) {
+  if constexpr (!LP) {
+    Vec<VW> t[NV];
+    gather_row<VW, NV>(static_cast<const float*>(base), r, hf, c, t);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i].v = t[i];
+  } else {
+    const uint64_t off = (uint64_t)r * (uint32_t)(hf * 2);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+      const char* p = static_cast<const char*>(base) + (c.ok[i] ? c.col[i] : 0) * 2 + off;
+      if constexpr (VW == 8) {
+        const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+        x[i].w[0] = t.x; x[i].w[1] = t.y; x[i].w[2] = t.z; x[i].w[3] = t.w;
+      } else if constexpr (VW == 4) {
+        const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+        x[i].w[0] = t.x; x[i].w[1] = t.y;
+      } else {
+        x[i].w[0] = __ldg(reinterpret_cast<const uint32_t*>(p));
+      }
+    }
+  }
+}
+
+// Rows in flight per warp for the bf16 table: the same ~64 registers of row data as the fp32
+// kernels (GatherDepth), i.e. twice the rows.
+template <int VW, int NV>
+struct LpDepth {
+  static constexpr int R = 128 / (NV * VW);
+  static constexpr int U = R > 16 ? 16 : (R < 1 ? 1 : R);
+};
 
 }  // namespace gat
 

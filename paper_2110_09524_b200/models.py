@@ -36,17 +36,18 @@ class GAT:
     """A stack of GAT layers: dims = [(F_in, heads, f), ...]; layer l+1 has F_in = heads*f of layer l."""
 
     def __init__(self, g: DeviceGraph, dims, seed: int = 0, slope: float = 0.2, chunk: int | None = None,
-                 mode: str = "auto"):
+                 mode: str = "auto", gather: str = "fp32"):
         self.g = g
         self.chunk = chunk
         self.mode = mode  # backward: "auto" (fast when supported) | "fast" | "deterministic"
+        self.gather = gather  # "fp32" | "bf16" gather tables (ops.GatParams)
         dev = g.device
         gen = torch.Generator(device=dev)
         gen.manual_seed(seed)
         self.layers: list[GatLayerParams] = []
         for fin, h, f in dims:
             self.layers.append(GatLayerParams(init_uniform(fin, h * f, gen, dev), init_uniform(h, f, gen, dev),
-                                              init_uniform(h, f, gen, dev), GatParams(h, f, slope)))
+                                              init_uniform(h, f, gen, dev), GatParams(h, f, slope, gather)))
         self.loss = torch.zeros(4, device=dev)  # [0] = loss; padded for alignment
         self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
         self._ones = None

@@ -141,9 +141,37 @@ def matmul_tn(a, b, ws=None):
 # ---------------------------------------------------------------------------
 @dataclass
 class GatParams:
+    """heads x f per-head width, LeakyReLU slope.  gather = "fp32" (default: the 1e-4 parity
+    contract) or "bf16": the fused kernels gather Ht / dOut rows from bf16 copies (half the
+    bytes per edge; all arithmetic, logits and outputs stay fp32) -- the north star's
+    "bf16 features" option, held to the looser bound BF16_BOUND."""
+
     heads: int
     f: int
     slope: float = DEFAULT_SLOPE
+    gather: str = "fp32"
+
+
+BF16_BOUND = 2e-2  # max-normalised relative error of the bf16-gather mode (tests/test_gpu_gat.py)
+
+
+def _check_gather(p: GatParams) -> bool:
+    if p.gather == "fp32":
+        return False
+    if p.gather != "bf16":
+        raise ValueError(f"gather must be 'fp32' or 'bf16', not {p.gather!r}")
+    if not _lib.lib().gnncg_gat_bf16_supported(p.heads, p.f):
+        raise _lib.UnsupportedError(f"bf16 gather unsupported for heads={p.heads} f={p.f}")
+    return True
+
+
+def pack_bf16(x: torch.Tensor, out: torch.Tensor | None = None) -> torch.Tensor:
+    """fp32 -> bf16 (round to nearest even) on the device, as raw int16 storage."""
+    x = _f32(x, "pack_bf16 input")
+    if out is None:
+        out = torch.empty(x.shape, dtype=torch.int16, device=x.device)
+    call("gnncg_pack_bf16", x.numel(), _ptr(x), _ptr(out), _stream())
+    return out
 
 
 @dataclass
@@ -157,6 +185,7 @@ class GatStash:
     m: torch.Tensor
     d: torch.Tensor
     out: torch.Tensor | None = None  # the layer output (kept anyway as the next layer's input)
+    Ht_lp: torch.Tensor | None = None  # bf16 gather copy of Ht (gather="bf16")
 
 
 @dataclass
@@ -167,8 +196,9 @@ class GatGrads:
     da_r: torch.Tensor
 
 
-def gat_region_forward(g: DeviceGraph, Ht, Al, Ar, p: GatParams, out=None, m=None, d=None, chunk=None):
-    """K2 alone: the fused region given the reorganized vertex tensors."""
+def gat_region_forward(g: DeviceGraph, Ht, Al, Ar, p: GatParams, out=None, m=None, d=None, chunk=None, Ht_lp=None):
+    """K2 alone: the fused region given the reorganized vertex tensors (gather="bf16": the rows
+    come from Ht_lp, packed here when not given)."""
     V, h, f = g.num_vertices, p.heads, p.f
     Ht, Al, Ar = _f32(Ht, "Ht"), _f32(Al, "A_l"), _f32(Ar, "A_r")
     _shape(Ht, (V, h * f), "Ht")
@@ -182,6 +212,12 @@ def gat_region_forward(g: DeviceGraph, Ht, Al, Ar, p: GatParams, out=None, m=Non
     sched = idx.sched(chunk) if chunk else idx.sched()
     need = _lib.lib().gnncg_gat_workspace(sched.struct(), None, h, f)
     wp, wn = g.ws.get(need)
+    if _check_gather(p):
+        Ht_lp = pack_bf16(Ht) if Ht_lp is None else Ht_lp
+        with PROBE("gat_fwd"):
+            call("gnncg_gat_fwd_bf16", idx.struct(), sched.struct(), h, f, p.slope, _ptr(Ht_lp), _ptr(Al), _ptr(Ar),
+                 _ptr(out), _ptr(m), _ptr(d), wp, wn, _stream())
+        return out, m, d
     with PROBE("gat_fwd"):
         call("gnncg_gat_fwd", idx.struct(), sched.struct(), h, f, p.slope, _ptr(Ht), _ptr(Al), _ptr(Ar), _ptr(out),
              _ptr(m), _ptr(d), wp, wn, _stream())
@@ -212,8 +248,9 @@ def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
     _shape(a_r, (h, f), "a_r")
     Ht = gemm(H, W, ws=g.ws)
     Al, Ar = attn_dots(Ht, a_l, a_r, h, f)
-    out, m, d = gat_region_forward(g, Ht, Al, Ar, p, chunk=chunk)
-    return out, GatStash(Ht, Al, Ar, m, d, out)
+    Ht_lp = pack_bf16(Ht) if _check_gather(p) else None
+    out, m, d = gat_region_forward(g, Ht, Al, Ar, p, chunk=chunk, Ht_lp=Ht_lp)
+    return out, GatStash(Ht, Al, Ar, m, d, out, Ht_lp)
 
 
 def fast_supported(p: GatParams) -> bool:
@@ -231,8 +268,11 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
     dOut = _f32(dOut, "dOut")
     _shape(dOut, (V, h * f), "dOut")
     a_l, a_r = _f32(a_l, "a_l"), _f32(a_r, "a_r")
+    lp = _check_gather(p)
     if mode == "auto":
-        mode = "fast" if (stash.out is not None and fast_supported(p)) else "deterministic"
+        mode = "fast" if (stash.out is not None and (lp or fast_supported(p))) else "deterministic"
+    if lp and mode != "fast":
+        raise TensorError("gather='bf16' needs the fast backward (stash.out)")
     dev = dOut.device
     c = torch.empty(V, h, device=dev)
     dAr = torch.empty(V, h, device=dev)
@@ -248,14 +288,29 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
         if stash.out is None:
             raise TensorError("gat_region_backward(fast): stash.out is required")
         rec = torch.empty(V, L.gnncg_gat_rec_stride(h), device=dev)
-        with PROBE("gat_bwd_prep"):
-            call("gnncg_gat_bwd_prep", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(stash.Ar), _ptr(stash.m),
-                 _ptr(stash.d), _ptr(rec), s)
+        if lp:
+            # c from the rounded dOut rows K4f gathers (written here), the own row from the same
+            # rounded Ht the forward aggregated: the softmax-backward identity stays exact
+            dOut_lp = torch.empty(dOut.shape, dtype=torch.int16, device=dev)
+            Ht_lp = stash.Ht_lp if stash.Ht_lp is not None else pack_bf16(stash.Ht)
+            with PROBE("gat_bwd_prep"):
+                call("gnncg_gat_bwd_prep_bf16", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(stash.Ar), _ptr(stash.m),
+                     _ptr(stash.d), _ptr(rec), _ptr(dOut_lp), s)
+        else:
+            with PROBE("gat_bwd_prep"):
+                call("gnncg_gat_bwd_prep", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(stash.Ar), _ptr(stash.m),
+                     _ptr(stash.d), _ptr(rec), s)
         c = rec[:, 2 * h:3 * h]
-        with PROBE("gat_bwd_src_fused"):
-            call("gnncg_gat_bwd_src_fused", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V, _ptr(stash.Ht),
-                 _ptr(stash.Al), _ptr(rec), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr), wp,
-                 wn, s)
+        if lp:
+            with PROBE("gat_bwd_src_fused"):
+                call("gnncg_gat_bwd_src_fused_bf16", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V,
+                     _ptr(Ht_lp), _ptr(stash.Al), _ptr(rec), _ptr(dOut_lp), _ptr(a_l), _ptr(a_r), _ptr(dHt),
+                     _ptr(dAl), _ptr(dAr), wp, wn, s)
+        else:
+            with PROBE("gat_bwd_src_fused"):
+                call("gnncg_gat_bwd_src_fused", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V,
+                     _ptr(stash.Ht), _ptr(stash.Al), _ptr(rec), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt),
+                     _ptr(dAl), _ptr(dAr), wp, wn, s)
     elif mode == "deterministic":
         with PROBE("gat_bwd_dst"):
             call("gnncg_gat_bwd_dst", g.csr_dst.struct(), sd.struct(), h, f, p.slope, _ptr(stash.Ht),
