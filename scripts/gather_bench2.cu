@@ -92,5 +92,18 @@ int main() {
     run<8>(table, idx, nblk, out, w);
     if (w <= 32) run<16>(table, idx, nblk, out, w);
   }
+  // L2 tiling probe: the same stream split into source tiles processed one after the other
+  // (ids of tile t restricted to [t V/T, (t+1) V/T), each tile's rows ~ 239/T MB), vs one pass
+  for (int T : {1, 2, 3, 4}) {
+    std::vector<uint32_t> hs(h);
+    // stable bucket by tile: a tile's edges are contiguous in the stream (2D-tiled order)
+    std::vector<int64_t> cnt(T + 1, 0);
+    for (int64_t e = 0; e < E; ++e) cnt[1 + (int64_t)h[e] * T / V]++;
+    for (int t = 0; t < T; ++t) cnt[t + 1] += cnt[t];
+    for (int64_t e = 0; e < E; ++e) hs[cnt[(int64_t)h[e] * T / V]++] = h[e];
+    cudaMemcpy(idx, hs.data(), E * 4, cudaMemcpyHostToDevice);
+    printf("tiles=%d: ", T);
+    run<8>(table, idx, nblk, out, 16);
+  }
   return 0;
 }

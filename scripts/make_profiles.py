@@ -73,8 +73,8 @@ def main():
     if os.path.exists(rep):
         full = full_summary(rep)
         json.dump(full, open(os.path.join(ROOT, "profiles", f"r{rnd}_{tag}_ncu_full.json"), "w"), indent=1)
-        name_map = {"gat_fwd_kernel": "gat_fwd", "gat_bwd_dst_kernel": "gat_bwd_dst", "gat_bwd_src_kernel": "gat_bwd_src",
-                    "gat_bwd_src_fast_kernel": "gat_bwd_src_fused"}
+        name_map = {"gat_fwd_kernel": "gat_fwd", "gat_fwd_ovl_kernel": "gat_fwd", "gat_bwd_dst_kernel": "gat_bwd_dst",
+                    "gat_bwd_src_kernel": "gat_bwd_src", "gat_bwd_src_fast_kernel": "gat_bwd_src_fused"}
         for d in full:
             base = d["kernel"].split("<")[0]
             if base in name_map and "dram__bytes_read.sum" in d:
