@@ -408,19 +408,30 @@ def run_ours(args):
         kernels[name] = k
     dominant = max((n for n in kernels if n in per_launch), key=lambda n: kernels[n]["share_of_step"])
     traffic = None
+    headline = args.config == "reddit" and world == 1 and args.gather == "fp32"  # what profiles/ captured
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if os.path.exists(tpath):
+    if headline and os.path.exists(tpath):
         with open(tpath) as fh:
             traffic = json.load(fh).get(dominant)
     roofline = {"bound": "hbm", "kernel": dominant, "achieved": kernels[dominant]["GBps"], "peak": peak,
                 "unit": "GB/s", "frac": kernels[dominant]["frac"], "traffic": traffic, "peak_source": peak_src}
-    if traffic and args.config == "reddit" and world == 1:
+    if traffic:
         # the algorithmic model counts every gathered row; hub rows are served from L2, so also
         # report the DRAM bytes ncu measured for this kernel over its live launch time
         dram = traffic / (kernels[dominant]["ms_per_launch"] / 1e3) / 1e9
         roofline.update({"dram_achieved": dram, "dram_frac": dram / peak,
                          "note": "achieved = algorithmic bytes (SURVEY §8d per-edge-gather model, DESIGN.md §4); "
                                  "traffic = ncu dram__bytes per launch (profiles/ncu_traffic.json)"})
+    cpath = os.path.join(ROOT, "profiles", "r01_gather_ceiling.json")
+    if headline and os.path.exists(cpath):
+        # the L2-served gather ceiling measured on this B200 for the same Zipf row stream
+        with open(cpath) as fh:
+            ceil = json.load(fh)["GBps_16warps_8rows"]
+        roofline.update({"gather_ceiling": ceil, "gather_frac": kernels[dominant]["GBps"] / ceil,
+                         "gather_ceiling_source": "profiles/r01_gather_ceiling.json (scripts/gather_bench2.cu)"})
+        for n in ("gat_fwd", "gat_bwd_src_fused"):
+            if n in kernels and "GBps" in kernels[n]:
+                kernels[n]["gather_frac"] = kernels[n]["GBps"] / ceil
 
     # --- end-to-end through the public API with host buffers ----------------------------
     e2e = None

@@ -169,15 +169,26 @@ class DeviceGraph {
   mutable DeviceBuffer ws_;
 };
 
+// Gather tables of the fused kernels: fp32 (the 1e-4 contract) or bf16 (Ht / dOut rows read
+// from bf16 copies, all arithmetic fp32; the north star's "bf16 features" option with a looser
+// bound, see gnncg_gat_fwd_bf16).
+enum class Gather { fp32, bf16 };
+// Backward: deterministic = K3 (csr_dst) + K4 (csc_src), fixed-order, bitwise reproducible;
+// fast = one fused csc_src pass with dA_r by global reductions (SPEC.md:378 fast mode).
+enum class Backward { deterministic, fast };
+
 struct GatParams {
   int heads;
   int f;
   float slope = 0.2f;  // tensor.hpp:93
+  Gather gather = Gather::fp32;
+  Backward backward = Backward::deterministic;  // bf16 gather always uses the fast backward
 };
 
-// O(|V|) forward state kept for the backward.
+// O(|V|) forward state kept for the backward, plus the layer output (the fast
+// backward's row dot) and the bf16 gather copy of Ht when gather == bf16.
 struct GatStash {
-  DeviceBuffer Ht, Al, Ar, m, d;
+  DeviceBuffer Ht, Al, Ar, m, d, out, Ht_lp;
 };
 
 struct GatGrads {
@@ -220,14 +231,24 @@ inline Tensor<float> gat_forward(const DeviceGraph& g, const Tensor<float>& H, c
   check(gnncg_gat_attn_dots(V, h, f, st.Ht.get<float>(), dal.get<float>(), dar.get<float>(), st.Al.get<float>(),
                             st.Ar.get<float>(), s),
         "gnncg_gat_attn_dots");
-  DeviceBuffer out(V * hf * 4);
+  st.out = DeviceBuffer(V * hf * 4);
   const gnncg_index_t idx = g.csr_dst().view();
   DeviceBuffer& ws = g.workspace(gnncg_gat_workspace(&g.csr_dst().sched, nullptr, h, f));
-  check(gnncg_gat_fwd(&idx, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
-                      st.Ar.get<float>(), out.get<float>(), st.m.get<float>(), st.d.get<float>(), ws.get(),
-                      ws.bytes(), s),
-        "gnncg_gat_fwd");
-  return download(out, V, hf, s);
+  if (p.gather == Gather::bf16) {
+    if (!gnncg_gat_bf16_supported(p.heads, p.f)) throw TensorError("gat_forward: bf16 gather unsupported for this shape");
+    st.Ht_lp = DeviceBuffer(V * hf * 2);
+    check(gnncg_pack_bf16(V * hf, st.Ht.get<float>(), st.Ht_lp.get<std::uint16_t>(), s), "gnncg_pack_bf16");
+    check(gnncg_gat_fwd_bf16(&idx, &g.csr_dst().sched, h, f, p.slope, st.Ht_lp.get<std::uint16_t>(),
+                             st.Al.get<float>(), st.Ar.get<float>(), st.out.get<float>(), st.m.get<float>(),
+                             st.d.get<float>(), ws.get(), ws.bytes(), s),
+          "gnncg_gat_fwd_bf16");
+  } else {
+    check(gnncg_gat_fwd(&idx, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
+                        st.Ar.get<float>(), st.out.get<float>(), st.m.get<float>(), st.d.get<float>(), ws.get(),
+                        ws.bytes(), s),
+          "gnncg_gat_fwd");
+  }
+  return download(st.out, V, hf, s);
 }
 
 // GAT layer backward with recomputation.
@@ -245,15 +266,44 @@ inline GatGrads gat_backward(const DeviceGraph& g, const Tensor<float>& H, const
   size_t need = gnncg_gat_workspace(&g.csr_dst().sched, &g.csc_src().sched, h, f);
   need = std::max(need, gnncg_gat_attn_grad_workspace(V, h, f));
   DeviceBuffer& ws = g.workspace(need);
-  check(gnncg_gat_bwd_dst(&csr, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
-                          st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), g_out.get<float>(), c.get<float>(),
-                          dAr.get<float>(), ws.get(), ws.bytes(), s),
-        "gnncg_gat_bwd_dst");
-  check(gnncg_gat_bwd_src(&csc, &g.csc_src().sched, h, f, p.slope, 0, V, st.Ht.get<float>(), st.Al.get<float>(),
-                          st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), c.get<float>(), g_out.get<float>(),
-                          dAr.get<float>(), dal_in.get<float>(), dar_in.get<float>(), dHt.get<float>(),
-                          dAl.get<float>(), ws.get(), ws.bytes(), s),
-        "gnncg_gat_bwd_src");
+  const bool lp = p.gather == Gather::bf16;
+  if (lp || p.backward == Backward::fast) {
+    if (!lp && !gnncg_gat_fast_supported(p.heads, p.f)) throw TensorError("gat_backward: fast mode unsupported here");
+    DeviceBuffer rec(V * gnncg_gat_rec_stride(p.heads) * 4);
+    if (lp) {
+      DeviceBuffer g_lp(V * hf * 2);
+      check(gnncg_gat_bwd_prep_bf16(V, h, f, g_out.get<float>(), st.out.get<float>(), st.Ar.get<float>(),
+                                    st.m.get<float>(), st.d.get<float>(), rec.get<float>(),
+                                    g_lp.get<std::uint16_t>(), s),
+            "gnncg_gat_bwd_prep_bf16");
+      check(gnncg_gat_bwd_src_fused_bf16(&csc, &g.csc_src().sched, h, f, p.slope, 0, V,
+                                         st.Ht_lp.get<std::uint16_t>(), st.Al.get<float>(), rec.get<float>(),
+                                         g_lp.get<std::uint16_t>(), dal_in.get<float>(), dar_in.get<float>(),
+                                         dHt.get<float>(), dAl.get<float>(), dAr.get<float>(), ws.get(), ws.bytes(), s),
+            "gnncg_gat_bwd_src_fused_bf16");
+      cuda_check(cudaStreamSynchronize(s), "sync");  // g_lp / rec are released at scope end
+    } else {
+      check(gnncg_gat_bwd_prep(V, h, f, g_out.get<float>(), st.out.get<float>(), st.Ar.get<float>(), st.m.get<float>(),
+                               st.d.get<float>(), rec.get<float>(), s),
+            "gnncg_gat_bwd_prep");
+      check(gnncg_gat_bwd_src_fused(&csc, &g.csc_src().sched, h, f, p.slope, 0, V, st.Ht.get<float>(),
+                                    st.Al.get<float>(), rec.get<float>(), g_out.get<float>(), dal_in.get<float>(),
+                                    dar_in.get<float>(), dHt.get<float>(), dAl.get<float>(), dAr.get<float>(), ws.get(),
+                                    ws.bytes(), s),
+            "gnncg_gat_bwd_src_fused");
+      cuda_check(cudaStreamSynchronize(s), "sync");
+    }
+  } else {
+    check(gnncg_gat_bwd_dst(&csr, &g.csr_dst().sched, h, f, p.slope, st.Ht.get<float>(), st.Al.get<float>(),
+                            st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), g_out.get<float>(),
+                            c.get<float>(), dAr.get<float>(), ws.get(), ws.bytes(), s),
+          "gnncg_gat_bwd_dst");
+    check(gnncg_gat_bwd_src(&csc, &g.csc_src().sched, h, f, p.slope, 0, V, st.Ht.get<float>(), st.Al.get<float>(),
+                            st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(), c.get<float>(),
+                            g_out.get<float>(), dAr.get<float>(), dal_in.get<float>(), dar_in.get<float>(),
+                            dHt.get<float>(), dAl.get<float>(), ws.get(), ws.bytes(), s),
+          "gnncg_gat_bwd_src");
+  }
   check(gnncg_gat_attn_grad(V, h, f, st.Ht.get<float>(), dAl.get<float>(), dAr.get<float>(), da_l.get<float>(),
                             da_r.get<float>(), ws.get(), ws.bytes(), s),
         "gnncg_gat_attn_grad");

@@ -83,7 +83,8 @@ def main():
                 wr = d["dram__bytes_write.sum"] * scale.get(d["dram__bytes_write.sum.unit"], 1)
                 traffic.setdefault(name_map[base], rd + wr)
         if traffic:
-            json.dump({**traffic, "_source": f"profiles/r{rnd}_{tag}_ncu_full.json (ncu --set full, first launch)"},
+            json.dump({**traffic, "_config": "bench.py default (reddit, fp32 gather, 1 GPU)",
+                       "_source": f"profiles/r{rnd}_{tag}_ncu_full.json (ncu --set full, first launch)"},
                       open(os.path.join(ROOT, "profiles", "ncu_traffic.json"), "w"), indent=1)
     lpath = os.path.join(ROOT, "gpurun_out", f"launches_{tag}.csv")
     if os.path.exists(lpath):
