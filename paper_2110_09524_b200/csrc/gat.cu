@@ -692,8 +692,17 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
   __syncwarp();
 
+  const void* tab = LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.dOut);
   for (uint64_t base = e0; base < e1; base += 32) {
     const int n = (int)min((uint64_t)32, e1 - base);
+    sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
+    __syncwarp();
+    // the first half of the block's first row group goes out before the dependent record
+    // loads of the edge phase (the whole group would not fit next to the records' registers)
+    constexpr int UH = U >= 2 ? U / 2 : 1;
+    Row<VW, LP> gv[U][NV];
+#pragma unroll
+    for (int t = 0; t < UH; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[t], hf, cols, gv[t]);
     {
       const bool valid = lane < n;
       // packed destination record {A_r | lse = m + log d | c} (gat_bwd_prep_kernel): one
@@ -714,14 +723,11 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
         }
       }
     }
-    sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
     __syncwarp();
     v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
-    const void* tab = LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.dOut);
-    for (int j = 0; j < n; j += U) {
-      Row<VW, LP> gv[U][NV];
 #pragma unroll
-      for (int t = 0; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[(j + t) & 31], hf, cols, gv[t]);
+    for (int t = UH; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[t], hf, cols, gv[t]);
+    for (int j = 0;;) {
       float pd[NVAL];
 #pragma unroll
       for (int t = 0; t < U; ++t) {
@@ -756,6 +762,10 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
           if (i == ii) dal[ii] += dz;
         if (valid) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
       }
+      j += U;
+      if (j >= n) break;
+#pragma unroll
+      for (int t = 0; t < U; ++t) gather_rows<VW, NV, LP>(tab, sm.nb[(j + t) & 31], hf, cols, gv[t]);
     }
     __syncwarp();
   }
