@@ -650,7 +650,7 @@ __device__ __forceinline__ void butterfly(float* v, int lane) {
   }
 }
 
-template <int VW, int NV, int PER, int OCC, bool LP = false>
+template <int VW, int NV, int PER, int OCC, bool LP = false, bool PAIR = false>
 __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_kernel(GatParams p) {
   constexpr int U = LP ? LpDepth<VW, NV>::U : GatherDepth<NV, OCC>::U;
   constexpr int NVAL = U * NV, NOUT = NVAL / PER;
@@ -669,7 +669,10 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   const int64_t u = it.row;
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
-  const Cols<VW, NV> cols(lane, hf, f);
+  // PAIR: lane's vectors in adjacent heads -> after the transpose-reduction a lane holds one
+  // edge's dz for heads (2g, 2g+1): one 8-byte reduction into dA_r instead of two
+  static_assert(!PAIR || (NV == 2 && NOUT == 2), "paired reductions: two vectors, two outputs per lane");
+  const Cols<VW, NV> cols(lane, hf, f, PAIR ? PER : 0);
   Vec<VW> x[NV], acc[NV];
   float dal[NV];
   if constexpr (LP) {
@@ -745,6 +748,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
         }
       }
       butterfly<NVAL, PER / 2>(pd, lane);
+      float dzp[NOUT];
 #pragma unroll
       for (int q = 0; q < NOUT; ++q) {
         const int idx = r * NOUT + q;
@@ -760,7 +764,18 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
 #pragma unroll
         for (int ii = 0; ii < NV; ++ii)
           if (i == ii) dal[ii] += dz;
-        if (valid) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
+        dzp[q] = dz;
+        if (!PAIR && valid) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
+      }
+      if constexpr (PAIR) {
+        // both outputs belong to edge r of the group, heads hd[0], hd[0] + 1; the lane group
+        // with the next two heads of the same edge is 8 lanes up: even groups collect them and
+        // add four adjacent heads at once (16-byte aligned: hd[0] = 4 g')
+        const float o0 = __shfl_down_sync(0xffffffffu, dzp[0], PER);
+        const float o1 = __shfl_down_sync(0xffffffffu, dzp[1], PER);
+        const int e = j + r;
+        if (((lane / PER) & 1) == 0 && e < n)
+          red_add_v4(p.dAro + (int64_t)sm.nb[e] * h + cols.hd[0], make_float4(dzp[0], dzp[1], o0, o1));
       }
       j += U;
       if (j >= n) break;
@@ -1070,11 +1085,19 @@ __global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, c
 enum class Kind { Fwd, FwdRoll, BwdDst, BwdSrc, BwdSrcFast };
 int num_sms();
 bool roll_enabled();
+bool pair_enabled();
 
 template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
   constexpr int NVAL = GatherDepth<NV, OCC>::U * NV;
   grid.x = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * (NV >= 8 ? 1 : OCC));  // persistent
+  if constexpr (NV == 2 && NVAL == 2 * 8) {
+    // paired columns (8 lanes per head, two adjacent heads per lane, h = 8): the Reddit shape
+    if (pair_enabled() && pair_lanes(p.h, p.f, VW, NV) == 8 && p.h == 8) {
+      gat_bwd_src_fast_kernel<VW, NV, 8, OCC, false, true><<<grid, THREADS, 0, s>>>(p);
+      return;
+    }
+  }
   switch (p.f / VW) {
     case 1: gat_bwd_src_fast_kernel<VW, NV, 1, OCC><<<grid, THREADS, 0, s>>>(p); break;
     case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2, OCC><<<grid, THREADS, 0, s>>>(p); break;
@@ -1233,6 +1256,16 @@ bool roll_enabled() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("GNNCG_GAT_ROLL");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+// GNNCG_GAT_PAIR=0 disables K4f's paired-head column mapping.
+bool pair_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_PAIR");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;

@@ -115,19 +115,41 @@ struct GatherDepth {
 // Runtime choice of OCC (GNNCG_GAT_OCC=2|4, default 2: measured faster at the Reddit shape).
 int gat_occupancy();
 
+// Lane -> column mapping.  Default: vector i of lane l covers columns [(32 i + l) VW, +VW).
+// Paired (pl = lanes per head P > 0; rows that fill the warp exactly, hf = 32 NV VW): lane l
+// owns the SAME VW columns of the NV consecutive heads NV (l / P) + i, so the per-head values a
+// lane ends up with after K4f's transpose-reduction are adjacent in memory (one vector
+// reduction into dA_r); every load instruction still covers whole 128-byte lines.
 template <int VW, int NV>
 struct Cols {
   int col[NV], hd[NV];
   bool ok[NV];
-  __device__ __forceinline__ Cols(int lane, int hf, int f) {
+  __device__ __forceinline__ Cols(int lane, int hf, int f, int pl = 0) {
+    if (pl > 0) {
 #pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      col[i] = (i * 32 + lane) * VW;
-      ok[i] = col[i] < hf;
-      hd[i] = ok[i] ? col[i] / f : 0;
+      for (int i = 0; i < NV; ++i) {
+        hd[i] = NV * (lane / pl) + i;
+        col[i] = hd[i] * f + (lane % pl) * VW;
+        ok[i] = true;
+      }
+    } else {
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        col[i] = (i * 32 + lane) * VW;
+        ok[i] = col[i] < hf;
+        hd[i] = ok[i] ? col[i] / f : 0;
+      }
     }
   }
 };
+
+// The paired mapping applies when the row fills the warp exactly and a head spans P = f / VW
+// lanes with P dividing 32: returns P, or 0.
+__host__ __device__ __forceinline__ int pair_lanes(int h, int f, int VW, int NV) {
+  if (h * f != 32 * NV * VW || f % VW != 0) return 0;
+  const int P = f / VW;
+  return (P >= 1 && P <= 32 && 32 % P == 0) ? P : 0;
+}
 
 template <int VW, int NV>
 __device__ __forceinline__ void zero(Vec<VW> (&v)[NV]) {
