@@ -139,6 +139,15 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
 int gnncg_gat_attn_dots(int64_t num_rows, int heads, int f, const float* Ht, const float* a_l, const float* a_r,
                         float* Al, float* Ar, void* stream);
 
+/* K1 with its epilogue: Ht = H W (H is M x K with row stride ldh, W is K x heads*f, Ht dense)
+ * AND the reorganized LPs A_l = Ht . a_l, A_r = Ht . a_r computed by the tensor-core GEMM's
+ * epilogue from the accumulator it already holds (SURVEY K1 "attn-dot epilogue"; bitwise equal
+ * to gnncg_gemm + gnncg_gat_attn_dots).  Shapes outside the fused kernel (f % 32 != 0, split-K)
+ * run those two calls instead.  Workspace: gnncg_gemm_workspace(0, 0, M, heads*f, K). */
+int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, int64_t ldh, const float* W,
+                        float* Ht, const float* a_l, const float* a_r, float* Al, float* Ar, void* workspace,
+                        size_t workspace_bytes, void* stream);
+
 /* Scratch for the split-row partials of all GAT kernels over these schedules. */
 size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* src_sched, int heads, int f);
 

@@ -227,10 +227,13 @@ inline Tensor<float> gat_forward(const DeviceGraph& g, const Tensor<float>& H, c
   st.Ar = DeviceBuffer(V * h * 4);
   st.m = DeviceBuffer(V * h * 4);
   st.d = DeviceBuffer(V * h * 4);
-  detail::gemm(g, 0, 0, V, hf, H.cols, dH.get<float>(), H.cols, dW.get<float>(), hf, st.Ht.get<float>(), hf);
-  check(gnncg_gat_attn_dots(V, h, f, st.Ht.get<float>(), dal.get<float>(), dar.get<float>(), st.Al.get<float>(),
-                            st.Ar.get<float>(), s),
-        "gnncg_gat_attn_dots");
+  {  // K1 with the attention-LP epilogue (one tensor-core GEMM)
+    DeviceBuffer& gws = g.workspace(gnncg_gemm_workspace(0, 0, V, hf, H.cols));
+    check(gnncg_gat_transform(V, H.cols, h, f, dH.get<float>(), H.cols, dW.get<float>(), st.Ht.get<float>(),
+                              dal.get<float>(), dar.get<float>(), st.Al.get<float>(), st.Ar.get<float>(), gws.get(),
+                              gws.bytes(), s),
+          "gnncg_gat_transform");
+  }
   st.out = DeviceBuffer(V * hf * 4);
   const gnncg_index_t idx = g.csr_dst().view();
   DeviceBuffer& ws = g.workspace(gnncg_gat_workspace(&g.csr_dst().sched, nullptr, h, f));

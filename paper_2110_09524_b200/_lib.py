@@ -87,6 +87,7 @@ _SIGS = {
     "gnncg_gemm_workspace": ([i32, i32, i64, i64, i64], sz),
     "gnncg_gemm": ([i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], i32),
     "gnncg_gat_attn_dots": ([i64, i32, i32, vp, vp, vp, vp, vp, vp], i32),
+    "gnncg_gat_transform": ([i64, i64, i32, i32, vp, i64, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_gat_workspace": ([P(Sched), P(Sched), i32, i32], sz),
     "gnncg_gat_fwd": ([P(Index), P(Sched), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_gat_bwd_dst": ([P(Index), P(Sched), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),

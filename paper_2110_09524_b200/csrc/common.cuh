@@ -146,6 +146,15 @@ __device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
+// Optional attention-LP epilogue of the tensor-core GEMM (K1 of the GAT layer; gemm_tc.cu).
+struct AttnEpi {
+  const float* a_l = nullptr;
+  const float* a_r = nullptr;
+  float* Al = nullptr;  // null: plain GEMM
+  float* Ar = nullptr;
+  int h = 0, f = 0;
+};
+
 __host__ __device__ inline int64_t ceil_div(int64_t a, int64_t b) { return (a + b - 1) / b; }
 inline size_t align_up(size_t x, size_t a = 256) { return (x + a - 1) / a * a; }
 

@@ -160,7 +160,8 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                       const float* B, int64_t ldb);
 int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s);
+            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s,
+            const AttnEpi& epi);
 
 namespace {
 // GNNCG_GEMM=simt forces the CUDA-core kernel (A/B comparisons); default: tensor cores when eligible.
@@ -216,7 +217,8 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
     int splits = tc_splits(M, N, K);
     const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), 32) * 32 : K;
     splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;  // every split gets >= 1 k-block
-    int rc = tc_gemm(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, splits, kchunk, static_cast<float*>(ws), s);
+    int rc = tc_gemm(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, splits, kchunk, static_cast<float*>(ws), s,
+                     AttnEpi{});
     if (rc != GNNCG_OK) return rc;
     if (splits > 1) {
       const int64_t total = M * N;
@@ -247,6 +249,29 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;
+}
+
+int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, int64_t ldh, const float* W,
+                        float* Ht, const float* a_l, const float* a_r, float* Al, float* Ar, void* ws,
+                        size_t ws_bytes, void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(M >= 0 && K >= 0 && heads >= 1 && f >= 1, GNNCG_ERR_SHAPE, "gat_transform: bad shape");
+  const int64_t N = (int64_t)heads * f;
+  if (M == 0) return GNNCG_OK;
+  GNNCG_REQUIRE(H && W && Ht && a_l && a_r && Al && Ar, GNNCG_ERR_ARG, "gat_transform: null pointer");
+  GNNCG_REQUIRE(ldh >= K, GNNCG_ERR_SHAPE, "gat_transform: ldh < K");
+  cudaStream_t s = as_stream(stream);
+  const int bn = N > 128 ? 256 : 128;
+  if (K > 0 && tc_enabled() && tc_splits(M, N, K) == 1 && f % 32 == 0 && bn % f == 0 &&
+      tc_gemm_eligible(0, 0, M, N, K, H, ldh, W, N)) {
+    AttnEpi epi;
+    epi.a_l = a_l; epi.a_r = a_r; epi.Al = Al; epi.Ar = Ar; epi.h = heads; epi.f = f;
+    return tc_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, 1, K, nullptr, s, epi);
+  }
+  // unfused: the GEMM, then the LP kernel
+  int rc = gnncg_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, ws, ws_bytes, stream);
+  if (rc != GNNCG_OK) return rc;
+  return gnncg_gat_attn_dots(M, heads, f, Ht, a_l, a_r, Al, Ar, stream);
 }
 
 }  // extern "C"

@@ -142,11 +142,15 @@ __device__ __forceinline__ void split_hi_lo(float* raw, float* lo, int bytes, in
 }
 
 // A_MN: A stored K x M (M contiguous); else M x K.  B_MN: B stored K x N (N contiguous); else N x K.
+// epi.Al != null (K1 of the GAT layer, no split-K, f % 32 == 0, BN % f == 0): the epilogue also
+// forms the reorganized attention LPs of every output row from the accumulator it already holds,
+//   Al[row, k] = <C[row, k*f : (k+1)*f], a_l[k, :]>,  Ar likewise,
+// in the same sequential order as gat.cu's attn_dots_kernel (bitwise identical results).
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(THREADS, 1)
     gemm_tf32x3_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
                        float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk,
-                       int64_t split_stride, int dbg) {
+                       int64_t split_stride, int dbg, AttnEpi epi) {
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
   extern __shared__ uint8_t smem_raw[];
@@ -265,6 +269,7 @@ __global__ void __launch_bounds__(THREADS, 1)
       mbar_wait(accum, 0);
       asm volatile("tcgen05.fence::after_thread_sync;");
     }
+    float dl = 0.f, dr = 0.f;  // attention-LP partial sums of the current head (epi.Al)
 #pragma unroll 1
     for (int c = 0; c < BN / 32; ++c) {
       uint32_t r[32];
@@ -292,6 +297,24 @@ __global__ void __launch_bounds__(THREADS, 1)
 #pragma unroll
           for (int j = 0; j < 32; ++j)
             if (col + j < N) dst[j] = __uint_as_float(r[j]);
+        }
+      }
+      if (epi.Al != nullptr && col < N) {  // whole chunk inside one head (f % 32 == 0)
+        const float* pl = epi.a_l + col;
+        const float* pr = epi.a_r + col;
+#pragma unroll
+        for (int j = 0; j < 32; ++j) {
+          const float x = __uint_as_float(r[j]);
+          dl = fmaf(x, __ldg(pl + j), dl);
+          dr = fmaf(x, __ldg(pr + j), dr);
+        }
+        if ((col + 32) % epi.f == 0) {
+          if (row < M) {
+            const int64_t k = (col + 32) / epi.f - 1;
+            epi.Al[row * epi.h + k] = dl;
+            epi.Ar[row * epi.h + k] = dr;
+          }
+          dl = dr = 0.f;
         }
       }
     }
@@ -337,7 +360,7 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, 
 
 template <int BN, bool A_MN, bool B_MN>
 int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
-           int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s) {
+           int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s, const AttnEpi& epi) {
   using CF = Cfg<BN>;
   CUtensorMap ma, mb;
   bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
@@ -355,7 +378,7 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
     const char* e = getenv("GNNCG_TC_DEBUG");
     dbg = e ? atoi(e) : 0;
   }
-  kern<<<grid, THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride, dbg);
+  kern<<<grid, THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride, dbg, epi);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }
@@ -376,13 +399,15 @@ bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
 }
 
 int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
-            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s) {
+            int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s,
+            const AttnEpi& epi) {
   float* out = splits > 1 ? partial : C;
   const int64_t ldo = splits > 1 ? N : ldc;
   const int64_t stride = splits > 1 ? M * N : 0;
   const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
   const bool wide = N > 128;
-#define GNNCG_TC(BN, AM, BMN) return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s)
+#define GNNCG_TC(BN, AM, BMN) \
+  return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s, epi)
   if (wide) {
     if (!a_mn && !b_mn) GNNCG_TC(256, false, false);
     if (!a_mn && b_mn) GNNCG_TC(256, false, true);

@@ -234,6 +234,27 @@ def attn_dots(Ht, a_l, a_r, heads, f, Al=None, Ar=None):
     return Al, Ar
 
 
+def gat_transform(H, W, a_l, a_r, heads, f, ws=None):
+    """K1 with the attention-LP epilogue: Ht = H W, A_l = Ht . a_l, A_r = Ht . a_r in one
+    tensor-core GEMM (gnncg_gat_transform)."""
+    M, K = H.shape
+    hf = heads * f
+    dev = H.device
+    Ht = torch.empty(M, hf, device=dev)
+    Al = torch.empty(M, heads, device=dev)
+    Ar = torch.empty(M, heads, device=dev)
+    need = _lib.lib().gnncg_gemm_workspace(0, 0, M, hf, K)
+    if ws is None:
+        buf = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
+        wp, wn = buf.data_ptr(), buf.numel()
+    else:
+        wp, wn = ws.get(need)
+    with PROBE("gat_transform"):
+        call("gnncg_gat_transform", M, K, heads, f, _ptr(H), H.stride(0), _ptr(W), _ptr(Ht), _ptr(a_l), _ptr(a_r),
+             _ptr(Al), _ptr(Ar), wp, wn, _stream())
+    return Ht, Al, Ar
+
+
 def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
     """One GAT layer forward, reorganized:
     Ht = H W (K1), A_l = Ht . a_l, A_r = Ht . a_r, then the fused region (K2).
@@ -246,8 +267,7 @@ def gat_forward(g: DeviceGraph, H, W, a_l, a_r, p: GatParams, chunk=None):
         raise TensorError(f"gat_forward: W shape {tuple(W.shape)} != ({H.shape[1]}, {h * f})")
     _shape(a_l, (h, f), "a_l")
     _shape(a_r, (h, f), "a_r")
-    Ht = gemm(H, W, ws=g.ws)
-    Al, Ar = attn_dots(Ht, a_l, a_r, h, f)
+    Ht, Al, Ar = gat_transform(H, W, _f32(a_l, "a_l"), _f32(a_r, "a_r"), h, f, ws=g.ws)
     Ht_lp = pack_bf16(Ht) if _check_gather(p) else None
     out, m, d = gat_region_forward(g, Ht, Al, Ar, p, chunk=chunk, Ht_lp=Ht_lp)
     return out, GatStash(Ht, Al, Ar, m, d, out, Ht_lp)

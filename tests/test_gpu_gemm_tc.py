@@ -72,3 +72,26 @@ def test_gemm_tall_m_beyond_grid_y(cuda, tc, monkeypatch):
     C = gemm(A, B)
     torch.cuda.synchronize()
     assert C.min().item() == 8.0 and C.max().item() == 8.0
+
+
+@pytest.mark.parametrize("M,K,h,f", [(1000, 602, 8, 32), (4097, 256, 8, 32), (777, 64, 4, 64), (300, 100, 2, 32),
+                                     (513, 128, 8, 16), (50, 20, 3, 5)])
+def test_gat_transform_epilogue(cuda, M, K, h, f):
+    """K1 with the attention-LP epilogue equals gemm + attn_dots bitwise (fused when f % 32 == 0,
+    the unfused pair otherwise)."""
+    from paper_2110_09524_b200.ops import attn_dots, gat_transform, gemm
+    g = torch.Generator(device=cuda)
+    g.manual_seed(M + K)
+    ld = (K + 3) // 4 * 4
+    Hb = torch.rand(M, ld, generator=g, device=cuda) * 2 - 1
+    H = Hb[:, :K]
+    W = (torch.rand(K, h * f, generator=g, device=cuda) * 2 - 1) / K ** 0.5
+    al = torch.rand(h, f, generator=g, device=cuda) - 0.5
+    ar = torch.rand(h, f, generator=g, device=cuda) - 0.5
+    Ht, Al, Ar = gat_transform(H, W, al, ar, h, f)
+    Ht2 = gemm(H, W)
+    Al2, Ar2 = attn_dots(Ht2, al, ar, h, f)
+    torch.cuda.synchronize()
+    assert torch.equal(Ht, Ht2)
+    assert torch.equal(Al, Al2)
+    assert torch.equal(Ar, Ar2)
