@@ -262,7 +262,8 @@ int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, 
   GNNCG_REQUIRE(ldh >= K, GNNCG_ERR_SHAPE, "gat_transform: ldh < K");
   cudaStream_t s = as_stream(stream);
   const int bn = N > 128 ? 256 : 128;
-  if (K > 0 && tc_enabled() && tc_splits(M, N, K) == 1 && f % 32 == 0 && bn % f == 0 &&
+  // (a head's column chunks must stay within one epilogue warp's half of the tile)
+  if (K > 0 && tc_enabled() && tc_splits(M, N, K) == 1 && f % 32 == 0 && (bn / 2) % f == 0 &&
       tc_gemm_eligible(0, 0, M, N, K, H, ldh, W, N)) {
     AttnEpi epi;
     epi.a_l = a_l; epi.a_r = a_r; epi.Al = Al; epi.Ar = Ar; epi.h = heads; epi.f = f;

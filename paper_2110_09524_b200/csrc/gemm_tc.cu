@@ -29,7 +29,8 @@ namespace gnncg_b200 {
 namespace tc {
 
 constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one SW128 row
-constexpr int THREADS = 192;
+constexpr int SPLIT_WARPS = 8;                     // split + epilogue warps (2 per TMEM lane quadrant)
+constexpr int THREADS = 64 + 32 * SPLIT_WARPS;    // + TMA producer warp + MMA warp
 
 template <int BN>
 struct Cfg {
@@ -172,7 +173,7 @@ __global__ void __launch_bounds__(THREADS, 1)
   if (threadIdx.x == 0) {
     for (int s = 0; s < S; ++s) {
       mbar_init(&full[s], 1);
-      mbar_init(&split[s], 128);
+      mbar_init(&split[s], 32 * SPLIT_WARPS);
       mbar_init(&empty[s], 1);
     }
     mbar_init(accum, 1);
@@ -258,12 +259,15 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = i % S;
       const uint32_t ph = (uint32_t)(i / S) & 1u;
       mbar_wait(&full[s], ph);
-      split_hi_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 128);
-      split_hi_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 128);
+      split_hi_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 32 * SPLIT_WARPS);
+      split_hi_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * SPLIT_WARPS);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&split[s]);
     }
-    const int q = warp & 3;  // TMEM lane quadrant of this warp
+    const int q = warp & 3;  // TMEM lane quadrant of this warp (hardware: warp w reads lanes 32 (w % 4) ..)
+    // the two warps of a quadrant take the first / second half of the column chunks
+    const int half = (warp - 2) / 4;
+    constexpr int NCH = BN / 32 / (SPLIT_WARPS / 4);
     const int64_t row = m0 + q * 32 + lane;
     if (nk > 0) {
       mbar_wait(accum, 0);
@@ -271,7 +275,7 @@ __global__ void __launch_bounds__(THREADS, 1)
     }
     float dl = 0.f, dr = 0.f;  // attention-LP partial sums of the current head (epi.Al)
 #pragma unroll 1
-    for (int c = 0; c < BN / 32; ++c) {
+    for (int c = half * NCH; c < (half + 1) * NCH; ++c) {
       uint32_t r[32];
       if (dbg == 1) {  // debug: bypass TMEM, write a coordinate pattern
 #pragma unroll
