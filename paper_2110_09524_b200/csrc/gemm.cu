@@ -157,6 +157,7 @@ int choose_splits(int64_t M, int64_t N, int64_t K) {
 }  // namespace
 
 // Tensor-core path (gemm_tc.cu).
+int tc_bn(int64_t N);
 bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
                       const float* B, int64_t ldb);
 int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
@@ -175,7 +176,7 @@ bool tc_enabled() {
 }
 
 int tc_splits(int64_t M, int64_t N, int64_t K) {
-  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, N > 128 ? 256 : 128);
+  const int64_t tiles = ceil_div(M, 128) * ceil_div(N, tc_bn(N));
   if (tiles >= 148 || K < 8 * 1024) return 1;
   int64_t s = std::min<int64_t>(ceil_div(148, tiles), K / 2048);
   return (int)std::max<int64_t>(std::min<int64_t>(s, 64), 1);
@@ -261,7 +262,7 @@ int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, 
   GNNCG_REQUIRE(H && W && Ht && a_l && a_r && Al && Ar, GNNCG_ERR_ARG, "gat_transform: null pointer");
   GNNCG_REQUIRE(ldh >= K, GNNCG_ERR_SHAPE, "gat_transform: ldh < K");
   cudaStream_t s = as_stream(stream);
-  const int bn = N > 128 ? 256 : 128;
+  const int bn = tc_bn(N);
   // (a head's column chunks must stay within one epilogue warp's half of the tile)
   if (K > 0 && tc_enabled() && tc_splits(M, N, K) == 1 && f % 32 == 0 && (bn / 2) % f == 0 &&
       tc_gemm_eligible(0, 0, M, N, K, H, ldh, W, N)) {

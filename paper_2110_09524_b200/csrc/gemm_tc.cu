@@ -389,6 +389,18 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
 
 }  // namespace tc
 
+// N-tile width: 256 for wide outputs, or 128 when GNNCG_TC_BN=128 (a 3-stage pipeline instead
+// of 2 stages of the 96 KB 128x256 tile).
+int tc_bn(int64_t N) {
+  static int force = -1;
+  if (force < 0) {
+    const char* e = getenv("GNNCG_TC_BN");
+    force = e ? atoi(e) : 0;
+  }
+  if (force == 128) return 128;
+  return N > 128 ? 256 : 128;
+}
+
 // Entry used by gnncg_gemm (gemm.cu).  trans_a: A stored K x M ; trans_b: B stored N x K.
 // In the tensor-core kernel's terms A is MN-major iff trans_a, B is MN-major iff !trans_b.
 bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
@@ -409,7 +421,7 @@ int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const flo
   const int64_t ldo = splits > 1 ? N : ldc;
   const int64_t stride = splits > 1 ? M * N : 0;
   const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
-  const bool wide = N > 128;
+  const bool wide = tc_bn(N) == 256;
 #define GNNCG_TC(BN, AM, BMN) \
   return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s, epi)
   if (wide) {
