@@ -11,4 +11,6 @@ timeout 900 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline -
 timeout 900 python bench.py --config c5 --steps 3 --warmup 3 --no-cpu-baseline --no-e2e --gather bf16 > gpurun_out/bench_${TAG}_c5_bf16.log 2>&1
 timeout 600 ncu --metrics gpu__time_duration.sum --clock-control none -c 400 --csv --log-file gpurun_out/launches_$TAG.csv python bench.py --steps 2 --warmup 1 --no-cpu-baseline --no-e2e > gpurun_out/bench_ncu_launch_$TAG.log 2>&1
 timeout 900 ncu --set full --clock-control none --import-source on -k regex:"gat_fwd_ovl|gat_bwd_src_fast" -c 3 -o gpurun_out/prof_$TAG python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/bench_ncu_full_$TAG.log 2>&1
-echo done
+echo done-main
+timeout 600 ncu --metrics gpu__time_duration.sum,sm__pipe_tensor_cycles_active.avg.pct_of_peak_sustained_elapsed,sm__ops_path_tensor_op_utchmma_src_tf32_dst_fp32_sparsity_off.sum.pct_of_peak_sustained_elapsed,dram__bytes_read.sum,gpu__dram_throughput.avg.pct_of_peak_sustained_elapsed,launch__grid_size --clock-control none -k regex:gemm_tf32x3 -c 5 --csv --log-file gpurun_out/gemm_$TAG.csv python bench.py --steps 1 --warmup 0 --no-cpu-baseline --no-e2e > gpurun_out/bench_ncu_gemm_$TAG.log 2>&1
+echo done-gemm
