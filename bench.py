@@ -48,6 +48,8 @@ def parse():
     ap.add_argument("--no-cpu-baseline", action="store_true")
     ap.add_argument("--no-e2e", action="store_true")
     ap.add_argument("--chunk", type=int, default=None)
+    ap.add_argument("--partitioned", action="store_true",
+                    help="run the multi-GPU (row-partitioned, NCCL) path even at world size 1 (smoke of the N>1 path)")
     ap.add_argument("--gather", choices=["fp32", "bf16"], default="fp32",
                     help="GAT gather tables: fp32 (the 1e-4 contract, default) or bf16 (stated looser bound)")
     ap.add_argument("--scale", type=float, default=1.0, help="shrink V and E (debug only)")
@@ -124,9 +126,10 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
 
     t0 = time.perf_counter()
     cfg = args.config
-    if world > 1 and cfg not in ("reddit", "c5"):
+    dmode = world > 1 or args.partitioned
+    if dmode and cfg not in ("reddit", "c5"):
         raise SystemExit(f"--config {cfg} is single-GPU only")
-    if args.gather == "bf16" and (world > 1 or cfg not in ("reddit", "c5")):
+    if args.gather == "bf16" and (dmode or cfg not in ("reddit", "c5")):
         raise SystemExit("--gather bf16 applies to the single-GPU GAT configs (reddit, c5)")
     gen = torch.Generator(device=dev)
     gen.manual_seed(1234 + rank)
@@ -143,7 +146,7 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
             V, E, offset, dims = 10_000_000, 1_000_000_000, 10_000, [(128, 8, 16)] * 3
             desc = "GAT 3-layer fwd+bwd+SGD, power-law 10M nodes / 1B edges, 128-dim (BASELINE configs[4])"
         V, E, offset = int(V * args.scale), int(E * args.scale), max(1, int(offset * args.scale))
-        if world > 1:
+        if dmode:
             from paper_2110_09524_b200.dist import PartitionedGAT, partitioned_chung_lu
 
             lg = partitioned_chung_lu(V * world, E * world, offset=offset * world, seed=0, rank=rank, world=world,
@@ -340,15 +343,18 @@ def run_ours(args):
     local = int(os.environ.get("LOCAL_RANK", "0"))
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
-    if world > 1:
-        dist.init_process_group("nccl", device_id=dev)
+    dmode = world > 1 or args.partitioned  # the row-partitioned NCCL path
+    if dmode:
+        os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
+        os.environ.setdefault("MASTER_PORT", "29533")
+        dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
     wl = build_workload(args, dev, world, rank)
     model, H_buf, fin, E_total, layers = wl["model"], wl["H_buf"], wl["fin"], wl["E_total"], wl["layers"]
     H = H_buf[:, :fin]
     build_s = wl["build_s"]
 
     def barrier():
-        if world > 1:
+        if dmode:
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
@@ -388,7 +394,7 @@ def run_ours(args):
         PROBE.enabled = False
         launches = graphed.kernels * args.steps  # each replay runs the kernels counted at capture
     totals = PROBE.collect()
-    if world > 1:
+    if dmode:
         t = torch.tensor([ms], device=dev)
         dist.all_reduce(t, op=dist.ReduceOp.MAX)
         ms = float(t.item())
@@ -408,7 +414,7 @@ def run_ours(args):
         kernels[name] = k
     dominant = max((n for n in kernels if n in per_launch), key=lambda n: kernels[n]["share_of_step"])
     traffic = None
-    headline = args.config == "reddit" and world == 1 and args.gather == "fp32"  # what profiles/ captured
+    headline = args.config == "reddit" and not dmode and args.gather == "fp32"  # what profiles/ captured
     tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
     if headline and os.path.exists(tpath):
         with open(tpath) as fh:
@@ -465,7 +471,8 @@ def run_ours(args):
             compute.wait_event(ready[b])
             loss, grads = model.train_step(bufs[b][:, :fin], lr=lr)
             free[b].record(compute)
-            res = [loss] + [t for gr in grads for t in _grad_tensors(gr)]
+            # parameter gradients only (dist.PartitionedGAT returns (dW, da_l, da_r, dH) per layer)
+            res = [loss] + [t for gr in grads for t in (gr[:3] if dmode else _grad_tensors(gr))]
             if out_bufs is None:
                 out_bufs = [torch.empty(t.shape, dtype=t.dtype, pin_memory=True) for t in res]
             for hb, t in zip(out_bufs, res):
@@ -473,7 +480,7 @@ def run_ours(args):
         e.record()
         barrier()
         ems = s.elapsed_time(e)
-        if world > 1:
+        if dmode:
             t = torch.tensor([ems], device=dev)
             dist.all_reduce(t, op=dist.ReduceOp.MAX)
             ems = float(t.item())
@@ -493,13 +500,13 @@ def run_ours(args):
                 "vs_baseline": None, "dtype": "f32" if args.gather == "fp32" else "f32 (bf16 gather tables)",
                 "data": "synthetic (Chung-Lu graph, uniform features, "
                 "random-init weights)",
-                "config": {**wl["config"], "parallelism": f"row-partition x{world}" if world > 1 else "single GPU",
+                "config": {**wl["config"], "parallelism": f"row-partition x{world}" if dmode else "single GPU",
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
                 "cost_model": wl.get("cost"),
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
-    if world > 1:
+    if dmode:
         dist.destroy_process_group()
 
 

@@ -5,17 +5,18 @@ edge counts (``gnncg_partition_rows``: bound[p] = lower_bound(off, ceil(p E / P)
 Rank p owns rows [r_p, r_{p+1}) and every tensor indexed by them (H, out, m, d, A_r, dOut).
 
 Per layer, forward:
-  Ht_p = H_p W                      (K1 on local rows)
-  all_gather(Ht)                    (NCCL over NVLink; blocks padded to the largest)
-  A_l, A_r = Ht_full . a_l / a_r    (cheap: one read of Ht_full)
+  Ht_p, A_l,p, A_r,p = K1(H_p)      (one tensor-core GEMM with the LP epilogue, local rows)
+  all_gather(Ht), all_gather(A_l)   (NCCL over NVLink; blocks padded to the largest)
   K2 over the local csr_dst block   (no collective: destination rows are independent)
 Backward:
   K3 over the local csr_dst block   (c, dA_r: local)
   K4 over the local csc_src         (rows = all sources, neighbours = local rows):
                                     partial dHt / dA_l for every source
-  reduce_scatter(dHt partials)      -> dHt for the owned rows (the terms are linear)
-  dW_p = H_p^T dHt_p, da_l/da_r partial -> all_reduce (tiny)
+  reduce_scatter(dHt), reduce_scatter(dA_l) -> the owned rows (the terms are linear)
+  LP grads over the owned rows, dW_p = H_p^T dHt_p -> all_reduce (tiny)
   dH_p = dHt_p W^T
+Every per-row computation touches only the rank's own rows; the gathered tensors are read
+only by the fused kernels.
 
 Source ids inside the local indexes are remapped to the PADDED global layout of the
 all-gather buffer (block p at rows [p*maxrows, p*maxrows + n_p)), so the kernels index
@@ -34,7 +35,7 @@ import torch.distributed as dist
 from . import _lib
 from ._lib import call
 from .graph import DeviceIndex, DeviceSched, Workspace, _ptr, _stream, chung_lu_cdf, partition_rows
-from .ops import GatParams, gemm, PROBE
+from .ops import GatParams, PROBE, gat_transform, gemm
 
 
 @dataclass
@@ -132,6 +133,10 @@ class CudaEngine:
     def gemm(self, A, B, ta=False, tb=False):
         return gemm(A, B, trans_a=ta, trans_b=tb, ws=self.ws)
 
+    def transform(self, H, W, a_l, a_r, p: GatParams):
+        """K1 with the LP epilogue on the local rows: (Ht, A_l, A_r)."""
+        return gat_transform(H, W, a_l, a_r, p.heads, p.f, ws=self.ws)
+
     def attn_dots(self, Ht, a_l, a_r, p: GatParams):
         V = Ht.shape[0]
         Al, Ar = self.empty(V, p.heads), self.empty(V, p.heads)
@@ -150,10 +155,9 @@ class CudaEngine:
                  _ptr(Ar_local), _ptr(out), _ptr(m), _ptr(d), wp, wn, _stream())
         return out, m, d
 
-    def region_bwd(self, lg: LocalGraph, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p: GatParams, out=None):
+    def region_bwd(self, lg: LocalGraph, Ht, Al, Ar_local, m, d, dOut, a_l, a_r, p: GatParams, out=None):
         """K3 + K4 (or the fused fast pass) -> (dHt partial over padded sources, dAl partial, dAr local)."""
         n, h, f = lg.num_local, p.heads, p.f
-        Ar_local = Ar_full[lg.row_base:lg.row_base + n]
         c, dAr = self.empty(n, h), self.empty(n, h)
         sd, ss = self._sched(lg.csr), self._sched(lg.csc)
         Vp = lg.plan.padded_V
@@ -267,13 +271,12 @@ class PartitionedGAT:
         E, lg, mr = self.engine, self.lg, self.lg.plan.maxrows
         xs, stashes = [H], []
         for L in self.layers:
-            Ht_local = E.gemm(xs[-1], L.W)
+            Ht_local, Al_local, Ar_local = E.transform(xs[-1], L.W, L.a_l, L.a_r, L.p)
             Ht = self.comm.all_gather_rows(Ht_local, mr)
-            Al, Ar = E.attn_dots(Ht, L.a_l, L.a_r, L.p)
-            Ar_local = Ar[lg.row_base:lg.row_base + lg.num_local]
+            Al = self.comm.all_gather_rows(Al_local, mr)
             out, m, d = E.region_fwd(lg, Ht, Al, Ar_local, L.p)
             xs.append(out)
-            stashes.append((Ht, Al, Ar, m, d, out))
+            stashes.append((Ht, Ht_local, Al, Ar_local, m, d, out))
         return xs, stashes
 
     def backward(self, xs, stashes, dOut):
@@ -283,12 +286,11 @@ class PartitionedGAT:
         g = dOut
         for i in reversed(range(len(self.layers))):
             L = self.layers[i]
-            Ht, Al, Ar, m, d, out = stashes[i]
-            dHt_part, dAl_part, dAr = E.region_bwd(lg, Ht, Al, Ar, m, d, g, L.a_l, L.a_r, L.p, out=out)
+            Ht, Ht_local, Al, Ar_local, m, d, out = stashes[i]
+            dHt_part, dAl_part, dAr = E.region_bwd(lg, Ht, Al, Ar_local, m, d, g, L.a_l, L.a_r, L.p, out=out)
             dHt = self.comm.reduce_scatter_rows(dHt_part, mr, n)
-            dAr_full = E.zeros(lg.plan.padded_V, L.p.heads)
-            dAr_full[lg.row_base:lg.row_base + n] = dAr
-            da_l, da_r = E.attn_grad(Ht, dAl_part, dAr_full, L.p)
+            dAl = self.comm.reduce_scatter_rows(dAl_part, mr, n)
+            da_l, da_r = E.attn_grad(Ht_local, dAl, dAr, L.p)  # owned rows only; summed by the all-reduce
             dW = E.gemm(xs[i], dHt, ta=True)
             packed = torch.cat([dW.reshape(-1), da_l.reshape(-1), da_r.reshape(-1)])
             self.comm.all_reduce(packed)

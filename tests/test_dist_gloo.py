@@ -37,19 +37,23 @@ class OracleEngine:
         H3 = Ht.view(Ht.shape[0], p.heads, p.f)
         return (H3 * a_l).sum(-1), (H3 * a_r).sum(-1)
 
+    def transform(self, H, W, a_l, a_r, p):
+        Ht = H @ W
+        return (Ht, *self.attn_dots(Ht, a_l, a_r, p))
+
     def region_fwd(self, lg, Ht, Al, Ar_local, p):
         c = lg.csr
         g = O.HostGraph(c["rows"], None, None, c["off"], c["nbr"], c["eid"], None, None, None)
         r = O.gat_region_fwd_f64(g, Ht.numpy(), Al.numpy(), Ar_local.numpy(), p.heads, p.f, p.slope)
         return torch.from_numpy(r["out"]), torch.from_numpy(r["m"]), torch.from_numpy(r["d"])
 
-    def region_bwd(self, lg, Ht, Al, Ar_full, m, d, dOut, a_l, a_r, p, out=None):
+    def region_bwd(self, lg, Ht, Al, Ar_local, m, d, dOut, a_l, a_r, p, out=None):
         h, f, n, base = p.heads, p.f, lg.num_local, lg.row_base
         c = lg.csr
         v = np.repeat(np.arange(n), np.diff(c["off"].astype(np.int64)))
         u = c["nbr"].astype(np.int64)
         Ht3, dO3 = Ht.numpy().reshape(-1, h, f), dOut.numpy().reshape(n, h, f)
-        Ar = Ar_full.numpy()[base:base + n]
+        Ar = Ar_local.numpy()
         z = Al.numpy()[u] + Ar[v]
         s = np.where(z > 0, z, p.slope * z)
         a = np.exp(s - m.numpy()[v]) / d.numpy()[v]
