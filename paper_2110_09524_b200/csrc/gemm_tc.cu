@@ -28,7 +28,10 @@
 namespace gnncg_b200 {
 namespace tc {
 
-constexpr int BM = 128, BK = 32;  // BK fp32 = 128 B = one SW128 row
+// BK fp32 = 64 B: K-major tiles are SWIZZLE_64B rows (8-row atoms 512 B apart); MN-major tiles
+// are SWIZZLE_128B_BASE32B boxes of 32 elements x BK k-rows.  A 48 KB stage (128 x 256 tile:
+// raw/hi + lo of A and B) gives a 4-deep pipeline in 192 KB.
+constexpr int BM = 128, BK = 16;
 constexpr int SPLIT_WARPS = 8;                     // split + epilogue warps (2 per TMEM lane quadrant)
 constexpr int THREADS = 64 + 32 * SPLIT_WARPS;    // + TMA producer warp + MMA warp
 
@@ -37,7 +40,7 @@ struct Cfg {
   static constexpr int A_BYTES = BM * BK * 4;
   static constexpr int B_BYTES = BN * BK * 4;
   static constexpr int STAGE_BYTES = 2 * (A_BYTES + B_BYTES);  // raw->hi and lo of A and B
-  static constexpr int STAGES = BN >= 256 ? 2 : 3;
+  static constexpr int STAGES = (192 * 1024) / STAGE_BYTES;
   static constexpr int SMEM = STAGES * STAGE_BYTES + 1024 /*align*/ + 256 /*barriers*/;
 };
 
@@ -72,7 +75,7 @@ __device__ __forceinline__ void tma_load_2d(void* dst, const CUtensorMap* map, i
       : "memory");
 }
 
-// SM100 shared-memory matrix descriptor, version 1.  layout: 2 = SWIZZLE_128B (K-major
+// SM100 shared-memory matrix descriptor, version 1.  layout: 4 = SWIZZLE_64B (K-major
 // operands), 1 = SWIZZLE_128B_BASE32B (the only layout for MN-major 32-bit operands:
 // Swizzle<2,5,2>, atoms of 32 elements x 4 k-rows).
 __device__ __forceinline__ uint64_t smem_desc(uint32_t addr, uint32_t lbo_bytes, uint32_t sbo_bytes,
@@ -211,26 +214,29 @@ __global__ void __launch_bounds__(THREADS, 1)
         } else {
 #pragma unroll
           for (int j = 0; j < BM / 32; ++j)
-            tma_load_2d(reinterpret_cast<uint8_t*>(a_hi(s)) + j * 4096, &map_a, (int)m0 + 32 * j, k, &full[s]);
+            tma_load_2d(reinterpret_cast<uint8_t*>(a_hi(s)) + j * (32 * BK * 4), &map_a, (int)m0 + 32 * j, k,
+                        &full[s]);
         }
         if (!B_MN) {
           tma_load_2d(b_hi(s), &map_b, k, (int)n0, &full[s]);
         } else {
 #pragma unroll
           for (int j = 0; j < BN / 32; ++j)
-            tma_load_2d(reinterpret_cast<uint8_t*>(b_hi(s)) + j * 4096, &map_b, (int)n0 + 32 * j, k, &full[s]);
+            tma_load_2d(reinterpret_cast<uint8_t*>(b_hi(s)) + j * (32 * BK * 4), &map_b, (int)n0 + 32 * j, k,
+                        &full[s]);
         }
       }
     }
   } else if (warp == 1) {
     if (lane == 0) {  // ---- MMA issuer
       constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
-      // K-major (SW128): rows of 128 B, 8-row atoms 1024 B apart (SBO), k-step = +32 B.
-      // MN-major (SW128_32B): 32-element x 32-k boxes (4 KB) along MN (LBO), 4-k-row atoms
-      // 512 B apart (SBO), k-step (8 rows) = +1024 B.
-      const uint32_t a_lbo = A_MN ? 4096u : 16u, a_sbo = A_MN ? 512u : 1024u, a_step = A_MN ? 1024u : 32u;
-      const uint32_t b_lbo = B_MN ? 4096u : 16u, b_sbo = B_MN ? 512u : 1024u, b_step = B_MN ? 1024u : 32u;
-      const uint32_t a_lay = A_MN ? 1u : 2u, b_lay = B_MN ? 1u : 2u;
+      // K-major (SW64): rows of 64 B, 8-row atoms 512 B apart (SBO), k-step = +32 B.
+      // MN-major (SW128_32B): 32-element x BK-k boxes (32 BK 4 B) along MN (LBO), 4-k-row
+      // atoms 512 B apart (SBO), k-step (8 rows) = +1024 B.
+      constexpr uint32_t MNBOX = 32 * BK * 4;
+      const uint32_t a_lbo = A_MN ? MNBOX : 16u, a_sbo = 512u, a_step = A_MN ? 1024u : 32u;
+      const uint32_t b_lbo = B_MN ? MNBOX : 16u, b_sbo = 512u, b_step = B_MN ? 1024u : 32u;
+      const uint32_t a_lay = A_MN ? 1u : 4u, b_lay = B_MN ? 1u : 4u;
       for (int i = 0; i < nk; ++i) {
         const int s = i % S;
         const uint32_t ph = (uint32_t)(i / S) & 1u;
@@ -356,7 +362,7 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, 
   cuuint32_t estr[2] = {1, 1};
   CUresult r = fn(map, CU_TENSOR_MAP_DATA_TYPE_FLOAT32, 2, const_cast<float*>(ptr), dims, strides, box, estr,
                   CU_TENSOR_MAP_INTERLEAVE_NONE,
-                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_128B,
+                  mn_major ? CU_TENSOR_MAP_SWIZZLE_128B_ATOM_32B : CU_TENSOR_MAP_SWIZZLE_64B,
                   CU_TENSOR_MAP_L2_PROMOTION_L2_256B,
                   CU_TENSOR_MAP_FLOAT_OOB_FILL_NONE);
   return r == CUDA_SUCCESS;
