@@ -3,22 +3,26 @@
 // Dense transforms on the 5th-gen tensor cores (K1 / K5 on sm_100a):
 //   C[M,N] = op(A)[M,K] op(B)[K,N], fp32 in / fp32 out, fp32-accurate via a 3xTF32
 //   split: x = hi + lo (hi = x with the low 13 mantissa bits cleared, lo = x - hi
-//   exactly), C = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.
+//   exactly), C = A_hi B_hi + A_hi B_lo + A_lo B_hi accumulated in TMEM.  The tensor core
+//   truncates fp32 operands to tf32, so the raw landed tile IS hi: only lo is materialised
+//   (pinned by tests/test_gpu_gemm_tc.py::test_tc_gemm_identity_split).
 // Replaces matmul / matmul_nt / matmul_tn (proj/src/tensor.cpp:8-60) for the
 // reorganized ApplyVertex(W) of the GNN layers and its two backward Applies.
 //
-// Structure (one 128 x BN output tile per CTA, K split across gridDim.z):
-//   warp 0      TMA producer: cp.async.bulk.tensor 2D boxes (SWIZZLE_128B) of A and B
-//   warp 1      TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32)
-//   warps 2..5  split warps: hi/lo of each landed stage in shared memory, then the
-//               epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
-// mbarrier pipeline: full (TMA bytes) -> split (128 threads) -> MMA -> empty
-// (tcgen05.commit) ; accum (tcgen05.commit after the last k-block) -> epilogue.
-// Operands may be K-major or MN-major (transposed), both through SW128 smem
-// descriptors: K-major rows of 32 fp32 (128 B), MN-major 32-element x 32-k boxes.
+// Default kernel (gemm_tf32x3_persist_kernel): one CTA per SM walks the output tiles;
+//   warp 0       TMA producer: cp.async.bulk.tensor 2D boxes of A and B
+//   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32)
+//   warps 2..7   split warps: lo of each landed stage in shared memory
+//   warps 8..11  epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
+// mbarrier pipeline: full (TMA bytes) -> split -> MMA -> empty (tcgen05.commit); the
+// accumulator is double-buffered in TMEM (accfull / accempty), so tile i's epilogue overlaps
+// tile i+1's main loop.  gemm_tf32x3_kernel (GNNCG_TC_PERSIST=0) is the one-tile-per-CTA form.
+// Operands may be K-major (SWIZZLE_64B rows of BK = 16 fp32) or MN-major (transposed;
+// SWIZZLE_128B_BASE32B boxes of 32 elements x BK k-rows).
 #include <cuda.h>
 #include <cudaTypedefs.h>
 
+#include <algorithm>
 #include <cstdlib>
 #include <cstring>
 #include <mutex>
@@ -128,19 +132,18 @@ __device__ __forceinline__ void tmem_ld32(uint32_t taddr, uint32_t (&r)[32]) {
       : "memory");
 }
 
-// Split a landed stage buffer in place: buf holds raw fp32; write hi (in place) and lo.
-__device__ __forceinline__ void split_hi_lo(float* raw, float* lo, int bytes, int tid, int nthr) {
-  float4* r4 = reinterpret_cast<float4*>(raw);
+// lo = x - hi of a landed stage (hi = the raw tile itself: the tensor core truncates to tf32).
+__device__ __forceinline__ void split_lo(const float* raw, float* lo, int bytes, int tid, int nthr) {
+  const float4* r4 = reinterpret_cast<const float4*>(raw);
   float4* l4 = reinterpret_cast<float4*>(lo);
   const int n = bytes / 16;
   for (int i = tid; i < n; i += nthr) {
-    float4 v = r4[i];
+    const float4 v = r4[i];
     float4 h;
     h.x = __uint_as_float(__float_as_uint(v.x) & 0xFFFFE000u);
     h.y = __uint_as_float(__float_as_uint(v.y) & 0xFFFFE000u);
     h.z = __uint_as_float(__float_as_uint(v.z) & 0xFFFFE000u);
     h.w = __uint_as_float(__float_as_uint(v.w) & 0xFFFFE000u);
-    r4[i] = h;
     l4[i] = make_float4(v.x - h.x, v.y - h.y, v.z - h.z, v.w - h.w);
   }
 }
@@ -265,8 +268,8 @@ __global__ void __launch_bounds__(THREADS, 1)
       const int s = i % S;
       const uint32_t ph = (uint32_t)(i / S) & 1u;
       mbar_wait(&full[s], ph);
-      split_hi_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 32 * SPLIT_WARPS);
-      split_hi_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * SPLIT_WARPS);
+      split_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 32 * SPLIT_WARPS);
+      split_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * SPLIT_WARPS);
       asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
       mbar_arrive(&split[s]);
     }
@@ -337,6 +340,225 @@ __global__ void __launch_bounds__(THREADS, 1)
   }
 }
 
+// ------------------------------------------------------------------------ persistent variant
+// One CTA per SM walks the output tiles (M fastest, then N, then the split-K slice).  The stage
+// ring runs continuously across tiles, and the accumulator is double-buffered in TMEM
+// (2 x BN columns), so the epilogue of tile i (its own 4 warps, one per TMEM lane quadrant)
+// overlaps the TMA / split / MMA work of tile i+1, and no CTA pays the TMEM allocation and
+// pipeline fill per tile.
+//   warp 0 TMA producer | warp 1 MMA issuer | warps 2..7 split | warps 8..11 epilogue
+constexpr int P_SPLIT_WARPS = 6;
+constexpr int P_EPI_WARP0 = 2 + P_SPLIT_WARPS;  // 8: warp % 4 == TMEM lane quadrant
+constexpr int P_THREADS = 32 * (P_EPI_WARP0 + 4);
+
+template <int BN, bool A_MN, bool B_MN>
+__global__ void __launch_bounds__(P_THREADS, 1)
+    gemm_tf32x3_persist_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
+                               float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk,
+                               int64_t split_stride, int tiles_m, int tiles_n, int64_t tiles, AttnEpi epi) {
+  static_assert(P_EPI_WARP0 % 4 == 0, "epilogue warps must start on a lane-quadrant boundary");
+  using CF = Cfg<BN>;
+  constexpr int S = CF::STAGES;
+  extern __shared__ uint8_t smem_raw[];
+  uint8_t* smem = reinterpret_cast<uint8_t*>((reinterpret_cast<uintptr_t>(smem_raw) + 1023) & ~uintptr_t(1023));
+  uint64_t* bars = reinterpret_cast<uint64_t*>(smem + S * CF::STAGE_BYTES);
+  uint64_t* full = bars;
+  uint64_t* split = bars + S;
+  uint64_t* empty = bars + 2 * S;
+  uint64_t* accfull = bars + 3 * S;       // [2]
+  uint64_t* accempty = bars + 3 * S + 2;  // [2]
+  uint32_t* tmem_slot = reinterpret_cast<uint32_t*>(bars + 3 * S + 4);
+  const int warp = threadIdx.x >> 5, lane = threadIdx.x & 31;
+
+  if (threadIdx.x == 0) {
+    for (int s = 0; s < S; ++s) {
+      mbar_init(&full[s], 1);
+      mbar_init(&split[s], 32 * P_SPLIT_WARPS);
+      mbar_init(&empty[s], 1);
+    }
+    for (int b = 0; b < 2; ++b) {
+      mbar_init(&accfull[b], 1);
+      mbar_init(&accempty[b], 128);
+    }
+    asm volatile("fence.mbarrier_init.release.cluster;" ::: "memory");
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_a));
+    asm volatile("prefetch.tensormap [%0];" ::"l"(&map_b));
+  }
+  if (warp == 1) {
+    asm volatile("tcgen05.alloc.cta_group::1.sync.aligned.shared::cta.b32 [%0], %1;" ::"r"(smem_u32(tmem_slot)),
+                 "r"(2 * BN));
+    asm volatile("tcgen05.relinquish_alloc_permit.cta_group::1.sync.aligned;");
+  }
+  asm volatile("tcgen05.fence::before_thread_sync;");
+  __syncthreads();
+  asm volatile("tcgen05.fence::after_thread_sync;");
+  const uint32_t tmem = *tmem_slot;
+
+  auto a_hi = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES); };
+  auto a_lo = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + CF::A_BYTES); };
+  auto b_hi = [&](int s) { return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES); };
+  auto b_lo = [&](int s) {
+    return reinterpret_cast<float*>(smem + s * CF::STAGE_BYTES + 2 * CF::A_BYTES + CF::B_BYTES);
+  };
+  // tile t -> (m0, n0, k range, split slice)
+  struct Tile {
+    int64_t m0, n0, kb0;
+    int nk, z;
+  };
+  auto tile_of = [&](int64_t t) {
+    Tile x;
+    const int64_t mt = t % tiles_m, rest = t / tiles_m;
+    x.m0 = mt * BM;
+    x.n0 = (rest % tiles_n) * BN;
+    x.z = (int)(rest / tiles_n);
+    x.kb0 = (int64_t)x.z * kchunk;
+    const int64_t kb1 = min(K, x.kb0 + kchunk);
+    x.nk = (int)((kb1 - x.kb0 + BK - 1) / BK);
+    return x;
+  };
+
+  if (warp == 0) {
+    if (lane == 0) {  // ---- TMA producer
+      uint32_t g = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+        const Tile x = tile_of(t);
+        for (int i = 0; i < x.nk; ++i, ++g) {
+          const int s = (int)(g % S);
+          const uint32_t ph = (g / S) & 1u;
+          mbar_wait(&empty[s], ph ^ 1u);
+          mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+          const int k = (int)(x.kb0 + (int64_t)i * BK);
+          if (!A_MN) {
+            tma_load_2d(a_hi(s), &map_a, k, (int)x.m0, &full[s]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BM / 32; ++j)
+              tma_load_2d(reinterpret_cast<uint8_t*>(a_hi(s)) + j * (32 * BK * 4), &map_a, (int)x.m0 + 32 * j, k,
+                          &full[s]);
+          }
+          if (!B_MN) {
+            tma_load_2d(b_hi(s), &map_b, k, (int)x.n0, &full[s]);
+          } else {
+#pragma unroll
+            for (int j = 0; j < BN / 32; ++j)
+              tma_load_2d(reinterpret_cast<uint8_t*>(b_hi(s)) + j * (32 * BK * 4), &map_b, (int)x.n0 + 32 * j, k,
+                          &full[s]);
+          }
+        }
+      }
+    }
+  } else if (warp == 1) {
+    if (lane == 0) {  // ---- MMA issuer
+      constexpr uint32_t idesc = instr_desc(BN, A_MN, B_MN);
+      constexpr uint32_t MNBOX = 32 * BK * 4;
+      const uint32_t a_lbo = A_MN ? MNBOX : 16u, a_sbo = 512u, a_step = A_MN ? 1024u : 32u;
+      const uint32_t b_lbo = B_MN ? MNBOX : 16u, b_sbo = 512u, b_step = B_MN ? 1024u : 32u;
+      const uint32_t a_lay = A_MN ? 1u : 4u, b_lay = B_MN ? 1u : 4u;
+      uint32_t g = 0, it = 0;
+      for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+        const Tile x = tile_of(t);
+        const uint32_t b = it & 1u, use = it >> 1;
+        mbar_wait(&accempty[b], (use & 1u) ^ 1u);  // the epilogue has drained this accumulator
+        asm volatile("tcgen05.fence::after_thread_sync;");
+        const uint32_t d = tmem + b * BN;
+        for (int i = 0; i < x.nk; ++i, ++g) {
+          const int s = (int)(g % S);
+          const uint32_t ph = (g / S) & 1u;
+          mbar_wait(&split[s], ph);
+          asm volatile("tcgen05.fence::after_thread_sync;");
+          const uint32_t ah = smem_u32(a_hi(s)), al = smem_u32(a_lo(s));
+          const uint32_t bh = smem_u32(b_hi(s)), bl = smem_u32(b_lo(s));
+#pragma unroll
+          for (int k = 0; k < BK / 8; ++k) {
+            const uint64_t dah = smem_desc(ah + k * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dal = smem_desc(al + k * a_step, a_lbo, a_sbo, a_lay);
+            const uint64_t dbh = smem_desc(bh + k * b_step, b_lbo, b_sbo, b_lay);
+            const uint64_t dbl = smem_desc(bl + k * b_step, b_lbo, b_sbo, b_lay);
+            mma_tf32(d, dah, dbh, idesc, (i > 0 || k > 0) ? 1u : 0u);
+            mma_tf32(d, dah, dbl, idesc, 1u);
+            mma_tf32(d, dal, dbh, idesc, 1u);
+          }
+          mma_commit(&empty[s]);
+        }
+        mma_commit(&accfull[b]);
+      }
+    }
+  } else if (warp < P_EPI_WARP0) {
+    // ---- split warps: lo of every landed stage
+    const int tid = threadIdx.x - 64;
+    uint32_t g = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x) {
+      const Tile x = tile_of(t);
+      for (int i = 0; i < x.nk; ++i, ++g) {
+        const int s = (int)(g % S);
+        const uint32_t ph = (g / S) & 1u;
+        mbar_wait(&full[s], ph);
+        split_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 32 * P_SPLIT_WARPS);
+        split_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * P_SPLIT_WARPS);
+        asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
+        mbar_arrive(&split[s]);
+      }
+    }
+  } else {
+    // ---- epilogue warps: TMEM -> registers -> global (+ the attention LPs)
+    const int q = warp & 3;
+    uint32_t it = 0;
+    for (int64_t t = blockIdx.x; t < tiles; t += gridDim.x, ++it) {
+      const Tile x = tile_of(t);
+      const uint32_t b = it & 1u, use = it >> 1;
+      mbar_wait(&accfull[b], use & 1u);
+      asm volatile("tcgen05.fence::after_thread_sync;");
+      float* Cz = C + (int64_t)x.z * split_stride;
+      const int64_t row = x.m0 + q * 32 + lane;
+      float dl = 0.f, dr = 0.f;
+#pragma unroll 1
+      for (int c = 0; c < BN / 32; ++c) {
+        uint32_t r[32];
+        tmem_ld32(tmem + b * BN + ((uint32_t)(q * 32) << 16) + (uint32_t)(c * 32), r);
+        const int64_t col = x.n0 + c * 32;
+        if (row < M) {
+          float* dst = Cz + row * ldc + col;
+          if (col + 32 <= N && (reinterpret_cast<uintptr_t>(dst) & 15) == 0) {
+#pragma unroll
+            for (int j = 0; j < 32; j += 4)
+              *reinterpret_cast<float4*>(dst + j) = make_float4(__uint_as_float(r[j]), __uint_as_float(r[j + 1]),
+                                                                __uint_as_float(r[j + 2]), __uint_as_float(r[j + 3]));
+          } else {
+#pragma unroll
+            for (int j = 0; j < 32; ++j)
+              if (col + j < N) dst[j] = __uint_as_float(r[j]);
+          }
+        }
+        if (epi.Al != nullptr && col < N) {  // whole chunk inside one head (f % 32 == 0)
+          const float* pl = epi.a_l + col;
+          const float* pr = epi.a_r + col;
+#pragma unroll
+          for (int j = 0; j < 32; ++j) {
+            const float xv = __uint_as_float(r[j]);
+            dl = fmaf(xv, __ldg(pl + j), dl);
+            dr = fmaf(xv, __ldg(pr + j), dr);
+          }
+          if ((col + 32) % epi.f == 0) {
+            if (row < M) {
+              const int64_t k = (col + 32) / epi.f - 1;
+              epi.Al[row * epi.h + k] = dl;
+              epi.Ar[row * epi.h + k] = dr;
+            }
+            dl = dr = 0.f;
+          }
+        }
+      }
+      asm volatile("tcgen05.fence::before_thread_sync;");
+      mbar_arrive(&accempty[b]);
+    }
+  }
+  __syncthreads();
+  if (warp == 1) {
+    asm volatile("tcgen05.fence::after_thread_sync;");
+    asm volatile("tcgen05.dealloc.cta_group::1.sync.aligned.b32 %0, %1;" ::"r"(tmem), "r"(2 * BN));
+  }
+}
+
 // ---------------------------------------------------------------------------------- host
 PFN_cuTensorMapEncodeTiled_v12000 encode_fn() {
   static PFN_cuTensorMapEncodeTiled_v12000 fn = nullptr;
@@ -368,6 +590,16 @@ bool make_map(CUtensorMap* map, const float* ptr, int64_t inner, int64_t outer, 
   return r == CUDA_SUCCESS;
 }
 
+// GNNCG_TC_PERSIST=0 selects the one-tile-per-CTA kernel.
+bool persist_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_TC_PERSIST");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int BN, bool A_MN, bool B_MN>
 int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
            int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s, const AttnEpi& epi) {
@@ -376,6 +608,26 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
   bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
   ok = ok && (B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true) : make_map(&mb, B, K, N, ldb, BK, BN, false));
   if (!ok) return fail(GNNCG_ERR_CUDA, "gemm_tc: cuTensorMapEncodeTiled failed");
+  if (persist_enabled()) {
+    auto pk = gemm_tf32x3_persist_kernel<BN, A_MN, B_MN>;
+    static bool pattr = false;
+    if (!pattr) {
+      GNNCG_CUDA_TRY(cudaFuncSetAttribute(pk, cudaFuncAttributeMaxDynamicSharedMemorySize, CF::SMEM));
+      pattr = true;
+    }
+    const int tm = (int)ceil_div(M, BM), tn = (int)ceil_div(N, BN);
+    const int64_t tiles = (int64_t)tm * tn * splits;
+    static int sms = 0;
+    if (sms == 0) {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
+    }
+    const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
+    pk<<<grid, P_THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride, tm, tn, tiles, epi);
+    GNNCG_LAUNCH_CHECK();
+    return GNNCG_OK;
+  }
   auto kern = gemm_tf32x3_kernel<BN, A_MN, B_MN>;
   static bool attr_set = false;
   if (!attr_set) {

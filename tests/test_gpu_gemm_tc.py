@@ -95,3 +95,20 @@ def test_gat_transform_epilogue(cuda, M, K, h, f):
     assert torch.equal(Ht, Ht2)
     assert torch.equal(Al, Al2)
     assert torch.equal(Ar, Ar2)
+
+
+@pytest.mark.parametrize("ta,tb", [(0, 0), (0, 1), (1, 0)])
+def test_tc_gemm_identity_split(cuda, ta, tb):
+    """C = A I reproduces every element of A to 2^-20 relative.  This pins the 3xTF32 split the
+    kernel relies on (a = hi + lo, hi = a with the low 13 mantissa bits cleared): the only loss
+    left is lo's own conversion to tf32 (<= 2^-21 |a|).  A split whose hi were ROUNDED rather
+    than truncated by the tensor core would leave up to 2^-11 |a| on about half of the entries."""
+    rng = np.random.default_rng(11)
+    M, K = 640, 96
+    A = padded(K, M, cuda, rng) if ta else padded(M, K, cuda, rng)
+    I = torch.eye(K, device=cuda, dtype=torch.float32)
+    C = gemm(A, I, trans_a=bool(ta), trans_b=bool(tb))
+    torch.cuda.synchronize()
+    ref = (A.T if ta else A).double()
+    rel = ((C.double() - ref).abs() / ref.abs().clamp_min(1e-30)).max().item()
+    assert rel <= 2.0 ** -20, rel
