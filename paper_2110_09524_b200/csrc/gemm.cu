@@ -162,7 +162,7 @@ bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
                       const float* B, int64_t ldb);
 int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
             int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s,
-            const AttnEpi& epi);
+            const AttnEpi& epi, const float* B_lo = nullptr, int64_t ldb_lo = 0);
 
 namespace {
 // GNNCG_GEMM=simt forces the CUDA-core kernel (A/B comparisons); default: tensor cores when eligible.
@@ -175,11 +175,30 @@ bool tc_enabled() {
   return v == 1;
 }
 
+// The reused operand of a tall GEMM (the weight: B of H W and of dHt W^T) is split into its
+// tf32 lo part once per call into the workspace, so the kernel's split warps only process A.
+// presplit_b_bytes: the bytes of that dense copy ((rows, cols) = B as stored), or 0 when unused.
+
+__global__ void presplit_lo_kernel(int64_t rows, int64_t cols, const float* __restrict__ B, int64_t ldb,
+                                   float* __restrict__ lo) {
+  const int64_t n = rows * cols;
+  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
+    const int64_t r = i / cols, c = i - r * cols;
+    const float x = __ldg(B + r * ldb + c);
+    lo[i] = x - __uint_as_float(__float_as_uint(x) & 0xFFFFE000u);
+  }
+}
+
 int tc_splits(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ceil_div(M, 128) * ceil_div(N, tc_bn(N));
   if (tiles >= 148 || K < 8 * 1024) return 1;
   int64_t s = std::min<int64_t>(ceil_div(148, tiles), K / 2048);
   return (int)std::max<int64_t>(std::min<int64_t>(s, 64), 1);
+}
+size_t presplit_b_bytes(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K) {
+  const int64_t rows = trans_b ? N : K, cols = trans_b ? K : N;
+  if (trans_a || cols % 4 != 0 || M < 16384 || rows * cols > (4 << 20) || tc_splits(M, N, K) != 1) return 0;
+  return align_up((size_t)rows * cols * sizeof(float));
 }
 }  // namespace
 }  // namespace gnncg_b200
@@ -189,10 +208,9 @@ using namespace gnncg_b200;
 extern "C" {
 
 size_t gnncg_gemm_workspace(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K) {
-  (void)trans_a;
-  (void)trans_b;
   const int s = std::max(choose_splits(M, N, K), tc_splits(M, N, K));
-  return s > 1 ? align_up((size_t)s * M * N * sizeof(float)) : 0;
+  const size_t split = s > 1 ? align_up((size_t)s * M * N * sizeof(float)) : 0;
+  return std::max(split, presplit_b_bytes(trans_a, trans_b, M, N, K));
 }
 
 int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda,
@@ -218,8 +236,18 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
     int splits = tc_splits(M, N, K);
     const int64_t kchunk = splits > 1 ? ceil_div(ceil_div(K, splits), 32) * 32 : K;
     splits = splits > 1 ? (int)ceil_div(K, kchunk) : 1;  // every split gets >= 1 k-block
+    const float* B_lo = nullptr;
+    int64_t ldb_lo = 0;
+    if (splits == 1 && presplit_b_bytes(trans_a, trans_b, M, N, K) > 0) {
+      const int64_t rows = trans_b ? N : K, cols = trans_b ? K : N;
+      presplit_lo_kernel<<<(unsigned)std::min<int64_t>(ceil_div(rows * cols, 256), 148 * 8), 256, 0, s>>>(
+          rows, cols, B, ldb, static_cast<float*>(ws));
+      GNNCG_LAUNCH_CHECK();
+      B_lo = static_cast<const float*>(ws);
+      ldb_lo = cols;
+    }
     int rc = tc_gemm(trans_a, trans_b, M, N, K, A, lda, B, ldb, C, ldc, splits, kchunk, static_cast<float*>(ws), s,
-                     AttnEpi{});
+                     AttnEpi{}, B_lo, ldb_lo);
     if (rc != GNNCG_OK) return rc;
     if (splits > 1) {
       const int64_t total = M * N;
@@ -268,7 +296,16 @@ int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, 
       tc_gemm_eligible(0, 0, M, N, K, H, ldh, W, N)) {
     AttnEpi epi;
     epi.a_l = a_l; epi.a_r = a_r; epi.Al = Al; epi.Ar = Ar; epi.h = heads; epi.f = f;
-    return tc_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, 1, K, nullptr, s, epi);
+    const float* W_lo = nullptr;
+    if (presplit_b_bytes(0, 0, M, N, K) > 0) {
+      GNNCG_REQUIRE(ws && ws_bytes >= presplit_b_bytes(0, 0, M, N, K), GNNCG_ERR_WORKSPACE,
+                    "gat_transform: workspace too small");
+      presplit_lo_kernel<<<(unsigned)std::min<int64_t>(ceil_div(K * N, 256), 148 * 8), 256, 0, s>>>(
+          K, N, W, N, static_cast<float*>(ws));
+      GNNCG_LAUNCH_CHECK();
+      W_lo = static_cast<const float*>(ws);
+    }
+    return tc_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, 1, K, nullptr, s, epi, W_lo, N);
   }
   // unfused: the GEMM, then the LP kernel
   int rc = gnncg_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, ws, ws_bytes, stream);

@@ -354,8 +354,9 @@ constexpr int P_THREADS = 32 * (P_EPI_WARP0 + 4);
 template <int BN, bool A_MN, bool B_MN>
 __global__ void __launch_bounds__(P_THREADS, 1)
     gemm_tf32x3_persist_kernel(const __grid_constant__ CUtensorMap map_a, const __grid_constant__ CUtensorMap map_b,
-                               float* __restrict__ C, int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk,
-                               int64_t split_stride, int tiles_m, int tiles_n, int64_t tiles, AttnEpi epi) {
+                               const __grid_constant__ CUtensorMap map_blo, int b_presplit, float* __restrict__ C,
+                               int64_t ldc, int64_t M, int64_t N, int64_t K, int64_t kchunk, int64_t split_stride,
+                               int tiles_m, int tiles_n, int64_t tiles, AttnEpi epi) {
   static_assert(P_EPI_WARP0 % 4 == 0, "epilogue warps must start on a lane-quadrant boundary");
   using CF = Cfg<BN>;
   constexpr int S = CF::STAGES;
@@ -426,8 +427,18 @@ __global__ void __launch_bounds__(P_THREADS, 1)
           const int s = (int)(g % S);
           const uint32_t ph = (g / S) & 1u;
           mbar_wait(&empty[s], ph ^ 1u);
-          mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES);
+          mbar_expect_tx(&full[s], CF::A_BYTES + CF::B_BYTES * (b_presplit ? 2 : 1));
           const int k = (int)(x.kb0 + (int64_t)i * BK);
+          if (b_presplit) {  // B's lo was materialised once in global memory (the reused weight)
+            if (!B_MN) {
+              tma_load_2d(b_lo(s), &map_blo, k, (int)x.n0, &full[s]);
+            } else {
+#pragma unroll
+              for (int j = 0; j < BN / 32; ++j)
+                tma_load_2d(reinterpret_cast<uint8_t*>(b_lo(s)) + j * (32 * BK * 4), &map_blo, (int)x.n0 + 32 * j, k,
+                            &full[s]);
+            }
+          }
           if (!A_MN) {
             tma_load_2d(a_hi(s), &map_a, k, (int)x.m0, &full[s]);
           } else {
@@ -494,7 +505,7 @@ __global__ void __launch_bounds__(P_THREADS, 1)
         const uint32_t ph = (g / S) & 1u;
         mbar_wait(&full[s], ph);
         split_lo(a_hi(s), a_lo(s), CF::A_BYTES, tid, 32 * P_SPLIT_WARPS);
-        split_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * P_SPLIT_WARPS);
+        if (!b_presplit) split_lo(b_hi(s), b_lo(s), CF::B_BYTES, tid, 32 * P_SPLIT_WARPS);
         asm volatile("fence.proxy.async.shared::cta;" ::: "memory");
         mbar_arrive(&split[s]);
       }
@@ -602,11 +613,17 @@ bool persist_enabled() {
 
 template <int BN, bool A_MN, bool B_MN>
 int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, int64_t ldc, int64_t M, int64_t N,
-           int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s, const AttnEpi& epi) {
+           int64_t K, int splits, int64_t kchunk, int64_t split_stride, cudaStream_t s, const AttnEpi& epi,
+           const float* B_lo, int64_t ldb_lo) {
   using CF = Cfg<BN>;
-  CUtensorMap ma, mb;
+  CUtensorMap ma, mb, mbl;
   bool ok = A_MN ? make_map(&ma, A, M, K, lda, 32, BK, true) : make_map(&ma, A, K, M, lda, BK, BM, false);
   ok = ok && (B_MN ? make_map(&mb, B, N, K, ldb, 32, BK, true) : make_map(&mb, B, K, N, ldb, BK, BN, false));
+  const bool presplit = B_lo != nullptr && persist_enabled();
+  mbl = mb;
+  if (presplit)
+    ok = ok && (B_MN ? make_map(&mbl, B_lo, N, K, ldb_lo, 32, BK, true)
+                     : make_map(&mbl, B_lo, K, N, ldb_lo, BK, BN, false));
   if (!ok) return fail(GNNCG_ERR_CUDA, "gemm_tc: cuTensorMapEncodeTiled failed");
   if (persist_enabled()) {
     auto pk = gemm_tf32x3_persist_kernel<BN, A_MN, B_MN>;
@@ -624,7 +641,8 @@ int launch(const float* A, int64_t lda, const float* B, int64_t ldb, float* C, i
       if (cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || sms <= 0) sms = 148;
     }
     const unsigned grid = (unsigned)std::min<int64_t>(tiles, sms);
-    pk<<<grid, P_THREADS, CF::SMEM, s>>>(ma, mb, C, ldc, M, N, K, kchunk, split_stride, tm, tn, tiles, epi);
+    pk<<<grid, P_THREADS, CF::SMEM, s>>>(ma, mb, mbl, presplit ? 1 : 0, C, ldc, M, N, K, kchunk, split_stride, tm, tn,
+                                         tiles, epi);
     GNNCG_LAUNCH_CHECK();
     return GNNCG_OK;
   }
@@ -674,14 +692,14 @@ bool tc_gemm_eligible(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K,
 
 int tc_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const float* A, int64_t lda, const float* B,
             int64_t ldb, float* C, int64_t ldc, int splits, int64_t kchunk, float* partial, cudaStream_t s,
-            const AttnEpi& epi) {
+            const AttnEpi& epi, const float* B_lo, int64_t ldb_lo) {
   float* out = splits > 1 ? partial : C;
   const int64_t ldo = splits > 1 ? N : ldc;
   const int64_t stride = splits > 1 ? M * N : 0;
   const bool a_mn = trans_a != 0, b_mn = trans_b == 0;
   const bool wide = tc_bn(N) == 256;
 #define GNNCG_TC(BN, AM, BMN) \
-  return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s, epi)
+  return tc::launch<BN, AM, BMN>(A, lda, B, ldb, out, ldo, M, N, K, splits, kchunk, stride, s, epi, B_lo, ldb_lo)
   if (wide) {
     if (!a_mn && !b_mn) GNNCG_TC(256, false, false);
     if (!a_mn && b_mn) GNNCG_TC(256, false, true);

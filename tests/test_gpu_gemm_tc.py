@@ -24,6 +24,8 @@ CASES = [  # (trans_a, trans_b, M, N, K)
     (0, 0, 4096, 256, 604), (0, 0, 233, 256, 256), (0, 0, 1000, 128, 100), (0, 0, 300, 64, 32),
     (0, 1, 2048, 256, 256), (0, 1, 777, 96, 64), (0, 1, 5000, 604, 256),
     (1, 0, 604, 256, 20000), (1, 0, 256, 256, 50000), (1, 0, 130, 128, 3000), (0, 0, 129, 17, 5),
+    # tall products with a small reused B: B's tf32 lo part is pre-split once into the workspace
+    (0, 0, 20000, 256, 602), (0, 1, 20003, 604, 256), (0, 0, 16500, 128, 100),
 ]
 
 
@@ -75,6 +77,7 @@ def test_gemm_tall_m_beyond_grid_y(cuda, tc, monkeypatch):
 
 
 @pytest.mark.parametrize("M,K,h,f", [(1000, 602, 8, 32), (4097, 256, 8, 32), (777, 64, 4, 64), (300, 100, 2, 32),
+                                     (20000, 602, 8, 32),
                                      (513, 128, 8, 16), (50, 20, 3, 5)])
 def test_gat_transform_epilogue(cuda, M, K, h, f):
     """K1 with the attention-LP epilogue equals gemm + attn_dots bitwise (fused when f % 32 == 0,
