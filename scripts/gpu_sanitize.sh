@@ -1,0 +1,15 @@
+#!/bin/bash
+# compute-sanitizer (memcheck, racecheck, synccheck) over small-graph GPU tests of the fused kernels,
+# the bf16 mode and the tcgen05 GEMM.  usage: scripts/gpu_sanitize.sh tag
+cd "$GRAFT_REPO_ROOT"; TAG=${1:-san}; mkdir -p gpurun_out
+SEL='tests/test_gpu_gat.py::test_region_forward_and_backward tests/test_gpu_gat_bf16.py::test_bf16_region tests/test_gpu_edgeconv_gmm.py'
+K='G3 or ER16 or cora'
+for tool in memcheck racecheck synccheck; do
+  timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
+    python -m pytest $SEL -q -x -p no:cacheprovider -k "$K" > gpurun_out/san_${tool}_$TAG.log 2>&1
+  echo "rc=$?" >> gpurun_out/san_${tool}_$TAG.log
+done
+timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 --print-limit 20 \
+  python -m pytest tests/test_gpu_gemm_tc.py -q -x -p no:cacheprovider -k "129 or 300 or identity" > gpurun_out/san_gemm_$TAG.log 2>&1
+echo "rc=$?" >> gpurun_out/san_gemm_$TAG.log
+echo done
