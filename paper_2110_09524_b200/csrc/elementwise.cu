@@ -29,8 +29,17 @@ __global__ void fill_kernel(int64_t n, float v, float* __restrict__ x) {
 __global__ void sum_partial_kernel(int64_t n, const float* __restrict__ x, double* __restrict__ part) {
   __shared__ double sh[32];
   double s = 0.0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x)
-    s += (double)x[i];
+  const int64_t tid = blockIdx.x * (int64_t)blockDim.x + threadIdx.x, nt = (int64_t)gridDim.x * blockDim.x;
+  if ((reinterpret_cast<uintptr_t>(x) & 15) == 0) {  // 16-byte loads, fixed per-thread order
+    const int64_t n4 = n >> 2;
+    for (int64_t i = tid; i < n4; i += nt) {
+      const float4 v = __ldg(reinterpret_cast<const float4*>(x) + i);
+      s += ((double)v.x + (double)v.y) + ((double)v.z + (double)v.w);
+    }
+    for (int64_t i = (n4 << 2) + tid; i < n; i += nt) s += (double)x[i];
+  } else {
+    for (int64_t i = tid; i < n; i += nt) s += (double)x[i];
+  }
 #pragma unroll
   for (int o = 16; o > 0; o >>= 1) s += __shfl_xor_sync(0xffffffffu, s, o);
   if ((threadIdx.x & 31) == 0) sh[threadIdx.x >> 5] = s;

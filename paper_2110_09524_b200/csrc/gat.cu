@@ -886,6 +886,23 @@ __global__ void gat_bwd_prep_bf16_kernel(int64_t rows, int h, int f, const float
 __global__ void gat_lp_dar_kernel(int64_t rows, int64_t row_base, int h, int f, const float* __restrict__ dAr,
                                   const float* __restrict__ a_r, float* __restrict__ dHt) {
   const int hf = h * f;
+  if ((f & 3) == 0) {
+    // float4 columns (one head each), threads = (row slot, column quad): no 64-bit division
+    const int q4 = hf >> 2;
+    const int rpb = max(1, (int)blockDim.x / q4);  // rows per block step
+    const int slot = threadIdx.x / q4, c4 = threadIdx.x - slot * q4;
+    if (slot >= rpb) return;
+    const float4 ar = __ldg(reinterpret_cast<const float4*>(a_r) + c4);
+    const int k = (c4 * 4) / f;
+    for (int64_t r = (int64_t)blockIdx.x * rpb + slot; r < rows; r += (int64_t)gridDim.x * rpb) {
+      const float g = __ldg(dAr + r * h + k);
+      float4* d = reinterpret_cast<float4*>(dHt + (row_base + r) * hf) + c4;
+      float4 v = *d;
+      v.x = fmaf(g, ar.x, v.x); v.y = fmaf(g, ar.y, v.y); v.z = fmaf(g, ar.z, v.z); v.w = fmaf(g, ar.w, v.w);
+      *d = v;
+    }
+    return;
+  }
   const int64_t n = rows * hf;
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
     const int64_t r = i / hf;
@@ -1526,7 +1543,8 @@ static int gat_bwd_src_fused_impl(const gnncg_index_t* csc_src, const gnncg_sche
   }
   if (num_local > 0) {
     const int g = (int)std::min<int64_t>(ceil_div(num_local * h * f, 256), 148 * 32);
-    gat_lp_dar_kernel<<<g, 256, 0, s>>>(num_local, row_base, h, f, dAr, a_r, dHt);
+    const int threads = (f % 4 == 0 && h * f / 4 <= 1024) ? std::max(256, h * f / 4) : 256;
+    gat_lp_dar_kernel<<<g, threads, 0, s>>>(num_local, row_base, h, f, dAr, a_r, dHt);
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;
