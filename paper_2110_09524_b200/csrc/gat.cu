@@ -1025,57 +1025,78 @@ __global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __rest
 
 constexpr int kGradBlocks = 1184;  // 8 per SM: enough independent row streams (C5: V = 10M)
 
-// Per-block partial of da_l / da_r: threads = (row group, column); each thread walks its
-// rows 4 at a time (independent loads in flight), then the row groups are combined in a
-// fixed order -> deterministic.
+// Per-block partial of da_l / da_r: threads = (row group, column quad) with 16-byte loads of
+// Ht (hf % 4 == 0 and f % 4 == 0; else single columns); each thread walks its rows 4 at a time
+// (independent loads in flight), then the row groups are combined in a fixed order ->
+// deterministic.
 __global__ void __launch_bounds__(256) attn_grad_partial_kernel(int64_t rows, int h, int f,
                                                                 const float* __restrict__ Ht,
                                                                 const float* __restrict__ dAl,
                                                                 const float* __restrict__ dAr,
                                                                 float* __restrict__ part) {
-  __shared__ float red[2][256];
+  __shared__ float red[2][256 * 4];
   const int hf = h * f;
-  const int cw = min(hf - (int)blockIdx.y * 256, 256);  // columns of this block
-  const int RG = 256 / cw;                               // row groups
+  const int vw = (f % 4 == 0) ? 4 : 1;                          // columns per thread
+  const int cw = min(hf - (int)blockIdx.y * 256 * vw, 256 * vw) / vw;  // column groups of this block
+  const int RG = 256 / cw;                                      // row groups
   const int t = threadIdx.x, grp = t / cw, cl = t % cw;
-  const int c = blockIdx.y * 256 + cl;
+  const int c = blockIdx.y * 256 * vw + cl * vw;                // first column of this thread
   const int k = c / f;
   const int64_t per = ceil_div(rows, (int64_t)gridDim.x);
   const int64_t r0 = blockIdx.x * per, r1 = min(rows, r0 + per);
-  float sl = 0.f, sr = 0.f;
+  float sl[4] = {0.f, 0.f, 0.f, 0.f}, sr[4] = {0.f, 0.f, 0.f, 0.f};
   if (grp < RG) {
     int64_t v = r0 + grp;
-    for (; v + 3 * RG < r1; v += 4 * RG) {
-      float x[4], l[4], r[4];
+    if (vw == 4) {
+      for (; v + 3 * RG < r1; v += 4 * RG) {
+        float4 x[4];
+        float l[4], r[4];
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        const int64_t vv = v + q * RG;
-        x[q] = __ldg(Ht + vv * hf + c);
-        l[q] = __ldg(dAl + vv * h + k);
-        r[q] = __ldg(dAr + vv * h + k);
-      }
+        for (int q = 0; q < 4; ++q) {
+          const int64_t vv = v + q * RG;
+          x[q] = __ldg(reinterpret_cast<const float4*>(Ht + vv * hf + c));
+          l[q] = __ldg(dAl + vv * h + k);
+          r[q] = __ldg(dAr + vv * h + k);
+        }
 #pragma unroll
-      for (int q = 0; q < 4; ++q) {
-        sl = fmaf(l[q], x[q], sl);
-        sr = fmaf(r[q], x[q], sr);
+        for (int q = 0; q < 4; ++q) {
+          sl[0] = fmaf(l[q], x[q].x, sl[0]); sl[1] = fmaf(l[q], x[q].y, sl[1]);
+          sl[2] = fmaf(l[q], x[q].z, sl[2]); sl[3] = fmaf(l[q], x[q].w, sl[3]);
+          sr[0] = fmaf(r[q], x[q].x, sr[0]); sr[1] = fmaf(r[q], x[q].y, sr[1]);
+          sr[2] = fmaf(r[q], x[q].z, sr[2]); sr[3] = fmaf(r[q], x[q].w, sr[3]);
+        }
       }
-    }
-    for (; v < r1; v += RG) {
-      const float x = __ldg(Ht + v * hf + c);
-      sl = fmaf(__ldg(dAl + v * h + k), x, sl);
-      sr = fmaf(__ldg(dAr + v * h + k), x, sr);
+      for (; v < r1; v += RG) {
+        const float4 x = __ldg(reinterpret_cast<const float4*>(Ht + v * hf + c));
+        const float l = __ldg(dAl + v * h + k), r = __ldg(dAr + v * h + k);
+        sl[0] = fmaf(l, x.x, sl[0]); sl[1] = fmaf(l, x.y, sl[1]); sl[2] = fmaf(l, x.z, sl[2]); sl[3] = fmaf(l, x.w, sl[3]);
+        sr[0] = fmaf(r, x.x, sr[0]); sr[1] = fmaf(r, x.y, sr[1]); sr[2] = fmaf(r, x.z, sr[2]); sr[3] = fmaf(r, x.w, sr[3]);
+      }
+    } else {
+      for (; v < r1; v += RG) {
+        const float x = __ldg(Ht + v * hf + c);
+        sl[0] = fmaf(__ldg(dAl + v * h + k), x, sl[0]);
+        sr[0] = fmaf(__ldg(dAr + v * h + k), x, sr[0]);
+      }
     }
   }
-  red[0][t] = sl;
-  red[1][t] = sr;
+#pragma unroll
+  for (int q = 0; q < 4; ++q) {
+    red[0][t * 4 + q] = sl[q];
+    red[1][t * 4 + q] = sr[q];
+  }
   __syncthreads();
   if (grp == 0) {
-    for (int g = 1; g < RG; ++g) {
-      sl += red[0][g * cw + cl];
-      sr += red[1][g * cw + cl];
+    for (int g = 1; g < RG; ++g)
+#pragma unroll
+      for (int q = 0; q < 4; ++q) {
+        sl[q] += red[0][(g * cw + cl) * 4 + q];
+        sr[q] += red[1][(g * cw + cl) * 4 + q];
+      }
+    for (int q = 0; q < vw; ++q) {
+      part[(int64_t)blockIdx.x * 2 * hf + c + q] = sl[q];
+      part[(int64_t)blockIdx.x * 2 * hf + hf + c + q] = sr[q];
     }
-    part[(int64_t)blockIdx.x * 2 * hf + c] = sl;
-    part[(int64_t)blockIdx.x * 2 * hf + hf + c] = sr;
   }
 }
 
@@ -1597,7 +1618,7 @@ int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float
   cudaStream_t s = as_stream(stream);
   const int hf = h * f;
   float* part = static_cast<float*>(ws);
-  dim3 g1(kGradBlocks, (unsigned)ceil_div(hf, 256));
+  dim3 g1(kGradBlocks, (unsigned)ceil_div(hf, f % 4 == 0 ? 1024 : 256));
   attn_grad_partial_kernel<<<g1, 256, 0, s>>>(rows, h, f, Ht, dAl, dAr, part);
   GNNCG_LAUNCH_CHECK();
   attn_grad_reduce_kernel<<<(unsigned)(2 * hf), 256, 0, s>>>(kGradBlocks, hf, part, da_l, da_r);
