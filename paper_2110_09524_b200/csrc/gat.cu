@@ -1120,9 +1120,9 @@ __global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, c
 // ---------------------------------------------------------------------------
 // Dispatch over the compiled (VW, NV) variants.
 // ---------------------------------------------------------------------------
-enum class Kind { Fwd, FwdRoll, BwdDst, BwdSrc, BwdSrcFast };
+enum class Kind { Fwd, FwdOvl, BwdDst, BwdSrc, BwdSrcFast };
 int num_sms();
-bool roll_enabled();
+bool ovl_enabled();
 bool pair_enabled();
 
 template <int VW, int NV, int OCC>
@@ -1150,7 +1150,7 @@ template <int VW, int NV, int OCC>
 void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
   switch (kind) {
     case Kind::Fwd: gat_fwd_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
-    case Kind::FwdRoll: {
+    case Kind::FwdOvl: {
       constexpr int U = GatherDepth<NV, OCC>::U;
       constexpr int MINB = NV >= 8 ? 1 : OCC;
       const unsigned g = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * MINB);
@@ -1218,7 +1218,7 @@ void launch_lp_fast_per(const GatParams& p, unsigned g, cudaStream_t s) {
 template <int VW, int NV>
 void launch_lp(Kind kind, const GatParams& p, cudaStream_t s) {
   const unsigned g = (unsigned)std::min<int64_t>(ceil_div(p.num_items, WARPS), (int64_t)num_sms() * 2);
-  if (kind == Kind::FwdRoll) {
+  if (kind == Kind::FwdOvl) {
     gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true><<<g, THREADS, 0, s>>>(p);
   } else {
     switch (p.f / VW) {
@@ -1288,12 +1288,12 @@ bool tma_enabled() {
   return v == 1;
 }
 
-// GNNCG_GAT_ROLL=0 selects the block-synchronous forward (gat_fwd_kernel) instead of the
-// rolling-gather one.
-bool roll_enabled() {
+// GNNCG_GAT_OVL=0 selects the block-synchronous forward (gat_fwd_kernel) instead of the
+// overlapped-edge-phase one (gat_fwd_ovl_kernel).
+bool ovl_enabled() {
   static int v = -1;
   if (v < 0) {
-    const char* e = getenv("GNNCG_GAT_ROLL");
+    const char* e = getenv("GNNCG_GAT_OVL");
     v = (e && e[0] == '0') ? 0 : 1;
   }
   return v == 1;
@@ -1384,13 +1384,13 @@ static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched
   p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
   if (Ht_lp) {
-    rc = dispatch_lp(Kind::FwdRoll, p, s);
+    rc = dispatch_lp(Kind::FwdOvl, p, s);
   } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
     int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
     GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
     rc = launch_fwd_tma(p, counter, s);
   } else {
-    rc = dispatch(roll_enabled() ? Kind::FwdRoll : Kind::Fwd, p, s);
+    rc = dispatch(ovl_enabled() ? Kind::FwdOvl : Kind::Fwd, p, s);
   }
   if (rc) return rc;
   if (sched->num_split_rows > 0) {
