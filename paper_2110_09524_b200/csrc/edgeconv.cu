@@ -94,7 +94,7 @@ int gnncg_edgeconv_fwd(const gnncg_index_t* csr, int C, int64_t row_base, const 
   GNNCG_REQUIRE(csr && C >= 1, GNNCG_ERR_SHAPE, "edgeconv_fwd: bad shape");
   GNNCG_REQUIRE(ldt >= C && ldp >= C && row_base >= 0, GNNCG_ERR_SHAPE, "edgeconv_fwd: leading dimension < C");
   if (csr->num_rows == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(csr->off && csr->nbr && csr->eid && Th && Ph && out && amax, GNNCG_ERR_ARG,
+  GNNCG_REQUIRE(csr->off && (csr->num_edges == 0 || (csr->nbr && csr->eid)) && Th && Ph && out && amax, GNNCG_ERR_ARG,
                 "edgeconv_fwd: null pointer (csr_dst.eid is required for the argmax)");
   edgeconv_fwd_kernel<<<(unsigned)ceil_div(csr->num_rows, 8), 256, 0, as_stream(stream)>>>(
       csr->num_rows, C, row_base, csr->off, csr->nbr, csr->eid, Th, ldt, Ph, ldp, out, amax);
@@ -108,7 +108,8 @@ int gnncg_edgeconv_bwd(const gnncg_index_t* csc, const gnncg_index_t* csr, int C
   GNNCG_REQUIRE(csc && csr && C >= 1 && ldt >= C && ldp >= C, GNNCG_ERR_SHAPE, "edgeconv_bwd: bad shape");
   GNNCG_REQUIRE(csc->num_rows == csr->num_rows, GNNCG_ERR_SHAPE, "edgeconv_bwd: csc/csr row mismatch");
   if (csc->num_rows == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(csc->off && csc->nbr && csc->eid && csr->off && amax && g && dTh && dPh, GNNCG_ERR_ARG,
+  GNNCG_REQUIRE(csc->off && (csc->num_edges == 0 || (csc->nbr && csc->eid)) && csr->off && amax && g && dTh && dPh,
+                GNNCG_ERR_ARG,
                 "edgeconv_bwd: null pointer (csc_src.eid is required)");
   edgeconv_bwd_kernel<<<(unsigned)ceil_div(csc->num_rows, 8), 256, 0, as_stream(stream)>>>(
       csc->num_rows, C, csc->off, csc->nbr, csc->eid, csr->off, amax, g, dTh, ldt, dPh, ldp);

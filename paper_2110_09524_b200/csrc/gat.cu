@@ -1390,7 +1390,8 @@ static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched
   int rc = check_common(csr_dst, sched, h, f);
   if (rc) return rc;
   if (sched->num_items == 0) return GNNCG_OK;
-  GNNCG_REQUIRE((Ht || Ht_lp) && Al && Ar && out && m && d && csr_dst->nbr, GNNCG_ERR_ARG, "gat_fwd: null pointer");
+  GNNCG_REQUIRE((Ht || Ht_lp) && Al && Ar && out && m && d && (csr_dst->num_edges == 0 || csr_dst->nbr),
+                GNNCG_ERR_ARG, "gat_fwd: null pointer");
   const size_t need = fwd_part_bytes(sched, h, f);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
                 ws_bytes, need);
@@ -1460,7 +1461,7 @@ int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, 
   int rc = check_common(csr_dst, sched, h, f);
   if (rc) return rc;
   if (sched->num_items == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(Ht && Al && Ar && m && d && dOut && c && dAr && csr_dst->nbr, GNNCG_ERR_ARG,
+  GNNCG_REQUIRE(Ht && Al && Ar && m && d && dOut && c && dAr && (csr_dst->num_edges == 0 || csr_dst->nbr), GNNCG_ERR_ARG,
                 "gat_bwd_dst: null pointer");
   const size_t need = dst_part_bytes(sched, h);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_dst: workspace %zu < %zu",

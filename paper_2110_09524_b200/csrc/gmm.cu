@@ -284,7 +284,8 @@ int gnncg_gmm_fwd(const gnncg_index_t* csr, int K, int r, int f, const float* Y,
   int rc = check(csr, K, r, f, ldy);
   if (rc) return rc;
   if (csr->num_rows == 0) return GNNCG_OK;
-  GNNCG_REQUIRE(csr->off && csr->nbr && Y && mu && sinv && out, GNNCG_ERR_ARG, "gmm_fwd: null pointer");
+  GNNCG_REQUIRE(csr->off && (csr->num_edges == 0 || csr->nbr) && Y && mu && sinv && out, GNNCG_ERR_ARG,
+                "gmm_fwd: null pointer");
   GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, nullptr, out, nullptr, nullptr};
   gmm_fwd_kernel<<<(unsigned)ceil_div(csr->num_rows, WARPS), 256, 0, as_stream(stream)>>>(a);
   GNNCG_LAUNCH_CHECK();
@@ -312,7 +313,9 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr, const gnncg_index_t* csc, int K, int
     GNNCG_CUDA_TRY(cudaMemsetAsync(dsinv, 0, sizeof(float) * K * r, s));
     return GNNCG_OK;
   }
-  GNNCG_REQUIRE(csr->off && csr->nbr && csc->off && csc->nbr && Y && mu && sinv && dOut && dY, GNNCG_ERR_ARG,
+  GNNCG_REQUIRE(csr->off && csc->off && (csr->num_edges == 0 || (csr->nbr && csc->nbr)) && Y && mu && sinv && dOut &&
+                    dY,
+                GNNCG_ERR_ARG,
                 "gmm_bwd: null pointer");
   GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, dOut, nullptr, dY,
             static_cast<float*>(ws)};

@@ -98,3 +98,30 @@ def test_gmm_layer_vs_oracle(cuda, V, E, Fin, K, r, f):
     for name, got in zip(("dH", "dW", "dPl", "dPr", "dmu", "dsinv"), grads):
         scale = max(1.0, np.abs(bw[name]).max())
         assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name
+
+
+def test_edgeless_graph_edgeconv_and_gmm(cuda):
+    """E = 0 through EdgeConv (out 0, argmax = no edge) and GMMConv (out 0), forward and backward."""
+    V, Fin, C, K, r, f = 29, 12, 16, 3, 2, 16
+    g = DeviceGraph.from_edges(V, [], [], device=cuda)
+    rng = np.random.default_rng(4)
+    H = t32(rng.uniform(-1, 1, (V, Fin)), cuda)
+    Th, Ph = t32(rng.uniform(-1, 1, (Fin, C)), cuda), t32(rng.uniform(-1, 1, (Fin, C)), cuda)
+    out, st = edgeconv_forward(g, H, Th, Ph)
+    grads = edgeconv_backward(g, H, Th, Ph, st, t32(rng.uniform(-1, 1, (V, C)), cuda))
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(out) == 0
+    assert bool((st.argmax == -1).all())  # 0xFFFFFFFF: empty row
+    for t in grads:
+        if t is not None:
+            assert torch.count_nonzero(t) == 0
+    args = [t32(x, cuda) for x in (rng.uniform(-1, 1, (V, Fin)), rng.uniform(-1, 1, (Fin, K * f)),
+                                   rng.uniform(-1, 1, (Fin, r)), rng.uniform(-1, 1, (Fin, r)),
+                                   rng.uniform(-0.5, 0.5, (K, r)), rng.uniform(0.5, 1.5, (K, r)))]
+    o2, st2 = gmm_forward(g, *args, K, r, f)
+    g2 = gmm_backward(g, *args, K, r, f, st2, t32(rng.uniform(-1, 1, (V, f)), cuda))
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(o2) == 0
+    for t in g2:
+        if t is not None:
+            assert torch.count_nonzero(t) == 0

@@ -179,3 +179,22 @@ def test_gemm_vs_reference_matmul(cuda, ta, tb, M, N, K):
     torch.cuda.synchronize()
     scale = max(1.0, np.abs(ref).max())
     assert O.max_rel_err(np64(got) / scale, ref / scale) < 1e-5
+
+
+@pytest.mark.parametrize("gather", ["fp32", "bf16"])
+def test_edgeless_graph(cuda, gather):
+    """E = 0: every row is empty -> out = 0, m = d = 0, all region gradients 0,
+    through the whole layer (GEMMs, fused kernels, LP grads)."""
+    V, Fin, h, f = 37, 64, 8, 32
+    g = DeviceGraph.from_edges(V, [], [], device=cuda)
+    rng = np.random.default_rng(2)
+    H = t32(rng.uniform(-1, 1, (V, Fin)), cuda)
+    W = t32(rng.uniform(-0.1, 0.1, (Fin, h * f)), cuda)
+    al, ar = t32(rng.uniform(-1, 1, (h, f)), cuda), t32(rng.uniform(-1, 1, (h, f)), cuda)
+    p = GatParams(h, f, gather=gather)
+    out, st = gat_forward(g, H, W, al, ar, p)
+    gr = gat_backward(g, H, W, al, ar, st, t32(rng.uniform(-1, 1, (V, h * f)), cuda), p, need_dH=True)
+    torch.cuda.synchronize()
+    assert torch.count_nonzero(out) == 0 and torch.count_nonzero(st.m) == 0 and torch.count_nonzero(st.d) == 0
+    for t in (gr.dH, gr.dW, gr.da_l, gr.da_r):
+        assert torch.count_nonzero(t) == 0
