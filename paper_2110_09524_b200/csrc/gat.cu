@@ -1383,14 +1383,15 @@ size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* 
   return align_up(b) + 256;  // + the work counter of the persistent TMA-fed kernels
 }
 
-static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
+static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
                         const float* Ht, const uint16_t* Ht_lp, const float* Al, const float* Ar, float* out, float* m,
                         float* d, void* ws, size_t ws_bytes, void* stream) {
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csr_dst, sched, h, f);
   if (rc) return rc;
   if (sched->num_items == 0) return GNNCG_OK;
-  GNNCG_REQUIRE((Ht || Ht_lp) && Al && Ar && out && m && d && (csr_dst->num_edges == 0 || csr_dst->nbr),
+  GNNCG_REQUIRE((lp ? Ht_lp != nullptr : Ht != nullptr) && Al && Ar && out && m && d &&
+                    (csr_dst->num_edges == 0 || csr_dst->nbr),
                 GNNCG_ERR_ARG, "gat_fwd: null pointer");
   const size_t need = fwd_part_bytes(sched, h, f);
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
@@ -1401,7 +1402,7 @@ static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched
   p.h = h; p.f = f; p.slope = slope;
   p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
-  if (Ht_lp) {
+  if (lp) {
     rc = dispatch_lp(Kind::FwdOvl, p, s);
   } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
     int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
@@ -1422,8 +1423,7 @@ static int gat_fwd_impl(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched
 int gnncg_gat_fwd(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
                   const float* Ht, const float* Al, const float* Ar, float* out, float* m, float* d, void* ws,
                   size_t ws_bytes, void* stream) {
-  GNNCG_REQUIRE(Ht, GNNCG_ERR_ARG, "gat_fwd: null Ht");
-  return gat_fwd_impl(csr_dst, sched, h, f, slope, Ht, nullptr, Al, Ar, out, m, d, ws, ws_bytes, stream);
+  return gat_fwd_impl(false, csr_dst, sched, h, f, slope, Ht, nullptr, Al, Ar, out, m, d, ws, ws_bytes, stream);
 }
 
 int gnncg_gat_bf16_supported(int h, int f) {
@@ -1448,10 +1448,9 @@ int gnncg_pack_bf16(int64_t n, const float* src, uint16_t* dst, void* stream) {
 int gnncg_gat_fwd_bf16(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
                        const uint16_t* Ht_bf16, const float* Al, const float* Ar, float* out, float* m, float* d,
                        void* ws, size_t ws_bytes, void* stream) {
-  GNNCG_REQUIRE(Ht_bf16, GNNCG_ERR_ARG, "gat_fwd_bf16: null Ht_bf16");
   GNNCG_REQUIRE(gnncg_gat_bf16_supported(h, f), GNNCG_ERR_UNSUPPORTED, "gat_fwd_bf16: heads=%d f=%d unsupported",
                 h, f);
-  return gat_fwd_impl(csr_dst, sched, h, f, slope, nullptr, Ht_bf16, Al, Ar, out, m, d, ws, ws_bytes, stream);
+  return gat_fwd_impl(true, csr_dst, sched, h, f, slope, nullptr, Ht_bf16, Al, Ar, out, m, d, ws, ws_bytes, stream);
 }
 
 int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, int h, int f, float slope,
@@ -1541,7 +1540,7 @@ int gnncg_gat_bwd_prep(int64_t rows, int h, int f, const float* dOut, const floa
   return GNNCG_OK;
 }
 
-static int gat_bwd_src_fused_impl(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f,
+static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f,
                                   float slope, int64_t row_base, int64_t num_local, const float* Ht,
                                   const uint16_t* Ht_lp, const float* Al,
                                   const float* dst_rec, const float* dOut, const uint16_t* dOut_lp, const float* a_l,
@@ -1550,14 +1549,15 @@ static int gat_bwd_src_fused_impl(const gnncg_index_t* csc_src, const gnncg_sche
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csc_src, sched, h, f);
   if (rc) return rc;
-  if (dOut_lp) {
+  if (lp) {
     GNNCG_REQUIRE(gnncg_gat_bf16_supported(h, f), GNNCG_ERR_UNSUPPORTED,
                   "gat_bwd_src_fused_bf16: heads=%d f=%d unsupported", h, f);
   } else {
     GNNCG_REQUIRE(gnncg_gat_fast_supported(h, f), GNNCG_ERR_UNSUPPORTED,
                   "gat_bwd_src_fused: f/VW must be a power of two <= 32 (use gnncg_gat_bwd_dst + gnncg_gat_bwd_src)");
   }
-  GNNCG_REQUIRE((dOut_lp ? (Ht_lp != nullptr) : (Ht && dOut)) && Al && dst_rec && a_l && a_r && dHt && dAl && dAr,
+  if (sched->num_items == 0 && num_local == 0) return GNNCG_OK;  // empty graph
+  GNNCG_REQUIRE((lp ? (Ht_lp && dOut_lp) : (Ht && dOut)) && Al && dst_rec && a_l && a_r && dHt && dAl && dAr,
                 GNNCG_ERR_ARG, "gat_bwd_src_fused: null pointer");
   GNNCG_REQUIRE(row_base >= 0 && num_local >= 0, GNNCG_ERR_ARG, "gat_bwd_src_fused: bad row block");
   const size_t need = src_part_bytes(sched, h, f);
@@ -1573,7 +1573,7 @@ static int gat_bwd_src_fused_impl(const gnncg_index_t* csc_src, const gnncg_sche
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;
-  rc = dOut_lp ? dispatch_lp(Kind::BwdSrcFast, p, s) : dispatch(Kind::BwdSrcFast, p, s);
+  rc = lp ? dispatch_lp(Kind::BwdSrcFast, p, s) : dispatch(Kind::BwdSrcFast, p, s);
   if (rc) return rc;
   if (sched->num_split_rows > 0) {
     gat_bwd_src_merge_kernel<<<(unsigned)ceil_div(sched->num_split_rows, WARPS), THREADS, 0, s>>>(
@@ -1606,8 +1606,7 @@ int gnncg_gat_bwd_src_fused(const gnncg_index_t* csc_src, const gnncg_sched_t* s
                             int64_t row_base, int64_t num_local, const float* Ht, const float* Al,
                             const float* dst_rec, const float* dOut, const float* a_l, const float* a_r, float* dHt,
                             float* dAl, float* dAr, void* ws, size_t ws_bytes, void* stream) {
-  GNNCG_REQUIRE(dOut, GNNCG_ERR_ARG, "gat_bwd_src_fused: null dOut");
-  return gat_bwd_src_fused_impl(csc_src, sched, h, f, slope, row_base, num_local, Ht, nullptr, Al, dst_rec, dOut,
+  return gat_bwd_src_fused_impl(false, csc_src, sched, h, f, slope, row_base, num_local, Ht, nullptr, Al, dst_rec, dOut,
                                 nullptr, a_l, a_r, dHt, dAl, dAr, ws, ws_bytes, stream);
 }
 
@@ -1616,8 +1615,7 @@ int gnncg_gat_bwd_src_fused_bf16(const gnncg_index_t* csc_src, const gnncg_sched
                                  const float* Al, const float* dst_rec, const uint16_t* dOut_bf16, const float* a_l,
                                  const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
                                  void* stream) {
-  GNNCG_REQUIRE(dOut_bf16 && Ht_bf16, GNNCG_ERR_ARG, "gat_bwd_src_fused_bf16: null bf16 table");
-  return gat_bwd_src_fused_impl(csc_src, sched, h, f, slope, row_base, num_local, nullptr, Ht_bf16, Al, dst_rec,
+  return gat_bwd_src_fused_impl(true, csc_src, sched, h, f, slope, row_base, num_local, nullptr, Ht_bf16, Al, dst_rec,
                                 nullptr, dOut_bf16, a_l, a_r, dHt, dAl, dAr, ws, ws_bytes, stream);
 }
 

@@ -182,10 +182,11 @@ def test_gemm_vs_reference_matmul(cuda, ta, tb, M, N, K):
 
 
 @pytest.mark.parametrize("gather", ["fp32", "bf16"])
-def test_edgeless_graph(cuda, gather):
+@pytest.mark.parametrize("V", [37, 1, 0])
+def test_edgeless_graph(cuda, gather, V):
     """E = 0: every row is empty -> out = 0, m = d = 0, all region gradients 0,
-    through the whole layer (GEMMs, fused kernels, LP grads)."""
-    V, Fin, h, f = 37, 64, 8, 32
+    through the whole layer (GEMMs, fused kernels, LP grads); V = 0 is the empty graph."""
+    Fin, h, f = 64, 8, 32
     g = DeviceGraph.from_edges(V, [], [], device=cuda)
     rng = np.random.default_rng(2)
     H = t32(rng.uniform(-1, 1, (V, Fin)), cuda)
