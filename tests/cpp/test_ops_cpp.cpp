@@ -177,6 +177,24 @@ int main() {
   b200::GcnGrads cg = b200::gcn_backward(dg, H, Wc, cst, TensorF(V, 12, 1.0f), true);
   ok = ok && worst_c < 1e-4 && all_finite(cg.dW) && all_finite(cg.db) && cg.dH.rows == V;
   std::printf("gcn forward max rel_err = %.3e\n", worst_c);
+
+  // A Graph without edges (empty neighbourhoods -> 0) through the C++ API.
+  {
+    const Graph g0(7, {});
+    b200::DeviceGraph dg0(g0);
+    const TensorF H0 = init_seeded<float>(7, Fin, 13);
+    b200::GatStash st0;
+    b200::GatParams q{h, f};
+    q.backward = b200::Backward::fast;
+    TensorF o0 = b200::gat_forward(dg0, H0, W, al, ar, q, &st0);
+    b200::GatGrads g0r = b200::gat_backward(dg0, H0, W, al, ar, st0, TensorF(7, hf, 1.0f), q, true);
+    bool zero = true;
+    for (float v : o0.data) zero = zero && v == 0.f;
+    for (float v : g0r.dW.data) zero = zero && v == 0.f;
+    for (float v : g0r.dH.data) zero = zero && v == 0.f;
+    std::printf("edge-less graph: outputs and gradients %s\n", zero ? "zero" : "NOT zero");
+    ok = ok && zero;
+  }
   std::printf("%s\n", ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
 }
