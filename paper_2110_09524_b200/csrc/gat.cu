@@ -1041,6 +1041,11 @@ __global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __rest
 }
 
 constexpr int kGradBlocks = 1184;  // 8 per SM: enough independent row streams (C5: V = 10M)
+// small tables (Cora: 2708 rows) take >= 32 rows per block instead of 2-3
+inline int grad_blocks(int64_t rows) {
+  const int64_t b = ceil_div(rows, (int64_t)32);
+  return (int)(b < 1 ? 1 : b > kGradBlocks ? kGradBlocks : b);
+}
 
 // Per-block partial of da_l / da_r: threads = (row group, column quad) with 16-byte loads of
 // Ht (hf % 4 == 0 and f % 4 == 0; else single columns); each thread walks its rows 4 at a time
@@ -1620,8 +1625,7 @@ int gnncg_gat_bwd_src_fused_bf16(const gnncg_index_t* csc_src, const gnncg_sched
 }
 
 size_t gnncg_gat_attn_grad_workspace(int64_t rows, int h, int f) {
-  (void)rows;
-  return align_up((size_t)kGradBlocks * 2 * h * f * sizeof(float));
+  return align_up((size_t)grad_blocks(rows) * 2 * h * f * sizeof(float));
 }
 
 int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float* dAl, const float* dAr,
@@ -1634,10 +1638,11 @@ int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float
   cudaStream_t s = as_stream(stream);
   const int hf = h * f;
   float* part = static_cast<float*>(ws);
-  dim3 g1(kGradBlocks, (unsigned)ceil_div(hf, f % 4 == 0 ? 1024 : 256));
+  const int nb = grad_blocks(rows);
+  dim3 g1(nb, (unsigned)ceil_div(hf, f % 4 == 0 ? 1024 : 256));
   attn_grad_partial_kernel<<<g1, 256, 0, s>>>(rows, h, f, Ht, dAl, dAr, part);
   GNNCG_LAUNCH_CHECK();
-  attn_grad_reduce_kernel<<<(unsigned)(2 * hf), 256, 0, s>>>(kGradBlocks, hf, part, da_l, da_r);
+  attn_grad_reduce_kernel<<<(unsigned)(2 * hf), 256, 0, s>>>(nb, hf, part, da_l, da_r);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }

@@ -191,10 +191,10 @@ __global__ void presplit_lo_kernel(int64_t rows, int64_t cols, const float* __re
 
 int tc_splits(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ceil_div(M, 128) * ceil_div(N, tc_bn(N));
-  if (tiles >= 148 || K < 2048) return 1;
+  if (tiles >= 148 || K < 1024) return 1;
   // floor: tiles * splits <= 148, one tile per SM of the persistent kernel (a 150th tile would
-  // double the kernel time); slices of >= 512 k (32 stages)
-  int64_t s = std::min<int64_t>(148 / tiles, K / 512);
+  // double the kernel time); slices of >= 256 k (16 stages)
+  int64_t s = std::min<int64_t>(148 / tiles, K / 256);
   return (int)std::max<int64_t>(std::min<int64_t>(s, 64), 1);
 }
 size_t presplit_b_bytes(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K) {

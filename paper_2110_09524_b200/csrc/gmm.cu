@@ -38,27 +38,28 @@ struct GmmArgs {
   float *out, *dY, *part;
 };
 
-__device__ __forceinline__ void gauss(const GmmArgs& a, const float* pl_u, const float* pr_v, float (&w)[MAXK],
-                                      float (&md)[MAXK][MAXR]) {
+// w_k of one edge: exp(-1/2 sum_t (pl_u + pr_v - mu_k)_t^2 sinv_kt^2).  k < K, t < r are runtime
+// guards inside fully unrolled loops, so pl / pr stay in registers; nothing of size K x r is
+// kept per lane (the earlier per-lane [K][r] arrays cost 174-216 registers: 8 warps per SM).
+__device__ __forceinline__ float gmm_w(const GmmArgs& a, int k, const float (&plu)[MAXR], const float (&prv)[MAXR]) {
+  float q = 0.f;
 #pragma unroll
-  for (int k = 0; k < MAXK; ++k) {
-    float q = 0.f;
-#pragma unroll
-    for (int t = 0; t < MAXR; ++t) {
-      if (k < a.K && t < a.r) {
-        const float x = pl_u[t] + pr_v[t] - __ldg(a.mu + k * a.r + t);
-        const float s = __ldg(a.sinv + k * a.r + t);
-        md[k][t] = x;
-        q = fmaf(x * x, s * s, q);
-      } else {
-        md[k][t] = 0.f;
-      }
+  for (int t = 0; t < MAXR; ++t) {
+    if (t < a.r) {
+      const float x = plu[t] + prv[t] - __ldg(a.mu + k * a.r + t);
+      const float s = __ldg(a.sinv + k * a.r + t);
+      q = fmaf(x * x, s * s, q);
     }
-    w[k] = k < a.K ? __expf(-0.5f * q) : 0.f;
   }
+  return __expf(-0.5f * q);
 }
 
-__global__ void __launch_bounds__(256) gmm_fwd_kernel(GmmArgs a) {
+__device__ __forceinline__ void load_p(const float* p, int r, float (&x)[MAXR]) {
+#pragma unroll
+  for (int t = 0; t < MAXR; ++t) x[t] = t < r ? __ldg(p + t) : 0.f;
+}
+
+__global__ void __launch_bounds__(256, 4) gmm_fwd_kernel(GmmArgs a) {
   __shared__ GmmSmem smem[WARPS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   GmmSmem& sm = smem[wid];
@@ -66,8 +67,7 @@ __global__ void __launch_bounds__(256) gmm_fwd_kernel(GmmArgs a) {
   if (v >= a.rows) return;
   const int K = a.K, r = a.r, f = a.f, Kf = K * f;
   float prv[MAXR];
-#pragma unroll
-  for (int t = 0; t < MAXR; ++t) prv[t] = t < r ? __ldg(a.Y + v * a.ldy + Kf + r + t) : 0.f;
+  load_p(a.Y + v * a.ldy + Kf + r, r, prv);
   float acc[MAXKF / 32];
 #pragma unroll
   for (int i = 0; i < MAXKF / 32; ++i) acc[i] = 0.f;
@@ -78,13 +78,10 @@ __global__ void __launch_bounds__(256) gmm_fwd_kernel(GmmArgs a) {
       const uint32_t u = __ldg(a.nbr + base + lane);
       sm.nb[lane] = u;
       float plu[MAXR];
-#pragma unroll
-      for (int t = 0; t < MAXR; ++t) plu[t] = t < r ? __ldg(a.Y + (int64_t)u * a.ldy + Kf + t) : 0.f;
-      float w[MAXK], md[MAXK][MAXR];
-      gauss(a, plu, prv, w, md);
+      load_p(a.Y + (int64_t)u * a.ldy + Kf, r, plu);
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
-        if (k < K) sm.w[lane * (MAXK + 1) + k] = w[k];
+        if (k < K) sm.w[lane * (MAXK + 1) + k] = gmm_w(a, k, plu, prv);
     }
     __syncwarp();
     for (int j = 0; j < n; ++j) {
@@ -111,73 +108,73 @@ __global__ void __launch_bounds__(256) gmm_fwd_kernel(GmmArgs a) {
   }
 }
 
-// pass 1 over csr_dst: lane per edge.
-__global__ void __launch_bounds__(256) gmm_bwd_dst_kernel(GmmArgs a) {
+// pass 1 over csr_dst: lane per edge.  The per-row dmu / dsinv partials (2 K r <= 64 values)
+// are reduced across the warp per 32-edge batch and held distributed: lane j keeps entries j
+// and 32 + j.
+__global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
   __shared__ GmmSmem smem[WARPS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   GmmSmem& sm = smem[wid];
   const int64_t v = (int64_t)blockIdx.x * WARPS + wid;
   if (v >= a.rows) return;
-  const int K = a.K, r = a.r, f = a.f, Kf = K * f;
+  const int K = a.K, r = a.r, f = a.f, Kf = K * f, Kr = K * r;
   const float invK = 1.f / (float)K;
   for (int c = lane; c < f; c += 32) sm.row[c] = __ldg(a.dOut + v * f + c);
   __syncwarp();
-  float prv[MAXR], dpr[MAXR], dmu[MAXK][MAXR], dsi[MAXK][MAXR];
+  float prv[MAXR], dpr[MAXR];
+  load_p(a.Y + v * a.ldy + Kf + r, r, prv);
 #pragma unroll
-  for (int t = 0; t < MAXR; ++t) {
-    prv[t] = t < r ? __ldg(a.Y + v * a.ldy + Kf + r + t) : 0.f;
-    dpr[t] = 0.f;
-#pragma unroll
-    for (int k = 0; k < MAXK; ++k) { dmu[k][t] = 0.f; dsi[k][t] = 0.f; }
-  }
+  for (int t = 0; t < MAXR; ++t) dpr[t] = 0.f;
+  float acc0 = 0.f, acc1 = 0.f;
   const uint64_t e0 = a.off[v], e1 = a.off[v + 1];
-  for (uint64_t e = e0 + lane; e < e1; e += 32) {
-    const int64_t u = __ldg(a.nbr + e);
+  for (uint64_t base = e0; base < e1; base += 32) {
+    const bool valid = base + lane < e1;
+    const int64_t u = valid ? (int64_t)__ldg(a.nbr + base + lane) : 0;
     const float* y = a.Y + u * a.ldy;
-    float plu[MAXR];
+    float plu[MAXR], dw[MAXK];
+    load_p(y + Kf, r, plu);
 #pragma unroll
-    for (int t = 0; t < MAXR; ++t) plu[t] = t < r ? __ldg(y + Kf + t) : 0.f;
-    float w[MAXK], md[MAXK][MAXR];
-    gauss(a, plu, prv, w, md);
+    for (int k = 0; k < MAXK; ++k) dw[k] = 0.f;
+    if (valid)
+      for (int c = 0; c < f; ++c) {
+        const float g = sm.row[c];
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k < K) dw[k] = fmaf(g, __ldg(y + k * f + c), dw[k]);
+      }
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) {
       if (k < K) {
-        float dw = 0.f;
-        for (int c = 0; c < f; ++c) dw = fmaf(sm.row[c], __ldg(y + k * f + c), dw);
-        const float dq = -0.5f * w[k] * dw * invK;
+        const float dq = valid ? -0.5f * gmm_w(a, k, plu, prv) * dw[k] * invK : 0.f;
 #pragma unroll
         for (int t = 0; t < MAXR; ++t) {
           if (t < r) {
-            const float s = __ldg(a.sinv + k * r + t), x = md[k][t];
+            const float s = __ldg(a.sinv + k * r + t), x = plu[t] + prv[t] - __ldg(a.mu + k * r + t);
             const float dmd = dq * 2.f * x * s * s;
-            dsi[k][t] = fmaf(dq * 2.f * x * x, s, dsi[k][t]);
-            dmu[k][t] -= dmd;
             dpr[t] += dmd;
+            const float gm = warp_sum(-dmd), gs = warp_sum(dq * 2.f * x * x * s);
+            const int jm = k * r + t, js = Kr + jm;
+            if ((jm & 31) == lane) { if (jm < 32) acc0 += gm; else acc1 += gm; }
+            if ((js & 31) == lane) { if (js < 32) acc0 += gs; else acc1 += gs; }
           }
         }
       }
     }
   }
-  float* part = a.part + v * (int64_t)(2 * K * r);
+  float* part = a.part + v * (int64_t)(2 * Kr);
+  if (lane < 2 * Kr) part[lane] = acc0;
+  if (32 + lane < 2 * Kr) part[32 + lane] = acc1;
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) {
     if (t < r) {
       const float s = warp_sum(dpr[t]);
       if (lane == 0) a.dY[v * a.ldy + Kf + r + t] = s;
-#pragma unroll
-      for (int k = 0; k < MAXK; ++k) {
-        if (k < K) {
-          const float m1 = warp_sum(dmu[k][t]);
-          const float s1 = warp_sum(dsi[k][t]);
-          if (lane == 0) { part[k * r + t] = m1; part[K * r + k * r + t] = s1; }
-        }
-      }
     }
   }
 }
 
 // pass 2 over csc_src.
-__global__ void __launch_bounds__(256) gmm_bwd_src_kernel(GmmArgs a) {
+__global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
   __shared__ GmmSmem smem[WARPS];
   const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
   GmmSmem& sm = smem[wid];
@@ -188,8 +185,9 @@ __global__ void __launch_bounds__(256) gmm_bwd_src_kernel(GmmArgs a) {
   const float* yu = a.Y + u * a.ldy;
   for (int c = lane; c < Kf; c += 32) sm.row[c] = __ldg(yu + c);
   float plu[MAXR], dpl[MAXR];
+  load_p(yu + Kf, r, plu);
 #pragma unroll
-  for (int t = 0; t < MAXR; ++t) { plu[t] = t < r ? __ldg(yu + Kf + t) : 0.f; dpl[t] = 0.f; }
+  for (int t = 0; t < MAXR; ++t) dpl[t] = 0.f;
   __syncwarp();
   float acc[MAXKF / 32];
 #pragma unroll
@@ -200,24 +198,28 @@ __global__ void __launch_bounds__(256) gmm_bwd_src_kernel(GmmArgs a) {
     if (lane < n) {
       const int64_t v = __ldg(a.nbr + base + lane);
       sm.nb[lane] = (uint32_t)v;
-      float prv[MAXR];
-#pragma unroll
-      for (int t = 0; t < MAXR; ++t) prv[t] = t < r ? __ldg(a.Y + v * a.ldy + Kf + r + t) : 0.f;
-      float w[MAXK], md[MAXK][MAXR];
-      gauss(a, plu, prv, w, md);
+      float prv[MAXR], dw[MAXK];
+      load_p(a.Y + v * a.ldy + Kf + r, r, prv);
       const float* g = a.dOut + v * f;
+#pragma unroll
+      for (int k = 0; k < MAXK; ++k) dw[k] = 0.f;
+      for (int c = 0; c < f; ++c) {
+        const float gc = __ldg(g + c);
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k < K) dw[k] = fmaf(gc, sm.row[k * f + c], dw[k]);
+      }
 #pragma unroll
       for (int k = 0; k < MAXK; ++k) {
         if (k < K) {
-          sm.w[lane * (MAXK + 1) + k] = w[k] * invK;
-          float dw = 0.f;
-          for (int c = 0; c < f; ++c) dw = fmaf(__ldg(g + c), sm.row[k * f + c], dw);
-          const float dq = -0.5f * w[k] * dw * invK;
+          const float w = gmm_w(a, k, plu, prv);
+          sm.w[lane * (MAXK + 1) + k] = w * invK;
+          const float dq = -0.5f * w * dw[k] * invK;
 #pragma unroll
           for (int t = 0; t < MAXR; ++t)
             if (t < r) {
-              const float s = __ldg(a.sinv + k * r + t);
-              dpl[t] = fmaf(dq * 2.f * md[k][t], s * s, dpl[t]);
+              const float s = __ldg(a.sinv + k * r + t), x = plu[t] + prv[t] - __ldg(a.mu + k * r + t);
+              dpl[t] = fmaf(dq * 2.f * x, s * s, dpl[t]);
             }
         }
       }
@@ -248,15 +250,44 @@ __global__ void __launch_bounds__(256) gmm_bwd_src_kernel(GmmArgs a) {
   }
 }
 
-// dmu / dsinv = sum over rows of the per-row partials, in row order.
-__global__ void gmm_param_reduce_kernel(int64_t rows, int n, const float* __restrict__ part, float* __restrict__ dmu,
+// dmu / dsinv = sum over rows of the per-row partials, in a fixed order (deterministic):
+// stage 1: block b sums rows [b R, (b+1) R) -- thread t owns parameter t % n and rows
+// t / n, t / n + G, ... (G = 256 / n groups), so each sweep reads G whole contiguous rows;
+// the groups are merged in shared memory in group order.  stage 2: one warp per parameter
+// sums the block partials.
+constexpr int RED_THREADS = 256, RED_BLOCKS = 592;
+
+int red_blocks(int64_t rows) {
+  const int64_t b = ceil_div(rows, (int64_t)64);
+  return (int)(b < 1 ? 1 : b > RED_BLOCKS ? RED_BLOCKS : b);
+}
+
+__global__ void __launch_bounds__(RED_THREADS) gmm_param_partial_kernel(int64_t rows, int n,
+                                                                       const float* __restrict__ part,
+                                                                       float* __restrict__ blk) {
+  __shared__ float sm[RED_THREADS];
+  const int t = threadIdx.x, G = RED_THREADS / n, grp = t / n, q = t - grp * n;
+  const int64_t per = ceil_div(rows, (int64_t)gridDim.x);
+  const int64_t r0 = blockIdx.x * per, r1 = r0 + per < rows ? r0 + per : rows;
+  float s = 0.f;
+  if (grp < G)
+    for (int64_t rr = r0 + grp; rr < r1; rr += G) s += __ldg(part + rr * n + q);
+  sm[t] = s;
+  __syncthreads();
+  if (t < n) {
+    float acc = 0.f;
+    for (int k = 0; k < G; ++k) acc += sm[k * n + t];
+    blk[(int64_t)blockIdx.x * n + t] = acc;
+  }
+}
+
+__global__ void gmm_param_reduce_kernel(int nblk, int n, const float* __restrict__ blk, float* __restrict__ dmu,
                                         float* __restrict__ dsinv, int Kr) {
-  // one warp per parameter entry; lanes stride rows, then a fixed-order tree.
   const int lane = threadIdx.x & 31;
   const int q = blockIdx.x * (blockDim.x >> 5) + (threadIdx.x >> 5);
   if (q >= n) return;
   float s = 0.f;
-  for (int64_t rr = lane; rr < rows; rr += 32) s += part[rr * n + q];
+  for (int b = lane; b < nblk; b += 32) s += blk[(int64_t)b * n + q];
   s = warp_sum(s);
   if (lane == 0) {
     if (q < Kr) dmu[q] = s; else dsinv[q - Kr] = s;
@@ -293,7 +324,9 @@ int gnncg_gmm_fwd(const gnncg_index_t* csr, int K, int r, int f, const float* Y,
 }
 
 size_t gnncg_gmm_bwd_workspace(const gnncg_index_t* csr, int K, int r) {
-  return csr ? align_up((size_t)csr->num_rows * 2 * K * r * sizeof(float)) : 0;
+  if (!csr) return 0;
+  const size_t n = (size_t)2 * K * r;
+  return align_up((size_t)csr->num_rows * n * sizeof(float)) + align_up((size_t)red_blocks(csr->num_rows) * n * sizeof(float));
 }
 
 int gnncg_gmm_bwd(const gnncg_index_t* csr, const gnncg_index_t* csc, int K, int r, int f, const float* Y,
@@ -326,8 +359,11 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr, const gnncg_index_t* csc, int K, int
   a.nbr = csc->nbr;
   gmm_bwd_src_kernel<<<grid, 256, 0, s>>>(a);
   GNNCG_LAUNCH_CHECK();
-  const int n = 2 * K * r;
-  gmm_param_reduce_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(csr->num_rows, n, a.part, dmu, dsinv, K * r);
+  const int n = 2 * K * r, nblk = red_blocks(csr->num_rows);
+  float* blk = a.part + align_up((size_t)csr->num_rows * n * sizeof(float)) / sizeof(float);
+  gmm_param_partial_kernel<<<nblk, RED_THREADS, 0, s>>>(csr->num_rows, n, a.part, blk);
+  GNNCG_LAUNCH_CHECK();
+  gmm_param_reduce_kernel<<<(unsigned)ceil_div(n, 8), 256, 0, s>>>(nblk, n, blk, dmu, dsinv, K * r);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }

@@ -420,6 +420,18 @@ class GmmStash:
     Y: torch.Tensor  # [hW | pl | pr], V x (K f + 2 r)
 
 
+def _gmm_wcat(W, P_l, P_r):
+    """[W | P_l | P_r] with its row padded with zero columns to a multiple of 4 floats: Y and dY
+    then have 16-byte rows, which the TMA tensor-core GEMM needs (K8 takes ldy >= K f + 2 r)."""
+    n = W.shape[1] + P_l.shape[1] + P_r.shape[1]
+    out = torch.zeros(W.shape[0], (n + 3) // 4 * 4, device=W.device)
+    a, b = W.shape[1], W.shape[1] + P_l.shape[1]
+    out[:, :a] = _f32(W, "W")
+    out[:, a:b] = _f32(P_l, "P_l")
+    out[:, b:n] = _f32(P_r, "P_r")
+    return out
+
+
 def gmm_forward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K: int, r: int, f: int):
     """GMMConv layer forward: Y = H [W | P_l | P_r], then the fused
     Gaussian-weighted aggregation (K8)."""
@@ -430,7 +442,7 @@ def gmm_forward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K: int, r: int, f: int
     _shape(P_r, (Fin, r), "P_r")
     _shape(mu, (K, r), "mu")
     _shape(sinv, (K, r), "sinv")
-    Y = gemm(H, torch.cat([_f32(W, "W"), _f32(P_l, "P_l"), _f32(P_r, "P_r")], dim=1), ws=g.ws)
+    Y = gemm(H, _gmm_wcat(W, P_l, P_r), ws=g.ws)
     out = torch.empty(g.num_vertices, f, device=H.device)
     with PROBE("gmm_fwd"):
         call("gnncg_gmm_fwd", g.csr_dst.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(_f32(mu, "mu")),
@@ -445,6 +457,8 @@ def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmSt
     V = g.num_vertices
     Y = stash.Y
     dY = torch.empty_like(Y)
+    if Y.shape[1] > K * f + 2 * r:
+        dY[:, K * f + 2 * r:].zero_()  # the alignment columns (K8 writes the first K f + 2 r)
     dmu = torch.empty(K, r, device=H.device)
     dsinv = torch.empty(K, r, device=H.device)
     need = _lib.lib().gnncg_gmm_bwd_workspace(g.csr_dst.struct(), K, r)
@@ -453,9 +467,9 @@ def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmSt
         call("gnncg_gmm_bwd", g.csr_dst.struct(), g.csc_src.struct(), K, r, f, _ptr(Y), Y.stride(0), _ptr(mu),
              _ptr(sinv), _ptr(dOut), _ptr(dY), _ptr(dmu), _ptr(dsinv), wp, wn, _stream())
     dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
-    dH = gemm(dY, torch.cat([W, P_l, P_r], dim=1), trans_b=True, ws=g.ws) if need_dH else None
+    dH = gemm(dY, _gmm_wcat(W, P_l, P_r), trans_b=True, ws=g.ws) if need_dH else None
     Kf = K * f
-    return dH, dWcat[:, :Kf].contiguous(), dWcat[:, Kf:Kf + r].contiguous(), dWcat[:, Kf + r:].contiguous(), dmu, dsinv
+    return dH, dWcat[:, :Kf].contiguous(), dWcat[:, Kf:Kf + r].contiguous(), dWcat[:, Kf + r:Kf + 2 * r].contiguous(), dmu, dsinv
 
 
 # ---------------------------------------------------------------------------
