@@ -186,7 +186,7 @@ __global__ void __launch_bounds__(256) edgeconv_bwd_kernel(int64_t rows, int C, 
 }
 
 // Column vector width: 4 / 2 floats per lane when every row start is 16 / 8-byte aligned.  (8 per
-// lane, one pass at C = 256, measured slower than two passes of 4: 148 vs 126 us bwd.)
+// lane, one pass at C = 256: 119-128 registers, no faster than two passes of 4.)
 template <int VW, bool EAGER>
 void launch_bwd(unsigned grid, void* stream, const gnncg_index_t* csc, const gnncg_index_t* csr, int C,
                 const uint32_t* amax, const float* g, float* dTh, int64_t ldt, float* dPh, int64_t ldp) {

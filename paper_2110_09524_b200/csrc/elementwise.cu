@@ -51,12 +51,15 @@ __global__ void sum_partial_kernel(int64_t n, const float* __restrict__ x, doubl
   }
 }
 
+// one warp: lane-strided partial sums, then a fixed xor tree (deterministic; the serial
+// single-thread loop over 296 partials took 12 us of dependent loads)
 __global__ void sum_final_kernel(int nb, const double* __restrict__ part, float* __restrict__ out) {
-  if (threadIdx.x == 0 && blockIdx.x == 0) {
-    double t = 0.0;
-    for (int b = 0; b < nb; ++b) t += part[b];
-    *out = (float)t;
-  }
+  const int lane = threadIdx.x & 31;
+  double t = 0.0;
+  for (int b = lane; b < nb; b += 32) t += part[b];
+#pragma unroll
+  for (int o = 16; o > 0; o >>= 1) t += __shfl_xor_sync(0xffffffffu, t, o);
+  if (threadIdx.x == 0) *out = (float)t;
 }
 
 }  // namespace
