@@ -408,10 +408,12 @@ struct GmmGrads {
 };
 
 namespace detail {
-inline Tensor<float> pack_cols(const std::vector<const Tensor<float>*>& parts) {
+// [parts...] side by side; ld > the total width pads with zero columns (16-byte rows for the
+// tensor-core GEMM)
+inline Tensor<float> pack_cols(const std::vector<const Tensor<float>*>& parts, std::uint64_t ld = 0) {
   std::uint64_t cols = 0;
   for (auto* p : parts) cols += p->cols;
-  Tensor<float> out(parts[0]->rows, cols);
+  Tensor<float> out(parts[0]->rows, std::max(cols, ld), 0.0f);
   std::uint64_t c0 = 0;
   for (auto* p : parts) {
     for (std::uint64_t i = 0; i < p->rows; ++i)
@@ -425,7 +427,8 @@ inline Tensor<float> pack_cols(const std::vector<const Tensor<float>*>& parts) {
 inline Tensor<float> gmm_forward(const DeviceGraph& g, const Tensor<float>& H, const Tensor<float>& W,
                                  const Tensor<float>& P_l, const Tensor<float>& P_r, const Tensor<float>& mu,
                                  const Tensor<float>& sinv, const GmmParams& p, GmmStash* stash) {
-  const std::int64_t V = g.num_vertices(), Fin = H.cols, Kf = (std::int64_t)p.K * p.f, ldy = Kf + 2 * p.r;
+  const std::int64_t V = g.num_vertices(), Fin = H.cols, Kf = (std::int64_t)p.K * p.f;
+  const std::int64_t ldy = (Kf + 2 * p.r + 3) / 4 * 4;  // zero-padded to 16-byte rows
   detail::require_shape(W, Fin, Kf, "gmm W");
   detail::require_shape(P_l, Fin, p.r, "gmm P_l");
   detail::require_shape(P_r, Fin, p.r, "gmm P_r");
@@ -434,7 +437,7 @@ inline Tensor<float> gmm_forward(const DeviceGraph& g, const Tensor<float>& H, c
   cudaStream_t s = g.stream();
   GmmStash local;
   GmmStash& st = stash ? *stash : local;
-  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}), s);
+  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}, ldy), s);
   DeviceBuffer dmu = upload(mu, s), dsi = upload(sinv, s), out(V * p.f * 4);
   st.Y = DeviceBuffer(V * ldy * 4);
   st.ldy = ldy;
@@ -453,9 +456,10 @@ inline GmmGrads gmm_backward(const DeviceGraph& g, const Tensor<float>& H, const
   const std::int64_t V = g.num_vertices(), Fin = H.cols, Kf = (std::int64_t)p.K * p.f, ldy = st.ldy;
   detail::require_shape(dOut, V, p.f, "gmm dOut");
   cudaStream_t s = g.stream();
-  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}), s);
+  DeviceBuffer dH = upload(H, s), dWc = upload(detail::pack_cols({&W, &P_l, &P_r}, ldy), s);
   DeviceBuffer dmu_in = upload(mu, s), dsi_in = upload(sinv, s), g_out = upload(dOut, s);
   DeviceBuffer dY(V * ldy * 4), dmu(p.K * p.r * 4), dsinv(p.K * p.r * 4), dW(Fin * ldy * 4);
+  if (V > 0) cuda_check(cudaMemsetAsync(dY.get(), 0, dY.bytes(), s), "memset dY");  // K8 leaves the padding
   const gnncg_index_t csr = g.csr_dst().view(), csc = g.csc_src().view();
   DeviceBuffer& ws = g.workspace(gnncg_gmm_bwd_workspace(&csr, p.K, p.r));
   check(gnncg_gmm_bwd(&csr, &csc, p.K, p.r, p.f, st.Y.get<float>(), ldy, dmu_in.get<float>(), dsi_in.get<float>(),
