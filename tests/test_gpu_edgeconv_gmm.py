@@ -20,7 +20,10 @@ def np64(t):
     return t.detach().cpu().double().numpy()
 
 
-@pytest.mark.parametrize("clouds,points,k,C", [(2, 256, 20, 64), (4, 1024, 40, 64), (1, 64, 8, 33)])
+# C picks K6/K7's column width per lane: 64 -> 2, 96 -> 2 with a partial second pass,
+# 128 / 256 -> 4 (16-byte loads; two passes at 256), 33 -> 1
+@pytest.mark.parametrize("clouds,points,k,C", [(2, 256, 20, 64), (4, 1024, 40, 64), (1, 64, 8, 33),
+                                               (2, 256, 20, 128), (1, 512, 16, 256), (2, 128, 10, 96)])
 def test_edgeconv_region_argmax_bit_exact(cuda, clouds, points, k, C):
     src, dst = knn_edges(clouds, points, k, seed=0)
     V = clouds * points
@@ -47,14 +50,14 @@ def test_edgeconv_empty_rows_and_ties(cuda):
     assert all(a[v, 0] == 0xFFFFFFFF and out[v, 0].item() == 0.0 for v in (1, 2, 3))
 
 
-@pytest.mark.parametrize("k", [20, 40])
-def test_edgeconv_layer_vs_oracle(cuda, k):
+@pytest.mark.parametrize("k,C", [(20, 64), (40, 64), (20, 256), (12, 36)])
+def test_edgeconv_layer_vs_oracle(cuda, k, C):
     src, dst = knn_edges(2, 512, k, seed=1)
     V = 1024
     hg = O.host_graph(V, src, dst)
     g = DeviceGraph.from_edges(V, src, dst, device=cuda)
     rng = np.random.default_rng(k)
-    Fin, C = 64, 64
+    Fin = 64
     H = rng.uniform(-1, 1, (V, Fin))
     Theta, Phi = rng.uniform(-0.125, 0.125, (Fin, C)), rng.uniform(-0.125, 0.125, (Fin, C))
     dOut = rng.uniform(-1, 1, (V, C))
