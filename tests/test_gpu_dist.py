@@ -20,6 +20,13 @@ def _port():
         return s.getsockname()[1]
 
 
+@pytest.fixture(scope="module", autouse=True)
+def _nccl_teardown():
+    yield
+    if dist.is_initialized():
+        dist.destroy_process_group()
+
+
 @pytest.mark.parametrize("mode", ["deterministic", "auto"])
 def test_partitioned_world1_matches_single_gpu(cuda, mode):
     from paper_2110_09524_b200.dist import CudaEngine, PartitionedGAT, partitioned_chung_lu
