@@ -12,4 +12,11 @@ done
 timeout 900 compute-sanitizer --tool memcheck --error-exitcode 99 --print-limit 20 \
   python -m pytest tests/test_gpu_gemm_tc.py -q -x -p no:cacheprovider -k "129 or 300 or identity" > gpurun_out/san_gemm_$TAG.log 2>&1
 echo "rc=$?" >> gpurun_out/san_gemm_$TAG.log
+# the K6/K7 column widths and K8 (small parametrisations)
+for tool in memcheck racecheck synccheck; do
+  timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
+    python -m pytest tests/test_gpu_edgeconv_gmm.py -q -x -p no:cacheprovider \
+    -k "1-64-8-33 or 2-128-10-96 or 2-256-20-128 or 200-1500 or 500-4000 or 12-36" > gpurun_out/san_ecgmm_${tool}_$TAG.log 2>&1
+  echo "rc=$?" >> gpurun_out/san_ecgmm_${tool}_$TAG.log
+done
 echo done
