@@ -252,7 +252,7 @@ __device__ __forceinline__ void ovl_edge_phase(OvlSmem& sm, int lane, int n, int
 }
 
 // U rows in flight per warp, CW warps per CTA, MINB CTAs per SM (register budget).
-template <int VW, int NV, int U, int CW, int MINB, bool LP = false>
+template <int VW, int NV, int U, int CW, int MINB, bool LP = false, bool DYN = false>
 __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / (MINB * CW * kWarp)) / 8 * 8 > 255 ? 255 : (65536 / (MINB * CW * kWarp)) / 8 * 8) : 255) gat_fwd_ovl_kernel(GatParams p) {
   static_assert(32 % U == 0, "U must divide the 32-edge block");
   __shared__ OvlSmem smem[CW];
@@ -264,9 +264,19 @@ __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / 
   // warp idles until the slowest warp of its CTA finishes
   // (the loop is CTA-uniform -- the compiler keeps the memory descriptor in a uniform register
   // -- but carries no barrier: warps advance independently)
-  for (int64_t g = blockIdx.x; g * CW < p.num_items; g += gridDim.x) {
-  const int64_t wi = g * CW + w;
-  if (wi >= p.num_items) continue;
+  // DYN: warps pull items from a counter instead (items come largest first, so this is a
+  // greedy longest-first assignment; the next index is requested at the start of an item)
+  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
+  for (int64_t g = blockIdx.x; DYN || g * CW < p.num_items; g += gridDim.x) {
+  int64_t wi;
+  if constexpr (DYN) {
+    wi = __shfl_sync(0xffffffffu, nx, 0);
+    if (wi >= p.num_items) break;
+    if (lane == 0) nx = atomicAdd(p.ctr, 1u);
+  } else {
+    wi = g * CW + w;
+    if (wi >= p.num_items) continue;
+  }
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
 
   if (lane < h) {
@@ -650,7 +660,7 @@ __device__ __forceinline__ void butterfly(float* v, int lane) {
   }
 }
 
-template <int VW, int NV, int PER, int OCC, bool LP = false, bool PAIR = false>
+template <int VW, int NV, int PER, int OCC, bool LP = false, bool PAIR = false, bool DYN = false>
 __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_kernel(GatParams p) {
   constexpr int U = LP ? LpDepth<VW, NV>::U : GatherDepth<NV, OCC>::U;
   // next-group loads issued per half-group: bf16 rows only (packed rows leave the registers for
@@ -665,9 +675,17 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   const float slope = p.slope;
   const int r = lane & (PER - 1);  // rank inside the head's lane group
   // persistent CTA-uniform item loop (as in gat_fwd_ovl_kernel), no barrier inside
-  for (int64_t g = blockIdx.x; g * WARPS < p.num_items; g += gridDim.x) {
-  const int64_t wi = g * WARPS + w;
-  if (wi >= p.num_items) continue;
+  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;  // as in gat_fwd_ovl_kernel
+  for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
+  int64_t wi;
+  if constexpr (DYN) {
+    wi = __shfl_sync(0xffffffffu, nx, 0);
+    if (wi >= p.num_items) break;
+    if (lane == 0) nx = atomicAdd(p.ctr, 1u);
+  } else {
+    wi = g * WARPS + w;
+    if (wi >= p.num_items) continue;
+  }
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
   const int64_t u = it.row;
 
@@ -1147,6 +1165,12 @@ int num_sms();
 bool ovl_enabled();
 bool pair_enabled();
 
+template <int VW, int NV, int PER, int OCC>
+void launch_fast_per(const GatParams& p, dim3 grid, cudaStream_t s) {
+  if (p.ctr) gat_bwd_src_fast_kernel<VW, NV, PER, OCC, false, false, true><<<grid, THREADS, 0, s>>>(p);
+  else gat_bwd_src_fast_kernel<VW, NV, PER, OCC><<<grid, THREADS, 0, s>>>(p);
+}
+
 template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
   constexpr int NVAL = GatherDepth<NV, OCC>::U * NV;
@@ -1154,16 +1178,17 @@ void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
   if constexpr (NV == 2 && NVAL == 2 * 8) {
     // paired columns (8 lanes per head, two adjacent heads per lane, h = 8): the Reddit shape
     if (pair_enabled() && pair_lanes(p.h, p.f, VW, NV) == 8 && p.h == 8) {
-      gat_bwd_src_fast_kernel<VW, NV, 8, OCC, false, true><<<grid, THREADS, 0, s>>>(p);
+      if (p.ctr) gat_bwd_src_fast_kernel<VW, NV, 8, OCC, false, true, true><<<grid, THREADS, 0, s>>>(p);
+      else gat_bwd_src_fast_kernel<VW, NV, 8, OCC, false, true><<<grid, THREADS, 0, s>>>(p);
       return;
     }
   }
   switch (p.f / VW) {
-    case 1: gat_bwd_src_fast_kernel<VW, NV, 1, OCC><<<grid, THREADS, 0, s>>>(p); break;
-    case 2: if constexpr (NVAL % 2 == 0) gat_bwd_src_fast_kernel<VW, NV, 2, OCC><<<grid, THREADS, 0, s>>>(p); break;
-    case 4: if constexpr (NVAL % 4 == 0) gat_bwd_src_fast_kernel<VW, NV, 4, OCC><<<grid, THREADS, 0, s>>>(p); break;
-    case 8: if constexpr (NVAL % 8 == 0) gat_bwd_src_fast_kernel<VW, NV, 8, OCC><<<grid, THREADS, 0, s>>>(p); break;
-    case 16: if constexpr (NVAL % 16 == 0) gat_bwd_src_fast_kernel<VW, NV, 16, OCC><<<grid, THREADS, 0, s>>>(p); break;
+    case 1: launch_fast_per<VW, NV, 1, OCC>(p, grid, s); break;
+    case 2: if constexpr (NVAL % 2 == 0) launch_fast_per<VW, NV, 2, OCC>(p, grid, s); break;
+    case 4: if constexpr (NVAL % 4 == 0) launch_fast_per<VW, NV, 4, OCC>(p, grid, s); break;
+    case 8: if constexpr (NVAL % 8 == 0) launch_fast_per<VW, NV, 8, OCC>(p, grid, s); break;
+    case 16: if constexpr (NVAL % 16 == 0) launch_fast_per<VW, NV, 16, OCC>(p, grid, s); break;
     default: break;  // excluded by gnncg_gat_fast_supported
   }
 }
@@ -1176,7 +1201,8 @@ void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
       constexpr int U = GatherDepth<NV, OCC>::U;
       constexpr int MINB = NV >= 8 ? 1 : OCC;
       const unsigned g = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * MINB);
-      gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB><<<g, THREADS, 0, s>>>(p);
+      if (p.ctr) gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB, false, true><<<g, THREADS, 0, s>>>(p);
+      else gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB><<<g, THREADS, 0, s>>>(p);
       break;
     }
     case Kind::BwdDst: gat_bwd_dst_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
@@ -1234,14 +1260,18 @@ bool lp_fast_ok(int f) {
 template <int VW, int NV, int PER>
 void launch_lp_fast_per(const GatParams& p, unsigned g, cudaStream_t s) {
   constexpr int NVAL = LpDepth<VW, NV>::U * NV;
-  if constexpr (NVAL % PER == 0) gat_bwd_src_fast_kernel<VW, NV, PER, 2, true><<<g, THREADS, 0, s>>>(p);
+  if constexpr (NVAL % PER == 0) {
+    if (p.ctr) gat_bwd_src_fast_kernel<VW, NV, PER, 2, true, false, true><<<g, THREADS, 0, s>>>(p);
+    else gat_bwd_src_fast_kernel<VW, NV, PER, 2, true><<<g, THREADS, 0, s>>>(p);
+  }
 }
 
 template <int VW, int NV>
 void launch_lp(Kind kind, const GatParams& p, cudaStream_t s) {
   const unsigned g = (unsigned)std::min<int64_t>(ceil_div(p.num_items, WARPS), (int64_t)num_sms() * 2);
   if (kind == Kind::FwdOvl) {
-    gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true><<<g, THREADS, 0, s>>>(p);
+    if (p.ctr) gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true, true><<<g, THREADS, 0, s>>>(p);
+    else gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true><<<g, THREADS, 0, s>>>(p);
   } else {
     switch (p.f / VW) {
       case 1: launch_lp_fast_per<VW, NV, 1>(p, g, s); break;
@@ -1312,6 +1342,31 @@ bool tma_enabled() {
 
 // GNNCG_GAT_OVL=0 selects the block-synchronous forward (gat_fwd_kernel) instead of the
 // overlapped-edge-phase one (gat_fwd_ovl_kernel).
+// K2 / K4f pull work items from a counter in the workspace (behind the partials, where
+// gnncg_gat_workspace reserves 256 bytes) instead of a fixed stride: the items are ordered
+// largest first, so warps take them longest-first and finish together (with a fixed stride
+// the busiest warp carries ~11% more edges than the mean on the Reddit shape, simulated).  Measured: K2 7.94 ->
+// 7.47 ms, K4f 11.75 -> 11.1 ms.  GNNCG_GAT_DYN=0 restores the fixed stride; a workspace
+// without the counter bytes also does.  (K4f: long items only, see gat_bwd_src_fused_impl.)
+constexpr int kDynMinEdgesPerItem = 256;
+
+bool dyn_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_DYN");
+    v = e ? atoi(e) : 1;
+  }
+  return v == 1;
+}
+
+int attach_counter(GatParams& p, void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
+  p.ctr = nullptr;
+  if (!dyn_enabled() || !ws || ws_bytes < align_up(need) + sizeof(unsigned)) return GNNCG_OK;
+  p.ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up(need));
+  GNNCG_CUDA_TRY(cudaMemsetAsync(p.ctr, 0, sizeof(unsigned), s));
+  return GNNCG_OK;
+}
+
 bool ovl_enabled() {
   static int v = -1;
   if (v < 0) {
@@ -1408,12 +1463,18 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
   p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
   if (lp) {
+    rc = attach_counter(p, ws, ws_bytes, need, s);
+    if (rc) return rc;
     rc = dispatch_lp(Kind::FwdOvl, p, s);
   } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
     int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
     GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
     rc = launch_fwd_tma(p, counter, s);
   } else {
+    if (ovl_enabled()) {
+      rc = attach_counter(p, ws, ws_bytes, need, s);
+      if (rc) return rc;
+    }
     rc = dispatch(ovl_enabled() ? Kind::FwdOvl : Kind::Fwd, p, s);
   }
   if (rc) return rc;
@@ -1578,6 +1639,13 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;
+  // K4f takes the counter only for long items (Reddit: 452 edges per item, 11.75 -> 11.1 ms);
+  // on C5's short items (~100 edges) it measured slower (fp32 132.5 -> 134.6 ms, bf16 90.2 ->
+  // 103.2 ms; the request two items ahead did not change that)
+  if (csc_src->num_edges >= (uint64_t)kDynMinEdgesPerItem * (uint64_t)sched->num_items) {
+    rc = attach_counter(p, ws, ws_bytes, need, s);
+    if (rc) return rc;
+  }
   rc = lp ? dispatch_lp(Kind::BwdSrcFast, p, s) : dispatch(Kind::BwdSrcFast, p, s);
   if (rc) return rc;
   if (sched->num_split_rows > 0) {

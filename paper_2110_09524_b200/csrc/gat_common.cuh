@@ -91,6 +91,7 @@ struct GatParams {
   int64_t row_base, num_local;
   const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
+  unsigned* ctr;  // dynamic item fetch (DYN kernels): zeroed work counter in the workspace
 };
 
 // ---------------------------------------------------------------------------
