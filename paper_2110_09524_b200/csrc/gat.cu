@@ -266,6 +266,8 @@ __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / 
   // -- but carries no barrier: warps advance independently)
   // DYN: warps pull items from a counter instead (items come largest first, so this is a
   // greedy longest-first assignment; the next index is requested at the start of an item)
+  // (one item per request: the batched form of K4f changed this kernel's code generation,
+  // 1688 -> 2352 instructions, and cost 0.4 ms on the Reddit shape)
   unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
   for (int64_t g = blockIdx.x; DYN || g * CW < p.num_items; g += gridDim.x) {
   int64_t wi;
@@ -675,13 +677,20 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
   const float slope = p.slope;
   const int r = lane & (PER - 1);  // rank inside the head's lane group
   // persistent CTA-uniform item loop (as in gat_fwd_ovl_kernel), no barrier inside
-  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;  // as in gat_fwd_ovl_kernel
+  // as in gat_fwd_ovl_kernel, but p.batch items per request when items are short (C5: one
+  // counter address serves ~10^8 requests per second)
+  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, (unsigned)p.batch) : 0u;
+  int64_t cur = 0, cend = 0;
   for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
   int64_t wi;
   if constexpr (DYN) {
-    wi = __shfl_sync(0xffffffffu, nx, 0);
+    if (cur >= cend) {
+      cur = __shfl_sync(0xffffffffu, nx, 0);
+      cend = cur + p.batch;
+      if (lane == 0) nx = atomicAdd(p.ctr, (unsigned)p.batch);
+    }
+    wi = cur++;
     if (wi >= p.num_items) break;
-    if (lane == 0) nx = atomicAdd(p.ctr, 1u);
   } else {
     wi = g * WARPS + w;
     if (wi >= p.num_items) continue;
@@ -1346,22 +1355,40 @@ bool tma_enabled() {
 // gnncg_gat_workspace reserves 256 bytes) instead of a fixed stride: the items are ordered
 // largest first, so warps take them longest-first and finish together (with a fixed stride
 // the busiest warp carries ~11% more edges than the mean on the Reddit shape, simulated).  Measured: K2 7.94 ->
-// 7.47 ms, K4f 11.75 -> 11.1 ms.  GNNCG_GAT_DYN=0 restores the fixed stride; a workspace
-// without the counter bytes also does.  (K4f: long items only, see gat_bwd_src_fused_impl.)
-constexpr int kDynMinEdgesPerItem = 256;
+// 7.47 ms, K4f 11.75 -> 11.1 ms; C5 K4f 132.5 -> 115.8 ms with 5 items per request.
+// GNNCG_GAT_DYN=0 restores the fixed stride; a workspace without the counter bytes also does.
+// GNNCG_GAT_DYN_BATCH caps the items per counter request (default 8; 1 = one at a time)
+uint64_t dyn_batch_cap() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_DYN_BATCH");
+    v = e ? std::max(1, atoi(e)) : 8;
+  }
+  return (uint64_t)v;
+}
 
-bool dyn_enabled() {
+// 0: fixed stride; 1: counter for graphs with >= 8 items per warp (default); 2: counter always
+// (tests: it exercises the counter and K4f's batched requests on small graphs)
+int dyn_mode() {
   static int v = -1;
   if (v < 0) {
     const char* e = getenv("GNNCG_GAT_DYN");
     v = e ? atoi(e) : 1;
   }
-  return v == 1;
+  return v;
 }
+bool dyn_enabled() { return dyn_mode() >= 1; }
 
-int attach_counter(GatParams& p, void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
+int attach_counter(GatParams& p, uint64_t num_edges, void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
   p.ctr = nullptr;
   if (!dyn_enabled() || !ws || ws_bytes < align_up(need) + sizeof(unsigned)) return GNNCG_OK;
+  // a few items per warp of the persistent grid balance themselves (Cora: 2708 items; the
+  // counter's memset cost more than it saved there)
+  const uint64_t warps = (uint64_t)num_sms() * 2 * WARPS;
+  if (dyn_mode() == 1 && (uint64_t)p.num_items < 8 * warps) return GNNCG_OK;
+  // K4f: about 512 edges per request (Reddit, 452 edges per item: 1; C5: 5)
+  const uint64_t mean = num_edges / (uint64_t)p.num_items;
+  p.batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(dyn_batch_cap(), 512 / std::max<uint64_t>(mean, 1)));
   p.ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up(need));
   GNNCG_CUDA_TRY(cudaMemsetAsync(p.ctr, 0, sizeof(unsigned), s));
   return GNNCG_OK;
@@ -1463,7 +1490,7 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
   p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
   cudaStream_t s = as_stream(stream);
   if (lp) {
-    rc = attach_counter(p, ws, ws_bytes, need, s);
+    rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
     if (rc) return rc;
     rc = dispatch_lp(Kind::FwdOvl, p, s);
   } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
@@ -1472,7 +1499,7 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
     rc = launch_fwd_tma(p, counter, s);
   } else {
     if (ovl_enabled()) {
-      rc = attach_counter(p, ws, ws_bytes, need, s);
+      rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
       if (rc) return rc;
     }
     rc = dispatch(ovl_enabled() ? Kind::FwdOvl : Kind::Fwd, p, s);
@@ -1639,13 +1666,10 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;
-  // K4f takes the counter only for long items (Reddit: 452 edges per item, 11.75 -> 11.1 ms);
-  // on C5's short items (~100 edges) it measured slower (fp32 132.5 -> 134.6 ms, bf16 90.2 ->
-  // 103.2 ms; the request two items ahead did not change that)
-  if (csc_src->num_edges >= (uint64_t)kDynMinEdgesPerItem * (uint64_t)sched->num_items) {
-    rc = attach_counter(p, ws, ws_bytes, need, s);
-    if (rc) return rc;
-  }
+  // (C5's ~100-edge items: one item per request was slower than the fixed stride, 132.5 ->
+  // 134.6 ms, the counter address being the limit; 5 per request: 115.8 ms)
+  rc = attach_counter(p, csc_src->num_edges, ws, ws_bytes, need, s);
+  if (rc) return rc;
   rc = lp ? dispatch_lp(Kind::BwdSrcFast, p, s) : dispatch(Kind::BwdSrcFast, p, s);
   if (rc) return rc;
   if (sched->num_split_rows > 0) {

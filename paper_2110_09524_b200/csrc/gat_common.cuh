@@ -92,6 +92,7 @@ struct GatParams {
   const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
   unsigned* ctr;  // dynamic item fetch (DYN kernels): zeroed work counter in the workspace
+  int batch;      // items taken per counter request
 };
 
 // ---------------------------------------------------------------------------
