@@ -148,7 +148,10 @@ int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, 
                         float* Ht, const float* a_l, const float* a_r, float* Al, float* Ar, void* workspace,
                         size_t workspace_bytes, void* stream);
 
-/* Scratch for the split-row partials of all GAT kernels over these schedules. */
+/* Scratch for the split-row partials of all GAT kernels over these schedules, plus the work
+ * counter K2 / K4f pull their items from (zeroed by the call itself; a smaller workspace that
+ * still holds the partials makes them walk the items with a fixed stride instead).  One
+ * workspace must not be shared by GAT calls running concurrently on different streams. */
 size_t gnncg_gat_workspace(const gnncg_sched_t* dst_sched, const gnncg_sched_t* src_sched, int heads, int f);
 
 /* K2: the fused region Scatter(u_add_v) -> ApplyEdge(LeakyReLU) ->
