@@ -19,4 +19,11 @@ for tool in memcheck racecheck synccheck; do
     -k "1-64-8-33 or 2-128-10-96 or 2-256-20-128 or 200-1500 or 500-4000 or 12-36" > gpurun_out/san_ecgmm_${tool}_$TAG.log 2>&1
   echo "rc=$?" >> gpurun_out/san_ecgmm_${tool}_$TAG.log
 done
+# the work-counter item fetch of K2 / K4f forced on small graphs
+for tool in memcheck racecheck synccheck; do
+  GNNCG_GAT_DYN=2 timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
+    python -m pytest tests/test_gpu_gat.py tests/test_gpu_gat_bf16.py -q -x -p no:cacheprovider \
+    -k "G3 or ER16 or cora or edgeless or star" > gpurun_out/san_dyn_${tool}_$TAG.log 2>&1
+  echo "rc=$?" >> gpurun_out/san_dyn_${tool}_$TAG.log
+done
 echo done
