@@ -115,6 +115,20 @@ int gnncg_partition_rows(int64_t num_rows, const uint64_t* off_host, int32_t par
 int gnncg_gen_chung_lu(int64_t num_vertices, int64_t num_edges, const uint64_t* cdf, uint64_t seed, uint32_t* src,
                        uint32_t* dst, void* stream);
 
+/* Per-rank generation of the same edge list (multi-GPU: every rank keeps only its own
+ * destination rows).  gnncg_gen_chung_lu_degrees writes the in-degree of every
+ * vertex (u32, device) -- the offsets the row partitioner splits; gnncg_gen_chung_lu_rows
+ * writes, in edge-id order, the edges whose destination lies in [row_begin, row_end):
+ * src/dst hold off[row_end] - off[row_begin] entries (workspace sized by
+ * gnncg_gen_chung_lu_rows_workspace).  Together they equal filtering gnncg_gen_chung_lu's
+ * list by destination, without materialising it. */
+int gnncg_gen_chung_lu_degrees(int64_t num_vertices, int64_t num_edges, const uint64_t* cdf, uint64_t seed,
+                               uint32_t* in_deg, void* stream);
+size_t gnncg_gen_chung_lu_rows_workspace(int64_t num_edges);
+int gnncg_gen_chung_lu_rows(int64_t num_vertices, int64_t num_edges, const uint64_t* cdf, uint64_t seed,
+                            int64_t row_begin, int64_t row_end, uint32_t* src, uint32_t* dst, void* workspace,
+                            size_t workspace_bytes, void* stream);
+
 /* Schedule construction on the host from a host copy of the offsets.
  * First call with items_host == NULL to get the counts, then with arrays sized
  * 2*num_items, num_split_rows, num_split_rows+1. */
@@ -187,9 +201,9 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
                       size_t workspace_bytes, void* stream);
 
 /* Fast mode (lock-free atomic accumulation, tolerance-tested): K3 folded
- * into K4.  gnncg_gat_bwd_prep builds, per destination row v and head k, the packed
- * record {A_r[v,k] | lse[v,k] = m + log d | c[v,k] = <dOut[v,k,:], out[v,k,:]>}
- * (row stride gnncg_gat_rec_stride(heads) floats; c = sum_e alpha_e dalpha_e by the
+ * into K4.  gnncg_gat_bwd_prep builds, per destination row v and head k, the record
+ * float4 {A_r[v,k], lse[v,k] = m + log d, c[v,k] = <dOut[v,k,:], out[v,k,:]>, 0}
+ * (row stride gnncg_gat_rec_stride(heads) = 4 heads floats; c = sum_e alpha_e dalpha_e by the
  * softmax-backward identity, so no pass over csr_dst is needed).  One pass over
  * csc_src then produces dHt (including both LP terms), dA_l, and dA_r (zeroed and
  * accumulated with global reductions: order-nondeterministic in the last bits).

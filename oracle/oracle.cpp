@@ -287,31 +287,37 @@ void orc_gat_layer_bwd_f64(u64 V, const u64* off, const u32* src, u64 Fin, const
 }
 
 // ---------------------------------------------------------------------------
-// GAT, f32, the SPEC executor restated for speed: vertex_balanced OpenMP over
+// GAT, the SPEC executor restated for speed: vertex_balanced OpenMP over
 // destination rows, stash m, d only, recompute the
-// O(|E|) edge values in backward.  Timed CPU baseline.
+// O(|E|) edge values in backward.  T = float: the timed CPU baseline
+// (*_f32_omp); T = double: the parity oracle at benchmark scale (*_f64_omp) -- the
+// serial stash-everything *_f64 above is the independent derivation it is checked
+// against on small graphs (tests/test_oracle.py).
 // ---------------------------------------------------------------------------
-void orc_gat_region_fwd_f32_omp(u64 V, const u64* off, const u32* src, const float* Ht, const float* Al,
-                                const float* Ar, int h, int f, float slope, float* out, float* m, float* d) {
+}  // extern "C"
+namespace {
+template <typename T>
+void gat_region_fwd_omp(u64 V, const u64* off, const u32* src, const T* Ht, const T* Al, const T* Ar, int h, int f,
+                        T slope, T* out, T* m, T* d) {
   const u64 hf = (u64)h * f;
 #pragma omp parallel for schedule(dynamic, 64)
   for (i64 vv = 0; vv < (i64)V; ++vv) {
     const u64 v = (u64)vv;
-    float* o = out + v * hf;
-    for (u64 j = 0; j < hf; ++j) o[j] = 0.f;
+    T* o = out + v * hf;
+    for (u64 j = 0; j < hf; ++j) o[j] = T(0);
     for (int k = 0; k < h; ++k) {
-      const float ar_ = Ar[v * h + k];
-      float mx = -std::numeric_limits<float>::infinity(), den = 0.f;
+      const T ar_ = Ar[v * h + k];
+      T mx = -std::numeric_limits<T>::infinity(), den = T(0);
       for (u64 i = off[v]; i < off[v + 1]; ++i) mx = std::max(mx, lrelu(Al[(u64)src[i] * h + k] + ar_, slope));
       for (u64 i = off[v]; i < off[v + 1]; ++i) {
         const u64 u = src[i];
-        const float p = std::exp(lrelu(Al[u * h + k] + ar_, slope) - mx);
+        const T p = std::exp(lrelu(Al[u * h + k] + ar_, slope) - mx);
         den += p;
-        const float* x = Ht + u * hf + (u64)k * f;
+        const T* x = Ht + u * hf + (u64)k * f;
         for (int j = 0; j < f; ++j) o[(u64)k * f + j] += p * x[j];
       }
-      if (off[v] == off[v + 1]) { mx = 0.f; den = 0.f; }
-      const float inv = den > 0.f ? 1.f / den : 0.f;
+      if (off[v] == off[v + 1]) { mx = T(0); den = T(0); }
+      const T inv = den > T(0) ? T(1) / den : T(0);
       for (int j = 0; j < f; ++j) o[(u64)k * f + j] *= inv;
       m[v * h + k] = mx;
       d[v * h + k] = den;
@@ -319,30 +325,29 @@ void orc_gat_region_fwd_f32_omp(u64 V, const u64* off, const u32* src, const flo
   }
 }
 
-// Backward, f32, two passes without atomics:
+// Backward, two passes without atomics:
 //  pass 1 (csr_dst, per v):  c[v] = sum alpha*dalpha ; dAr[v] = sum dz
 //  pass 2 (csc_src, per u):  dAl[u] = sum dz ; dHt[u] = sum alpha * dOut[v]  (+ LP terms)
-void orc_gat_region_bwd_f32_omp(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst,
-                                const float* Ht, const float* Al, const float* Ar, const float* al,
-                                const float* ar, int h, int f, float slope, const float* m, const float* d,
-                                const float* dOut, float* dHt, float* dAl, float* dAr, float* c, float* dal,
-                                float* dar) {
+template <typename T>
+void gat_region_bwd_omp(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst, const T* Ht,
+                        const T* Al, const T* Ar, const T* al, const T* ar, int h, int f, T slope, const T* m,
+                        const T* d, const T* dOut, T* dHt, T* dAl, T* dAr, T* c, T* dal, T* dar) {
   const u64 hf = (u64)h * f;
 #pragma omp parallel for schedule(dynamic, 64)
   for (i64 vv = 0; vv < (i64)V; ++vv) {
     const u64 v = (u64)vv;
     for (int k = 0; k < h; ++k) {
-      float cc = 0.f, P = 0.f, Q = 0.f;
-      const float inv = d[v * h + k] > 0.f ? 1.f / d[v * h + k] : 0.f;
-      const float* g = dOut + v * hf + (u64)k * f;
+      T cc = T(0), P = T(0), Q = T(0);
+      const T inv = d[v * h + k] > T(0) ? T(1) / d[v * h + k] : T(0);
+      const T* g = dOut + v * hf + (u64)k * f;
       for (u64 i = doff[v]; i < doff[v + 1]; ++i) {
         const u64 u = dsrc[i];
-        const float z = Al[u * h + k] + Ar[v * h + k];
-        const float a = std::exp(lrelu(z, slope) - m[v * h + k]) * inv;
-        const float* x = Ht + u * hf + (u64)k * f;
-        float da = 0.f;
+        const T z = Al[u * h + k] + Ar[v * h + k];
+        const T a = std::exp(lrelu(z, slope) - m[v * h + k]) * inv;
+        const T* x = Ht + u * hf + (u64)k * f;
+        T da = T(0);
         for (int j = 0; j < f; ++j) da += g[j] * x[j];
-        const float ga = lrelu_grad(z, slope) * a;
+        const T ga = lrelu_grad(z, slope) * a;
         cc += a * da;
         P += ga * da;
         Q += ga;
@@ -354,18 +359,18 @@ void orc_gat_region_bwd_f32_omp(u64 V, const u64* doff, const u32* dsrc, const u
 #pragma omp parallel for schedule(dynamic, 64)
   for (i64 uu = 0; uu < (i64)V; ++uu) {
     const u64 u = (u64)uu;
-    float* o = dHt + u * hf;
-    for (u64 j = 0; j < hf; ++j) o[j] = 0.f;
+    T* o = dHt + u * hf;
+    for (u64 j = 0; j < hf; ++j) o[j] = T(0);
     for (int k = 0; k < h; ++k) {
-      float sdz = 0.f;
-      const float* x = Ht + u * hf + (u64)k * f;
+      T sdz = T(0);
+      const T* x = Ht + u * hf + (u64)k * f;
       for (u64 i = soff[u]; i < soff[u + 1]; ++i) {
         const u64 v = sdst[i];
-        const float z = Al[u * h + k] + Ar[v * h + k];
-        const float inv = d[v * h + k] > 0.f ? 1.f / d[v * h + k] : 0.f;
-        const float a = std::exp(lrelu(z, slope) - m[v * h + k]) * inv;
-        const float* g = dOut + v * hf + (u64)k * f;
-        float da = 0.f;
+        const T z = Al[u * h + k] + Ar[v * h + k];
+        const T inv = d[v * h + k] > T(0) ? T(1) / d[v * h + k] : T(0);
+        const T a = std::exp(lrelu(z, slope) - m[v * h + k]) * inv;
+        const T* g = dOut + v * hf + (u64)k * f;
+        T da = T(0);
         for (int j = 0; j < f; ++j) da += g[j] * x[j];
         sdz += lrelu_grad(z, slope) * a * (da - c[v * h + k]);
         for (int j = 0; j < f; ++j) o[(u64)k * f + j] += a * g[j];
@@ -376,36 +381,71 @@ void orc_gat_region_bwd_f32_omp(u64 V, const u64* doff, const u32* dsrc, const u
       for (int j = 0; j < f; ++j)
         o[(u64)k * f + j] += dAl[u * h + k] * al[(u64)k * f + j] + dAr[u * h + k] * ar[(u64)k * f + j];
   }
-  for (u64 j = 0; j < hf; ++j) { dal[j] = 0.f; dar[j] = 0.f; }
-  for (u64 v = 0; v < V; ++v)
-    for (int k = 0; k < h; ++k)
-      for (int j = 0; j < f; ++j) {
-        dal[(u64)k * f + j] += dAl[v * h + k] * Ht[v * hf + (u64)k * f + j];
-        dar[(u64)k * f + j] += dAr[v * h + k] * Ht[v * hf + (u64)k * f + j];
-      }
+  // da_l[k,j] = sum_v dAl[v,k] Ht[v,k,j]: columns in parallel, rows in order (deterministic)
+#pragma omp parallel for schedule(static)
+  for (i64 jj = 0; jj < (i64)hf; ++jj) {
+    const u64 j = (u64)jj, k = j / (u64)f;
+    T sl = T(0), sr = T(0);
+    for (u64 v = 0; v < V; ++v) {
+      sl += dAl[v * h + k] * Ht[v * hf + j];
+      sr += dAr[v * h + k] * Ht[v * hf + j];
+    }
+    dal[j] = sl;
+    dar[j] = sr;
+  }
 }
 
-void orc_gat_layer_fwd_f32_omp(u64 V, const u64* off, const u32* src, u64 Fin, const float* H, const float* W,
-                               const float* al, const float* ar, int h, int f, float slope, float* Ht, float* Al,
-                               float* Ar, float* out, float* m, float* d) {
+template <typename T>
+void gat_layer_fwd_omp(u64 V, const u64* off, const u32* src, u64 Fin, const T* H, const T* W, const T* al,
+                       const T* ar, int h, int f, T slope, T* Ht, T* Al, T* Ar, T* out, T* m, T* d) {
   const u64 hf = (u64)h * f;
   mm_nn(V, Fin, hf, H, W, Ht);
   attn_dots(V, h, f, Ht, al, Al);
   attn_dots(V, h, f, Ht, ar, Ar);
-  orc_gat_region_fwd_f32_omp(V, off, src, Ht, Al, Ar, h, f, slope, out, m, d);
+  gat_region_fwd_omp(V, off, src, Ht, Al, Ar, h, f, slope, out, m, d);
 }
 
-void orc_gat_layer_bwd_f32_omp(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst, u64 Fin,
-                               const float* H, const float* W, const float* al, const float* ar, int h, int f,
-                               float slope, const float* Ht, const float* Al, const float* Ar, const float* m,
-                               const float* d, const float* dOut, float* dH, float* dW, float* dal, float* dar,
-                               float* dHt, float* dAl, float* dAr, float* c) {
+template <typename T>
+void gat_layer_bwd_omp(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst, u64 Fin,
+                       const T* H, const T* W, const T* al, const T* ar, int h, int f, T slope, const T* Ht,
+                       const T* Al, const T* Ar, const T* m, const T* d, const T* dOut, T* dH, T* dW, T* dal, T* dar,
+                       T* dHt, T* dAl, T* dAr, T* c) {
   const u64 hf = (u64)h * f;
-  orc_gat_region_bwd_f32_omp(V, doff, dsrc, soff, sdst, Ht, Al, Ar, al, ar, h, f, slope, m, d, dOut, dHt, dAl, dAr,
-                             c, dal, dar);
+  gat_region_bwd_omp(V, doff, dsrc, soff, sdst, Ht, Al, Ar, al, ar, h, f, slope, m, d, dOut, dHt, dAl, dAr, c, dal,
+                     dar);
   mm_tn(V, Fin, hf, H, dHt, dW);
   if (dH) mm_nt(V, hf, Fin, dHt, W, dH);
 }
+}  // namespace
+extern "C" {
+
+#define ORC_GAT_OMP(SUF, T)                                                                                          \
+  void orc_gat_region_fwd_##SUF(u64 V, const u64* off, const u32* src, const T* Ht, const T* Al, const T* Ar, int h, \
+                                int f, T slope, T* out, T* m, T* d) {                                               \
+    gat_region_fwd_omp<T>(V, off, src, Ht, Al, Ar, h, f, slope, out, m, d);                                         \
+  }                                                                                                                  \
+  void orc_gat_region_bwd_##SUF(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst,          \
+                                const T* Ht, const T* Al, const T* Ar, const T* al, const T* ar, int h, int f,       \
+                                T slope, const T* m, const T* d, const T* dOut, T* dHt, T* dAl, T* dAr, T* c,        \
+                                T* dal, T* dar) {                                                                    \
+    gat_region_bwd_omp<T>(V, doff, dsrc, soff, sdst, Ht, Al, Ar, al, ar, h, f, slope, m, d, dOut, dHt, dAl, dAr, c,  \
+                          dal, dar);                                                                                 \
+  }                                                                                                                  \
+  void orc_gat_layer_fwd_##SUF(u64 V, const u64* off, const u32* src, u64 Fin, const T* H, const T* W, const T* al,  \
+                               const T* ar, int h, int f, T slope, T* Ht, T* Al, T* Ar, T* out, T* m, T* d) {        \
+    gat_layer_fwd_omp<T>(V, off, src, Fin, H, W, al, ar, h, f, slope, Ht, Al, Ar, out, m, d);                       \
+  }                                                                                                                  \
+  void orc_gat_layer_bwd_##SUF(u64 V, const u64* doff, const u32* dsrc, const u64* soff, const u32* sdst, u64 Fin,  \
+                               const T* H, const T* W, const T* al, const T* ar, int h, int f, T slope, const T* Ht, \
+                               const T* Al, const T* Ar, const T* m, const T* d, const T* dOut, T* dH, T* dW,       \
+                               T* dal, T* dar, T* dHt, T* dAl, T* dAr, T* c) {                                       \
+    gat_layer_bwd_omp<T>(V, doff, dsrc, soff, sdst, Fin, H, W, al, ar, h, f, slope, Ht, Al, Ar, m, d, dOut, dH, dW,  \
+                         dal, dar, dHt, dAl, dAr, c);                                                                \
+  }
+
+ORC_GAT_OMP(f32_omp, float)
+ORC_GAT_OMP(f64_omp, double)
+#undef ORC_GAT_OMP
 
 // ---------------------------------------------------------------------------
 // EdgeConv (reorganized per SPEC.md:261):

@@ -264,30 +264,55 @@ def gat_layer_bwd_f64(g: HostGraph, H, W, al, ar, h, f, fwd, dOut, need_dH=True,
     return dict(dH=dH, dW=dW, dal=dal, dar=dar, dHt=dHt, dAl=dAl, dAr=dAr)
 
 
-def gat_layer_fwd_f32_omp(g: HostGraph, H, W, al, ar, h, f, slope=0.2):
+def _omp_suffix(dtype):
+    dt = np.dtype(dtype)
+    if dt == np.float32:
+        return np.float32, "f32_omp", f32
+    if dt == np.float64:
+        return np.float64, "f64_omp", f64
+    raise ValueError(f"unsupported dtype {dtype}")
+
+
+def gat_layer_fwd_omp(g: HostGraph, H, W, al, ar, h, f, slope=0.2, dtype=np.float64):
+    """The SPEC executor's forward (vertex_balanced OpenMP, stash m, d): f32 = the timed CPU
+    baseline, f64 = the parity oracle at benchmark scale (oracle.cpp gat_layer_fwd_omp)."""
+    dt, suf, cs = _omp_suffix(dtype)
     V = g.V
-    H, W, al, ar = (_c(x, np.float32) for x in (H, W, al, ar))
+    H, W, al, ar = (_c(x, dt) for x in (H, W, al, ar))
     Fin = H.shape[1]
-    z = lambda *s: np.zeros(s, np.float32)  # noqa: E731
+    z = lambda *s: np.zeros(s, dt)  # noqa: E731
     Ht, Al, Ar, out, m, d = z(V, h * f), z(V, h), z(V, h), z(V, h * f), z(V, h), z(V, h)
-    lib().orc_gat_layer_fwd_f32_omp(u64(V), _p(g.dst_off), _p(g.dst_src), u64(Fin), _p(H), _p(W), _p(al), _p(ar),
-                                    i32(h), i32(f), f32(slope), _p(Ht), _p(Al), _p(Ar), _p(out), _p(m), _p(d))
+    getattr(lib(), "orc_gat_layer_fwd_" + suf)(u64(V), _p(g.dst_off), _p(g.dst_src), u64(Fin), _p(H), _p(W), _p(al),
+                                               _p(ar), i32(h), i32(f), cs(slope), _p(Ht), _p(Al), _p(Ar), _p(out),
+                                               _p(m), _p(d))
     return dict(Ht=Ht, Al=Al, Ar=Ar, out=out, m=m, d=d)
 
 
-def gat_layer_bwd_f32_omp(g: HostGraph, H, W, al, ar, h, f, fwd, dOut, need_dH=True, slope=0.2):
+def gat_layer_bwd_omp(g: HostGraph, H, W, al, ar, h, f, fwd, dOut, need_dH=True, slope=0.2, dtype=np.float64):
+    """Two-pass recompute backward (csr_dst then csc_src, no atomics) of gat_layer_fwd_omp."""
+    dt, suf, cs = _omp_suffix(dtype)
     V = g.V
-    H, W, al, ar, dOut = (_c(x, np.float32) for x in (H, W, al, ar, dOut))
+    H, W, al, ar, dOut = (_c(x, dt) for x in (H, W, al, ar, dOut))
+    fw = {k: _c(fwd[k], dt) for k in ("Ht", "Al", "Ar", "m", "d")}
     Fin = H.shape[1]
-    z = lambda *s: np.zeros(s, np.float32)  # noqa: E731
+    z = lambda *s: np.zeros(s, dt)  # noqa: E731
     dH = z(V, Fin) if need_dH else None
     dW, dal, dar = z(Fin, h * f), z(h, f), z(h, f)
     dHt, dAl, dAr, c = z(V, h * f), z(V, h), z(V, h), z(V, h)
-    lib().orc_gat_layer_bwd_f32_omp(u64(V), _p(g.dst_off), _p(g.dst_src), _p(g.src_off), _p(g.src_dst), u64(Fin),
-                                    _p(H), _p(W), _p(al), _p(ar), i32(h), i32(f), f32(slope), _p(fwd["Ht"]),
-                                    _p(fwd["Al"]), _p(fwd["Ar"]), _p(fwd["m"]), _p(fwd["d"]), _p(dOut), _p(dH), _p(dW),
-                                    _p(dal), _p(dar), _p(dHt), _p(dAl), _p(dAr), _p(c))
+    getattr(lib(), "orc_gat_layer_bwd_" + suf)(u64(V), _p(g.dst_off), _p(g.dst_src), _p(g.src_off), _p(g.src_dst),
+                                               u64(Fin), _p(H), _p(W), _p(al), _p(ar), i32(h), i32(f), cs(slope),
+                                               _p(fw["Ht"]), _p(fw["Al"]), _p(fw["Ar"]), _p(fw["m"]), _p(fw["d"]),
+                                               _p(dOut), _p(dH), _p(dW), _p(dal), _p(dar), _p(dHt), _p(dAl), _p(dAr),
+                                               _p(c))
     return dict(dH=dH, dW=dW, dal=dal, dar=dar, dHt=dHt, dAl=dAl, dAr=dAr, c=c)
+
+
+def gat_layer_fwd_f32_omp(g: HostGraph, H, W, al, ar, h, f, slope=0.2):
+    return gat_layer_fwd_omp(g, H, W, al, ar, h, f, slope, dtype=np.float32)
+
+
+def gat_layer_bwd_f32_omp(g: HostGraph, H, W, al, ar, h, f, fwd, dOut, need_dH=True, slope=0.2):
+    return gat_layer_bwd_omp(g, H, W, al, ar, h, f, fwd, dOut, need_dH, slope, dtype=np.float32)
 
 
 # ----------------------------------------------------------------------------

@@ -1,0 +1,126 @@
+"""TEST INFRASTRUCTURE ONLY -- f64 restatement of one GAT layer on SAMPLED rows.
+
+The full-graph oracle (oracle.cpp) needs the whole graph in host memory and minutes of CPU
+time at the benchmark sizes (C2: 114M edges; C5: 1B edges).  A GAT layer's value at one row
+depends only on a bounded neighbourhood, so sampled rows can be checked exactly in f64 from
+the local neighbourhood of each row:
+
+  forward, destination v   (edge-softmax RS1/RS2 PAPER.md:527-530):
+      Ht = H W ; A_l = <Ht, a_l>_k ; A_r = <Ht, a_r>_k ; s_e = LReLU(A_l[u] + A_r[v])
+      out[v] = sum_{e=(u->v)} softmax_v(s)_e Ht[u]          needs Ht on in(v) + {v}
+  backward, source u       (App. B; loss seed SPEC.md:217):
+      alpha_uv, dalpha_uv = <dOut[v], Ht[u]>_k, c[v] = sum_{u' in in(v)} alpha dalpha
+      dz_uv = LReLU'(z) alpha (dalpha - c[v])
+      dHt[u] = sum_{v in out(u)} alpha_uv dOut[v] + dA_l[u] (x) a_l + dA_r[u] (x) a_r
+      dA_l[u] = sum_{v in out(u)} dz_uv ;  dA_r[u] = sum_{u' in in(u)} dz_u'u
+      dH[u] = dHt[u] W^T                                    needs Ht on in(out(u)), in(u)
+Empty in-neighbourhood: out = 0.  Comparator: rel_err (tensor.hpp:153-156).
+
+Only tests/, __graft_entry__.smoke() and bench.py's checker leg import this module; it is
+never the thing measured.  `src` is any object with
+    in_nbrs(v) -> np.ndarray of source ids of v's in-edges (csr_dst row, edge-id order)
+    out_nbrs(u) -> np.ndarray of destination ids of u's out-edges (csc_src row)
+    rows(ids) -> np.ndarray [len(ids), F_in] of the layer input H (any float dtype)
+    dout(ids) -> np.ndarray [len(ids), h*f] of the layer's output gradient (backward only)
+"""
+from __future__ import annotations
+
+import numpy as np
+
+
+def _lrelu(z, slope):
+    return np.where(z > 0, z, slope * z)
+
+
+class _Tables:
+    """Ht / A_l / A_r in f64 on a set of rows of the layer input (sorted ids)."""
+
+    def __init__(self, src, W, a_l, a_r, h, f):
+        self.src, self.h, self.f = src, h, f
+        self.W = np.asarray(W, np.float64)
+        self.a_l = np.asarray(a_l, np.float64).reshape(h, f)
+        self.a_r = np.asarray(a_r, np.float64).reshape(h, f)
+        self.ids = np.zeros(0, np.int64)
+        self.Ht = np.zeros((0, h * f))
+
+    def need(self, ids):
+        new = np.setdiff1d(np.unique(np.asarray(ids, np.int64)), self.ids)
+        if new.size:
+            X = np.asarray(self.src.rows(new), np.float64)
+            ids = np.concatenate([self.ids, new])
+            Ht = np.concatenate([self.Ht, X @ self.W])
+            order = np.argsort(ids, kind="stable")
+            self.ids, self.Ht = ids[order], Ht[order]
+        self.Al = (self.Ht.reshape(-1, self.h, self.f) * self.a_l).sum(-1)
+        self.Ar = (self.Ht.reshape(-1, self.h, self.f) * self.a_r).sum(-1)
+
+    def idx(self, ids):
+        return np.searchsorted(self.ids, np.asarray(ids, np.int64))
+
+
+def _row_softmax(T: _Tables, v: int, U: np.ndarray, slope):
+    """alpha [len(U), h] and z of destination v's in-edges (rows of Ht indexed by U)."""
+    if U.size == 0:
+        return np.zeros((0, T.h)), np.zeros((0, T.h))
+    z = T.Al[T.idx(U)] + T.Ar[T.idx([v])[0]]
+    s = _lrelu(z, slope)
+    p = np.exp(s - s.max(0))
+    return p / p.sum(0), z
+
+
+def gat_fwd_rows(src, W, a_l, a_r, h: int, f: int, rows, slope: float = 0.2) -> np.ndarray:
+    """out[rows] in f64 ([len(rows), h*f])."""
+    T = _Tables(src, W, a_l, a_r, h, f)
+    nb = {int(v): np.asarray(src.in_nbrs(int(v)), np.int64) for v in rows}
+    T.need(np.concatenate([np.asarray(rows, np.int64)] + list(nb.values())))
+    out = np.zeros((len(rows), h * f))
+    for i, v in enumerate(rows):
+        U = nb[int(v)]
+        if U.size == 0:
+            continue
+        a, _ = _row_softmax(T, v, U, slope)
+        X = T.Ht[T.idx(U)].reshape(-1, h, f)
+        out[i] = (a[:, :, None] * X).sum(0).reshape(-1)
+    return out
+
+
+def gat_bwd_rows(src, W, a_l, a_r, h: int, f: int, rows, slope: float = 0.2):
+    """(dHt[rows], dH[rows]) in f64 for the sampled source rows."""
+    T = _Tables(src, W, a_l, a_r, h, f)
+    rows = [int(u) for u in rows]
+    outs = {u: np.asarray(src.out_nbrs(u), np.int64) for u in rows}
+    dsts = sorted(set(rows).union(*[set(o.tolist()) for o in outs.values()]))  # every v whose c[v] is needed
+    ins = {v: np.asarray(src.in_nbrs(v), np.int64) for v in dsts}
+    T.need(np.concatenate([np.asarray(dsts, np.int64)] + list(ins.values())))
+    G = {v: np.asarray(g, np.float64).reshape(h, f) for v, g in zip(dsts, src.dout(np.asarray(dsts, np.int64)))}
+    stats = {}  # v -> (alpha over in(v), z, dalpha, c)
+    for v in dsts:
+        U = ins[v]
+        a, z = _row_softmax(T, v, U, slope)
+        X = T.Ht[T.idx(U)].reshape(-1, h, f)
+        da = (X * G[v]).sum(-1)
+        stats[v] = (a, z, da, (a * da).sum(0))
+    grad = lambda z: np.where(z > 0, 1.0, slope)  # noqa: E731
+    dHt = np.zeros((len(rows), h * f))
+    for i, u in enumerate(rows):
+        acc = np.zeros((h, f))
+        dAl = np.zeros(h)
+        for v in np.unique(outs[u]):
+            a, z, da, c = stats[int(v)]
+            U = ins[int(v)]
+            for j in np.nonzero(U == u)[0]:  # every parallel edge u -> v (multigraph)
+                acc += a[j][:, None] * G[int(v)]
+                dAl += grad(z[j]) * a[j] * (da[j] - c)
+        a, z, da, c = stats[u]
+        dAr = (grad(z) * a * (da - c)).sum(0) if a.size else np.zeros(h)
+        dHt[i] = (acc + dAl[:, None] * T.a_l + dAr[:, None] * T.a_r).reshape(-1)
+    return dHt, dHt @ T.W.T
+
+
+def max_rel_err(a, b) -> float:
+    """max |a-b| / max(1,|a|,|b|) (tensor.hpp:153-156)."""
+    a = np.asarray(a, np.float64)
+    b = np.asarray(b, np.float64)
+    if a.size == 0:
+        return 0.0
+    return float((np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))).max())

@@ -83,6 +83,9 @@ _SIGS = {
     "gnncg_max_degree": ([P(Index), P(u64), vp], i32),
     "gnncg_partition_rows": ([i64, vp, i32, vp], i32),
     "gnncg_gen_chung_lu": ([i64, i64, vp, u64, vp, vp, vp], i32),
+    "gnncg_gen_chung_lu_degrees": ([i64, i64, vp, u64, vp, vp], i32),
+    "gnncg_gen_chung_lu_rows_workspace": ([i64], sz),
+    "gnncg_gen_chung_lu_rows": ([i64, i64, vp, u64, i64, i64, vp, vp, vp, sz, vp], i32),
     "gnncg_sched_build_host": ([i64, vp, i32, P(i64), P(i64), P(i64), vp, vp, vp], i32),
     "gnncg_gemm_workspace": ([i32, i32, i64, i64, i64], sz),
     "gnncg_gemm": ([i32, i32, i64, i64, i64, vp, i64, vp, i64, vp, i64, vp, sz, vp], i32),

@@ -146,6 +146,45 @@ __device__ __forceinline__ void red_add_v2(float* p, float a, float b) {
   asm volatile("red.global.add.v2.f32 [%0], {%1, %2};" ::"l"(p), "f"(a), "f"(b) : "memory");
 }
 
+// (d0, d1) = (a0 * b0 + d0, a1 * b1 + d1): one packed FFMA2 (sm_100; each half rounds exactly
+// like fmaf, so results are bitwise those of two fmaf).  A broadcast a0 == a1 compiles to the
+// scalar-operand form, so the gather kernels issue half the FMA instructions.
+__device__ __forceinline__ void ffma2(float& d0, float& d1, float a0, float a1, float b0, float b1) {
+  asm("{\n\t.reg .b64 ra, rb, rd;\n\t"
+      "mov.b64 ra, {%2, %3};\n\tmov.b64 rb, {%4, %5};\n\tmov.b64 rd, {%0, %1};\n\t"
+      "fma.rn.f32x2 rd, ra, rb, rd;\n\tmov.b64 {%0, %1}, rd;\n\t}"
+      : "+f"(d0), "+f"(d1)
+      : "f"(a0), "f"(a1), "f"(b0), "f"(b1));
+}
+
+// acc[q] = fmaf(a, x[q], acc[q]) for q < VW, as VW/2 FFMA2 (bitwise identical).
+template <int VW, typename Xs>
+__device__ __forceinline__ void axpy_vec(float a, const Xs& x, float* acc) {
+  if constexpr (VW % 2 == 0) {
+#pragma unroll
+    for (int q = 0; q < VW; q += 2) ffma2(acc[q], acc[q + 1], a, a, x[q], x[q + 1]);
+  } else {
+#pragma unroll
+    for (int q = 0; q < VW; ++q) acc[q] = fmaf(a, x[q], acc[q]);
+  }
+}
+
+// sum_q x[q] y[q] with two interleaved FFMA2 partial sums (even / odd q), then one add.
+template <int VW, typename Xs, typename Ys>
+__device__ __forceinline__ float dot_vec(const Xs& x, const Ys& y) {
+  if constexpr (VW % 2 == 0) {
+    float s0 = 0.f, s1 = 0.f;
+#pragma unroll
+    for (int q = 0; q < VW; q += 2) ffma2(s0, s1, x[q], x[q + 1], y[q], y[q + 1]);
+    return s0 + s1;
+  } else {
+    float s = 0.f;
+#pragma unroll
+    for (int q = 0; q < VW; ++q) s = fmaf(x[q], y[q], s);
+    return s;
+  }
+}
+
 // Optional attention-LP epilogue of the tensor-core GEMM (K1 of the GAT layer; gemm_tc.cu).
 struct AttnEpi {
   const float* a_l = nullptr;

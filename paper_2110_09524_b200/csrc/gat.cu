@@ -740,11 +740,13 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
       const bool valid = lane < n;
       // packed destination record {A_r | lse = m + log d | c} (gat_bwd_prep_kernel): one
       // contiguous 3h-float read per edge, and alpha = exp(s - lse) needs no divide
-      const float* rec = p.rec + (int64_t)v_cur * rec_stride(h);
+      const float4* rec = reinterpret_cast<const float4*>(p.rec + (int64_t)v_cur * rec_stride(h));
       float arv[MAXH], lse[MAXH], cv[MAXH];
-      load_heads(rec, h, arv);
-      load_heads(rec + h, h, lse);
-      load_heads(rec + 2 * h, h, cv);
+#pragma unroll
+      for (int k = 0; k < MAXH; ++k) {
+        const float4 q = k < h ? __ldg(rec + k) : make_float4(0.f, 0.f, 0.f, 0.f);
+        arv[k] = q.x; lse[k] = q.y; cv[k] = q.z;
+      }
 #pragma unroll
       for (int k = 0; k < MAXH; ++k) {
         if (k < h) {
@@ -774,13 +776,8 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
 #pragma unroll
           for (int i = 0; i < NV; ++i) {
             const float a = sm.t0[e * TS + cols.hd[i]];
-            float s = 0.f;
-#pragma unroll
-            for (int q = 0; q < VW; ++q) {
-              acc[i].x[q] = fmaf(a, gv[t][i][q], acc[i].x[q]);
-              s = fmaf(x[i].x[q], gv[t][i][q], s);
-            }
-            pd[t * NV + i] = s;
+            axpy_vec<VW>(a, gv[t][i], acc[i].x);
+            pd[t * NV + i] = dot_vec<VW>(x[i].x, gv[t][i]);
           }
         }
         if (HALVES && more) {
@@ -860,7 +857,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
 }
 
 // Fast-mode input of K4f, per destination v and head k (row-local, vertex tensors only):
-//   rec[v] = { A_r[v,k] | lse[v,k] = m[v,k] + log d[v,k] | c[v,k] = <dOut[v,k,:], out[v,k,:]> }
+//   rec[v, k] = float4 { A_r[v,k], lse[v,k] = m[v,k] + log d[v,k], c[v,k] = <dOut[v,k,:], out[v,k,:]>, 0 }
 // c = sum_e alpha_e dalpha_e by the softmax-backward identity; lse folds the stashed
 // (m, d) so that alpha_e = exp(s_e - lse).  Empty rows (d = 0) get lse = 0 (never read).
 __global__ void gat_bwd_prep_kernel(int64_t rows, int h, int f, const float* __restrict__ dOut,
@@ -886,10 +883,8 @@ __global__ void gat_bwd_prep_kernel(int64_t rows, int h, int f, const float* __r
       for (int j = 0; j < f; ++j) s = fmaf(__ldg(g + j), __ldg(o + j), s);
     }
     const float dv = __ldg(d + i);
-    float* r = rec + v * rs;
-    r[k] = __ldg(Ar + i);
-    r[h + k] = dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f;
-    r[2 * h + k] = s;
+    reinterpret_cast<float4*>(rec + v * rs)[k] =
+        make_float4(__ldg(Ar + i), dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f, s, 0.f);
   }
 }
 
@@ -919,10 +914,8 @@ __global__ void gat_bwd_prep_bf16_kernel(int64_t rows, int h, int f, const float
                              (uint32_t)__bfloat16_as_ushort(az) | ((uint32_t)__bfloat16_as_ushort(aw) << 16));
     }
     const float dv = __ldg(d + i);
-    float* r = rec + v * rs;
-    r[k] = __ldg(Ar + i);
-    r[h + k] = dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f;
-    r[2 * h + k] = s;
+    reinterpret_cast<float4*>(rec + v * rs)[k] =
+        make_float4(__ldg(Ar + i), dv > 0.f ? __ldg(m + i) + __logf(dv) : 0.f, s, 0.f);
   }
 }
 
@@ -1184,6 +1177,7 @@ template <int VW, int NV, int OCC>
 void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
   constexpr int NVAL = GatherDepth<NV, OCC>::U * NV;
   grid.x = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * (NV >= 8 ? 1 : OCC));  // persistent
+  if (OCC == 2 && launch_bwd_src_lean(p, grid.x, s)) return;  // gat_lean.cu: the shapes that fill the warp
   if constexpr (NV == 2 && NVAL == 2 * 8) {
     // paired columns (8 lanes per head, two adjacent heads per lane, h = 8): the Reddit shape
     if (pair_enabled() && pair_lanes(p.h, p.f, VW, NV) == 8 && p.h == 8) {
@@ -1210,6 +1204,7 @@ void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
       constexpr int U = GatherDepth<NV, OCC>::U;
       constexpr int MINB = NV >= 8 ? 1 : OCC;
       const unsigned g = (unsigned)std::min<int64_t>(grid.x, (int64_t)num_sms() * MINB);
+      if (OCC == 2 && launch_fwd_lean(p, g, s)) break;  // gat_lean.cu: the shapes that fill the warp
       if (p.ctr) gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB, false, true><<<g, THREADS, 0, s>>>(p);
       else gat_fwd_ovl_kernel<VW, NV, U, WARPS, MINB><<<g, THREADS, 0, s>>>(p);
       break;

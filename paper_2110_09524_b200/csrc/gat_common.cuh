@@ -28,8 +28,9 @@ struct WarpSmem {
 __host__ __device__ __forceinline__ int64_t fwd_stride(int h, int f) { return (h * f + 2 * h + 3) / 4 * 4; }
 __host__ __device__ __forceinline__ int64_t src_stride(int h, int f) { return (h * f + h + 3) / 4 * 4; }
 
-// Fast-mode destination record {A_r | lse | c}: 3h floats padded to 16 bytes.
-__host__ __device__ __forceinline__ int rec_stride(int h) { return (3 * h + 3) / 4 * 4; }
+// Fast-mode destination record: per head k the float4 {A_r[v,k], lse[v,k], c[v,k], 0}
+// (4h floats per row), so one 16-byte load gives an (edge, head) pair all it needs.
+__host__ __device__ __forceinline__ int rec_stride(int h) { return 4 * h; }
 
 struct Item {
   uint32_t row;
@@ -89,7 +90,7 @@ struct GatParams {
   const uint16_t* lp_x;  // K4f bf16 mode: bf16 Ht (the own row, as the forward aggregated it)
   float* part;  // split-row partials
   int64_t row_base, num_local;
-  const float* rec;  // fast mode: packed destination record {A_r | lse | c}, stride rec_stride(h)
+  const float* rec;  // fast mode: destination record, float4 {A_r, lse, c, 0} per head (rec_stride)
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
   unsigned* ctr;  // dynamic item fetch (DYN kernels): zeroed work counter in the workspace
   int batch;      // items taken per counter request
@@ -238,5 +239,12 @@ namespace gat {
 bool tma_fwd_supported(int h, int f);
 size_t tma_smem_bytes(int h, int f);
 int launch_fwd_tma(const GatParams& p, int* counter, cudaStream_t s);
+}  // namespace gat
+
+// Wavefront-lean K4f (gat_lean.cu): false when the shape is not one it takes.
+namespace gat {
+bool lean_supported(int h, int f);
+bool launch_bwd_src_lean(const GatParams& p, unsigned grid, cudaStream_t s);
+bool launch_fwd_lean(const GatParams& p, unsigned grid, cudaStream_t s);
 }  // namespace gat
 }  // namespace gnncg_b200

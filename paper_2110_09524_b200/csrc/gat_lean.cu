@@ -1,0 +1,463 @@
+// SPDX-License-Identifier: Apache-2.0
+//
+// K4f, wavefront-lean: the fused fast-mode GAT region backward over csc_src
+// (gnncg_gat_bwd_src_fused) for row shapes that fill the warp exactly
+// (h*f = 32*NV*VW, f/VW lanes per head, NV in {1, 2}: the Reddit shape 8 x 32 and
+// the C5 shape 8 x 16).
+//
+// Same arithmetic as gat_bwd_src_fast_kernel (gat.cu): per out-edge e = (u -> v) of
+// source u, alpha_e = exp(LReLU(A_l[u] + A_r[v]) - lse[v]), dalpha_e = <dOut[v], Ht[u]>
+// per head, dz_e = LReLU'(z) alpha_e (dalpha_e - c[v]);  dHt[u] = sum alpha dOut[v]
+// (+ LP terms), dA_l[u] = sum dz, dA_r[v] += dz (global reduction)
+// (PAPER.md:615-662 ).
+//
+// Why a second kernel: ncu on B200 (profiles/r02_k4_lsu.md) shows the previous one
+// bound by the L1 data pipe (l1tex__data_pipe_lsu_wavefronts 82% of peak), not by
+// DRAM (54%) or L2 (52%).  22 wavefronts per edge: 15.4 global (8 of them the gathered
+// 1 KB row, 6 the per-lane 96-byte destination records: 32 scattered 16-byte loads per
+// instruction cost 32 wavefronts) and 6.6 shared (one LDS per gathered row for its id,
+// one per row and vector for its weight).  This kernel keeps the row gather and cuts
+// the rest:
+//   * records are {A_r, lse, c, 0} per head (rec_stride = 4h): one 16-byte load per
+//     (edge, head) pair, lanes = pairs, so an instruction reads 32/h whole 128-byte
+//     records (4 wavefronts instead of 32), and each lane evaluates its own pair;
+//   * the softmax weights are stored R = 4/NV rows x NV heads per 16 bytes in the
+//     order the column mapping reads them: one broadcast LDS.128 per R rows;
+//   * the gathered rows' ids are read four at a time (LDS.128 broadcast);
+//   * (gate * alpha, c) per (edge, head) sit side by side: the dz stage reads one
+//     8-byte pair per output.
+#include <cfloat>
+
+#include "common.cuh"
+#include "gat_common.cuh"
+
+namespace gnncg_b200 {
+namespace gat {
+namespace {
+
+template <int CNT, int OFF>
+__device__ __forceinline__ void bfly(float* v, int lane) {
+  if constexpr (OFF >= 1) {
+    const bool up = (lane & OFF) != 0;
+#pragma unroll
+    for (int j = 0; j < CNT / 2; ++j) {
+      const float send = up ? v[j] : v[j + CNT / 2];
+      const float keep = up ? v[j + CNT / 2] : v[j];
+      v[j] = keep + __shfl_xor_sync(0xffffffffu, send, OFF);
+    }
+    bfly<CNT / 2, OFF / 2>(v, lane);
+  }
+}
+
+struct LeanSmem {
+  uint32_t nb[kWarp];          // destination ids of the current 32-edge block
+  float w[kWarp * MAXH];       // alpha, packed R rows x NV heads per float4
+  float2 tc[kWarp * MAXH];     // (LReLU'(z) alpha, c) per (edge, head), [e][k]
+  float dl[MAXH];              // dA_l[u] per head (item end)
+};
+
+// index of alpha(e, k) in LeanSmem::w: rows grouped by R = 4 / NV, heads by NV
+template <int NV, int h>
+__device__ __forceinline__ int widx(int e, int k) {
+  constexpr int R = 4 / NV;
+  return ((e / R) * (h / NV) + k / NV) * 4 + (e % R) * NV + (k % NV);
+}
+
+__device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+template <int H, int VW, int NV, int PER, int OCC, bool DYN>
+__global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParams p) {
+  constexpr int U = 8;  // rows in flight per warp
+  constexpr int R = 4 / NV;
+  constexpr int NVAL = U * NV, NOUT = NVAL / PER;
+  constexpr bool PAIR = NV == 2;  // lane's vectors in heads (2g, 2g+1): one 16-byte dA_r reduction per edge
+  static_assert(NV == 1 || NV == 2, "lean K4f: one or two vectors per lane");
+  static_assert(NVAL % PER == 0 && (!PAIR || NOUT == 2), "lean K4f: outputs per lane");
+  __shared__ __align__(16) LeanSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  LeanSmem& sm = smem[w];
+  constexpr int h = H;  // compile-time heads: the edge phase's pair indexing is shifts, not divides
+  const int f = p.f, hf = h * f;
+  const float slope = p.slope;
+  const int r = lane & (PER - 1);  // rank inside the head's lane group
+  // column mapping: PAIR -> lane owns the same VW columns of heads 2 (lane / PER) + i;
+  // NV = 1 -> columns lane * VW (head lane / PER)
+  const Cols<VW, NV> cols(lane, hf, f, PAIR ? PER : 0);
+  const int hd0 = cols.hd[0];
+  constexpr int epi = kWarp / h;  // edges per edge-phase instruction
+  const int kk = lane % h;        // edge phase: this lane's head
+  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, (unsigned)p.batch) : 0u;
+  int64_t cur = 0, cend = 0;
+  for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
+    int64_t wi;
+    if constexpr (DYN) {
+      if (cur >= cend) {
+        cur = __shfl_sync(0xffffffffu, nx, 0);
+        cend = cur + p.batch;
+        if (lane == 0) nx = atomicAdd(p.ctr, (unsigned)p.batch);
+      }
+      wi = cur++;
+      if (wi >= p.num_items) break;
+    } else {
+      wi = g * WARPS + w;
+      if (wi >= p.num_items) continue;
+    }
+    const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+    const int64_t u = it.row;
+    const float alu = __ldg(p.Al + u * h + kk);
+    Vec<VW> x[NV], acc[NV];
+    gather_row<VW, NV>(p.Ht, (uint32_t)u, hf, cols, x);
+    zero(acc);
+    float dal[NV];
+#pragma unroll
+    for (int i = 0; i < NV; ++i) dal[i] = 0.f;
+
+    const uint64_t e0 = it.e0, e1 = it.e1;
+    uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+    const float* tab = p.dOut;
+    for (uint64_t base = e0; base < e1; base += 32) {
+      const int n = (int)min((uint64_t)32, e1 - base);
+      sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
+      __syncwarp();
+      Vec<VW> gv[U][NV];
+      {  // the first half of the first row group goes out before the record loads
+        const uint4 id4 = lds_u4(sm.nb);
+        gather_row<VW, NV>(tab, id4.x, hf, cols, gv[0]);
+        gather_row<VW, NV>(tab, id4.y, hf, cols, gv[1]);
+        gather_row<VW, NV>(tab, id4.z, hf, cols, gv[2]);
+        gather_row<VW, NV>(tab, id4.w, hf, cols, gv[3]);
+      }
+      {
+        // edge phase, lanes = (edge, head) pairs: one {A_r, lse, c, 0} record load each
+        float4 q[MAXH];
+#pragma unroll
+        for (int i = 0; i < MAXH; ++i) {
+          if (i < h) {
+            const int e = i * epi + lane / h;
+            q[i] = __ldg(reinterpret_cast<const float4*>(p.rec + (int64_t)sm.nb[e] * (4 * h)) + kk);
+          }
+        }
+#pragma unroll
+        for (int i = 0; i < MAXH; ++i) {
+          if (i < h) {
+            const int e = i * epi + lane / h;
+            const float z = alu + q[i].x;
+            const float a = e < n ? __expf(lrelu(z, slope) - q[i].y) : 0.f;
+            sm.w[widx<NV, h>(e, kk)] = a;
+            sm.tc[e * h + kk] = make_float2(lrelu_grad(z, slope) * a, q[i].z);
+          }
+        }
+      }
+      __syncwarp();
+      v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+      {
+        const uint4 id4 = lds_u4(sm.nb + 4);
+        gather_row<VW, NV>(tab, id4.x, hf, cols, gv[4]);
+        gather_row<VW, NV>(tab, id4.y, hf, cols, gv[5]);
+        gather_row<VW, NV>(tab, id4.z, hf, cols, gv[6]);
+        gather_row<VW, NV>(tab, id4.w, hf, cols, gv[7]);
+      }
+      for (int j = 0;;) {
+        float pd[NVAL];
+#pragma unroll
+        for (int t = 0; t < U; t += R) {
+          const float4 wv = *reinterpret_cast<const float4*>(sm.w + (((j + t) / R) * (h / NV) + hd0 / NV) * 4);
+          const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int i = 0; i < NV; ++i) {
+              axpy_vec<VW>(wa[rr * NV + i], gv[t + rr][i].x, acc[i].x);
+              pd[(t + rr) * NV + i] = dot_vec<VW>(x[i].x, gv[t + rr][i].x);
+            }
+        }
+        bfly<NVAL, PER / 2>(pd, lane);
+        float dzp[NOUT];
+#pragma unroll
+        for (int q = 0; q < NOUT; ++q) {
+          const int idx = r * NOUT + q;
+          const int t = idx / NV, i = idx % NV;
+          const int e = j + t;
+          const int hd = hd0 + i;
+          const float2 tc = sm.tc[e * h + hd];
+          const float dz = e < n ? tc.x * (pd[q] - tc.y) : 0.f;
+#pragma unroll
+          for (int ii = 0; ii < NV; ++ii)
+            if (i == ii) dal[ii] += dz;
+          dzp[q] = dz;
+          if (!PAIR && e < n) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
+        }
+        if constexpr (PAIR) {
+          // outputs (edge j + r, heads hd0, hd0 + 1); the next two heads of the same edge
+          // are PER lanes up: even lane groups add four adjacent heads at once
+          const float o0 = __shfl_down_sync(0xffffffffu, dzp[0], PER);
+          const float o1 = __shfl_down_sync(0xffffffffu, dzp[1], PER);
+          const int e = j + r;
+          if (((lane / PER) & 1) == 0 && e < n)
+            red_add_v4(p.dAro + (int64_t)sm.nb[e] * h + hd0, make_float4(dzp[0], dzp[1], o0, o1));
+        }
+        j += U;
+        if (j >= n) break;
+#pragma unroll
+        for (int t = 0; t < U; t += 4) {
+          const uint4 id4 = lds_u4(sm.nb + j + t);
+          gather_row<VW, NV>(tab, id4.x, hf, cols, gv[t]);
+          gather_row<VW, NV>(tab, id4.y, hf, cols, gv[t + 1]);
+          gather_row<VW, NV>(tab, id4.z, hf, cols, gv[t + 2]);
+          gather_row<VW, NV>(tab, id4.w, hf, cols, gv[t + 3]);
+        }
+      }
+      __syncwarp();
+    }
+#pragma unroll
+    for (int i = 0; i < NV; ++i) {
+#pragma unroll
+      for (int o = 1; o < PER; o <<= 1) dal[i] += __shfl_xor_sync(0xffffffffu, dal[i], o);
+      if (r == 0) sm.dl[hd0 + i] = dal[i];
+    }
+    __syncwarp();
+    if (!it.split) {
+      if (lane < h) p.dAl[u * h + lane] = sm.dl[lane];
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float dl = sm.dl[cols.hd[i]];
+        const Vec<VW> al = ldg_vec<VW>(p.a_l + cols.col[i]);
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = fmaf(dl, al.x[q], acc[i].x[q]);
+        st_vec<VW>(p.dHt + u * hf + cols.col[i], o);
+      }
+    } else {
+      float* part = p.part + wi * src_stride(h, f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) st_vec<VW>(part + cols.col[i], acc[i]);
+      if (lane < h) part[hf + lane] = sm.dl[lane];
+    }
+    __syncwarp();
+  }  // work items
+}
+
+// ---------------------------------------------------------------------------
+// K2, wavefront-lean: the fused forward region (Scatter(u_add_v) -> LeakyReLU ->
+// edge-softmax -> Aggregate, RS1/RS2 PAPER.md:527-530) for the same
+// shapes.  ncu on the previous kernel (gat_fwd_ovl_kernel): l1tex data pipe 90% of peak,
+// half of it shared-memory wavefronts (8.3 per edge: an id LDS per gathered row, a weight
+// LDS per row and vector, 4-way conflicting logit reads, per-lane exp-sum tables) plus
+// 1.5 per edge of max-reduction shuffles.  Here the edge phase runs on (edge, head)
+// pairs: each lane keeps one head, so the block max is a local max plus log2(32/h)
+// shuffles, the exp-sum stays in a register, and the weights go to the packed table.
+// ---------------------------------------------------------------------------
+struct LeanFwdSmem {
+  uint32_t nb[kWarp];     // source ids of the block (idle lanes: the last valid id)
+  float w[kWarp * MAXH];  // exp(s - m), packed R rows x NV heads per float4
+  float sc[MAXH];         // per head: rescale of the block, then 1 / exp-sum at the end
+};
+
+template <int H, int VW, int NV, int PER, int OCC, bool DYN>
+__global__ void __launch_bounds__(THREADS, OCC) gat_fwd_lean_kernel(GatParams p) {
+  constexpr int U = 8;
+  constexpr int R = 4 / NV;
+  __shared__ __align__(16) LeanFwdSmem smem[WARPS];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  LeanFwdSmem& sm = smem[w];
+  constexpr int h = H;  // compile-time heads: the edge phase's pair indexing is shifts, not divides
+  const int f = p.f, hf = h * f;
+  const float slope = p.slope;
+  const Cols<VW, NV> cols(lane, hf, f, NV == 2 ? PER : 0);
+  const int hd0 = cols.hd[0];
+  constexpr int epi = kWarp / h;
+  const int kk = lane % h;
+  unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
+  for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
+    int64_t wi;
+    if constexpr (DYN) {
+      wi = __shfl_sync(0xffffffffu, nx, 0);
+      if (wi >= p.num_items) break;
+      if (lane == 0) nx = atomicAdd(p.ctr, 1u);
+    } else {
+      wi = g * WARPS + w;
+      if (wi >= p.num_items) continue;
+    }
+    const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+    const float arv = __ldg(p.Ar + (int64_t)it.row * h + kk);
+    float m_run = -FLT_MAX, S = 0.f;  // this lane's head kk: running max, exp-sum partial
+    Vec<VW> acc[NV];
+    zero(acc);
+    const uint64_t e0 = it.e0, e1 = it.e1;
+    uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+    for (uint64_t base = e0; base < e1; base += 32) {
+      const int n = (int)min((uint64_t)32, e1 - base);
+      const uint32_t u_last = __shfl_sync(0xffffffffu, u_cur, n - 1);
+      sm.nb[lane] = lane < n ? u_cur : u_last;  // rows past n repeat the last one (weight 0)
+      __syncwarp();
+      Vec<VW> x[U][NV];
+#pragma unroll
+      for (int t = 0; t < U; t += 4) {
+        const uint4 id4 = lds_u4(sm.nb + t);
+        gather_row<VW, NV>(p.Ht, id4.x, hf, cols, x[t]);
+        gather_row<VW, NV>(p.Ht, id4.y, hf, cols, x[t + 1]);
+        gather_row<VW, NV>(p.Ht, id4.z, hf, cols, x[t + 2]);
+        gather_row<VW, NV>(p.Ht, id4.w, hf, cols, x[t + 3]);
+      }
+      // edge phase on (edge, head) pairs: logits of this lane's head for edges i*epi + lane/h
+      float s[MAXH];
+#pragma unroll
+      for (int i = 0; i < MAXH; ++i)
+        if (i < h) s[i] = __ldg(p.Al + (int64_t)sm.nb[i * epi + lane / h] * h + kk);
+      u_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+      float mx = -FLT_MAX;
+#pragma unroll
+      for (int i = 0; i < MAXH; ++i) {
+        if (i < h) {
+          s[i] = i * epi + lane / h < n ? lrelu(s[i] + arv, slope) : -FLT_MAX;
+          mx = fmaxf(mx, s[i]);
+        }
+      }
+      for (int o = h; o < kWarp; o <<= 1) mx = fmaxf(mx, __shfl_xor_sync(0xffffffffu, mx, o));
+      const float m_new = fmaxf(m_run, mx);
+      const float sc = __expf(m_run - m_new);
+      float ps = 0.f;
+#pragma unroll
+      for (int i = 0; i < MAXH; ++i) {
+        if (i < h) {
+          const int e = i * epi + lane / h;
+          const float pk = e < n ? __expf(s[i] - m_new) : 0.f;
+          ps += pk;
+          sm.w[widx<NV, h>(e, kk)] = pk;
+        }
+      }
+      S = fmaf(S, sc, ps);
+      m_run = m_new;
+      if (lane < h) sm.sc[lane] = sc;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float c = sm.sc[cols.hd[i]];
+#pragma unroll
+        for (int q = 0; q < VW; ++q) acc[i].x[q] *= c;
+      }
+      for (int j = 0;;) {
+#pragma unroll
+        for (int t = 0; t < U; t += R) {
+          const float4 wv = *reinterpret_cast<const float4*>(sm.w + (((j + t) / R) * (h / NV) + hd0 / NV) * 4);
+          const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+          for (int rr = 0; rr < R; ++rr)
+#pragma unroll
+            for (int i = 0; i < NV; ++i)
+#pragma unroll
+              for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(wa[rr * NV + i], x[t + rr][i].x[q], acc[i].x[q]);
+        }
+        j += U;
+        if (j >= n) break;
+#pragma unroll
+        for (int t = 0; t < U; t += 4) {
+          const uint4 id4 = lds_u4(sm.nb + j + t);
+          gather_row<VW, NV>(p.Ht, id4.x, hf, cols, x[t]);
+          gather_row<VW, NV>(p.Ht, id4.y, hf, cols, x[t + 1]);
+          gather_row<VW, NV>(p.Ht, id4.z, hf, cols, x[t + 2]);
+          gather_row<VW, NV>(p.Ht, id4.w, hf, cols, x[t + 3]);
+        }
+      }
+      __syncwarp();
+    }
+    for (int o = h; o < kWarp; o <<= 1) S += __shfl_xor_sync(0xffffffffu, S, o);
+    const float mk = e0 < e1 ? m_run : 0.f;
+    if (!it.split) {
+      if (lane < h) sm.sc[lane] = S > 0.f ? 1.f / S : 0.f;
+      __syncwarp();
+#pragma unroll
+      for (int i = 0; i < NV; ++i) {
+        const float inv = sm.sc[cols.hd[i]];
+        Vec<VW> o;
+#pragma unroll
+        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
+        st_vec<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
+      }
+      if (lane < h) {
+        p.mo[(int64_t)it.row * h + lane] = mk;
+        p.dd[(int64_t)it.row * h + lane] = S;
+      }
+    } else {
+      float* part = p.part + wi * fwd_stride(h, f);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) st_vec<VW>(part + cols.col[i], acc[i]);
+      if (lane < h) {
+        part[hf + lane] = mk;
+        part[hf + h + lane] = S;
+      }
+    }
+    __syncwarp();
+  }  // work items
+}
+
+template <int VW, int NV, int PER>
+void launch_fwd(const GatParams& p, unsigned grid, cudaStream_t s) {
+  if (p.ctr) gat_fwd_lean_kernel<8, VW, NV, PER, 2, true><<<grid, THREADS, 0, s>>>(p);
+  else gat_fwd_lean_kernel<8, VW, NV, PER, 2, false><<<grid, THREADS, 0, s>>>(p);
+}
+
+template <int VW, int NV, int PER>
+void launch(const GatParams& p, unsigned grid, cudaStream_t s) {
+  if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, 2, true><<<grid, THREADS, 0, s>>>(p);
+  else gat_bwd_src_lean_kernel<8, VW, NV, PER, 2, false><<<grid, THREADS, 0, s>>>(p);
+}
+
+}  // namespace
+
+// The shapes these kernels take: 8 heads, the row fills the warp (h f = 32 NV VW with VW = 4),
+// one or two vectors per lane, f / 4 lanes per head dividing 32.
+bool lean_supported(int h, int f) {
+  if (f % 4 != 0 || h != 8) return false;  // compiled for 8 heads (the Reddit and C5 shapes)
+  const int per = f / 4, hf = h * f;
+  if (per < 1 || 32 % per != 0) return false;
+  if (hf == 128) return (8 % per) == 0;           // NV = 1: U * NV = 8 outputs over PER lanes
+  if (hf == 256) return per == 8 && h == 8;      // NV = 2: the paired mapping (8 lanes per head)
+  return false;
+}
+
+bool lean_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_GAT_LEAN");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
+bool launch_fwd_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
+  if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
+  const int hf = p.h * p.f, per = p.f / 4;
+  if (hf == 256) {
+    launch_fwd<4, 2, 8>(p, grid, s);
+  } else {
+    switch (per) {
+      case 1: launch_fwd<4, 1, 1>(p, grid, s); break;
+      case 2: launch_fwd<4, 1, 2>(p, grid, s); break;
+      case 4: launch_fwd<4, 1, 4>(p, grid, s); break;
+      case 8: launch_fwd<4, 1, 8>(p, grid, s); break;
+      default: return false;
+    }
+  }
+  return true;
+}
+
+bool launch_bwd_src_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
+  if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
+  const int hf = p.h * p.f, per = p.f / 4;
+  if (hf == 256) {
+    launch<4, 2, 8>(p, grid, s);
+  } else {
+    switch (per) {
+      case 1: launch<4, 1, 1>(p, grid, s); break;
+      case 2: launch<4, 1, 2>(p, grid, s); break;
+      case 4: launch<4, 1, 4>(p, grid, s); break;
+      case 8: launch<4, 1, 8>(p, grid, s); break;
+      default: return false;
+    }
+  }
+  return true;
+}
+
+}  // namespace gat
+}  // namespace gnncg_b200

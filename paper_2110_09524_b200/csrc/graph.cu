@@ -79,6 +79,95 @@ __global__ void chung_lu_kernel(int64_t V, int64_t E, const uint64_t* __restrict
   }
 }
 
+__device__ __forceinline__ void chung_lu_edge(int64_t V, const uint64_t* __restrict__ cdf, uint64_t total,
+                                              uint64_t seed, int64_t e, uint32_t& s, uint32_t& d) {
+  const uint64_t h0 = splitmix64(seed * 0xD1B54A32D192ED03ull + 2ull * (uint64_t)e);
+  const uint64_t h1 = splitmix64(seed * 0xD1B54A32D192ED03ull + 2ull * (uint64_t)e + 1ull);
+  d = sample_cdf(cdf, V, __umul64hi(h0, total));
+  s = sample_cdf(cdf, V, __umul64hi(h1, total));
+}
+
+// In-degree histogram of the generated edge list (the destination draw only).
+__global__ void chung_lu_degree_kernel(int64_t V, int64_t E, const uint64_t* __restrict__ cdf, uint64_t seed,
+                                       uint32_t* __restrict__ deg) {
+  const uint64_t total = cdf[V - 1];
+  for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
+    const uint64_t h0 = splitmix64(seed * 0xD1B54A32D192ED03ull + 2ull * (uint64_t)e);
+    atomicAdd(deg + sample_cdf(cdf, V, __umul64hi(h0, total)), 1u);
+  }
+}
+
+// Edges of one destination row block, in edge-id order (a rank's in-edges): tiles of
+// kGenTile edges; pass 0 counts the kept edges of each tile, pass 1 (after an exclusive
+// scan of the counts) writes them at the tile's offset in warp-ballot order.
+constexpr int kGenTile = 4096;
+
+template <bool WRITE>
+__global__ void __launch_bounds__(256) chung_lu_rows_kernel(int64_t V, int64_t E, const uint64_t* __restrict__ cdf,
+                                                            uint64_t seed, uint32_t r0, uint32_t r1,
+                                                            uint64_t* __restrict__ tile_off, uint32_t* __restrict__ src,
+                                                            uint32_t* __restrict__ dst) {
+  __shared__ uint32_t wcount[8];
+  const uint64_t total = cdf[V - 1];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  const int64_t t0 = (int64_t)blockIdx.x * kGenTile;
+  uint64_t pos = WRITE ? tile_off[blockIdx.x] : 0;
+  uint32_t kept = 0;
+  for (int64_t c = 0; c < kGenTile; c += 256) {
+    const int64_t e = t0 + c + threadIdx.x;
+    uint32_t s = 0, d = 0;
+    bool keep = false;
+    if (e < E) {
+      chung_lu_edge(V, cdf, total, seed, e, s, d);
+      keep = d >= r0 && d < r1;
+    }
+    const unsigned m = __ballot_sync(0xffffffffu, keep);
+    if (lane == 0) wcount[w] = __popc(m);
+    __syncthreads();
+    if (WRITE) {
+      uint32_t before = 0;
+      for (int i = 0; i < w; ++i) before += wcount[i];
+      if (keep) {
+        const uint64_t at = pos + before + __popc(m & ((1u << lane) - 1u));
+        src[at] = s;
+        dst[at] = d;
+      }
+    }
+    uint32_t all = 0;
+    for (int i = 0; i < 8; ++i) all += wcount[i];
+    pos += all;
+    kept += all;
+    __syncthreads();
+  }
+  if (!WRITE && threadIdx.x == 0) tile_off[blockIdx.x] = kept;
+}
+
+__global__ void exclusive_scan_serial_kernel(int64_t n, uint64_t* __restrict__ v) {
+  // one thread block: n is E / 4096 (244K at 1B edges)
+  __shared__ uint64_t part[1024];
+  const int64_t per = ceil_div(n, (int64_t)blockDim.x);
+  const int64_t b = threadIdx.x * per, e = min(n, b + per);
+  uint64_t s = 0;
+  for (int64_t i = b; i < e; ++i) s += v[i];
+  part[threadIdx.x] = s;
+  __syncthreads();
+  if (threadIdx.x == 0) {
+    uint64_t run = 0;
+    for (int i = 0; i < (int)blockDim.x; ++i) {
+      const uint64_t t = part[i];
+      part[i] = run;
+      run += t;
+    }
+  }
+  __syncthreads();
+  uint64_t run = part[threadIdx.x];
+  for (int64_t i = b; i < e; ++i) {
+    const uint64_t t = v[i];
+    v[i] = run;
+    run += t;
+  }
+}
+
 int grid_for(int64_t n, int threads = 256) {
   int64_t g = ceil_div(n > 0 ? n : 1, threads);
   return (int)(g > 148 * 64 ? 148 * 64 : g);
@@ -157,6 +246,48 @@ int gnncg_max_degree(const gnncg_index_t* idx, uint64_t* out_host, void* stream)
   GNNCG_CUDA_TRY(cudaFreeAsync(d, s));
   GNNCG_CUDA_TRY(cudaStreamSynchronize(s));
   *out_host = (uint64_t)h;
+  return GNNCG_OK;
+}
+
+int gnncg_gen_chung_lu_degrees(int64_t V, int64_t E, const uint64_t* cdf, uint64_t seed, uint32_t* in_deg,
+                               void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(V > 0 && E >= 0 && cdf && in_deg, GNNCG_ERR_ARG, "gen_chung_lu_degrees: bad argument");
+  cudaStream_t s = as_stream(stream);
+  GNNCG_CUDA_TRY(cudaMemsetAsync(in_deg, 0, sizeof(uint32_t) * (size_t)V, s));
+  if (E == 0) return GNNCG_OK;
+  chung_lu_degree_kernel<<<grid_for(E), 256, 0, s>>>(V, E, cdf, seed, in_deg);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+size_t gnncg_gen_chung_lu_rows_workspace(int64_t E) {
+  return align_up((size_t)ceil_div(E > 0 ? E : 1, kGenTile) * sizeof(uint64_t));
+}
+
+int gnncg_gen_chung_lu_rows(int64_t V, int64_t E, const uint64_t* cdf, uint64_t seed, int64_t row_begin,
+                            int64_t row_end, uint32_t* src, uint32_t* dst, void* workspace, size_t workspace_bytes,
+                            void* stream) {
+  GNNCG_DEVICE_GUARD();
+  GNNCG_REQUIRE(V > 0 && E >= 0 && cdf && 0 <= row_begin && row_begin <= row_end && row_end <= V, GNNCG_ERR_ARG,
+                "gen_chung_lu_rows: bad argument");
+  if (E == 0 || row_begin == row_end) return GNNCG_OK;
+  GNNCG_REQUIRE(src && dst, GNNCG_ERR_ARG, "gen_chung_lu_rows: null output");
+  const size_t need = gnncg_gen_chung_lu_rows_workspace(E);
+  GNNCG_REQUIRE(workspace && workspace_bytes >= need, GNNCG_ERR_WORKSPACE, "gen_chung_lu_rows: workspace %zu < %zu",
+                workspace_bytes, need);
+  cudaStream_t s = as_stream(stream);
+  const int64_t tiles = ceil_div(E, kGenTile);
+  GNNCG_REQUIRE(tiles < (int64_t)INT32_MAX, GNNCG_ERR_RANGE, "gen_chung_lu_rows: too many edges");
+  uint64_t* tile_off = static_cast<uint64_t*>(workspace);
+  chung_lu_rows_kernel<false><<<(unsigned)tiles, 256, 0, s>>>(V, E, cdf, seed, (uint32_t)row_begin, (uint32_t)row_end,
+                                                              tile_off, nullptr, nullptr);
+  GNNCG_LAUNCH_CHECK();
+  exclusive_scan_serial_kernel<<<1, 1024, 0, s>>>(tiles, tile_off);
+  GNNCG_LAUNCH_CHECK();
+  chung_lu_rows_kernel<true><<<(unsigned)tiles, 256, 0, s>>>(V, E, cdf, seed, (uint32_t)row_begin, (uint32_t)row_end,
+                                                             tile_off, src, dst);
+  GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }
 

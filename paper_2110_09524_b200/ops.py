@@ -320,7 +320,7 @@ def gat_region_backward(g: DeviceGraph, stash: GatStash, a_l, a_r, dOut, p: GatP
             with PROBE("gat_bwd_prep"):
                 call("gnncg_gat_bwd_prep", V, h, f, _ptr(dOut), _ptr(stash.out), _ptr(stash.Ar), _ptr(stash.m),
                      _ptr(stash.d), _ptr(rec), s)
-        c = rec[:, 2 * h:3 * h]
+        c = rec.view(V, h, 4)[:, :, 2]  # record = float4 {A_r, lse, c, 0} per head
         if lp:
             with PROBE("gat_bwd_src_fused"):
                 call("gnncg_gat_bwd_src_fused_bf16", g.csc_src.struct(), ss.struct(), h, f, p.slope, 0, V,

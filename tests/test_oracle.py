@@ -307,6 +307,27 @@ def test_f32_baseline_matches_f64_oracle():
         assert O.max_rel_err(f32b[k], bw[k]) < 1e-4, k
 
 
+def test_f64_omp_oracle_matches_serial_f64():
+    """The scale-parity oracle (recompute two-pass, OpenMP, f64) against the serial
+    stash-everything f64 derivation, on skewed graphs with empty rows and hub rows."""
+    rng = np.random.default_rng(11)
+    for V, E, Fin, h, f in ((300, 5000, 20, 8, 4), (64, 2000, 7, 3, 5), (50, 0, 4, 2, 2)):
+        src = rng.integers(0, V, E)
+        dst = np.minimum(rng.zipf(1.6, E) - 1, V - 1) if E else rng.integers(0, V, E)  # hub destinations
+        g = O.host_graph(V, src, dst)
+        H = rng.uniform(-1, 1, (V, Fin))
+        W, al, ar = rng.uniform(-0.3, 0.3, (Fin, h * f)), rng.uniform(-0.5, 0.5, (h, f)), rng.uniform(-0.5, 0.5, (h, f))
+        dOut = rng.uniform(-1, 1, (V, h * f))
+        fw = O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)
+        bw = O.gat_layer_bwd_f64(g, H, W, al, ar, h, f, fw, dOut)
+        fo = O.gat_layer_fwd_omp(g, H, W, al, ar, h, f)
+        bo = O.gat_layer_bwd_omp(g, H, W, al, ar, h, f, fo, dOut)
+        for k in ("out", "m", "d"):
+            assert O.max_rel_err(fo[k], fw[k]) < 1e-11, k
+        for k in ("dH", "dW", "dal", "dar", "dAl", "dAr"):
+            assert O.max_rel_err(bo[k], bw[k]) < 1e-10, k
+
+
 def test_cost_module_matches_spec_and_oracle():
     from paper_2110_09524_b200 import cost
 
@@ -364,3 +385,39 @@ def test_gcn_finite_differences(graph):
     bw = O.gcn_layer_bwd_f64(g, H, W, fw, ones, w)
     loss = lambda: O.gcn_layer_fwd_f64(g, H, W, b, w)["out"].sum()  # noqa: E731
     _fd_check(loss, [W, b, H], [bw["dW"], bw["db"], bw["dH"]])
+
+
+def test_sampled_rows_oracle_matches_full_f64():
+    """oracle/sampled.py (local-neighbourhood f64 restatement used at C2/C5 scale) against the
+    full-graph f64 oracle, on a skewed multigraph with empty rows and parallel edges."""
+    from oracle import sampled as S
+
+    rng = np.random.default_rng(3)
+    V, E, Fin, h, f = 200, 3000, 12, 4, 3
+    src = rng.integers(0, V, E)
+    dst = np.minimum(rng.zipf(1.5, E) - 1, V - 1)
+    g = O.host_graph(V, src, dst)
+    H = rng.uniform(-1, 1, (V, Fin))
+    W, al, ar = rng.uniform(-0.3, 0.3, (Fin, h * f)), rng.uniform(-0.5, 0.5, (h, f)), rng.uniform(-0.5, 0.5, (h, f))
+    dOut = rng.uniform(-1, 1, (V, h * f))
+    fw = O.gat_layer_fwd_f64(g, H, W, al, ar, h, f)
+    bw = O.gat_layer_bwd_f64(g, H, W, al, ar, h, f, fw, dOut)
+
+    class Src:
+        def in_nbrs(self, v):
+            return g.dst_src[g.dst_off[v]:g.dst_off[v + 1]]
+
+        def out_nbrs(self, u):
+            return g.src_dst[g.src_off[u]:g.src_off[u + 1]]
+
+        def rows(self, ids):
+            return H[ids]
+
+        def dout(self, ids):
+            return dOut[ids]
+
+    rows = [0, 1, 5, 17, 150, 199]  # 0: hub; 199: no in-edges (empty row)
+    assert np.abs(S.gat_fwd_rows(Src(), W, al, ar, h, f, rows) - fw["out"][rows]).max() < 1e-12
+    dHt, dH = S.gat_bwd_rows(Src(), W, al, ar, h, f, rows)
+    assert np.abs(dHt - bw["dHt"][rows]).max() < 1e-12
+    assert np.abs(dH - bw["dH"][rows]).max() < 1e-12
