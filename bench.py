@@ -10,15 +10,26 @@ loss (sum of exits) + backward with recomputation + SGD update.
   value  = E * layers * steps / device time of the K timed steps (inputs resident in HBM)
   e2e    = the same metric through the public API with HOST buffers: every step copies the
            features host->device (pinned) and reads loss + parameter gradients back
-  roofline  -> the dominant fused kernel: algorithmic bytes per launch / its CUDA-event
-               time inside the timed region, vs MEASURED_PEAKS.json hbm_gbs
-  cpu_baseline -> the oracle's f32 OpenMP port of the spec executor on a bounded sample
+  roofline  -> the dominant fused kernel: DRAM bytes per launch (ncu, captured in this run
+               by a one-launch replay of the same configuration) / its CUDA-event time
+               inside the timed region, vs MEASURED_PEAKS.json hbm_gbs; the per-edge
+               algorithmic byte rate is reported beside it as l2_gather_rate
+  memory -> peak device memory of one training step (allocator high-water mark), the part
+               above the resident graph / parameters / inputs, and the O(|E|) stash the
+               recompute design avoids
+  parity -> sampled rows of the benchmarked model's own outputs and input gradients against
+               the f64 restatement (oracle/sampled.py; the checker, never the measured path)
+  cpu_baseline -> the reference arm's measurement on this box (full C2 graph) when present,
+               else the oracle's f32 OpenMP port on a bounded sample
 
-Multi-GPU (torchrun, N > 1): weak scaling -- the graph grows with N (V*N, E*N), destination
-rows are partitioned into N edge-balanced blocks (gnncg_partition_rows), every rank
-all-gathers the transformed features each layer over NCCL (paper_2110_09524_b200.dist).
+Multi-GPU (--gpus N; spawns N ranks itself when not launched by torchrun): destination rows
+are partitioned into N edge-balanced blocks (gnncg_partition_rows), each rank generates only
+its own in-edges (gnncg_gen_chung_lu_rows) and all-gathers the transformed features each
+layer over NCCL (paper_2110_09524_b200.dist).  --config reddit scales weakly (V*N, E*N);
+--config c5 is the fixed 10M-vertex / 1B-edge graph (strong scaling, BASELINE configs[4]).
 
-`--impl reference` times the CPU port of the reference path (oracle/) on the host cores.
+`--impl reference` times the CPU port of the reference path (oracle/) on the host cores on
+the full C2 graph (a few steps) and leaves its result for the GPU arm's cpu_baseline.
 """
 from __future__ import annotations
 
@@ -57,6 +68,9 @@ def parse():
                     help="replay the step as a CUDA graph (auto: on for the small, launch-bound configs)")
     ap.add_argument("--config", default="reddit", choices=["reddit", "cora", "edgeconv20", "edgeconv40", "monet", "c5", "gcn"],
                     help="reddit = the headline (BASELINE configs[1]); the others are configs[0,2,3,4]")
+    ap.add_argument("--no-ncu", action="store_true", help="skip the one-launch ncu DRAM-byte capture")
+    ap.add_argument("--no-parity", action="store_true", help="skip the sampled-row f64 parity check")
+    ap.add_argument("--ncu-probe", action="store_true", help=argparse.SUPPRESS)  # the ncu child run
     return ap.parse_args()
 
 
@@ -146,11 +160,14 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
             V, E, offset, dims = 10_000_000, 1_000_000_000, 10_000, [(128, 8, 16)] * 3
             desc = "GAT 3-layer fwd+bwd+SGD, power-law 10M nodes / 1B edges, 128-dim (BASELINE configs[4])"
         V, E, offset = int(V * args.scale), int(E * args.scale), max(1, int(offset * args.scale))
+        # c5 is one fixed graph at every N (strong scaling); reddit grows with N (weak scaling)
+        strong = cfg == "c5"
+        if not strong:
+            V, E, offset = V * world, E * world, offset * world
         if dmode:
             from paper_2110_09524_b200.dist import PartitionedGAT, partitioned_chung_lu
 
-            lg = partitioned_chung_lu(V * world, E * world, offset=offset * world, seed=0, rank=rank, world=world,
-                                      device=dev)
+            lg = partitioned_chung_lu(V, E, offset=offset, seed=0, rank=rank, world=world, device=dev)
             model = PartitionedGAT(lg, dims, seed=1, chunk=args.chunk)
             V_loc, E_loc = lg.num_local, int(lg.csr.num_edges)
         else:
@@ -160,13 +177,14 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
         h, f = dims[0][1], dims[0][2]
         from paper_2110_09524_b200.cost import gat_layer_report
 
-        wl_cost = {"per_layer": gat_layer_report(V * world, E * world, h, f), "source": "SPEC.md:282-289"}
-        wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E * world, cost=wl_cost,
+        wl_cost = {"per_layer": gat_layer_report(V, E, h, f), "source": "SPEC.md:282-289"}
+        wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E, cost=wl_cost,
                   layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f, 2 if args.gather == "bf16" else 4),
-                  config={"workload": desc, "V": V * world, "E": E * world, "layers": len(dims),
+                  scaling="strong" if strong else "weak", gat=(V_loc, E_loc, h, f),
+                  config={"workload": desc, "V": V, "E": E, "layers": len(dims),
                           "gather": args.gather,
                           "dims": ", ".join(f"{a}->{b}x{c}" for a, b, c in dims),
-                          "graph": f"Chung-Lu w_i=2^40/(i+{offset * world}), seed 0",
+                          "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0",
                           "l2": "inputs larger than L2 (features and index exceed 126 MB)"})
     elif cfg == "cora":
         V, E, dims = 2708, 10556, [(1433, 8, 8)]
@@ -265,17 +283,40 @@ class ClockSampler:
 
 
 # ----------------------------------------------------------------------------- CPU arms
-def cpu_sample_step(scale: int = CPU_SCALE, steps: int = 3, warmup: int = 1):
-    """The oracle's f32 OpenMP port (vertex_balanced, recompute backward)
-    on the Reddit-shaped generator scaled by 1/scale.  Returns (GTEPS, seconds/step, info)."""
+CPU_RESULT = os.path.join(ROOT, "baseline", "cpu_baseline.json")  # reference arm -> GPU arm (same box)
+
+
+def host_info() -> dict:
+    """What the CPU numbers ran on: logical CPUs, the ones this process may use, the model."""
+    model = ""
+    try:
+        with open("/proc/cpuinfo") as fh:
+            for line in fh:
+                if line.startswith("model name"):
+                    model = line.split(":", 1)[1].strip()
+                    break
+    except OSError:
+        pass
+    try:
+        usable = len(os.sched_getaffinity(0))
+    except AttributeError:
+        usable = os.cpu_count()
+    return {"nproc": os.cpu_count(), "usable_cpus": usable, "cpu_model": model}
+
+
+def cpu_step_runner(scale: int):
+    """The oracle's f32 OpenMP port (vertex_balanced, recompute backward) of
+    the C2 step on the Reddit-shaped generator with V, E (and the Zipf offset) divided by
+    `scale` (1 = the full benchmark graph).  Returns (step(), info)."""
     import numpy as np
 
     from oracle import oracle as O
-    from paper_2110_09524_b200.graph import chung_lu_edges_host
 
     V, E = REDDIT["V"] // scale, REDDIT["E"] // scale
-    src, dst = chung_lu_edges_host(V, E, max(1, REDDIT["offset"] // scale), 0)
+    t0 = time.perf_counter()
+    src, dst = O.gen_chung_lu(V, E, max(1, REDDIT["offset"] // scale), 0)
     g = O.host_graph(V, src, dst)
+    del src, dst
     rng = np.random.default_rng(0)
     H = rng.uniform(-1, 1, (V, REDDIT["dims"][0][0])).astype(np.float32)
     params = []
@@ -284,6 +325,7 @@ def cpu_sample_step(scale: int = CPU_SCALE, steps: int = 3, warmup: int = 1):
         params.append((rng.uniform(-s, s, (fin, h * f)).astype(np.float32),
                        rng.uniform(-1 / np.sqrt(f), 1 / np.sqrt(f), (h, f)).astype(np.float32),
                        rng.uniform(-1 / np.sqrt(f), 1 / np.sqrt(f), (h, f)).astype(np.float32), h, f))
+    setup_s = time.perf_counter() - t0
 
     def step():
         xs, fws = [H], []
@@ -299,6 +341,15 @@ def cpu_sample_step(scale: int = CPU_SCALE, steps: int = 3, warmup: int = 1):
             for p_, dp in ((W, bw["dW"]), (al, bw["dal"]), (ar, bw["dar"])):
                 p_ -= np.float32(1e-4) * dp  # SGD, as in the GPU step
 
+    what = "the full C2 graph" if scale == 1 else f"Reddit-shaped Chung-Lu scaled 1/{scale}"
+    info = dict(V=V, E=E, cores=O.num_threads(), setup_s=setup_s, scale=scale,
+                sample=f"{what}: V={V}, E={E} (mean in-degree {E / V:.0f}), dims 602->8x32->8x32, "
+                       "2-layer fwd+bwd+SGD, f32 OpenMP port of the spec executor (oracle/oracle.cpp)")
+    return step, info
+
+
+def cpu_time(scale: int, steps: int, warmup: int):
+    step, info = cpu_step_runner(scale)
     for _ in range(warmup):
         step()
     t0 = time.perf_counter()
@@ -306,36 +357,148 @@ def cpu_sample_step(scale: int = CPU_SCALE, steps: int = 3, warmup: int = 1):
         step()
     dt = (time.perf_counter() - t0) / steps
     layers = len(REDDIT["dims"])
-    info = dict(V=V, E=E, cores=O.num_threads(),
-                sample=f"Reddit-shaped Chung-Lu scaled 1/{scale}: V={V}, E={E} (mean in-degree {E / V:.0f}), "
-                       f"dims 602->8x32->8x32, 2-layer fwd+bwd+SGD, f32, {steps} timed steps")
-    return layers * E / dt / 1e9, dt, info
+    info["sample"] += f", {steps} timed step(s) after {warmup} warm-up"
+    return layers * info["E"] / dt / 1e9, dt, info
 
 
 def run_reference(args):
+    """The reference's path on this box's host cores: the CPU port of the spec executor
+    (the reference ships no layer code to install) on the FULL C2 graph --
+    the bench config itself, so the ratio the driver computes is like for like.  A C2 step
+    takes tens of seconds on the CPU, so at most 2 timed steps after at most 1 warm-up are
+    run whatever --steps / --warmup ask (a few minutes in total)."""
     rank = int(os.environ.get("RANK", "0"))
     if rank != 0:
         return
-    gteps, dt, info = cpu_sample_step(steps=args.steps, warmup=args.warmup)
+    steps, warmup = max(1, min(args.steps, 2)), min(args.warmup, 1)
+    gteps, dt, info = cpu_time(1, steps, warmup)
+    hi = host_info()
+    cpu = {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port", "sample": info["sample"],
+           "s_per_step": dt, **hi}
     line = {"impl": "reference", "metric": METRIC, "value": gteps, "unit": UNIT, "n_gpus": args.gpus,
-            "steps": args.steps, "warmup": args.warmup, "ms_per_step": dt * 1e3, "higher_is_better": True,
-            "scaling": "weak", "vs_baseline": None, "dtype": "f32", "data": "synthetic",
-            "config": {"workload": "GAT 2-layer fwd+bwd, Reddit-shaped (configs[1]) -- CPU port on a bounded sample",
-                       "V": info["V"], "E": info["E"], "layers": 2, "dims": "602->8x32, 256->8x32"},
-            "cpu_baseline": {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port",
-                             "sample": info["sample"]},
+            "steps": steps, "warmup": warmup, "steps_requested": args.steps, "warmup_requested": args.warmup,
+            "ms_per_step": dt * 1e3, "higher_is_better": True, "scaling": "weak", "vs_baseline": None,
+            "dtype": "f32", "data": "synthetic",
+            "config": {"workload": "GAT 2-layer fwd+bwd+SGD, Reddit-shaped (BASELINE configs[1]) -- CPU port",
+                       "V": info["V"], "E": info["E"], "layers": 2, "dims": "602->8x32, 256->8x32",
+                       "graph": f"Chung-Lu w_i=2^40/(i+{REDDIT['offset']}), seed 0", "same_config": True,
+                       "graph_build_s": info["setup_s"]},
+            "cpu_baseline": cpu,
             "e2e": {"value": gteps, "unit": UNIT, "h2d_bytes_per_step": 0, "d2h_bytes_per_step": 0}}
+    try:
+        os.makedirs(os.path.dirname(CPU_RESULT), exist_ok=True)
+        with open(CPU_RESULT, "w") as fh:
+            json.dump({**cpu, "config": "reddit", "when": time.time()}, fh)
+    except OSError:
+        pass
     print(json.dumps(line), flush=True)
 
 
+def cpu_baseline_for_gpu_arm() -> dict:
+    """The reference arm's full-C2 measurement from this box when it ran in the last hour,
+    else a bounded 1/50 sample of the same generator (~20 s)."""
+    try:
+        with open(CPU_RESULT) as fh:
+            d = json.load(fh)
+        if d.get("config") == "reddit" and time.time() - float(d.get("when", 0)) < 3600:
+            d = dict(d)
+            d.pop("when", None)
+            d["source"] = "this box's --impl reference run (baseline/cpu_baseline.json)"
+            return d
+    except (OSError, ValueError):
+        pass
+    gteps, dt, info = cpu_time(CPU_SCALE, steps=3, warmup=1)
+    return {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port", "sample": info["sample"],
+            "s_per_step": dt, "source": "measured in this run (bounded sample)", **host_info()}
+
+
+# ----------------------------------------------------------------------------- ncu leg
+NCU_METRICS = "dram__bytes_read.sum,dram__bytes_write.sum,gpu__time_duration.sum"
+KERNEL_REGEX = {"gat_fwd": "gat_fwd", "gat_bwd_src_fused": "gat_bwd_src_(lean|fast)",
+                "gat_bwd_src": "gat_bwd_src_kernel", "gat_bwd_dst": "gat_bwd_dst"}
+
+
+def ncu_dram_bytes(args, kernel: str):
+    """DRAM bytes of one launch of `kernel` in this configuration, from an ncu replay of a
+    one-step child run (the second launch: a warm one).  Returns (bytes, ncu_ms, note)."""
+    import csv
+    import io
+    import shutil
+    import tempfile
+
+    ncu = shutil.which("ncu") or "/usr/local/cuda/bin/ncu"
+    if not os.path.exists(ncu):
+        return None, None, "ncu not found"
+    regex = KERNEL_REGEX.get(kernel, kernel)
+    with tempfile.TemporaryDirectory() as td:
+        log = os.path.join(td, "ncu.csv")
+        cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", f"regex:{regex}", "-s", "1", "-c", "1",
+               "--csv", "--log-file", log, sys.executable, os.path.abspath(__file__), "--steps", "1", "--warmup", "0",
+               "--config", args.config, "--gather", args.gather, "--no-cpu-baseline", "--no-e2e", "--no-ncu",
+               "--no-parity", "--ncu-probe"]
+        if args.chunk:
+            cmd += ["--chunk", str(args.chunk)]
+        try:
+            subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=600, check=False,
+                           env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
+            with open(log) as fh:
+                text = fh.read()
+        except (OSError, subprocess.TimeoutExpired) as e:
+            return None, None, f"ncu capture failed: {e}"
+    rows = [r for r in csv.reader(io.StringIO(text[text.find('"ID"'):])) if r]
+    if len(rows) < 2:
+        return None, None, "ncu capture produced no rows"
+    hdr = rows[0]
+    mi, ui, vi = hdr.index("Metric Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
+    scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
+             "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}
+    vals = {}
+    for r in rows[1:]:
+        try:
+            vals[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+        except (ValueError, IndexError):
+            continue
+    if "dram__bytes_read.sum" not in vals:
+        return None, None, "ncu capture lacks dram__bytes"
+    return (vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0), vals.get("gpu__time_duration.sum"),
+            f"ncu --metrics {NCU_METRICS} on one warm launch (regex {regex}) of a child run of this config")
+
+
 # ----------------------------------------------------------------------------- GPU arm
+def memory_block(model, H, lr, wl) -> dict:
+    """Peak device memory of one training step (torch's allocator holds every buffer the
+    library uses: it allocates nothing itself).  `resident` = graph, parameters, inputs and
+    workspaces before the step; `step_working` = the peak above that.  For GAT also the
+    vertex-only stash the forward keeps for the backward and the O(|E| h) stash a
+    fusion+stash plan would keep instead (cost.gat_stash_units)."""
+    import torch
+
+    torch.cuda.synchronize()
+    resident = torch.cuda.memory_allocated()
+    torch.cuda.reset_peak_memory_stats()
+    model.train_step(H, lr=lr)
+    torch.cuda.synchronize()
+    peak = torch.cuda.max_memory_allocated()
+    free, total = torch.cuda.mem_get_info()
+    out = {"peak_allocated_gb": peak / 1e9, "resident_gb": resident / 1e9, "step_working_gb": (peak - resident) / 1e9,
+           "device_used_gb": (total - free) / 1e9, "device_total_gb": total / 1e9,
+           "method": "torch.cuda.max_memory_allocated over one train_step (the library allocates nothing)"}
+    if "gat" in wl:
+        V, E, h, f = wl["gat"]
+        L = wl["layers"]
+        # per layer: Ht, out (V x hf) + A_l, A_r, m, d (V x h), fp32
+        out["stash_vertex_gb"] = L * V * (2 * h * f + 4 * h) * 4 / 1e9
+        out["stash_edge_avoided_gb"] = L * 2 * E * h * 4 / 1e9  # scores + weights per edge and head
+        out["paper_reddit_gb"] = {"ours_rtx3090": 3.88, "dgl": 13.7, "fusegnn": 9.89,
+                                  "note": "PAPER.md:406-407, 2 layers x 128 hidden x 1 head: context only"}
+    return out
+
+
 def run_ours(args):
     import torch
     import torch.distributed as dist
 
     from paper_2110_09524_b200 import _lib
-    from paper_2110_09524_b200.graph import DeviceGraph
-    from paper_2110_09524_b200.models import GAT
     from paper_2110_09524_b200.ops import PROBE
 
     world = int(os.environ.get("WORLD_SIZE", "1"))
@@ -344,10 +507,16 @@ def run_ours(args):
     torch.cuda.set_device(local)
     dev = torch.device("cuda", local)
     dmode = world > 1 or args.partitioned  # the row-partitioned NCCL path
+    comm = None
     if dmode:
         os.environ.setdefault("MASTER_ADDR", "127.0.0.1")
         os.environ.setdefault("MASTER_PORT", "29533")
         dist.init_process_group("nccl", device_id=dev, rank=rank, world_size=world)
+        t = torch.ones(1, device=dev)
+        dist.all_reduce(t)  # communicator up (NCCL_DEBUG=INFO logs comm_nranks on stderr)
+        nv = torch.cuda.nccl.version()
+        comm = {"backend": "nccl", "nranks": dist.get_world_size(), "ranks_counted": int(t.item()),
+                "nccl_version": ".".join(map(str, nv)) if isinstance(nv, tuple) else str(nv)}
     wl = build_workload(args, dev, world, rank)
     model, H_buf, fin, E_total, layers = wl["model"], wl["H_buf"], wl["fin"], wl["E_total"], wl["layers"]
     H = H_buf[:, :fin]
@@ -371,6 +540,10 @@ def run_ours(args):
         for _ in range(args.warmup):
             step()
     barrier()
+    if args.ncu_probe:  # child of ncu_dram_bytes: the warm-up step above was the profiled work
+        step()
+        torch.cuda.synchronize()
+        return
     launches0 = _lib.lib().gnncg_launch_count()
     clocks = ClockSampler(local)
     clocks.start()
@@ -401,43 +574,17 @@ def run_ours(args):
     ms_step = ms / args.steps
     value = E_total * layers * args.steps / (ms / 1e3) / 1e9
 
-    # --- per-kernel roofline (rank 0's graph; bytes summed over the layers) -----------
+    # --- per-kernel times and algorithmic byte rates (rank 0's graph) -------------------
     peak, peak_src = measured_peaks()
     per_launch = wl["bytes"]
     kernels = {}
     for name, (tot_ms, cnt) in sorted(totals.items()):
         k = {"ms_per_launch": tot_ms / max(cnt, 1), "launches": cnt, "share_of_step": tot_ms / ms}
         if name in per_launch:
-            k["bytes_per_launch"] = per_launch[name]
-            k["GBps"] = per_launch[name] / (k["ms_per_launch"] / 1e3) / 1e9
-            k["frac"] = k["GBps"] / peak
+            k["algorithmic_bytes_per_launch"] = per_launch[name]
+            k["l2_gather_rate_GBps"] = per_launch[name] / (k["ms_per_launch"] / 1e3) / 1e9
         kernels[name] = k
     dominant = max((n for n in kernels if n in per_launch), key=lambda n: kernels[n]["share_of_step"])
-    traffic = None
-    headline = args.config == "reddit" and not dmode and args.gather == "fp32"  # what profiles/ captured
-    tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
-    if headline and os.path.exists(tpath):
-        with open(tpath) as fh:
-            traffic = json.load(fh).get(dominant)
-    roofline = {"bound": "hbm", "kernel": dominant, "achieved": kernels[dominant]["GBps"], "peak": peak,
-                "unit": "GB/s", "frac": kernels[dominant]["frac"], "traffic": traffic, "peak_source": peak_src}
-    if traffic:
-        # the algorithmic model counts every gathered row; hub rows are served from L2, so also
-        # report the DRAM bytes ncu measured for this kernel over its live launch time
-        dram = traffic / (kernels[dominant]["ms_per_launch"] / 1e3) / 1e9
-        roofline.update({"dram_achieved": dram, "dram_frac": dram / peak,
-                         "note": "achieved = algorithmic bytes (SURVEY §8d per-edge-gather model, DESIGN.md §4); "
-                                 "traffic = ncu dram__bytes per launch (profiles/ncu_traffic.json)"})
-    cpath = os.path.join(ROOT, "profiles", "r01_gather_ceiling.json")
-    if headline and os.path.exists(cpath):
-        # the L2-served gather ceiling measured on this B200 for the same Zipf row stream
-        with open(cpath) as fh:
-            ceil = json.load(fh)["GBps_16warps_8rows"]
-        roofline.update({"gather_ceiling": ceil, "gather_frac": kernels[dominant]["GBps"] / ceil,
-                         "gather_ceiling_source": "profiles/r01_gather_ceiling.json (scripts/gather_bench2.cu)"})
-        for n in ("gat_fwd", "gat_bwd_src_fused"):
-            if n in kernels and "GBps" in kernels[n]:
-                kernels[n]["gather_frac"] = kernels[n]["GBps"] / ceil
 
     # --- end-to-end through the public API with host buffers ----------------------------
     e2e = None
@@ -487,35 +634,104 @@ def run_ours(args):
         e2e = {"value": E_total * layers * args.steps / (ems / 1e3) / 1e9, "unit": UNIT,
                "h2d_bytes_per_step": H_host.numel() * 4, "d2h_bytes_per_step": sum(b.numel() * 4 for b in out_bufs),
                "ms_per_step": ems / args.steps}
+        del bufs
 
-    cpu = None
-    if rank == 0 and world == 1 and not args.no_cpu_baseline and args.config == "reddit":
-        gteps, dt, info = cpu_sample_step()
-        cpu = {"value": gteps, "unit": UNIT, "cores": info["cores"], "kind": "port", "sample": info["sample"],
-               "s_per_step": dt}
+    mem = memory_block(model, H, 0.0, wl)
+
+    # --- roofline: DRAM bytes of the dominant kernel (ncu, this configuration) ----------
+    traffic, ncu_ms, tnote = (None, None, "skipped (--no-ncu)")
+    single = rank == 0 and world == 1 and not dmode
+    if single and not args.no_ncu:
+        traffic, ncu_ms, tnote = ncu_dram_bytes(args, dominant)
+    if traffic is None and args.config == "reddit" and args.gather == "fp32":
+        tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
+        if os.path.exists(tpath):
+            with open(tpath) as fh:
+                traffic = json.load(fh).get(dominant)
+            tnote += "; fell back to the committed profiles/ncu_traffic.json"
+    k = kernels[dominant]
+    t_live = k["ms_per_launch"] / 1e3
+    roofline = {"bound": "hbm", "kernel": dominant, "unit": "GB/s", "peak": peak, "peak_source": peak_src,
+                "traffic": traffic, "traffic_source": tnote}
+    if traffic:
+        achieved = traffic / t_live / 1e9
+        roofline.update({"achieved": achieved, "frac": achieved / peak,
+                         "achieved_def": "ncu DRAM bytes (read + write) per launch / CUDA-event time per launch "
+                                         "inside the timed region"})
+        if ncu_ms:
+            roofline["ncu_launch_ms"] = ncu_ms
+    else:
+        roofline.update({"achieved": None, "frac": None})
+    # the per-edge-gather byte model counts L2 and L1 hits: a gather rate, not DRAM
+    roofline["algorithmic_bytes"] = per_launch[dominant]
+    roofline["l2_gather_rate_GBps"] = per_launch[dominant] / t_live / 1e9
+    cpath = os.path.join(ROOT, "profiles", "r01_gather_ceiling.json")
+    if args.config == "reddit" and args.gather == "fp32" and os.path.exists(cpath):
+        with open(cpath) as fh:
+            ceil = json.load(fh)["GBps_16warps_8rows"]
+        roofline.update({"gather_ceiling_GBps": ceil, "gather_frac": roofline["l2_gather_rate_GBps"] / ceil,
+                         "gather_ceiling_source": "profiles/r01_gather_ceiling.json (scripts/gather_bench2.cu)"})
+
+    # --- checker leg (oracle/: never the measured path) ---------------------------------
+    cpu = parity = None
+    if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
+        from oracle.sampled import gat_model_sampled_check
+
+        t0 = time.perf_counter()
+        parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0)
+        errs = parity["max_rel_err"].values()
+        parity.update({"comparator": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
+                       "bound": 1e-4, "pass": all(e < 1e-4 for e in errs),
+                       "max_rel_err_out": max(parity["max_rel_err"].get("out_layer1", 0),
+                                              parity["max_rel_err"].get("out_last", 0)),
+                       "max_rel_err_grads": parity["max_rel_err"].get("dH_last"),
+                       "oracle": "oracle/sampled.py: f64 local-neighbourhood restatement on the GPU model's own "
+                                 "layer inputs (one extra fwd+bwd after the timed steps)",
+                       "check_s": time.perf_counter() - t0})
+    if single and not args.no_cpu_baseline and args.config == "reddit":
+        cpu = cpu_baseline_for_gpu_arm()
 
     if rank == 0:
         line = {"metric": METRIC, "value": value, "unit": UNIT, "n_gpus": world, "steps": args.steps,
-                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": "weak",
+                "warmup": args.warmup, "ms_per_step": ms_step, "higher_is_better": True, "scaling": wl.get("scaling",
+                                                                                                          "weak"),
                 "vs_baseline": None, "dtype": "f32" if args.gather == "fp32" else "f32 (bf16 gather tables)",
-                "data": "synthetic (Chung-Lu graph, uniform features, "
-                "random-init weights)",
+                "data": "synthetic (Chung-Lu graph, uniform features, random-init weights)",
                 "config": {**wl["config"], "parallelism": f"row-partition x{world}" if dmode else "single GPU",
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
-                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e,
-                "cost_model": wl.get("cost"),
+                "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "memory": mem,
+                "parity": parity, "cost_model": wl.get("cost"), "comm": comm,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     if dmode:
         dist.destroy_process_group()
 
 
+def spawn_ranks(args) -> int:
+    """`bench.py --gpus N` outside torchrun: launch N ranks (one process per GPU) through
+    torch.distributed.run on 127.0.0.1 and return their exit code."""
+    import random
+
+    port = 29500 + random.Random(os.getpid()).randint(0, 2000)
+    env = dict(os.environ)
+    env.setdefault("NCCL_DEBUG", "INFO")
+    env.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    cmd = [sys.executable, "-m", "torch.distributed.run", "--nnodes=1", f"--nproc-per-node={args.gpus}",
+           "--master-addr", "127.0.0.1", "--master-port", str(port), os.path.abspath(__file__), *sys.argv[1:]]
+    return subprocess.run(cmd, env=env).returncode
+
+
 def main():
     args = parse()
     if args.impl == "reference":
         run_reference(args)
-    else:
-        run_ours(args)
+        return
+    if args.gpus > 1 and "WORLD_SIZE" not in os.environ:
+        sys.exit(spawn_ranks(args))
+    if int(os.environ.get("WORLD_SIZE", "1")) > 1:
+        os.environ.setdefault("NCCL_DEBUG", "INFO")
+        os.environ.setdefault("NCCL_DEBUG_SUBSYS", "INIT")
+    run_ours(args)
 
 
 if __name__ == "__main__":

@@ -711,6 +711,35 @@ u64 orc_gat_attn_flops_reorg(u64 V, u64 E, u64 f) { return 4 * V * f + 2 * E; }
 u64 orc_gat_io_unfused(u64 V, u64 E, u64 h, u64 f) { return V * h * f + 7 * E * h + 3 * E * h * f; }
 u64 orc_gat_io_fused(u64 V, u64 E, u64 h, u64 f) { return V * h * f + 5 * E * h + 2 * E * h * f; }
 
+// ---------------------------------------------------------------------------
+// Chung-Lu generator restated on the host (OpenMP): the same counter-based draws as the
+// device's gnncg_gen_chung_lu and graph.py:chung_lu_edges_host (test / CPU-arm input
+// only; the full C2 graph for bench.py --impl reference).
+// ---------------------------------------------------------------------------
+static inline u64 orc_splitmix64(u64 x) {
+  x += 0x9E3779B97F4A7C15ull;
+  x = (x ^ (x >> 30)) * 0xBF58476D1CE4E5B9ull;
+  x = (x ^ (x >> 27)) * 0x94D049BB133111EBull;
+  return x ^ (x >> 31);
+}
+
+static inline u32 orc_sample_cdf(const u64* cdf, u64 V, u64 r) {
+  // smallest i with cdf[i] > r
+  return (u32)(std::upper_bound(cdf, cdf + V, r) - cdf);
+}
+
+void orc_gen_chung_lu(u64 V, u64 E, const u64* cdf, u64 seed, u32* src, u32* dst) {
+  const u64 total = cdf[V - 1];
+#pragma omp parallel for schedule(static)
+  for (i64 ee = 0; ee < (i64)E; ++ee) {
+    const u64 e = (u64)ee;
+    const u64 h0 = orc_splitmix64(seed * 0xD1B54A32D192ED03ull + 2ull * e);
+    const u64 h1 = orc_splitmix64(seed * 0xD1B54A32D192ED03ull + 2ull * e + 1ull);
+    dst[e] = orc_sample_cdf(cdf, V, (u64)(((unsigned __int128)h0 * total) >> 64));
+    src[e] = orc_sample_cdf(cdf, V, (u64)(((unsigned __int128)h1 * total) >> 64));
+  }
+}
+
 int orc_num_threads(void) {
 #ifdef _OPENMP
   return omp_get_max_threads();

@@ -446,5 +446,16 @@ def cost_counts(V, E, h, f):
                 io_fused=L.orc_gat_io_fused(u64(V), u64(E), u64(h), u64(f)))
 
 
+def gen_chung_lu(V: int, E: int, offset: int, seed: int):
+    """Host restatement of gnncg_gen_chung_lu (OpenMP): (src, dst) uint32, bit-identical to the
+    device generator and to graph.py:chung_lu_edges_host."""
+    i = np.arange(V, dtype=np.uint64)
+    cdf = np.cumsum(np.uint64(1 << 40) // (i + np.uint64(offset)), dtype=np.uint64)
+    src = np.zeros(E, np.uint32)
+    dst = np.zeros(E, np.uint32)
+    lib().orc_gen_chung_lu(u64(V), u64(E), _p(cdf), u64(seed), _p(src), _p(dst))
+    return src, dst
+
+
 def num_threads() -> int:
     return int(lib().orc_num_threads())

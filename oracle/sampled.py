@@ -124,3 +124,94 @@ def max_rel_err(a, b) -> float:
     if a.size == 0:
         return 0.0
     return float((np.abs(a - b) / np.maximum(1.0, np.maximum(np.abs(a), np.abs(b)))).max())
+
+
+# ---------------------------------------------------------------------------
+# Device-backed row sources and the model-level sampled check (tests/ and bench.py's
+# checker leg): the GPU model's own layer inputs and outputs, fetched row by row.
+# ---------------------------------------------------------------------------
+class DeviceRows:
+    """`src` for gat_fwd_rows / gat_bwd_rows over a DeviceGraph-like pair of indexes
+    (csr_dst, csc_src with .off / .nbr device tensors) and device tensors H (layer input)
+    and dOut (layer output gradient; None = all ones, the loss seed of SPEC.md:217)."""
+
+    def __init__(self, csr, csc, H, dOut=None, hf=None):
+        import torch
+
+        self.torch = torch
+        self.csr, self.csc, self.H, self.dOut, self.hf = csr, csc, H, dOut, hf
+        self.doff = csr.off.cpu().numpy().view(np.uint64)
+        self.soff = csc.off.cpu().numpy().view(np.uint64)
+
+    def _slice(self, idx, off, i):
+        a, b = int(off[i]), int(off[i + 1])
+        return idx.nbr[a:b].cpu().numpy().view(np.uint32).astype(np.int64)
+
+    def in_nbrs(self, v):
+        return self._slice(self.csr, self.doff, int(v))
+
+    def out_nbrs(self, u):
+        return self._slice(self.csc, self.soff, int(u))
+
+    def _rows(self, T, ids):
+        t = self.torch
+        ids = t.as_tensor(np.asarray(ids, np.int64), device=T.device)
+        return T.index_select(0, ids).double().cpu().numpy()
+
+    def rows(self, ids):
+        return self._rows(self.H, ids)
+
+    def dout(self, ids):
+        if self.dOut is None:
+            return np.ones((len(ids), self.hf))
+        return self._rows(self.dOut, ids)
+
+
+def gat_model_sampled_check(model, H, n_rows: int = 16, n_src: int = 4, seed: int = 0, dOut=None,
+                            hub_src: bool = True) -> dict:
+    """Sampled-row f64 parity of a models.GAT-like stack (layers with W, a_l, a_r, p.heads, p.f,
+    p.slope; graph model.g with csr_dst / csc_src): one forward + backward on the device through
+    the model's own path, then
+      * out rows of the first and the last layer (destinations: the two largest in-degree
+        rows -- split into edge-balance chunks -- the smallest, and random rows),
+      * dH rows of the last layer's backward (its input gradient; sources: the largest
+        out-degree row and random rows),
+    each against the f64 local-neighbourhood restatement above, with the GPU's own layer
+    input as the input.  Comparator: rel_err (tensor.hpp:153-156)."""
+    import torch
+
+    g = model.g
+    V = g.num_vertices
+    xs, stashes = model.forward(H)
+    seed_grad = model.seed_grad(xs[-1]) if dOut is None else dOut
+    grads = model.backward(xs, stashes, seed_grad)
+    torch.cuda.synchronize()
+    rng = np.random.default_rng(seed)
+    din = np.diff(g.csr_dst.off.cpu().numpy().view(np.uint64).astype(np.int64))
+    dout_deg = np.diff(g.csc_src.off.cpu().numpy().view(np.uint64).astype(np.int64))
+    top = np.argsort(-din, kind="stable")[:2]
+    rows = np.unique(np.concatenate([top, [int(np.argmin(din))], rng.integers(0, V, max(0, n_rows - 3))]))
+    hub = [int(np.argmax(dout_deg))] if hub_src else []
+    srcs = np.unique(np.concatenate([hub, rng.integers(0, V, max(0, n_src - len(hub)))]).astype(np.int64))
+    res = {"rows_checked": {}, "max_rel_err": {}}
+    for name, li in (("out_layer1", 0), ("out_last", len(model.layers) - 1)):
+        L = model.layers[li]
+        src = DeviceRows(g.csr_dst, g.csc_src, xs[li])
+        ref = gat_fwd_rows(src, L.W.double().cpu().numpy(), L.a_l.double().cpu().numpy(),
+                           L.a_r.double().cpu().numpy(), L.p.heads, L.p.f, rows, L.p.slope)
+        got = xs[li + 1].index_select(0, torch.as_tensor(rows, device=H.device)).double().cpu().numpy()
+        res["max_rel_err"][name] = max_rel_err(got, ref)
+        res["rows_checked"][name] = int(rows.size)
+    L = model.layers[-1]
+    dO = None if dOut is None else dOut
+    src = DeviceRows(g.csr_dst, g.csc_src, xs[-2], dO, hf=L.p.heads * L.p.f)
+    _, dH = gat_bwd_rows(src, L.W.double().cpu().numpy(), L.a_l.double().cpu().numpy(), L.a_r.double().cpu().numpy(),
+                         L.p.heads, L.p.f, srcs, L.p.slope)
+    gdH = grads[-1].dH
+    if gdH is not None:
+        got = gdH.index_select(0, torch.as_tensor(srcs, device=H.device)).double().cpu().numpy()
+        res["max_rel_err"]["dH_last"] = max_rel_err(got, dH)
+        res["rows_checked"]["dH_last"] = int(srcs.size)
+    res["max_in_degree_checked"] = int(din[top[0]])
+    res["max_out_degree_checked"] = int(dout_deg[srcs].max())
+    return res

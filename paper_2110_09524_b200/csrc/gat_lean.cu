@@ -52,7 +52,7 @@ __device__ __forceinline__ void bfly(float* v, int lane) {
 struct LeanSmem {
   uint32_t nb[kWarp];          // destination ids of the current 32-edge block
   float w[kWarp * MAXH];       // alpha, packed R rows x NV heads per float4
-  float2 tc[kWarp * MAXH];     // (LReLU'(z) alpha, c) per (edge, head), [e][k]
+  float2 tc[kWarp * MAXH];     // (LReLU'(z) alpha, c) per (edge, head), tcidx order
   float dl[MAXH];              // dA_l[u] per head (item end)
 };
 
@@ -61,6 +61,15 @@ template <int NV, int h>
 __device__ __forceinline__ int widx(int e, int k) {
   constexpr int R = 4 / NV;
   return ((e / R) * (h / NV) + k / NV) * 4 + (e % R) * NV + (k % NV);
+}
+
+// index of (gate * alpha, c)(e, k) in LeanSmem::tc, laid out so that the two outputs of a
+// lane in the dz stage are one conflict-free 16-byte read: NV = 2 -> heads (2g, 2g+1) of one
+// edge are adjacent; NV = 1 -> edges (2r, 2r+1) of one head are adjacent
+template <int NV, int h>
+__device__ __forceinline__ int tcidx(int e, int k) {
+  if constexpr (NV == 2) return e * h + k;
+  else return ((e >> 1) * h + k) * 2 + (e & 1);
 }
 
 __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
@@ -144,7 +153,7 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParam
             const float z = alu + q[i].x;
             const float a = e < n ? __expf(lrelu(z, slope) - q[i].y) : 0.f;
             sm.w[widx<NV, h>(e, kk)] = a;
-            sm.tc[e * h + kk] = make_float2(lrelu_grad(z, slope) * a, q[i].z);
+            sm.tc[tcidx<NV, h>(e, kk)] = make_float2(lrelu_grad(z, slope) * a, q[i].z);
           }
         }
       }
@@ -173,13 +182,16 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParam
         }
         bfly<NVAL, PER / 2>(pd, lane);
         float dzp[NOUT];
+        static_assert(NOUT == 2, "lean K4f: two dz outputs per lane (one 16-byte tc read)");
+        // outputs q = 0, 1: NV = 2 -> edge j + r, heads hd0 + q; NV = 1 -> edge j + 2r + q, head hd0
+        const float4 tc4 = *reinterpret_cast<const float4*>(sm.tc + tcidx<NV, h>(j + r * NOUT / NV, hd0));
 #pragma unroll
         for (int q = 0; q < NOUT; ++q) {
           const int idx = r * NOUT + q;
           const int t = idx / NV, i = idx % NV;
           const int e = j + t;
           const int hd = hd0 + i;
-          const float2 tc = sm.tc[e * h + hd];
+          const float2 tc = q == 0 ? make_float2(tc4.x, tc4.y) : make_float2(tc4.z, tc4.w);
           const float dz = e < n ? tc.x * (pd[q] - tc.y) : 0.f;
 #pragma unroll
           for (int ii = 0; ii < NV; ++ii)
@@ -408,12 +420,9 @@ void launch(const GatParams& p, unsigned grid, cudaStream_t s) {
 // The shapes these kernels take: 8 heads, the row fills the warp (h f = 32 NV VW with VW = 4),
 // one or two vectors per lane, f / 4 lanes per head dividing 32.
 bool lean_supported(int h, int f) {
-  if (f % 4 != 0 || h != 8) return false;  // compiled for 8 heads (the Reddit and C5 shapes)
-  const int per = f / 4, hf = h * f;
-  if (per < 1 || 32 % per != 0) return false;
-  if (hf == 128) return (8 % per) == 0;           // NV = 1: U * NV = 8 outputs over PER lanes
-  if (hf == 256) return per == 8 && h == 8;      // NV = 2: the paired mapping (8 lanes per head)
-  return false;
+  // compiled for 8 heads: f = 32 (the Reddit shape, two vectors per lane in adjacent heads)
+  // and f = 16 (the C5 shape, one vector per lane)
+  return h == 8 && (f == 32 || f == 16);
 }
 
 bool lean_enabled() {
@@ -427,35 +436,15 @@ bool lean_enabled() {
 
 bool launch_fwd_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-  const int hf = p.h * p.f, per = p.f / 4;
-  if (hf == 256) {
-    launch_fwd<4, 2, 8>(p, grid, s);
-  } else {
-    switch (per) {
-      case 1: launch_fwd<4, 1, 1>(p, grid, s); break;
-      case 2: launch_fwd<4, 1, 2>(p, grid, s); break;
-      case 4: launch_fwd<4, 1, 4>(p, grid, s); break;
-      case 8: launch_fwd<4, 1, 8>(p, grid, s); break;
-      default: return false;
-    }
-  }
+  if (p.f == 32) launch_fwd<4, 2, 8>(p, grid, s);
+  else launch_fwd<4, 1, 4>(p, grid, s);
   return true;
 }
 
 bool launch_bwd_src_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-  const int hf = p.h * p.f, per = p.f / 4;
-  if (hf == 256) {
-    launch<4, 2, 8>(p, grid, s);
-  } else {
-    switch (per) {
-      case 1: launch<4, 1, 1>(p, grid, s); break;
-      case 2: launch<4, 1, 2>(p, grid, s); break;
-      case 4: launch<4, 1, 4>(p, grid, s); break;
-      case 8: launch<4, 1, 8>(p, grid, s); break;
-      default: return false;
-    }
-  }
+  if (p.f == 32) launch<4, 2, 8>(p, grid, s);
+  else launch<4, 1, 4>(p, grid, s);
   return true;
 }
 

@@ -317,14 +317,26 @@ class PartitionedGAT:
 
 
 def partitioned_chung_lu(V: int, E: int, *, offset: int, seed: int, rank: int, world: int, device) -> LocalGraph:
-    """Every rank generates the same global Chung-Lu edge list on its device (counter-based,
-    deterministic), partitions the destination rows and keeps only its block."""
+    """This rank's share of the Chung-Lu graph gnncg_gen_chung_lu would produce, without the
+    global edge list: the in-degree histogram gives the offsets the partitioner splits
+    (bit-exact, gnncg_partition_rows), then gnncg_gen_chung_lu_rows regenerates the edge
+    stream and keeps the rank's destination rows in edge-id order (so the local indexes
+    equal the global ones restricted to the block).  Per-rank memory is O(E / P)."""
+    L = _lib.lib()
     cdf = torch.from_numpy(chung_lu_cdf(V, offset).view(np.int64)).to(device)
-    src = torch.empty(E, dtype=torch.int32, device=device)
-    dst = torch.empty(E, dtype=torch.int32, device=device)
-    call("gnncg_gen_chung_lu", V, E, _ptr(cdf), seed, _ptr(src), _ptr(dst), _stream())
-    plan = PartitionPlan.from_dst(V, dst, world)
+    deg = torch.empty(V, dtype=torch.int32, device=device)
+    call("gnncg_gen_chung_lu_degrees", V, E, _ptr(cdf), seed, _ptr(deg), _stream())
+    off = np.zeros(V + 1, np.uint64)
+    off[1:] = np.cumsum(deg.cpu().numpy().view(np.uint32), dtype=np.uint64)
+    del deg
+    plan = PartitionPlan(partition_rows(off, world))
+    r0, r1 = int(plan.bounds[rank]), int(plan.bounds[rank + 1])
+    n = int(off[r1] - off[r0])
+    src = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    dst = torch.empty(max(n, 1), dtype=torch.int32, device=device)
+    ws = torch.empty(L.gnncg_gen_chung_lu_rows_workspace(E), dtype=torch.uint8, device=device)
+    call("gnncg_gen_chung_lu_rows", V, E, _ptr(cdf), seed, r0, r1, _ptr(src), _ptr(dst), _ptr(ws), ws.numel(),
+         _stream())
+    del ws, cdf
     engine = CudaEngine(device)
-    lg = build_local(plan, rank, src, dst, engine)
-    del src, dst
-    return lg
+    return build_local(plan, rank, src[:n], dst[:n], engine)

@@ -56,3 +56,30 @@ def test_chung_lu_is_skewed(cuda):
     mi, mean, mo = g.degree_stats()
     assert mean == 100.0 and mi > 10 * mean and mo > 10 * mean
     torch.cuda.synchronize()
+
+
+@pytest.mark.parametrize("P", [1, 3, 8])
+def test_per_rank_chung_lu_equals_filtered_global_list(cuda, P):
+    """Multi-GPU graph build: each rank's edges (gnncg_gen_chung_lu_rows) are the global edge
+    list filtered to its destination block, in edge-id order; the in-degree histogram and the
+    row bounds equal those of the global list; the local CSR is the global CSR's row block."""
+    from paper_2110_09524_b200.dist import partitioned_chung_lu
+
+    V, E, off, seed = 20000, 1_000_000, 100, 5
+    src, dst = chung_lu_edges_host(V, E, off, seed)
+    ref = O.host_graph(V, src, dst)
+    bounds = O.partition_rows(ref.dst_off, P)
+    total = 0
+    for rank in range(P):
+        lg = partitioned_chung_lu(V, E, offset=off, seed=seed, rank=rank, world=P, device=cuda)
+        np.testing.assert_array_equal(lg.plan.bounds, bounds)
+        r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
+        loff, lnbr, _ = lg.csr.to_host()
+        np.testing.assert_array_equal(loff, ref.dst_off[r0:r1 + 1] - ref.dst_off[r0])
+        # local source ids live in the padded all-gather layout: map back to global ids
+        pid = lnbr.astype(np.int64)
+        owner = pid // lg.plan.maxrows
+        gsrc = lg.plan.bounds[owner].astype(np.int64) + pid % lg.plan.maxrows
+        np.testing.assert_array_equal(gsrc, ref.dst_src[ref.dst_off[r0]:ref.dst_off[r1]])
+        total += int(loff[-1])
+    assert total == E

@@ -421,3 +421,15 @@ def test_sampled_rows_oracle_matches_full_f64():
     dHt, dH = S.gat_bwd_rows(Src(), W, al, ar, h, f, rows)
     assert np.abs(dHt - bw["dHt"][rows]).max() < 1e-12
     assert np.abs(dH - bw["dH"][rows]).max() < 1e-12
+
+
+def test_host_chung_lu_generators_agree():
+    """oracle.gen_chung_lu (C, OpenMP; the CPU arm's full C2 graph) == graph.chung_lu_edges_host
+    (numpy restatement of the device generator, itself pinned to the device in test_gpu_graph)."""
+    from paper_2110_09524_b200.graph import chung_lu_edges_host
+
+    for V, E, off, seed in ((5000, 200000, 50, 3), (233, 10000, 11, 0)):
+        s1, d1 = O.gen_chung_lu(V, E, off, seed)
+        s2, d2 = chung_lu_edges_host(V, E, off, seed)
+        np.testing.assert_array_equal(s1, s2)
+        np.testing.assert_array_equal(d1, d2)
