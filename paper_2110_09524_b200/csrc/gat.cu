@@ -1376,7 +1376,8 @@ bool dyn_enabled() { return dyn_mode() >= 1; }
 
 int attach_counter(GatParams& p, uint64_t num_edges, void* ws, size_t ws_bytes, size_t need, cudaStream_t s) {
   p.ctr = nullptr;
-  if (!dyn_enabled() || !ws || ws_bytes < align_up(need) + sizeof(unsigned)) return GNNCG_OK;
+  // no items (a rank whose block has no in-edges): nothing to fetch, and no mean to take
+  if (p.num_items <= 0 || !dyn_enabled() || !ws || ws_bytes < align_up(need) + sizeof(unsigned)) return GNNCG_OK;
   // a few items per warp of the persistent grid balance themselves (Cora: 2708 items; the
   // counter's memset cost more than it saved there)
   const uint64_t warps = (uint64_t)num_sms() * 2 * WARPS;
@@ -1384,6 +1385,9 @@ int attach_counter(GatParams& p, uint64_t num_edges, void* ws, size_t ws_bytes, 
   // K4f: about 512 edges per request (Reddit, 452 edges per item: 1; C5: 5)
   const uint64_t mean = num_edges / (uint64_t)p.num_items;
   p.batch = (int)std::max<uint64_t>(1, std::min<uint64_t>(dyn_batch_cap(), 512 / std::max<uint64_t>(mean, 1)));
+  // the counter is 32-bit and every warp makes one request past the end: keep it from
+  // wrapping (schedule item ids are u32, so this only bites near 2^32 items)
+  if ((uint64_t)p.num_items + warps * (uint64_t)p.batch >= (1ull << 32)) return GNNCG_OK;
   p.ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up(need));
   GNNCG_CUDA_TRY(cudaMemsetAsync(p.ctr, 0, sizeof(unsigned), s));
   return GNNCG_OK;

@@ -241,6 +241,9 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
     const int c = i * 32 + lane;
     if (c < Kf) dy[c] = acc[i];
   }
+  // alignment columns past K f + 2 r (rows padded to 16 bytes for the TMA GEMM): zero, so
+  // dWcat = H^T dY leaves the padding of [W | P_l | P_r] at zero
+  for (int64_t c = Kf + 2 * r + lane; c < a.ldy; c += 32) dy[c] = 0.f;
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) {
     if (t < r) {

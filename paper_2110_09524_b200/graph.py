@@ -126,7 +126,9 @@ class DeviceSched:
 
 class Workspace:
     """Grow-only device scratch shared by the calls of one graph (never allocated in a hot call
-    once warm)."""
+    once warm).  The GAT calls keep per-call state in it (split-row partials and the work
+    counter of the item fetch), so calls that may run concurrently -- on different streams --
+    need one Workspace each; calls on one stream can share it."""
 
     def __init__(self, device):
         self.device = device

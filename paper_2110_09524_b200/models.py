@@ -98,48 +98,64 @@ class GAT:
 class EdgeConvNet:
     """EdgeConv stack (the paper's DGCNN setting uses layers {64,64,128,256},
     PAPER.md:409): dims = [F0, F1, ...]; layer l maps F_l -> F_{l+1}; identity between layers,
-    loss = sum of exits, SGD."""
+    loss = sum of exits, SGD.  Each layer's Theta and Phi are the two column halves of one
+    parameter buffer [Theta | Phi], so the step runs on the library's kernels only (no
+    concatenation or slicing copies)."""
 
     def __init__(self, g: DeviceGraph, dims, seed: int = 0):
-        from .ops import edgeconv_backward, edgeconv_forward  # noqa: F401
-
         self.g = g
         dev = g.device
         gen = torch.Generator(device=dev)
         gen.manual_seed(seed)
-        self.layers = [(init_uniform(a, b, gen, dev), init_uniform(a, b, gen, dev)) for a, b in zip(dims[:-1], dims[1:])]
+        self.layers = []
+        for a, b in zip(dims[:-1], dims[1:]):
+            Th, Ph = init_uniform(a, b, gen, dev), init_uniform(a, b, gen, dev)
+            Wcat = torch.cat([Th, Ph], dim=1)  # once, at init
+            self.layers.append(Wcat)
         self.loss = torch.zeros(4, device=dev)
         self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
+        self._ones = None
+
+    @staticmethod
+    def split(Wcat):
+        """(Theta, Phi) views of a layer's [Theta | Phi]."""
+        C = Wcat.shape[1] // 2
+        return Wcat[:, :C], Wcat[:, C:]
 
     def train_step(self, H: torch.Tensor, lr: float = 0.0):
-        from .ops import edgeconv_backward, edgeconv_forward
+        from .ops import edgeconv_backward_cat, edgeconv_forward_cat
 
         xs, stashes = [H], []
-        for Th, Ph in self.layers:
-            out, st = edgeconv_forward(self.g, xs[-1], Th, Ph)
+        for Wcat in self.layers:
+            out, st = edgeconv_forward_cat(self.g, xs[-1], Wcat)
             xs.append(out)
             stashes.append(st)
         out = xs[-1]
         call("gnncg_sum", out.numel(), _ptr(out), _ptr(self.loss), _ptr(self._sum_ws), self._sum_ws.numel(), _stream())
-        g = torch.empty_like(out)
-        call("gnncg_fill", g.numel(), 1.0, _ptr(g), _stream())
+        if self._ones is None or self._ones.shape != out.shape:
+            self._ones = torch.empty_like(out)
+            call("gnncg_fill", self._ones.numel(), 1.0, _ptr(self._ones), _stream())
+        g = self._ones
         grads = [None] * len(self.layers)
         for i in reversed(range(len(self.layers))):
-            Th, Ph = self.layers[i]
-            dH, dTh, dPh = edgeconv_backward(self.g, xs[i], Th, Ph, stashes[i], g, need_dH=i > 0)
-            grads[i] = (dTh, dPh)
+            dH, dWcat = edgeconv_backward_cat(self.g, xs[i], self.layers[i], stashes[i], g, need_dH=i > 0)
+            grads[i] = self.split(dWcat)
             g = dH
-        for (Th, Ph), (dTh, dPh) in zip(self.layers, grads):
-            call("gnncg_sgd_update", Th.numel(), lr, _ptr(dTh), _ptr(Th), _stream())
-            call("gnncg_sgd_update", Ph.numel(), lr, _ptr(dPh), _ptr(Ph), _stream())
+        for Wcat, (dTh, dPh) in zip(self.layers, grads):
+            # dTh / dPh are the halves of one contiguous d[Theta | Phi]: one update
+            call("gnncg_sgd_update", Wcat.numel(), lr, _ptr(dTh), _ptr(Wcat), _stream())
         return self.loss[:1], grads
 
 
 class MoNet:
     """GMMConv stack: dims = [F0, F1, ...] with K kernels and r pseudo-coordinate
-    dimensions per layer; identity between layers, loss = sum of exits, SGD on W, P_l, P_r, mu, sinv."""
+    dimensions per layer; identity between layers, loss = sum of exits, SGD on W, P_l, P_r, mu, sinv.
+    W, P_l and P_r of a layer are column blocks of one row-padded parameter buffer
+    [W | P_l | P_r | 0] (ops.gmm_weight_width), so neither the forward nor the backward copies."""
 
     def __init__(self, g: DeviceGraph, dims, K: int, r: int, seed: int = 0):
+        from .ops import gmm_weight_width
+
         self.g, self.K, self.r = g, K, r
         dev = g.device
         gen = torch.Generator(device=dev)
@@ -147,32 +163,47 @@ class MoNet:
         self.layers = []
         for a, b in zip(dims[:-1], dims[1:]):
             sinv = torch.rand(K, r, generator=gen, device=dev).add_(0.5)
-            self.layers.append([init_uniform(a, K * b, gen, dev), init_uniform(a, r, gen, dev),
-                                init_uniform(a, r, gen, dev), init_uniform(K, r, gen, dev), sinv, b])
+            W, Pl, Pr = init_uniform(a, K * b, gen, dev), init_uniform(a, r, gen, dev), init_uniform(a, r, gen, dev)
+            mu = init_uniform(K, r, gen, dev)
+            Wcat = torch.zeros(a, gmm_weight_width(K, r, b), device=dev)  # once, at init
+            Kf = K * b
+            Wcat[:, :Kf], Wcat[:, Kf:Kf + r], Wcat[:, Kf + r:Kf + 2 * r] = W, Pl, Pr
+            self.layers.append([Wcat, mu, sinv, b])
         self.loss = torch.zeros(4, device=dev)
         self._sum_ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=dev)
+        self._ones = None
+
+    def views(self, Wcat, f):
+        """(W, P_l, P_r) column views of a layer's [W | P_l | P_r | 0]."""
+        Kf, r = self.K * f, self.r
+        return Wcat[:, :Kf], Wcat[:, Kf:Kf + r], Wcat[:, Kf + r:Kf + 2 * r]
 
     def train_step(self, H: torch.Tensor, lr: float = 0.0):
         from .ops import gmm_backward, gmm_forward
 
         xs, stashes = [H], []
-        for W, Pl, Pr, mu, sinv, f in self.layers:
-            out, st = gmm_forward(self.g, xs[-1], W, Pl, Pr, mu, sinv, self.K, self.r, f)
+        for Wcat, mu, sinv, f in self.layers:
+            out, st = gmm_forward(self.g, xs[-1], *self.views(Wcat, f), mu, sinv, self.K, self.r, f)
             xs.append(out)
             stashes.append(st)
         out = xs[-1]
         call("gnncg_sum", out.numel(), _ptr(out), _ptr(self.loss), _ptr(self._sum_ws), self._sum_ws.numel(), _stream())
-        g = torch.empty_like(out)
-        call("gnncg_fill", g.numel(), 1.0, _ptr(g), _stream())
+        if self._ones is None or self._ones.shape != out.shape:
+            self._ones = torch.empty_like(out)
+            call("gnncg_fill", self._ones.numel(), 1.0, _ptr(self._ones), _stream())
+        g = self._ones
         grads = [None] * len(self.layers)
         for i in reversed(range(len(self.layers))):
-            W, Pl, Pr, mu, sinv, f = self.layers[i]
-            res = gmm_backward(self.g, xs[i], W, Pl, Pr, mu, sinv, self.K, self.r, f, stashes[i], g, need_dH=i > 0)
+            Wcat, mu, sinv, f = self.layers[i]
+            res = gmm_backward(self.g, xs[i], *self.views(Wcat, f), mu, sinv, self.K, self.r, f, stashes[i], g,
+                               need_dH=i > 0)
             grads[i] = res[1:]
             g = res[0]
-        for L, gr in zip(self.layers, grads):
-            for p, dp in zip(L[:5], gr):
-                call("gnncg_sgd_update", p.numel(), lr, _ptr(dp.contiguous()), _ptr(p), _stream())
+        for (Wcat, mu, sinv, f), gr in zip(self.layers, grads):
+            dWcat, dmu, dsinv = gr[5], gr[3], gr[4]
+            call("gnncg_sgd_update", Wcat.numel(), lr, _ptr(dWcat), _ptr(Wcat), _stream())
+            call("gnncg_sgd_update", mu.numel(), lr, _ptr(dmu), _ptr(mu), _stream())
+            call("gnncg_sgd_update", sinv.numel(), lr, _ptr(dsinv), _ptr(sinv), _stream())
         return self.loss[:1], grads
 
 

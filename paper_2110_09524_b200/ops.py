@@ -385,22 +385,60 @@ def edgeconv_region_forward(g: DeviceGraph, Th, Ph):
     return out, amax
 
 
+def _adjacent_columns(parts, name):
+    """When the column blocks `parts` are consecutive slices of one row-major buffer (the
+    models keep [Theta | Phi] and [W | P_l | P_r] that way), that buffer as one matrix view --
+    no copy; else None."""
+    A = parts[0]
+    if not all(isinstance(p, torch.Tensor) and p.is_cuda and p.dtype == torch.float32 and p.dim() == 2 for p in parts):
+        raise TensorError(f"{name}: expected 2-D float32 CUDA tensors")
+    ld = A.stride(0)
+    col = 0
+    for p in parts:
+        if p.stride(1) != 1 or p.stride(0) != ld or p.shape[0] != A.shape[0] or p.data_ptr() != A.data_ptr() + 4 * col:
+            return None
+        col += p.shape[1]
+    if col > ld:
+        return None
+    return A.as_strided((A.shape[0], col), (ld, 1))
+
+
 def edgeconv_forward(g: DeviceGraph, H, Theta, Phi):
     """EdgeConv layer forward, reorganized: Y = H [Theta | Phi] (one GEMM),
-    then the fused max region."""
-    H, Theta, Phi = _f32(H, "H"), _f32(Theta, "Theta"), _f32(Phi, "Phi")
+    then the fused max region.  Theta / Phi given as adjacent column blocks of one buffer
+    (EdgeConvNet's parameters) are used in place; separate tensors are concatenated."""
+    H = _f32(H, "H")
     if Theta.shape != Phi.shape or Theta.shape[0] != H.shape[1]:
         raise TensorError("edgeconv_forward: Theta/Phi must both be (F_in, C)")
-    C_ = Theta.shape[1]
-    Y = gemm(H, torch.cat([Theta, Phi], dim=1), ws=g.ws)
+    Wcat = _adjacent_columns([Theta, Phi], "edgeconv_forward")
+    if Wcat is None:
+        Wcat = torch.cat([_f32(Theta, "Theta"), _f32(Phi, "Phi")], dim=1)
+    return edgeconv_forward_cat(g, H, Wcat)
+
+
+def edgeconv_forward_cat(g: DeviceGraph, H, Wcat):
+    """edgeconv_forward on the concatenated weight [Theta | Phi] (F_in x 2C)."""
+    C_ = Wcat.shape[1] // 2
+    Y = gemm(H, Wcat, ws=g.ws)
     out, amax = edgeconv_region_forward(g, Y[:, :C_], Y[:, C_:])
     return out, EdgeConvStash(Y, amax)
 
 
 def edgeconv_backward(g: DeviceGraph, H, Theta, Phi, stash: EdgeConvStash, dOut, need_dH=True):
-    """Argmax routing (K7) then dY -> d[Theta|Phi] = H^T dY, dH = dY [Theta|Phi]^T."""
-    H = _f32(H, "H")
+    """Argmax routing (K7) then dY -> d[Theta|Phi] = H^T dY, dH = dY [Theta|Phi]^T.
+    Returns (dH, dTheta, dPhi); dTheta / dPhi are column views of one d[Theta|Phi] buffer."""
+    Wcat = _adjacent_columns([Theta, Phi], "edgeconv_backward")
+    if Wcat is None:
+        Wcat = torch.cat([_f32(Theta, "Theta"), _f32(Phi, "Phi")], dim=1)
+    dH, dWcat = edgeconv_backward_cat(g, H, Wcat, stash, dOut, need_dH)
     C_ = Theta.shape[1]
+    return dH, dWcat[:, :C_], dWcat[:, C_:]
+
+
+def edgeconv_backward_cat(g: DeviceGraph, H, Wcat, stash: EdgeConvStash, dOut, need_dH=True):
+    """(dH, d[Theta|Phi]) of edgeconv_forward_cat."""
+    H = _f32(H, "H")
+    C_ = Wcat.shape[1] // 2
     dOut = _f32(dOut, "dOut")
     V = g.num_vertices
     dY = torch.empty(V, 2 * C_, device=H.device)
@@ -408,8 +446,8 @@ def edgeconv_backward(g: DeviceGraph, H, Theta, Phi, stash: EdgeConvStash, dOut,
         call("gnncg_edgeconv_bwd", g.csc_src.struct(), g.csr_dst.struct(), C_, _ptr(stash.argmax), _ptr(dOut),
              _ptr(dY), dY.stride(0), _ptr(dY) + 4 * C_, dY.stride(0), _stream())
     dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
-    dH = gemm(dY, torch.cat([Theta, Phi], dim=1), trans_b=True, ws=g.ws) if need_dH else None
-    return dH, dWcat[:, :C_].contiguous(), dWcat[:, C_:].contiguous()
+    dH = gemm(dY, Wcat, trans_b=True, ws=g.ws) if need_dH else None
+    return dH, dWcat
 
 
 # ---------------------------------------------------------------------------
@@ -420,10 +458,20 @@ class GmmStash:
     Y: torch.Tensor  # [hW | pl | pr], V x (K f + 2 r)
 
 
+def gmm_weight_width(K: int, r: int, f: int) -> int:
+    """Row width of [W | P_l | P_r]: K f + 2 r padded to a multiple of 4 floats, so Y and dY
+    have 16-byte rows (the TMA tensor-core GEMM needs them; K8 takes ldy >= K f + 2 r)."""
+    return (K * f + 2 * r + 3) // 4 * 4
+
+
 def _gmm_wcat(W, P_l, P_r):
-    """[W | P_l | P_r] with its row padded with zero columns to a multiple of 4 floats: Y and dY
-    then have 16-byte rows, which the TMA tensor-core GEMM needs (K8 takes ldy >= K f + 2 r)."""
+    """[W | P_l | P_r] as one padded matrix: the buffer itself when the three are adjacent
+    column blocks of it (MoNet's parameters), else a zero-padded copy (the reference API
+    with separate tensors)."""
     n = W.shape[1] + P_l.shape[1] + P_r.shape[1]
+    cat = _adjacent_columns([W, P_l, P_r], "gmm")
+    if cat is not None and W.stride(0) == (n + 3) // 4 * 4:
+        return cat.as_strided((W.shape[0], W.stride(0)), (W.stride(0), 1))
     out = torch.zeros(W.shape[0], (n + 3) // 4 * 4, device=W.device)
     a, b = W.shape[1], W.shape[1] + P_l.shape[1]
     out[:, :a] = _f32(W, "W")
@@ -451,14 +499,12 @@ def gmm_forward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K: int, r: int, f: int
 
 
 def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmStash, dOut, need_dH=True):
-    """Returns (dH, dW, dP_l, dP_r, dmu, dsinv)."""
+    """Returns (dH, dW, dP_l, dP_r, dmu, dsinv); dW / dP_l / dP_r are column views of one
+    d[W | P_l | P_r] buffer (padding columns zero), which is returned as the 7th item."""
     H = _f32(H, "H")
     dOut = _f32(dOut, "dOut")
-    V = g.num_vertices
     Y = stash.Y
-    dY = torch.empty_like(Y)
-    if Y.shape[1] > K * f + 2 * r:
-        dY[:, K * f + 2 * r:].zero_()  # the alignment columns (K8 writes the first K f + 2 r)
+    dY = torch.empty_like(Y)  # K8 writes every column, the alignment padding as zeros
     dmu = torch.empty(K, r, device=H.device)
     dsinv = torch.empty(K, r, device=H.device)
     need = _lib.lib().gnncg_gmm_bwd_workspace(g.csr_dst.struct(), K, r)
@@ -469,7 +515,7 @@ def gmm_backward(g: DeviceGraph, H, W, P_l, P_r, mu, sinv, K, r, f, stash: GmmSt
     dWcat = gemm(H, dY, trans_a=True, ws=g.ws)
     dH = gemm(dY, _gmm_wcat(W, P_l, P_r), trans_b=True, ws=g.ws) if need_dH else None
     Kf = K * f
-    return dH, dWcat[:, :Kf].contiguous(), dWcat[:, Kf:Kf + r].contiguous(), dWcat[:, Kf + r:Kf + 2 * r].contiguous(), dmu, dsinv
+    return dH, dWcat[:, :Kf], dWcat[:, Kf:Kf + r], dWcat[:, Kf + r:Kf + 2 * r], dmu, dsinv, dWcat
 
 
 # ---------------------------------------------------------------------------

@@ -22,7 +22,8 @@ def np64(t):
     return t.detach().cpu().double().numpy()
 
 
-def make_graph(kind, dev, seed=0):
+def graph_edges(kind, seed=0):
+    """(V, src, dst) of the named test graph."""
     rng = np.random.default_rng(seed)
     if kind == "G3":
         V, src, dst = 3, np.array([0, 1, 0]), np.array([2, 2, 1])
@@ -43,6 +44,11 @@ def make_graph(kind, dev, seed=0):
         src, dst = rng.choice(V, E, p=w), rng.choice(V, E, p=w)
     else:
         raise ValueError(kind)
+    return V, src, dst
+
+
+def make_graph(kind, dev, seed=0):
+    V, src, dst = graph_edges(kind, seed)
     hg = O.host_graph(V, src, dst)
     return hg, DeviceGraph.from_edges(V, src, dst, device=dev)
 

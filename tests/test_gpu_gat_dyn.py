@@ -2,8 +2,10 @@
 takes the counter on graphs with >= 8 items per warp of the persistent grid, so the small
 test graphs run the fixed stride; here GNNCG_GAT_DYN=2 forces the counter (and K4f's batched
 requests: small graphs have few edges per item) and the results are compared with the fixed
-stride (GNNCG_GAT_DYN=0) and with the f64 oracle.  Each mode runs in its own process (the
-switch is read once per process)."""
+stride (GNNCG_GAT_DYN=0) bitwise per item, and the counter path with the f64 oracle
+(elementwise rel_err).  Each mode runs in its own process (the switch is read once per
+process).  The default selection (counter on, one item per request for ~450-edge rows, ~5
+for ~100-edge rows) is exercised at the benchmark sizes by tests/test_gpu_scale.py."""
 import os
 import subprocess
 import sys
@@ -63,3 +65,18 @@ def test_counter_fetch_matches_fixed_stride(cuda, tmp_path, kind, h, f, chunk, g
     for k in ("dAr", "dHt"):
         s = max(1.0, np.abs(a[k]).max())
         assert O.max_rel_err(b[k].astype(np.float64) / s, a[k].astype(np.float64) / s) < 1e-5, k
+    if gather == "fp32":
+        # and the counter path against the f64 oracle, elementwise rel_err (tensor.hpp:153-156)
+        from tests.test_gpu_gat import graph_edges
+
+        hg = O.host_graph(*graph_edges(kind))
+        rng = np.random.default_rng(h * 100 + f)
+        V = hg.V
+        Ht = rng.uniform(-1, 1, (V, h * f)); Al, Ar = rng.uniform(-1, 1, (V, h)), rng.uniform(-1, 1, (V, h))
+        al, ar = rng.uniform(-1, 1, (h, f)), rng.uniform(-1, 1, (h, f)); dOut = rng.uniform(-1, 1, (V, h * f))
+        q = lambda x: x.astype(np.float32).astype(np.float64)  # noqa: E731  (the fp32 inputs the GPU saw)
+        fw = O.gat_region_fwd_f64(hg, q(Ht), q(Al), q(Ar), h, f)
+        bw = O.gat_region_bwd_f64(hg, q(Ht), q(Al), q(Ar), q(al), q(ar), h, f, q(dOut))
+        for k, ref in (("out", fw["out"]), ("dHt", bw["dHt"]), ("dAl", bw["dAl"]), ("dAr", bw["dAr"])):
+            assert O.max_rel_err(b[k], ref) < 1e-4, k
+
