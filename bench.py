@@ -553,9 +553,11 @@ def run_ours(args):
             dist.barrier(device_ids=[local])
         torch.cuda.synchronize()
 
-    # SGD on loss = sum of the exits: a small step keeps the parameters finite
+    # SGD on loss = sum of the exits.  That loss is unbounded below: at lr >= 1e-6
+    # the parameters grow geometrically and overflow fp32 within ~6 steps on C2
+    # (profiles/r02_sgd_divergence.txt), so the step uses lr = 1e-8, which keeps every loss finite
     # over the warm-up + timed + e2e steps (the update's cost does not depend on lr)
-    lr = 1e-6
+    lr = 1e-8
     init_params = [p.detach().clone() for p in model_params(model)]
     use_graph = args.graph == "on" or (args.graph == "auto" and args.config in ("cora", "monet", "edgeconv20",
                                                                                  "edgeconv40") and world == 1)
@@ -569,6 +571,7 @@ def run_ours(args):
         for _ in range(args.warmup):
             step()
     barrier()
+    loss_warm = float(model.loss[0].item())
     if args.ncu_probe:  # child of ncu_dram_bytes: the warm-up step above was the profiled work
         step()
         torch.cuda.synchronize()
@@ -590,6 +593,8 @@ def run_ours(args):
     launches = int(_lib.lib().gnncg_launch_count() - launches0)
     ms = start.elapsed_time(end)
     loss_after = float(model.loss[0].item())
+    if loss_after != loss_after or abs(loss_after) == float("inf"):
+        print(f"bench: non-finite loss {loss_after} after the timed steps", file=sys.stderr)
     if use_graph:  # per-kernel times from one eager step (the graph replays the same kernels)
         PROBE.reset()
         PROBE.enabled = True
@@ -735,7 +740,7 @@ def run_ours(args):
                            "chunk": args.chunk or 2048, "graph_build_s": build_s},
                 "roofline": roofline, "kernels": kernels, "cpu_baseline": cpu, "e2e": e2e, "memory": mem,
                 "parity": parity, "cost_model": wl.get("cost"), "comm": comm,
-                "loss_after_timed_steps": loss_after, "lr": lr,
+                "loss_after_warmup": loss_warm, "loss_after_timed_steps": loss_after, "lr": lr,
                 "gpu_launches": launches, "clocks": clk}
         print(json.dumps(line), flush=True)
     if dmode:

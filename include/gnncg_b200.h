@@ -98,6 +98,13 @@ size_t gnncg_csr_build_workspace(int64_t num_vertices, int64_t num_edges);
 int gnncg_csr_build(int64_t num_vertices, int64_t num_edges, const uint32_t* key, const uint32_t* other,
                     uint64_t* off, uint32_t* nbr, uint32_t* eid, void* workspace, size_t workspace_bytes,
                     void* stream);
+/* Rectangular variant for rank-local indexes (multi-GPU, dist.py): keys are rows
+ * [0, num_rows) of a destination block, neighbour ids range over [0, num_other) (the
+ * padded all-gather layout of every rank's sources).  Same sort and error contract;
+ * gnncg_csr_build(V, ...) == gnncg_csr_build_rect(V, V, ...). */
+int gnncg_csr_build_rect(int64_t num_rows, int64_t num_other, int64_t num_edges, const uint32_t* key,
+                         const uint32_t* other, uint64_t* off, uint32_t* nbr, uint32_t* eid, void* workspace,
+                         size_t workspace_bytes, void* stream);
 
 /* degree_stats (graph.cpp:47-57) over a device index: out_host[0] = max degree
  * of `idx` (blocking call; stream is synchronised). */

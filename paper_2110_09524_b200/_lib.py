@@ -80,6 +80,7 @@ _SIGS = {
     "gnncg_launch_count": ([], u64),
     "gnncg_csr_build_workspace": ([i64, i64], sz),
     "gnncg_csr_build": ([i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    "gnncg_csr_build_rect": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_max_degree": ([P(Index), P(u64), vp], i32),
     "gnncg_partition_rows": ([i64, vp, i32, vp], i32),
     "gnncg_gen_chung_lu": ([i64, i64, vp, u64, vp, vp, vp], i32),

@@ -17,12 +17,12 @@
 namespace gnncg_b200 {
 namespace {
 
-__global__ void make_keys_kernel(int64_t E, int64_t V, const uint32_t* __restrict__ key,
+__global__ void make_keys_kernel(int64_t E, int64_t V, int64_t n_other, const uint32_t* __restrict__ key,
                                  const uint32_t* __restrict__ other, uint64_t* __restrict__ keys,
                                  int* __restrict__ bad) {
   for (int64_t e = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; e < E; e += (int64_t)gridDim.x * blockDim.x) {
     const uint32_t k = key[e];
-    if (k >= (uint64_t)V || other[e] >= (uint64_t)V) atomicOr(bad, 1);  // graph.cpp:37-39
+    if (k >= (uint64_t)V || other[e] >= (uint64_t)n_other) atomicOr(bad, 1);  // graph.cpp:37-39
     keys[e] = ((uint64_t)k << 32) | (uint64_t)(uint32_t)e;
   }
 }
@@ -199,8 +199,14 @@ size_t gnncg_csr_build_workspace(int64_t V, int64_t E) {
 
 int gnncg_csr_build(int64_t V, int64_t E, const uint32_t* key, const uint32_t* other, uint64_t* off, uint32_t* nbr,
                     uint32_t* eid, void* ws, size_t ws_bytes, void* stream) {
+  return gnncg_csr_build_rect(V, V, E, key, other, off, nbr, eid, ws, ws_bytes, stream);
+}
+
+int gnncg_csr_build_rect(int64_t V, int64_t n_other, int64_t E, const uint32_t* key, const uint32_t* other,
+                         uint64_t* off, uint32_t* nbr, uint32_t* eid, void* ws, size_t ws_bytes, void* stream) {
   GNNCG_DEVICE_GUARD();
-  GNNCG_REQUIRE(V >= 0 && E >= 0, GNNCG_ERR_ARG, "csr_build: negative size");
+  GNNCG_REQUIRE(V >= 0 && E >= 0 && n_other >= 0, GNNCG_ERR_ARG, "csr_build: negative size");
+  GNNCG_REQUIRE(n_other <= ((int64_t)1 << 32), GNNCG_ERR_RANGE, "csr_build: neighbour ids exceed u32");
   GNNCG_REQUIRE(E < ((int64_t)1 << 31), GNNCG_ERR_UNSUPPORTED, "csr_build: E >= 2^31 not supported by this build");
   GNNCG_REQUIRE(V < ((int64_t)1 << 32) - 1, GNNCG_ERR_RANGE, "csr_build: V exceeds u32 vertex ids");
   GNNCG_REQUIRE(off && (E == 0 || (key && other && nbr && eid)), GNNCG_ERR_ARG, "csr_build: null pointer");
@@ -217,7 +223,7 @@ int gnncg_csr_build(int64_t V, int64_t E, const uint32_t* key, const uint32_t* o
   int* bad = reinterpret_cast<int*>(p);
   GNNCG_CUDA_TRY(cudaMemsetAsync(bad, 0, sizeof(int), s));
   if (E > 0) {
-    make_keys_kernel<<<grid_for(E), 256, 0, s>>>(E, V, key, other, keys_in, bad);
+    make_keys_kernel<<<grid_for(E), 256, 0, s>>>(E, V, n_other, key, other, keys_in, bad);
     GNNCG_LAUNCH_CHECK();
     GNNCG_CUDA_TRY(cub::DeviceRadixSort::SortKeys(temp, temp_bytes, keys_in, keys_out, (int)E, 0, 32 + bits_for(V), s));
   }

@@ -100,8 +100,8 @@ def build_local(plan: PartitionPlan, rank: int, src: torch.Tensor, dst: torch.Te
     mask = (d64 >= r0) & (d64 < r1)
     ls = plan.padded_id(src.to(torch.int64)[mask])
     ld = d64[mask] - r0
-    csr = engine.build_index(r1 - r0, ld, ls)
-    csc = engine.build_index(plan.padded_V, ls, ld)
+    csr = engine.build_index(r1 - r0, ld, ls, plan.padded_V)
+    csc = engine.build_index(plan.padded_V, ls, ld, r1 - r0)
     return LocalGraph(plan, rank, csr, csc)
 
 
@@ -114,12 +114,12 @@ class CudaEngine:
         self.chunk = chunk
         self.mode = mode
 
-    def build_index(self, rows: int, key: torch.Tensor, other: torch.Tensor):
+    def build_index(self, rows: int, key: torch.Tensor, other: torch.Tensor, n_other: int):
         from .graph import DeviceGraph
 
         k = key.to(torch.int32).contiguous()
         o = other.to(torch.int32).contiguous()
-        return DeviceGraph.build_index(rows, k, o, self.ws)
+        return DeviceGraph.build_index(rows, k, o, self.ws, n_other)
 
     def _sched(self, idx: DeviceIndex) -> DeviceSched:
         return idx.sched(self.chunk) if self.chunk else idx.sched()

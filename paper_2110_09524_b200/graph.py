@@ -159,8 +159,10 @@ class DeviceGraph:
 
     # -- construction ------------------------------------------------------
     @staticmethod
-    def build_index(V: int, key: torch.Tensor, other: torch.Tensor, ws: Workspace) -> DeviceIndex:
-        """Device counting sort by key vertex, stable in edge id (graph.cpp:14-28)."""
+    def build_index(V: int, key: torch.Tensor, other: torch.Tensor, ws: Workspace, n_other: int | None = None
+                    ) -> DeviceIndex:
+        """Device counting sort by key vertex, stable in edge id (graph.cpp:14-28).  Keys range
+        over [0, V), neighbour ids over [0, n_other) (default V; larger for rank-local indexes)."""
         E = key.numel()
         dev = key.device
         off = torch.empty(V + 1, dtype=torch.int64, device=dev)
@@ -168,7 +170,8 @@ class DeviceGraph:
         eid = torch.empty(E, dtype=torch.int32, device=dev)
         need = _lib.lib().gnncg_csr_build_workspace(V, E)
         wp, wn = ws.get(need)
-        call("gnncg_csr_build", V, E, _ptr(key), _ptr(other), _ptr(off), _ptr(nbr), _ptr(eid), wp, wn, _stream())
+        call("gnncg_csr_build_rect", V, V if n_other is None else n_other, E, _ptr(key), _ptr(other), _ptr(off),
+             _ptr(nbr), _ptr(eid), wp, wn, _stream())
         return DeviceIndex(off, nbr, eid)
 
     @classmethod

@@ -20,7 +20,7 @@ from oracle import oracle as O
 class OracleEngine:
     device = torch.device("cpu")
 
-    def build_index(self, rows, key, other):
+    def build_index(self, rows, key, other, n_other):
         off, nbr, eid = O.build_index(rows, key.numpy().astype(np.uint32), other.numpy().astype(np.uint32))
         return dict(off=off, nbr=nbr, eid=eid, rows=rows)
 
