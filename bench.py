@@ -102,6 +102,15 @@ def gat_kernel_bytes(V: int, E: int, h: int, f: int, gather_bytes: int = 4) -> d
     }
 
 
+def _gat_bytes(V: int, E: int, h: int, f: int, gather_bytes: int, dmode: bool) -> dict:
+    """The per-launch byte model keyed by the names the step's probes use: the partitioned path
+    (dist.py) runs K2 / K4f through gnncg_gat_fwd_dist / gnncg_gat_bwd_dist over the rank's edges."""
+    b = gat_kernel_bytes(V, E, h, f, gather_bytes)
+    if dmode:
+        return {"gat_fwd_dist": b["gat_fwd"], "gat_bwd_dist": b["gat_bwd_src_fused"]}
+    return b
+
+
 def edgeconv_kernel_bytes(V: int, E: int, C: int) -> dict:
     """K6: nbr + eid + Th[u] row per edge; offsets, Th[v], Ph[v], out, argmax per row.
     K7 (inverse argmax over csc_src): nbr + eid + argmax[v] + g[v] rows per edge; g[u], dTh, dPh per row."""
@@ -180,7 +189,7 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
 
             lg = partitioned_chung_lu(V, E, offset=offset, seed=0, rank=rank, world=world, device=dev)
             model = PartitionedGAT(lg, dims, seed=1, chunk=args.chunk)
-            V_loc, E_loc = lg.num_local, int(lg.csr.num_edges)
+            V_loc, E_loc = lg.num_local, lg.num_edges
         else:
             g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
             model = GAT(g, dims, seed=1, chunk=args.chunk, gather=args.gather)
@@ -190,7 +199,7 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
 
         wl_cost = {"per_layer": gat_layer_report(V, E, h, f), "source": "SPEC.md:282-289"}
         wl = dict(model=model, H_buf=features(V_loc, dims[0][0]), fin=dims[0][0], E_total=E, cost=wl_cost,
-                  layers=len(dims), bytes=gat_kernel_bytes(V_loc, E_loc, h, f, 2 if args.gather == "bf16" else 4),
+                  layers=len(dims), bytes=_gat_bytes(V_loc, E_loc, h, f, 2 if args.gather == "bf16" else 4, dmode),
                   scaling="strong" if strong else "weak", gat=(V_loc, E_loc, h, f),
                   config={"workload": desc, "V": V, "E": E, "layers": len(dims),
                           "gather": args.gather,

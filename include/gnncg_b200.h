@@ -52,7 +52,8 @@ typedef enum gnncg_status {
   GNNCG_ERR_CUDA = 4,        /* CUDA runtime / launch failure */
   GNNCG_ERR_WORKSPACE = 5,   /* caller workspace smaller than the *_workspace() query */
   GNNCG_ERR_UNSUPPORTED = 6, /* shape outside the compiled kernel variants */
-  GNNCG_ERR_ARG = 7          /* null pointer / invalid argument */
+  GNNCG_ERR_ARG = 7,         /* null pointer / invalid argument */
+  GNNCG_ERR_NCCL = 8         /* NCCL library missing or a collective failed */
 } gnncg_status;
 
 /* One adjacency index (AdjIndex, graph.hpp:19-29), possibly a row block of it. */
@@ -305,6 +306,88 @@ int gnncg_relu_bwd(int64_t rows, int cols, const float* dOut, const float* out, 
  *   w[e] = 1 / sqrt(max(1, deg_in(dst e)) * max(1, deg_out(src e))) */
 int gnncg_gcn_norm(int64_t num_edges, const uint32_t* edge_src, const uint32_t* edge_dst,
                    const gnncg_index_t* csr_dst, const gnncg_index_t* csc_src, float* w, void* stream);
+
+/* ------------------------------------------------ multi-GPU
+ * The reference's executor is single-process; north_star partitions the graph's destination
+ * rows over P GPUs (one process each) with one all-gather per layer forward and a
+ * reduce-scatter per layer backward.  These entry points replace the spec's run_forward /
+ * run_backward for one rank of such a run.
+ *
+ * Communicator: a thin handle over an NCCL communicator plus a private collective stream.
+ * NCCL is resolved at run time (dlopen of libnccl.so.2: the copy already loaded in the
+ * process if any, e.g. torch's, else the system one), so this library has no link-time
+ * NCCL dependency; GNNCG_ERR_NCCL if it is absent.  Either create one from an NCCL unique
+ * id (rank 0 calls gnncg_comm_unique_id and the caller distributes the 128 bytes), or wrap a
+ * caller-owned ncclComm_t (gnncg_comm_init_nccl; not destroyed by gnncg_comm_destroy). */
+typedef struct gnncg_comm gnncg_comm_t;
+int gnncg_comm_unique_id(void* id_128_bytes_host);
+int gnncg_comm_init(gnncg_comm_t** comm_out_host, int nranks, int rank, const void* id_128_bytes_host);
+int gnncg_comm_init_nccl(gnncg_comm_t** comm_out_host, void* nccl_comm);
+int gnncg_comm_destroy(gnncg_comm_t* comm);
+int gnncg_comm_size(const gnncg_comm_t* comm);
+int gnncg_comm_rank(const gnncg_comm_t* comm);
+/* fp32 collectives on `stream` (the caller's; ordered with its other work):
+ * recv[P*count] = concat over ranks of send[count] (send may be recv + rank*count: in place);
+ * recv[count] = sum over ranks of send[rank*count : (rank+1)*count];  buf[count] summed in place. */
+int gnncg_comm_allgather(gnncg_comm_t* comm, const float* send, float* recv, int64_t count, void* stream);
+int gnncg_comm_reduce_scatter(gnncg_comm_t* comm, const float* send, float* recv, int64_t count, void* stream);
+int gnncg_comm_allreduce(gnncg_comm_t* comm, float* buf, int64_t count, void* stream);
+
+/* One rank's share of a destination-row partition (dist.py builds it):
+ *   rows [r_p, r_p + num_local) of csr_dst are owned; every source-side table (Ht, A_l) lives
+ *   in the PADDED all-gather layout: rank q's rows at [q*maxrows, q*maxrows + n_q).
+ *   The rank's in-edges are split by the owner of their source:
+ *     csr_local  / csc_local  -- sources in this rank's block (available before the all-gather);
+ *     csr_remote / csc_remote -- sources of other ranks.
+ *   csr_*: rows = num_local destinations, neighbour = padded source id.
+ *   csc_local: rows = num_local own sources (row r = padded id rank*maxrows + r),
+ *              neighbour = local destination row.
+ *   csc_remote: rows = nparts*maxrows padded sources (this rank's block empty),
+ *              neighbour = local destination row.
+ * Each index carries its edge-balance schedule (gnncg_sched_build_host). */
+typedef struct gnncg_part {
+  int64_t num_local;
+  int64_t maxrows;
+  int32_t nparts;
+  int32_t rank;
+  const gnncg_index_t* csr_local;
+  const gnncg_sched_t* csr_local_sched;
+  const gnncg_index_t* csr_remote;
+  const gnncg_sched_t* csr_remote_sched;
+  const gnncg_index_t* csc_local;
+  const gnncg_sched_t* csc_local_sched;
+  const gnncg_index_t* csc_remote;
+  const gnncg_sched_t* csc_remote_sched;
+} gnncg_part_t;
+
+size_t gnncg_gat_dist_workspace(const gnncg_part_t* part, int heads, int f);
+
+/* Partitioned K2 (the fused GAT region forward of one rank):
+ *   the caller has written its own rows of Ht_all (nparts*maxrows x h*f) and Al_all
+ *   (nparts*maxrows x h) at block `rank` (gnncg_gat_transform into those rows);
+ *   the all-gather of both tables runs on the communicator's stream while K2 aggregates the
+ *   local-source edges on `stream`; K2 then aggregates the remote-source edges and the two
+ *   online-softmax partials are merged:  m = max(m1, m2), d = d1 e^(m1-m) + d2 e^(m2-m),
+ *   out = (d1 e^(m1-m) out1 + d2 e^(m2-m) out2) / d  (an empty part contributes nothing).
+ *   out / m / d / Ar: num_local rows.  comm == NULL: the tables are already complete (no
+ *   collective; e.g. a caller that gathered them itself). */
+int gnncg_gat_fwd_dist(gnncg_comm_t* comm, const gnncg_part_t* part, int heads, int f, float slope, float* Ht_all,
+                       float* Al_all, const float* Ar, float* out, float* m, float* d, void* workspace,
+                       size_t workspace_bytes, void* stream);
+
+/* Partitioned fused backward (fast mode) of one rank:
+ *   records of the owned rows; K4f over csc_remote -> the partials of other ranks' sources in
+ *   dHt_send / dAl_send (nparts*maxrows rows; this rank's block zero); their reduce-scatter
+ *   runs on the communicator's stream while K4f over csc_local writes the own sources' terms;
+ *   then dHt = own + received + dA_r (x) a_r, dAl = own + received (num_local rows each) and
+ *   dA_r (num_local x h) is complete.  comm == NULL: nothing is received -- dHt / dAl hold the
+ *   own-source terms (+ the dA_r LP term) and the caller reduces dHt_send / dAl_send.
+ *   Supported where gnncg_gat_fast_supported(heads, f). */
+int gnncg_gat_bwd_dist(gnncg_comm_t* comm, const gnncg_part_t* part, int heads, int f, float slope,
+                       const float* Ht_all, const float* Al_all, const float* Ar, const float* m, const float* d,
+                       const float* out, const float* dOut, const float* a_l, const float* a_r, float* dHt,
+                       float* dAl, float* dAr, float* dHt_send, float* dAl_send, void* workspace,
+                       size_t workspace_bytes, void* stream);
 
 /* ------------------------------------------------- training-step helpers */
 /* params -= lr * grad  (train_step). */

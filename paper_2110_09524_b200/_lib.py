@@ -55,8 +55,14 @@ class ArgumentError(GnncgError):
     status = 7
 
 
+class NcclError(GnncgError):
+    """NCCL missing at run time or a collective failed."""
+
+    status = 8
+
+
 _ERRORS = {c.status: c for c in (TensorError, GraphError, DeviceError, CudaError, WorkspaceError, UnsupportedError,
-                                 ArgumentError)}
+                                 ArgumentError, NcclError)}
 
 
 class Index(C.Structure):
@@ -73,6 +79,17 @@ class Sched(C.Structure):
 
 
 P = C.POINTER
+
+
+class Part(C.Structure):
+    """gnncg_part_t -- one rank's share of a destination-row partition (multi-GPU)."""
+
+    _fields_ = [("num_local", i64), ("maxrows", i64), ("nparts", i32), ("rank", i32),
+                ("csr_local", P(Index)), ("csr_local_sched", P(Sched)), ("csr_remote", P(Index)),
+                ("csr_remote_sched", P(Sched)), ("csc_local", P(Index)), ("csc_local_sched", P(Sched)),
+                ("csc_remote", P(Index)), ("csc_remote_sched", P(Sched))]
+
+
 _SIGS = {
     "gnncg_last_error": ([], C.c_char_p),
     "gnncg_version": ([], C.c_char_p),
@@ -126,6 +143,22 @@ _SIGS = {
     "gnncg_fill": ([i64, f32, vp, vp], i32),
     "gnncg_sum_workspace": ([], sz),
     "gnncg_sum": ([i64, vp, vp, vp, sz, vp], i32),
+    "gnncg_comm_unique_id": ([vp], i32),
+    "gnncg_comm_init": ([P(vp), i32, i32, vp], i32),
+    "gnncg_comm_init_nccl": ([P(vp), vp], i32),
+    "gnncg_comm_destroy": ([vp], i32),
+    "gnncg_comm_size": ([vp], i32),
+    "gnncg_comm_rank": ([vp], i32),
+    "gnncg_comm_allgather": ([vp, vp, vp, i64, vp], i32),
+    "gnncg_comm_reduce_scatter": ([vp, vp, vp, i64, vp], i32),
+    "gnncg_comm_allreduce": ([vp, vp, i64, vp], i32),
+    "gnncg_gat_dist_workspace": ([P(Part), i32, i32], sz),
+    # comm, part, heads, f, slope, Ht_all, Al_all, Ar, out, m, d, workspace, stream
+    "gnncg_gat_fwd_dist": ([vp, P(Part), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, sz, vp], i32),
+    # comm, part, heads, f, slope, Ht_all, Al_all, Ar, m, d, out, dOut, a_l, a_r, dHt, dAl, dAr,
+    # dHt_send, dAl_send, workspace, stream
+    "gnncg_gat_bwd_dist": ([vp, P(Part), i32, i32, f32, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp, vp,
+                            sz, vp], i32),
 }
 
 EXPORTED = tuple(_SIGS)

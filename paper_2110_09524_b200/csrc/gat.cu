@@ -25,6 +25,7 @@
 
 #include "common.cuh"
 #include "gat_common.cuh"
+#include "gat_internal.h"
 
 #include <cuda_bf16.h>
 
@@ -1637,7 +1638,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
                                   const uint16_t* Ht_lp, const float* Al,
                                   const float* dst_rec, const float* dOut, const uint16_t* dOut_lp, const float* a_l,
                                   const float* a_r, float* dHt, float* dAl, float* dAr, void* ws, size_t ws_bytes,
-                                  void* stream) {
+                                  void* stream, int flags = 0) {
   GNNCG_DEVICE_GUARD();
   int rc = check_common(csc_src, sched, h, f);
   if (rc) return rc;
@@ -1656,7 +1657,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE,
                 "gat_bwd_src_fused: workspace %zu < %zu", ws_bytes, need);
   cudaStream_t s = as_stream(stream);
-  GNNCG_CUDA_TRY(cudaMemsetAsync(dAr, 0, sizeof(float) * (size_t)num_local * h, s));
+  if (!(flags & kFusedKeepDar)) GNNCG_CUDA_TRY(cudaMemsetAsync(dAr, 0, sizeof(float) * (size_t)num_local * h, s));
   GatParams p{};
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
@@ -1676,7 +1677,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
         p, sched->split_rows, sched->split_first, sched->num_split_rows);
     GNNCG_LAUNCH_CHECK();
   }
-  if (num_local > 0) {
+  if (num_local > 0 && !(flags & kFusedNoLpDar)) {
     const int g = (int)std::min<int64_t>(ceil_div(num_local * h * f, 256), 148 * 32);
     const int threads = (f % 4 == 0 && h * f / 4 <= 1024) ? std::max(256, h * f / 4) : 256;
     gat_lp_dar_kernel<<<g, threads, 0, s>>>(num_local, row_base, h, f, dAr, a_r, dHt);
@@ -1684,6 +1685,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   }
   return GNNCG_OK;
 }
+
 
 int gnncg_gat_bwd_prep_bf16(int64_t rows, int h, int f, const float* dOut, const float* out, const float* Ar,
                             const float* m, const float* d, float* rec, uint16_t* dOut_bf16, void* stream) {
@@ -1739,3 +1741,28 @@ int gnncg_gat_attn_grad(int64_t rows, int h, int f, const float* Ht, const float
 }
 
 }  // extern "C"
+
+namespace gnncg_b200 {
+
+// One K4f pass of the partitioned backward (csrc/dist.cu): fp32 tables, dA_r zeroed only
+// when asked, the dA_r (x) a_r LP term left to the caller (it needs every pass's reductions).
+int gat_bwd_src_fused_pass(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, int h, int f, float slope,
+                           int64_t num_local, const float* Ht, const float* Al, const float* dst_rec,
+                           const float* dOut, const float* a_l, const float* a_r, float* dHt, float* dAl, float* dAr,
+                           bool zero_dar, void* ws, size_t ws_bytes, cudaStream_t stream) {
+  return gat_bwd_src_fused_impl(false, csc_src, sched, h, f, slope, 0, num_local, Ht, nullptr, Al, dst_rec, dOut,
+                                nullptr, a_l, a_r, dHt, dAl, dAr, ws, ws_bytes, stream,
+                                kFusedNoLpDar | (zero_dar ? 0 : kFusedKeepDar));
+}
+
+// dHt[r, :] += dA_r[r] (x) a_r over rows [0, rows) (the fast-mode LP epilogue, dist.cu).
+int gat_lp_dar(int64_t rows, int h, int f, const float* dAr, const float* a_r, float* dHt, cudaStream_t s) {
+  if (rows <= 0) return GNNCG_OK;
+  const int g = (int)std::min<int64_t>(ceil_div(rows * h * f, 256), 148 * 32);
+  const int threads = (f % 4 == 0 && h * f / 4 <= 1024) ? std::max(256, h * f / 4) : 256;
+  gat_lp_dar_kernel<<<g, threads, 0, s>>>(rows, 0, h, f, dAr, a_r, dHt);
+  GNNCG_LAUNCH_CHECK();
+  return GNNCG_OK;
+}
+
+}  // namespace gnncg_b200

@@ -3,37 +3,42 @@
 Destination vertices are split into P contiguous row blocks of csr_dst with balanced
 edge counts (``gnncg_partition_rows``: bound[p] = lower_bound(off, ceil(p E / P))).
 Rank p owns rows [r_p, r_{p+1}) and every tensor indexed by them (H, out, m, d, A_r, dOut).
+Source-side tables (Ht, A_l) live in the PADDED all-gather layout: rank q's rows at
+[q*maxrows, q*maxrows + n_q), so the kernels index the gathered tables directly.
 
-Per layer, forward:
-  Ht_p, A_l,p, A_r,p = K1(H_p)      (one tensor-core GEMM with the LP epilogue, local rows)
-  all_gather(Ht), all_gather(A_l)   (NCCL over NVLink; blocks padded to the largest)
-  K2 over the local csr_dst block   (no collective: destination rows are independent)
-Backward:
-  K3 over the local csr_dst block   (c, dA_r: local)
-  K4 over the local csc_src         (rows = all sources, neighbours = local rows):
-                                    partial dHt / dA_l for every source
-  reduce_scatter(dHt), reduce_scatter(dA_l) -> the owned rows (the terms are linear)
-  LP grads over the owned rows, dW_p = H_p^T dHt_p -> all_reduce (tiny)
+A rank's in-edges are split by the owner of their source (``build_local``): local-source
+edges need only the rank's own rows of Ht / A_l, remote-source edges need the all-gather.
+
+Per layer, forward (``gnncg_gat_fwd_dist``):
+  Ht, A_l, A_r = K1(H_p)            tensor-core GEMM with the LP epilogue, written straight
+                                    into the rank's block of the gather tables
+  all_gather(Ht || A_l)             NCCL, on the communicator's stream ...
+  K2(local-source edges)            ... overlapped with the aggregation that needs no remote row
+  K2(remote-source edges), merge    two online-softmax partials -> out, m, d
+Backward (``gnncg_gat_bwd_dist``, fused fast mode):
+  K4f(remote-source edges)          partial dHt / dA_l of other ranks' sources
+  reduce_scatter(dHt || dA_l)       NCCL, overlapped with ...
+  K4f(local-source edges)           ... the own sources' terms
+  combine                           dHt = own + received + dA_r (x) a_r
+  LP grads over the owned rows, dW_p = H_p^T dHt_p, one all-reduce of (dW, da_l, da_r)
   dH_p = dHt_p W^T
-Every per-row computation touches only the rank's own rows; the gathered tensors are read
-only by the fused kernels.
+Every per-row computation touches only the rank's own rows.
 
-Source ids inside the local indexes are remapped to the PADDED global layout of the
-all-gather buffer (block p at rows [p*maxrows, p*maxrows + n_p)), so the kernels index
-the gathered tensors directly.  The orchestration is written against a small engine
-interface: ``CudaEngine`` (the product: libgnncg_b200 + NCCL) here, and an oracle-backed
-engine in tests/ that runs the same schedule under gloo on CPU.
+The orchestration is written against a small engine interface: ``CudaEngine`` (the
+product: libgnncg_b200 kernels + its NCCL communicator) here, and an oracle-backed engine in
+tests/ that runs the same schedule under gloo on CPU.
 """
 from __future__ import annotations
 
-from dataclasses import dataclass
+import ctypes as C
+from dataclasses import dataclass, field
 
 import numpy as np
 import torch
 import torch.distributed as dist
 
 from . import _lib
-from ._lib import call
+from ._lib import Part, call
 from .graph import DeviceIndex, DeviceSched, Workspace, _ptr, _stream, chung_lu_cdf, partition_rows
 from .ops import GatParams, PROBE, gat_transform, gemm
 
@@ -77,12 +82,18 @@ class PartitionPlan:
 
 @dataclass
 class LocalGraph:
-    """Rank-local view: csr over owned destination rows, csc over all (padded) sources."""
+    """Rank-local view (gnncg_part_t): the owned destination rows' in-edges split by the owner
+    of their source.  csr_*: rows = owned destinations, neighbour = padded source id;
+    csc_local: rows = own sources (rebased to the block), csc_remote: rows = all padded
+    sources; csc neighbours are local destination rows."""
 
     plan: PartitionPlan
     rank: int
-    csr: object  # engine-specific index
-    csc: object
+    csr_local: object  # engine-specific indexes
+    csr_remote: object
+    csc_local: object
+    csc_remote: object
+    _part: object = field(default=None, repr=False)
 
     @property
     def num_local(self) -> int:
@@ -92,27 +103,73 @@ class LocalGraph:
     def row_base(self) -> int:
         return self.rank * self.plan.maxrows
 
+    @property
+    def num_edges(self) -> int:
+        return int(self.csr_local.num_edges) + int(self.csr_remote.num_edges)
+
 
 def build_local(plan: PartitionPlan, rank: int, src: torch.Tensor, dst: torch.Tensor, engine) -> LocalGraph:
-    """Select the in-edges of the owned rows (stable in edge id) and build both local indexes."""
+    """Select the in-edges of the owned rows (stable in edge id), split them by source owner
+    and build the four rank-local indexes."""
     r0, r1 = int(plan.bounds[rank]), int(plan.bounds[rank + 1])
+    n, base, Vp = r1 - r0, rank * plan.maxrows, plan.padded_V
     d64 = dst.to(torch.int64)
     mask = (d64 >= r0) & (d64 < r1)
-    ls = plan.padded_id(src.to(torch.int64)[mask])
+    ps = plan.padded_id(src.to(torch.int64)[mask])
     ld = d64[mask] - r0
-    csr = engine.build_index(r1 - r0, ld, ls, plan.padded_V)
-    csc = engine.build_index(plan.padded_V, ls, ld, r1 - r0)
-    return LocalGraph(plan, rank, csr, csc)
+    del d64, mask
+    own = (ps >= base) & (ps < base + n)
+    ps_l, ld_l = ps[own], ld[own]
+    ps_r, ld_r = ps[~own], ld[~own]
+    del ps, ld, own
+    csr_local = engine.build_index(n, ld_l, ps_l, Vp)
+    csc_local = engine.build_index(n, ps_l - base, ld_l, n)
+    del ps_l, ld_l
+    csr_remote = engine.build_index(n, ld_r, ps_r, Vp)
+    csc_remote = engine.build_index(Vp, ps_r, ld_r, n)
+    return LocalGraph(plan, rank, csr_local, csr_remote, csc_local, csc_remote)
+
+
+class NcclComm:
+    """The library's communicator (gnncg_comm_t over NCCL) for the ranks of a torch.distributed
+    group: rank 0 draws the NCCL unique id, the group broadcasts it, every rank joins."""
+
+    def __init__(self, group=None):
+        self.rank, self.world = dist.get_rank(group), dist.get_world_size(group)
+        uid = C.create_string_buffer(128)
+        if self.rank == 0:
+            call("gnncg_comm_unique_id", uid)
+        obj = [uid.raw]
+        dist.broadcast_object_list(obj, src=dist.get_global_rank(group, 0) if group is not None else 0, group=group)
+        self.handle = C.c_void_p()
+        call("gnncg_comm_init", C.byref(self.handle), self.world, self.rank, C.c_char_p(obj[0]))
+
+    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        call("gnncg_comm_allreduce", self.handle, _ptr(t), t.numel(), _stream())
+        return t
+
+    def close(self):
+        if self.handle:
+            _lib.lib().gnncg_comm_destroy(self.handle)
+            self.handle = C.c_void_p()
+
+    def __del__(self):
+        try:
+            self.close()
+        except Exception:  # interpreter shutdown
+            pass
 
 
 class CudaEngine:
-    """The product engine: libgnncg_b200 kernels on the current CUDA device."""
+    """The product engine: libgnncg_b200 kernels on the current CUDA device; `comm` is the
+    library's NCCL communicator (None: the caller completes the gather tables and reduces the
+    remote partials itself -- used to emulate ranks on one GPU)."""
 
-    def __init__(self, device, chunk=None, mode="auto"):
+    def __init__(self, device, chunk=None, comm: NcclComm | None = None):
         self.device = device
         self.ws = Workspace(device)
         self.chunk = chunk
-        self.mode = mode
+        self.comm = comm
 
     def build_index(self, rows: int, key: torch.Tensor, other: torch.Tensor, n_other: int):
         from .graph import DeviceGraph
@@ -124,74 +181,73 @@ class CudaEngine:
     def _sched(self, idx: DeviceIndex) -> DeviceSched:
         return idx.sched(self.chunk) if self.chunk else idx.sched()
 
+    def part(self, lg: LocalGraph) -> Part:
+        if lg._part is None:
+            idx = [lg.csr_local, lg.csr_remote, lg.csc_local, lg.csc_remote]
+            keep = [(i.struct(), self._sched(i).struct()) for i in idx]
+            pt = Part(lg.num_local, lg.plan.maxrows, lg.plan.P, lg.rank,
+                      *[C.pointer(x) for pair in keep for x in pair])
+            lg._part = (pt, keep)
+        return lg._part[0]
+
     def zeros(self, *shape):
         return torch.zeros(*shape, dtype=torch.float32, device=self.device)
 
     def empty(self, *shape):
         return torch.empty(*shape, dtype=torch.float32, device=self.device)
 
-    def gemm(self, A, B, ta=False, tb=False):
-        return gemm(A, B, trans_a=ta, trans_b=tb, ws=self.ws)
+    def gemm(self, A, B, ta=False, tb=False, out=None):
+        return gemm(A, B, trans_a=ta, trans_b=tb, out=out, ws=self.ws)
 
-    def transform(self, H, W, a_l, a_r, p: GatParams):
-        """K1 with the LP epilogue on the local rows: (Ht, A_l, A_r)."""
-        return gat_transform(H, W, a_l, a_r, p.heads, p.f, ws=self.ws)
+    def transform(self, H, W, a_l, a_r, p: GatParams, Ht_out, Al_out):
+        """K1 with the LP epilogue on the local rows, written into the rank's block of the
+        gather tables; returns A_r (destination side, local)."""
+        _, _, Ar = gat_transform(H, W, a_l, a_r, p.heads, p.f, ws=self.ws, Ht=Ht_out, Al=Al_out)
+        return Ar
 
-    def attn_dots(self, Ht, a_l, a_r, p: GatParams):
-        V = Ht.shape[0]
-        Al, Ar = self.empty(V, p.heads), self.empty(V, p.heads)
-        with PROBE("attn_dots"):
-            call("gnncg_gat_attn_dots", V, p.heads, p.f, _ptr(Ht), _ptr(a_l), _ptr(a_r), _ptr(Al), _ptr(Ar),
-                 _stream())
-        return Al, Ar
+    def _comm(self):
+        return self.comm.handle if self.comm is not None else None
 
-    def region_fwd(self, lg: LocalGraph, Ht, Al, Ar_local, p: GatParams):
-        n = lg.num_local
+    def region_fwd(self, lg: LocalGraph, Ht_all, Al_all, Ar, p: GatParams):
+        n = max(lg.num_local, 1)
         out, m, d = self.empty(n, p.heads * p.f), self.empty(n, p.heads), self.empty(n, p.heads)
-        s = self._sched(lg.csr)
-        wp, wn = self.ws.get(_lib.lib().gnncg_gat_workspace(s.struct(), None, p.heads, p.f))
-        with PROBE("gat_fwd"):
-            call("gnncg_gat_fwd", lg.csr.struct(), s.struct(), p.heads, p.f, p.slope, _ptr(Ht), _ptr(Al),
-                 _ptr(Ar_local), _ptr(out), _ptr(m), _ptr(d), wp, wn, _stream())
-        return out, m, d
+        pt = self.part(lg)
+        wp, wn = self.ws.get(_lib.lib().gnncg_gat_dist_workspace(C.byref(pt), p.heads, p.f))
+        with PROBE("gat_fwd_dist"):
+            call("gnncg_gat_fwd_dist", self._comm(), C.byref(pt), p.heads, p.f, p.slope, _ptr(Ht_all), _ptr(Al_all),
+                 _ptr(Ar), _ptr(out), _ptr(m), _ptr(d), wp, wn, _stream())
+        k = lg.num_local
+        return out[:k], m[:k], d[:k]
 
-    def region_bwd(self, lg: LocalGraph, Ht, Al, Ar_local, m, d, dOut, a_l, a_r, p: GatParams, out=None):
-        """K3 + K4 (or the fused fast pass) -> (dHt partial over padded sources, dAl partial, dAr local)."""
-        n, h, f = lg.num_local, p.heads, p.f
-        c, dAr = self.empty(n, h), self.empty(n, h)
-        sd, ss = self._sched(lg.csr), self._sched(lg.csc)
+    def region_bwd(self, lg: LocalGraph, Ht_all, Al_all, Ar, m, d, out, dOut, a_l, a_r, p: GatParams, send=None):
+        """-> (dHt, dAl, dAr) of the owned rows.  `send` = (dHt_send, dAl_send) buffers to keep
+        (comm None: the caller reduces them)."""
+        n, h, f = max(lg.num_local, 1), p.heads, p.f
         Vp = lg.plan.padded_V
-        dHt, dAl = self.empty(Vp, h * f), self.empty(Vp, h)
-        wp, wn = self.ws.get(_lib.lib().gnncg_gat_workspace(sd.struct(), ss.struct(), h, f))
-        st = _stream()
-        if out is not None and self.mode != "deterministic" and _lib.lib().gnncg_gat_fast_supported(h, f):
-            rec = self.empty(n, _lib.lib().gnncg_gat_rec_stride(h))
-            Ar_loc = Ar_local.contiguous()
-            with PROBE("gat_bwd_prep"):
-                call("gnncg_gat_bwd_prep", n, h, f, _ptr(dOut), _ptr(out), _ptr(Ar_loc), _ptr(m), _ptr(d), _ptr(rec),
-                     st)
-            with PROBE("gat_bwd_src_fused"):
-                call("gnncg_gat_bwd_src_fused", lg.csc.struct(), ss.struct(), h, f, p.slope, lg.row_base, n,
-                     _ptr(Ht), _ptr(Al), _ptr(rec), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr),
-                     wp, wn, st)
-            return dHt, dAl, dAr
-        with PROBE("gat_bwd_dst"):
-            call("gnncg_gat_bwd_dst", lg.csr.struct(), sd.struct(), h, f, p.slope, _ptr(Ht), _ptr(Al),
-                 _ptr(Ar_local), _ptr(m), _ptr(d), _ptr(dOut), _ptr(c), _ptr(dAr), wp, wn, st)
-        with PROBE("gat_bwd_src"):
-            call("gnncg_gat_bwd_src", lg.csc.struct(), ss.struct(), h, f, p.slope, lg.row_base, n, _ptr(Ht),
-                 _ptr(Al), _ptr(Ar_local), _ptr(m), _ptr(d), _ptr(c), _ptr(dOut), _ptr(dAr), _ptr(a_l), _ptr(a_r),
-                 _ptr(dHt), _ptr(dAl), wp, wn, st)
-        return dHt, dAl, dAr
+        dHt, dAl, dAr = self.empty(n, h * f), self.empty(n, h), self.empty(n, h)
+        hs, als = send if send is not None else (self.empty(Vp, h * f), self.empty(Vp, h))
+        pt = self.part(lg)
+        wp, wn = self.ws.get(_lib.lib().gnncg_gat_dist_workspace(C.byref(pt), h, f))
+        with PROBE("gat_bwd_dist"):
+            call("gnncg_gat_bwd_dist", self._comm(), C.byref(pt), h, f, p.slope, _ptr(Ht_all), _ptr(Al_all), _ptr(Ar),
+                 _ptr(m), _ptr(d), _ptr(out), _ptr(dOut), _ptr(a_l), _ptr(a_r), _ptr(dHt), _ptr(dAl), _ptr(dAr),
+                 _ptr(hs), _ptr(als), wp, wn, _stream())
+        k = lg.num_local
+        return dHt[:k], dAl[:k], dAr[:k]
 
-    def attn_grad(self, Ht, dAl, dAr, p: GatParams):
+    def attn_grad(self, Ht, dAl, dAr, p: GatParams, out=None):
         V = Ht.shape[0]
-        da_l, da_r = self.empty(p.heads, p.f), self.empty(p.heads, p.f)
+        da_l, da_r = out if out is not None else (self.empty(p.heads, p.f), self.empty(p.heads, p.f))
         wp, wn = self.ws.get(_lib.lib().gnncg_gat_attn_grad_workspace(V, p.heads, p.f))
         with PROBE("attn_grad"):
             call("gnncg_gat_attn_grad", V, p.heads, p.f, _ptr(Ht), _ptr(dAl), _ptr(dAr), _ptr(da_l), _ptr(da_r),
                  wp, wn, _stream())
         return da_l, da_r
+
+    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
+        if self.comm is not None:
+            self.comm.all_reduce(t)
+        return t
 
     def sgd(self, param, grad, lr):
         call("gnncg_sgd_update", param.numel(), lr, _ptr(grad), _ptr(param), _stream())
@@ -204,34 +260,6 @@ class CudaEngine:
     def total(self, x, out):
         ws = torch.empty(_lib.lib().gnncg_sum_workspace(), dtype=torch.uint8, device=self.device)
         call("gnncg_sum", x.numel(), _ptr(x), _ptr(out), _ptr(ws), ws.numel(), _stream())
-
-
-class Comm:
-    """torch.distributed collectives over the padded row-block layout."""
-
-    def __init__(self, group=None):
-        self.group = group
-
-    def all_gather_rows(self, local: torch.Tensor, maxrows: int) -> torch.Tensor:
-        P = dist.get_world_size(self.group)
-        n, cols = local.shape
-        if n == maxrows:
-            send = local.contiguous()
-        else:
-            send = torch.zeros(maxrows, cols, dtype=local.dtype, device=local.device)
-            send[:n] = local
-        out = torch.empty(P * maxrows, cols, dtype=local.dtype, device=local.device)
-        dist.all_gather_into_tensor(out, send, group=self.group)
-        return out
-
-    def reduce_scatter_rows(self, full: torch.Tensor, maxrows: int, n: int) -> torch.Tensor:
-        out = torch.empty(maxrows, full.shape[1], dtype=full.dtype, device=full.device)
-        dist.reduce_scatter_tensor(out, full.contiguous(), op=dist.ReduceOp.SUM, group=self.group)
-        return out[:n]
-
-    def all_reduce(self, t: torch.Tensor) -> torch.Tensor:
-        dist.all_reduce(t, op=dist.ReduceOp.SUM, group=self.group)
-        return t
 
 
 @dataclass
@@ -248,8 +276,10 @@ class PartitionedGAT:
 
     def __init__(self, lg: LocalGraph, dims, seed=0, slope=0.2, chunk=None, engine=None, params=None):
         self.lg = lg
-        self.engine = engine or CudaEngine(torch.device("cuda", torch.cuda.current_device()), chunk)
-        self.comm = Comm()
+        if engine is None:
+            dev = torch.device("cuda", torch.cuda.current_device())
+            engine = CudaEngine(dev, chunk, comm=NcclComm() if dist.is_initialized() else None)
+        self.engine = engine
         self.layers = []
         if params is None:
             from .models import init_uniform
@@ -268,36 +298,34 @@ class PartitionedGAT:
         return self.lg.num_local
 
     def forward(self, H):
-        E, lg, mr = self.engine, self.lg, self.lg.plan.maxrows
+        E, lg = self.engine, self.lg
+        Vp, b, n = lg.plan.padded_V, lg.row_base, lg.num_local
         xs, stashes = [H], []
         for L in self.layers:
-            Ht_local, Al_local, Ar_local = E.transform(xs[-1], L.W, L.a_l, L.a_r, L.p)
-            Ht = self.comm.all_gather_rows(Ht_local, mr)
-            Al = self.comm.all_gather_rows(Al_local, mr)
-            out, m, d = E.region_fwd(lg, Ht, Al, Ar_local, L.p)
+            h, hf = L.p.heads, L.p.heads * L.p.f
+            Ht_all, Al_all = E.empty(Vp, hf), E.empty(Vp, h)
+            Ar = E.transform(xs[-1], L.W, L.a_l, L.a_r, L.p, Ht_all[b:b + n], Al_all[b:b + n])
+            out, m, d = E.region_fwd(lg, Ht_all, Al_all, Ar, L.p)
             xs.append(out)
-            stashes.append((Ht, Ht_local, Al, Ar_local, m, d, out))
+            stashes.append((Ht_all, Al_all, Ar, m, d, out))
         return xs, stashes
 
     def backward(self, xs, stashes, dOut):
         E, lg = self.engine, self.lg
-        mr, n = lg.plan.maxrows, lg.num_local
+        b, n = lg.row_base, lg.num_local
         grads = [None] * len(self.layers)
         g = dOut
         for i in reversed(range(len(self.layers))):
             L = self.layers[i]
-            Ht, Ht_local, Al, Ar_local, m, d, out = stashes[i]
-            dHt_part, dAl_part, dAr = E.region_bwd(lg, Ht, Al, Ar_local, m, d, g, L.a_l, L.a_r, L.p, out=out)
-            dHt = self.comm.reduce_scatter_rows(dHt_part, mr, n)
-            dAl = self.comm.reduce_scatter_rows(dAl_part, mr, n)
-            da_l, da_r = E.attn_grad(Ht_local, dAl, dAr, L.p)  # owned rows only; summed by the all-reduce
-            dW = E.gemm(xs[i], dHt, ta=True)
-            packed = torch.cat([dW.reshape(-1), da_l.reshape(-1), da_r.reshape(-1)])
-            self.comm.all_reduce(packed)
-            nW = dW.numel()
-            dW = packed[:nW].view_as(dW)
-            da_l = packed[nW:nW + da_l.numel()].view_as(da_l)
-            da_r = packed[nW + da_l.numel():].view_as(da_r)
+            Ht_all, Al_all, Ar, m, d, out = stashes[i]
+            dHt, dAl, dAr = E.region_bwd(lg, Ht_all, Al_all, Ar, m, d, out, g, L.a_l, L.a_r, L.p)
+            # (dW, da_l, da_r) in one buffer: one all-reduce, no packing copies
+            nW, hf = L.W.numel(), L.a_l.numel()
+            packed = E.empty(nW + 2 * hf)
+            dW, da_l, da_r = packed[:nW].view_as(L.W), packed[nW:nW + hf].view_as(L.a_l), packed[nW + hf:].view_as(L.a_r)
+            E.attn_grad(Ht_all[b:b + n], dAl, dAr, L.p, out=(da_l, da_r))  # owned rows; summed by the all-reduce
+            E.gemm(xs[i], dHt, ta=True, out=dW)
+            E.all_reduce(packed)
             dH = E.gemm(dHt, L.W, tb=True) if i > 0 else None
             grads[i] = (dW, da_l, da_r, dH)
             g = dH
@@ -307,7 +335,7 @@ class PartitionedGAT:
         xs, stashes = self.forward(H)
         out = xs[-1]
         self.engine.total(out, self.loss)
-        self.comm.all_reduce(self.loss)
+        self.engine.all_reduce(self.loss)
         grads = self.backward(xs, stashes, self.engine.fill_ones(out))
         for L, (dW, da_l, da_r, _) in zip(self.layers, grads):
             self.engine.sgd(L.W, dW, lr)

@@ -93,6 +93,9 @@ def _f32_rows(t: torch.Tensor, name: str) -> torch.Tensor:
 def _shape(t: torch.Tensor, shape, name: str):
     if tuple(t.shape) != tuple(shape):
         raise TensorError(f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
+    if t.dtype != torch.float32 or not t.is_contiguous():
+        raise TensorError(f"{name}: expected a contiguous float32 tensor")
+    return t
 
 
 # ---------------------------------------------------------------------------
@@ -234,15 +237,16 @@ def attn_dots(Ht, a_l, a_r, heads, f, Al=None, Ar=None):
     return Al, Ar
 
 
-def gat_transform(H, W, a_l, a_r, heads, f, ws=None):
+def gat_transform(H, W, a_l, a_r, heads, f, ws=None, Ht=None, Al=None, Ar=None):
     """K1 with the attention-LP epilogue: Ht = H W, A_l = Ht . a_l, A_r = Ht . a_r in one
-    tensor-core GEMM (gnncg_gat_transform)."""
+    tensor-core GEMM (gnncg_gat_transform).  Ht / Al / Ar may be given (contiguous, e.g. a
+    rank's block of the all-gather tables)."""
     M, K = H.shape
     hf = heads * f
     dev = H.device
-    Ht = torch.empty(M, hf, device=dev)
-    Al = torch.empty(M, heads, device=dev)
-    Ar = torch.empty(M, heads, device=dev)
+    Ht = torch.empty(M, hf, device=dev) if Ht is None else _shape(Ht, (M, hf), "Ht")
+    Al = torch.empty(M, heads, device=dev) if Al is None else _shape(Al, (M, heads), "Al")
+    Ar = torch.empty(M, heads, device=dev) if Ar is None else _shape(Ar, (M, heads), "Ar")
     need = _lib.lib().gnncg_gemm_workspace(0, 0, M, hf, K)
     if ws is None:
         buf = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)

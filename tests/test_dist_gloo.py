@@ -1,10 +1,14 @@
 """CPU, world_size 2 and 3 over gloo: the multi-GPU orchestration of dist.py (row
-partition, padded all-gather of Ht, K4 partials reduce-scattered, dW / da all-reduced,
-SGD in lock-step) reproduces the single-process f64 oracle.
+partition, edges split by source owner, padded all-gather of Ht || A_l, the two-part forward
+with its online-softmax merge, the two-pass backward whose remote partials are
+reduce-scattered, dW / da all-reduced, SGD in lock-step) reproduces the single-process f64
+oracle.
 
-The product engine (CudaEngine) cannot run here; the same PartitionedGAT schedule is
-driven by an oracle-backed engine (test infrastructure) whose region backward is an
-independent per-edge numpy restatement of K3/K4 on the rank-local indexes."""
+The product engine (CudaEngine + gnncg_gat_*_dist) cannot run here; the same PartitionedGAT
+schedule is driven by an oracle-backed engine (test infrastructure) that restates
+gnncg_gat_fwd_dist / gnncg_gat_bwd_dist per edge in numpy on the rank-local indexes.  The
+GPU side of the same entry points is tested by tests/test_gpu_dist.py (world 1 over NCCL and
+P ranks emulated on one GPU)."""
 import os
 import socket
 
@@ -17,62 +21,124 @@ import torch.multiprocessing as mp
 from oracle import oracle as O
 
 
+def merge2(A, B):
+    """Online-softmax merge of two partials (out, m, d) of the same rows (gnncg_gat_fwd_dist)."""
+    (oa, ma, da), (ob, mb, db) = A, B
+    M = np.where(da == 0, mb, np.where(db == 0, ma, np.maximum(ma, mb)))
+    ea = np.where(da == 0, 0.0, da * np.exp(ma - M))
+    eb = np.where(db == 0, 0.0, db * np.exp(mb - M))
+    D = ea + eb
+    wa = np.divide(ea, D, out=np.zeros_like(D), where=D > 0)
+    wb = np.divide(eb, D, out=np.zeros_like(D), where=D > 0)
+    h = M.shape[1]
+    f = oa.shape[1] // h
+    out = (np.repeat(wa, f, 1) * oa + np.repeat(wb, f, 1) * ob)
+    return out, M, D
+
+
+class _Idx(dict):
+    """An oracle-side index: the dict of O.build_index outputs, with num_edges as an attribute."""
+
+    @property
+    def num_edges(self):
+        return self["num_edges"]
+
+
 class OracleEngine:
     device = torch.device("cpu")
 
     def build_index(self, rows, key, other, n_other):
-        off, nbr, eid = O.build_index(rows, key.numpy().astype(np.uint32), other.numpy().astype(np.uint32))
-        return dict(off=off, nbr=nbr, eid=eid, rows=rows)
+        key, other = key.numpy().astype(np.int64), other.numpy().astype(np.int64)
+        assert key.size == 0 or (key.max() < rows and other.max() < n_other)
+        off, nbr, eid = O.build_index(rows, key.astype(np.uint32), other.astype(np.uint32))
+        return _Idx(off=off, nbr=nbr, eid=eid, rows=rows, num_edges=key.size)
 
     def zeros(self, *s):
         return torch.zeros(*s, dtype=torch.float64)
 
-    def empty(self, *s):
-        return torch.zeros(*s, dtype=torch.float64)
+    empty = zeros
 
-    def gemm(self, A, B, ta=False, tb=False):
-        return (A.T if ta else A) @ (B.T if tb else B)
+    def gemm(self, A, B, ta=False, tb=False, out=None):
+        r = (A.T if ta else A) @ (B.T if tb else B)
+        if out is None:
+            return r
+        out.copy_(r)
+        return out
 
-    def attn_dots(self, Ht, a_l, a_r, p):
-        H3 = Ht.view(Ht.shape[0], p.heads, p.f)
-        return (H3 * a_l).sum(-1), (H3 * a_r).sum(-1)
-
-    def transform(self, H, W, a_l, a_r, p):
+    def transform(self, H, W, a_l, a_r, p, Ht_out, Al_out):
         Ht = H @ W
-        return (Ht, *self.attn_dots(Ht, a_l, a_r, p))
+        H3 = Ht.view(Ht.shape[0], p.heads, p.f)
+        Ht_out.copy_(Ht)
+        Al_out.copy_((H3 * a_l).sum(-1))
+        return (H3 * a_r).sum(-1)
 
-    def region_fwd(self, lg, Ht, Al, Ar_local, p):
-        c = lg.csr
-        g = O.HostGraph(c["rows"], None, None, c["off"], c["nbr"], c["eid"], None, None, None)
-        r = O.gat_region_fwd_f64(g, Ht.numpy(), Al.numpy(), Ar_local.numpy(), p.heads, p.f, p.slope)
-        return torch.from_numpy(r["out"]), torch.from_numpy(r["m"]), torch.from_numpy(r["d"])
+    @staticmethod
+    def _edges(idx):
+        """(v = local destination row, u = neighbour) of a csr index, in index order."""
+        v = np.repeat(np.arange(idx["rows"]), np.diff(idx["off"].astype(np.int64)))
+        return v, idx["nbr"].astype(np.int64)
 
-    def region_bwd(self, lg, Ht, Al, Ar_local, m, d, dOut, a_l, a_r, p, out=None):
-        h, f, n, base = p.heads, p.f, lg.num_local, lg.row_base
-        c = lg.csr
-        v = np.repeat(np.arange(n), np.diff(c["off"].astype(np.int64)))
-        u = c["nbr"].astype(np.int64)
-        Ht3, dO3 = Ht.numpy().reshape(-1, h, f), dOut.numpy().reshape(n, h, f)
-        Ar = Ar_local.numpy()
-        z = Al.numpy()[u] + Ar[v]
-        s = np.where(z > 0, z, p.slope * z)
-        a = np.exp(s - m.numpy()[v]) / d.numpy()[v]
-        da = (dO3[v] * Ht3[u]).sum(-1)
-        cc = np.zeros((n, h))
-        np.add.at(cc, v, a * da)
-        dz = np.where(z > 0, 1.0, p.slope) * a * (da - cc[v])
-        Vp = lg.plan.padded_V
-        dAl, dAr, dHt = np.zeros((Vp, h)), np.zeros((n, h)), np.zeros((Vp, h, f))
-        np.add.at(dAl, u, dz)
-        np.add.at(dAr, v, dz)
-        np.add.at(dHt, u, a[:, :, None] * dO3[v])
-        dHt += dAl[:, :, None] * a_l.numpy()[None]
-        dHt[base:base + n] += dAr[:, :, None] * a_r.numpy()[None]
-        return torch.from_numpy(dHt.reshape(Vp, h * f)), torch.from_numpy(dAl), torch.from_numpy(dAr)
+    def _region(self, idx, Ht, Al, Ar, p):
+        g = O.HostGraph(idx["rows"], None, None, idx["off"], idx["nbr"], idx["eid"], None, None, None)
+        r = O.gat_region_fwd_f64(g, Ht, Al, Ar, p.heads, p.f, p.slope)
+        return r["out"], r["m"], r["d"]
 
-    def attn_grad(self, Ht, dAl, dAr, p):
-        H3 = Ht.view(-1, p.heads, p.f)
-        return (dAl[:, :, None] * H3).sum(0), (dAr[:, :, None] * H3).sum(0)
+    def region_fwd(self, lg, Ht_all, Al_all, Ar, p):
+        mr, b = lg.plan.maxrows, lg.row_base
+        for t in (Ht_all, Al_all):  # the all-gather of the rank's block
+            dist.all_gather_into_tensor(t, t[b:b + mr].clone())
+        Ht, Al, Arn = Ht_all.numpy(), Al_all.numpy(), Ar.numpy()
+        A = self._region(lg.csr_local, Ht, Al, Arn, p)
+        B = self._region(lg.csr_remote, Ht, Al, Arn, p)
+        return tuple(torch.from_numpy(x) for x in merge2(A, B))
+
+    def region_bwd(self, lg, Ht_all, Al_all, Ar, m, d, out, dOut, a_l, a_r, p):
+        h, f, n, b, mr, Vp = p.heads, p.f, lg.num_local, lg.row_base, lg.plan.maxrows, lg.plan.padded_V
+        Ht3, Al, Arn = Ht_all.numpy().reshape(-1, h, f), Al_all.numpy(), Ar.numpy()
+        dO3, mn, dn = dOut.numpy().reshape(n, h, f), m.numpy(), d.numpy()
+        al, ar = a_l.numpy(), a_r.numpy()
+
+        def edge_terms(idx):
+            v, u = self._edges(idx)
+            z = Al[u] + Arn[v]
+            a = np.exp(np.where(z > 0, z, p.slope * z) - mn[v]) / dn[v]
+            da = (dO3[v] * Ht3[u]).sum(-1)
+            return v, u, z, a, da
+
+        parts = [edge_terms(lg.csr_remote), edge_terms(lg.csr_local)]
+        c = np.zeros((n, h))
+        for v, u, z, a, da in parts:  # c[v] over ALL in-edges of v (both parts)
+            np.add.at(c, v, a * da)
+        dAr = np.zeros((n, h))
+        outs = []
+        for (v, u, z, a, da), rows, shift in zip(parts, (Vp, n), (0, b)):
+            dz = np.where(z > 0, 1.0, p.slope) * a * (da - c[v])
+            dHt, dAl = np.zeros((rows, h, f)), np.zeros((rows, h))
+            np.add.at(dAl, u - shift, dz)
+            np.add.at(dAr, v, dz)
+            np.add.at(dHt, u - shift, a[:, :, None] * dO3[v])
+            dHt += dAl[:, :, None] * al[None]
+            outs.append((dHt.reshape(rows, h * f), dAl))
+        (sendH, sendAl), (ownH, ownAl) = outs
+        recvH, recvAl = torch.zeros(mr, h * f, dtype=torch.float64), torch.zeros(mr, h, dtype=torch.float64)
+        dist.reduce_scatter_tensor(recvH, torch.from_numpy(sendH))
+        dist.reduce_scatter_tensor(recvAl, torch.from_numpy(sendAl))
+        dHt = ownH + recvH.numpy()[:n] + np.repeat(dAr, f, 1) * ar.reshape(1, h * f)
+        dAl = ownAl + recvAl.numpy()[:n]
+        return torch.from_numpy(dHt), torch.from_numpy(dAl), torch.from_numpy(dAr)
+
+    def attn_grad(self, Ht, dAl, dAr, p, out=None):
+        H3 = Ht.reshape(-1, p.heads, p.f)
+        r = ((dAl[:, :, None] * H3).sum(0), (dAr[:, :, None] * H3).sum(0))
+        if out is None:
+            return r
+        for o, x in zip(out, r):
+            o.copy_(x)
+        return out
+
+    def all_reduce(self, t):
+        dist.all_reduce(t)
+        return t
 
     def sgd(self, param, grad, lr):
         param -= lr * grad
@@ -82,6 +148,11 @@ class OracleEngine:
 
     def total(self, x, out):
         out[0] = x.sum()
+
+
+def _pairs(idx, transpose=False):
+    v, u = OracleEngine._edges(idx)
+    return sorted(zip(u.tolist(), v.tolist())) if transpose else sorted(zip(v.tolist(), u.tolist()))
 
 
 def _free_port():
@@ -101,6 +172,13 @@ def _worker(rank, world, port, case, q):
         plan = PartitionPlan.from_dst(V, torch.from_numpy(dst.astype(np.int64)), world)
         lg = build_local(plan, rank, torch.from_numpy(src.astype(np.int64)), torch.from_numpy(dst.astype(np.int64)),
                          eng)
+        # the csc indexes are the transposes of the csr ones (csc_local rows rebased to the block)
+        base = lg.row_base
+        assert _pairs(lg.csr_remote) == sorted(_pairs(lg.csc_remote, transpose=True))
+        assert _pairs(lg.csr_local) == sorted((v, u + base) for v, u in _pairs(lg.csc_local, transpose=True))
+        assert all(base <= u < base + lg.num_local for _, u in _pairs(lg.csr_local))
+        assert not any(base <= u < base + lg.num_local for _, u in _pairs(lg.csr_remote))
+        assert lg.num_edges == int((dst >= plan.bounds[rank]).sum() - (dst >= plan.bounds[rank + 1]).sum())
         r0, r1 = int(plan.bounds[rank]), int(plan.bounds[rank + 1])
         tparams = [tuple(torch.from_numpy(x.copy()) for x in p) for p in params]
         model = PartitionedGAT(lg, dims, engine=eng, params=tparams)
@@ -130,7 +208,17 @@ def test_partitioned_gat_matches_single_process_oracle(world):
     procs = [ctx.Process(target=_worker, args=(r, world, port, (V, src, dst, H, params, dims), q)) for r in range(world)]
     for p in procs:
         p.start()
-    res = sorted(q.get(timeout=300) for _ in range(world))
+    import queue
+    import time
+
+    res, t0 = [], time.time()
+    while len(res) < world:  # fail fast when a rank dies instead of waiting out the queue
+        try:
+            res.append(q.get(timeout=2))
+        except queue.Empty:
+            dead = [p.exitcode for p in procs if p.exitcode not in (None, 0)]
+            assert not dead and time.time() - t0 < 300, f"rank exit codes {dead}"
+    res.sort(key=lambda r: r[0])
     for p in procs:
         p.join(timeout=60)
         assert p.exitcode == 0

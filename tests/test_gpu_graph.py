@@ -74,12 +74,21 @@ def test_per_rank_chung_lu_equals_filtered_global_list(cuda, P):
         lg = partitioned_chung_lu(V, E, offset=off, seed=seed, rank=rank, world=P, device=cuda)
         np.testing.assert_array_equal(lg.plan.bounds, bounds)
         r0, r1 = int(bounds[rank]), int(bounds[rank + 1])
-        loff, lnbr, _ = lg.csr.to_host()
-        np.testing.assert_array_equal(loff, ref.dst_off[r0:r1 + 1] - ref.dst_off[r0])
+        mr, base, n = lg.plan.maxrows, lg.row_base, r1 - r0
+        ref_off = ref.dst_off[r0:r1 + 1].astype(np.int64)
+        ref_src = ref.dst_src[ref.dst_off[r0]:ref.dst_off[r1]].astype(np.int64)
+        ref_row = np.repeat(np.arange(n), np.diff(ref_off))
+        own = (ref_src >= r0) & (ref_src < r1)
         # local source ids live in the padded all-gather layout: map back to global ids
-        pid = lnbr.astype(np.int64)
-        owner = pid // lg.plan.maxrows
-        gsrc = lg.plan.bounds[owner].astype(np.int64) + pid % lg.plan.maxrows
-        np.testing.assert_array_equal(gsrc, ref.dst_src[ref.dst_off[r0]:ref.dst_off[r1]])
-        total += int(loff[-1])
+        pid_to_global = lambda pid: lg.plan.bounds[pid // mr].astype(np.int64) + pid % mr  # noqa: E731
+        for idx, sel in ((lg.csr_local, own), (lg.csr_remote, ~own)):
+            loff, lnbr, _ = idx.to_host()
+            # each part is the global row block filtered by source owner, in edge-id order
+            np.testing.assert_array_equal(np.diff(loff.astype(np.int64)), np.bincount(ref_row[sel], minlength=n))
+            np.testing.assert_array_equal(pid_to_global(lnbr.astype(np.int64)), ref_src[sel])
+        # csc_local: own sources rebased to the block, rows sorted by source then edge id
+        coff, cnbr, _ = lg.csc_local.to_host()
+        np.testing.assert_array_equal(np.diff(coff.astype(np.int64)), np.bincount(ref_src[own] - r0, minlength=n))
+        assert lg.csc_remote.num_rows == lg.plan.padded_V and lg.csc_remote.num_edges == int((~own).sum())
+        total += int(lg.num_edges)
     assert total == E
