@@ -139,29 +139,40 @@ class DeviceGraph {
  private:
   void build(DeviceIndex& idx, const DeviceBuffer& key, const DeviceBuffer& other, DeviceBuffer& ws,
              std::int32_t chunk) {
-    idx.rows = V_;
-    idx.edges = E_;
-    idx.off = DeviceBuffer((V_ + 1) * sizeof(std::uint64_t));
-    idx.nbr = DeviceBuffer(E_ * sizeof(std::uint32_t));
-    idx.eid = DeviceBuffer(E_ * sizeof(std::uint32_t));
-    check(gnncg_csr_build(V_, E_, key.get<std::uint32_t>(), other.get<std::uint32_t>(), idx.off.get<std::uint64_t>(),
-                          idx.nbr.get<std::uint32_t>(), idx.eid.get<std::uint32_t>(), ws.get(), ws.bytes(), s_),
-          "gnncg_csr_build");
-    std::vector<std::uint64_t> off(V_ + 1);
-    cuda_check(cudaMemcpyAsync(off.data(), idx.off.get(), off.size() * 8, cudaMemcpyDeviceToHost, s_), "offsets");
-    cuda_check(cudaStreamSynchronize(s_), "sync");
+    build_index(idx, V_, V_, E_, key.get<std::uint32_t>(), other.get<std::uint32_t>(), ws, chunk, s_);
+  }
+
+ public:
+  // One index of `rows` rows over neighbour ids [0, n_other) from device key / other arrays
+  // (gnncg_csr_build_rect: the reference's counting sort, stable in edge id) plus its schedule.
+  static void build_index(DeviceIndex& idx, std::int64_t rows, std::int64_t n_other, std::int64_t E,
+                          const std::uint32_t* key, const std::uint32_t* other, DeviceBuffer& ws, std::int32_t chunk,
+                          cudaStream_t s) {
+    ws.ensure(gnncg_csr_build_workspace(rows, E));
+    idx.rows = rows;
+    idx.edges = E;
+    idx.off = DeviceBuffer((rows + 1) * sizeof(std::uint64_t));
+    idx.nbr = DeviceBuffer(std::max<std::int64_t>(E, 1) * sizeof(std::uint32_t));
+    idx.eid = DeviceBuffer(std::max<std::int64_t>(E, 1) * sizeof(std::uint32_t));
+    check(gnncg_csr_build_rect(rows, n_other, E, key, other, idx.off.get<std::uint64_t>(), idx.nbr.get<std::uint32_t>(),
+                               idx.eid.get<std::uint32_t>(), ws.get(), ws.bytes(), s),
+          "gnncg_csr_build_rect");
+    std::vector<std::uint64_t> off(rows + 1);
+    cuda_check(cudaMemcpyAsync(off.data(), idx.off.get(), off.size() * 8, cudaMemcpyDeviceToHost, s), "offsets");
+    cuda_check(cudaStreamSynchronize(s), "sync");
     std::int64_t n = 0, ns = 0, nr = 0;
-    check(gnncg_sched_build_host(V_, off.data(), chunk, &n, &ns, &nr, nullptr, nullptr, nullptr), "sched");
-    std::vector<std::uint32_t> items(2 * n + 2), rows(nr + 1), first(nr + 1);
-    check(gnncg_sched_build_host(V_, off.data(), chunk, &n, &ns, &nr, items.data(), rows.data(), first.data()),
+    check(gnncg_sched_build_host(rows, off.data(), chunk, &n, &ns, &nr, nullptr, nullptr, nullptr), "sched");
+    std::vector<std::uint32_t> items(2 * n + 2), srows(nr + 1), first(nr + 1);
+    check(gnncg_sched_build_host(rows, off.data(), chunk, &n, &ns, &nr, items.data(), srows.data(), first.data()),
           "sched");
-    idx.items = upload(items.data(), items.size(), s_);
-    idx.split_rows = upload(rows.data(), rows.size(), s_);
-    idx.split_first = upload(first.data(), first.size(), s_);
+    idx.items = upload(items.data(), items.size(), s);
+    idx.split_rows = upload(srows.data(), srows.size(), s);
+    idx.split_first = upload(first.data(), first.size(), s);
     idx.sched = gnncg_sched_t{n, ns, nr, chunk, 0, idx.items.get<std::uint32_t>(), idx.split_rows.get<std::uint32_t>(),
                               idx.split_first.get<std::uint32_t>()};
   }
 
+ private:
   std::int64_t V_, E_;
   cudaStream_t s_;
   DeviceBuffer edge_src_, edge_dst_;
@@ -547,6 +558,223 @@ inline GcnGrads gcn_backward(const DeviceGraph& g, const Tensor<float>& H, const
     DeviceBuffer dHb(V * Fin * 4);
     detail::gemm(g, 0, 1, V, Fin, C, dHt.get<float>(), C, dWin.get<float>(), C, dHb.get<float>(), Fin);
     out.dH = download(dHb, V, Fin, s);
+  }
+  return out;
+}
+
+// ------------------------------------------------------------------ multi-GPU
+// One process per GPU, destination rows partitioned over the ranks (north_star).
+// A reference executor running P ranks calls these in place of its run_forward / run_backward
+// for the rank's rows; the collectives run inside the library
+// (gnncg_gat_fwd_dist / gnncg_gat_bwd_dist) over a Comm.
+
+// The library's NCCL communicator (gnncg_comm_t).  Rank 0 calls unique_id() and the caller
+// distributes the 128 bytes (MPI, a file, a TCP store ...); or wrap an existing ncclComm_t.
+class Comm {
+ public:
+  static std::vector<char> unique_id() {
+    std::vector<char> id(128);
+    check(gnncg_comm_unique_id(id.data()), "gnncg_comm_unique_id");
+    return id;
+  }
+  Comm(int nranks, int rank, const std::vector<char>& id) {
+    if (id.size() != 128) throw std::invalid_argument("Comm: the unique id is 128 bytes");
+    check(gnncg_comm_init(&c_, nranks, rank, id.data()), "gnncg_comm_init");
+  }
+  explicit Comm(void* nccl_comm) { check(gnncg_comm_init_nccl(&c_, nccl_comm), "gnncg_comm_init_nccl"); }
+  Comm(const Comm&) = delete;
+  Comm& operator=(const Comm&) = delete;
+  ~Comm() { gnncg_comm_destroy(c_); }
+  int size() const { return gnncg_comm_size(c_); }
+  int rank() const { return gnncg_comm_rank(c_); }
+  gnncg_comm_t* get() const { return c_; }
+
+ private:
+  gnncg_comm_t* c_ = nullptr;
+};
+
+// Rank `rank`'s share of a P-way destination-row partition of a gnncg::Graph: rows
+// [row_begin, row_end) = gnncg_partition_rows over the csr_dst offsets (edge-balanced), and
+// the rank's in-edges split by the owner of their source (see gnncg_part_t).
+class PartitionedGraph {
+ public:
+  PartitionedGraph(const Graph& g, int nparts, int rank, std::int32_t chunk = 2048, cudaStream_t stream = nullptr)
+      : P_(nparts), rank_(rank), s_(stream) {
+    check(gnncg_device_check(), "gnncg_device_check");
+    if (nparts < 1 || rank < 0 || rank >= nparts) throw std::invalid_argument("PartitionedGraph: bad rank / nparts");
+    const AdjIndex& in = g.csr_dst();
+    const std::int64_t V = (std::int64_t)g.num_vertices();
+    bounds_.resize(P_ + 1);
+    check(gnncg_partition_rows(V, in.offsets.data(), P_, bounds_.data()), "gnncg_partition_rows");
+    for (int q = 0; q < P_; ++q) maxrows_ = std::max<std::int64_t>(maxrows_, bounds_[q + 1] - bounds_[q]);
+    r0_ = (std::int64_t)bounds_[rank];
+    n_ = (std::int64_t)bounds_[rank + 1] - r0_;
+    const std::int64_t base = rank * maxrows_, Vp = P_ * maxrows_;
+    // the rank's in-edges (csr_dst rows r0.., edge-id order), split by source owner
+    std::vector<std::uint32_t> kl, ol, kr, orr;
+    for (std::int64_t v = 0; v < n_; ++v)
+      for (auto i = in.offsets[r0_ + v]; i < in.offsets[r0_ + v + 1]; ++i) {
+        const std::uint64_t u = in.entries[i].vertex;
+        const int q = (int)(std::upper_bound(bounds_.begin() + 1, bounds_.end(), u) - (bounds_.begin() + 1));
+        const std::uint32_t pid = (std::uint32_t)(q * maxrows_ + (std::int64_t)(u - bounds_[q]));
+        if (q == rank) {
+          kl.push_back((std::uint32_t)v);
+          ol.push_back(pid);
+        } else {
+          kr.push_back((std::uint32_t)v);
+          orr.push_back(pid);
+        }
+      }
+    DeviceBuffer ws;
+    auto two = [&](DeviceIndex& csr, DeviceIndex& csc, std::vector<std::uint32_t>& dst, std::vector<std::uint32_t>& src,
+                   std::int64_t csc_rows, std::int64_t shift) {
+      DeviceBuffer dk = upload(dst.data(), dst.size(), s_);
+      for (auto& x : src) x -= (std::uint32_t)shift;  // csc_local rows are rebased to the block
+      DeviceBuffer sk = upload(src.data(), src.size(), s_);
+      DeviceGraph::build_index(csc, csc_rows, n_, (std::int64_t)src.size(), sk.get<std::uint32_t>(),
+                               dk.get<std::uint32_t>(), ws, chunk, s_);
+      for (auto& x : src) x += (std::uint32_t)shift;
+      DeviceBuffer sk2 = upload(src.data(), src.size(), s_);
+      DeviceGraph::build_index(csr, n_, Vp, (std::int64_t)dst.size(), dk.get<std::uint32_t>(),
+                               sk2.get<std::uint32_t>(), ws, chunk, s_);
+    };
+    two(csr_l_, csc_l_, kl, ol, n_, base);
+    two(csr_r_, csc_r_, kr, orr, Vp, 0);
+    views_[0] = csr_l_.view(); views_[1] = csr_r_.view(); views_[2] = csc_l_.view(); views_[3] = csc_r_.view();
+    part_ = gnncg_part_t{n_, maxrows_, P_, rank_, &views_[0], &csr_l_.sched, &views_[1], &csr_r_.sched,
+                         &views_[2], &csc_l_.sched, &views_[3], &csc_r_.sched};
+  }
+  PartitionedGraph(const PartitionedGraph&) = delete;
+  PartitionedGraph& operator=(const PartitionedGraph&) = delete;
+
+  int nparts() const { return P_; }
+  int rank() const { return rank_; }
+  std::int64_t row_begin() const { return r0_; }
+  std::int64_t num_local() const { return n_; }
+  std::int64_t maxrows() const { return maxrows_; }
+  const gnncg_part_t* part() const { return &part_; }
+  cudaStream_t stream() const { return s_; }
+  DeviceBuffer& workspace(size_t bytes) const {
+    ws_.ensure(bytes);
+    return ws_;
+  }
+
+ private:
+  int P_, rank_;
+  cudaStream_t s_;
+  std::vector<std::uint64_t> bounds_;
+  std::int64_t maxrows_ = 0, r0_ = 0, n_ = 0;
+  DeviceIndex csr_l_, csr_r_, csc_l_, csc_r_;
+  gnncg_index_t views_[4];
+  gnncg_part_t part_{};
+  mutable DeviceBuffer ws_;
+};
+
+// Forward state of a rank: the gathered source tables (padded layout) and its rows' stash.
+struct DistStash {
+  DeviceBuffer Ht_all, Al_all, Ar, m, d, out;
+};
+
+namespace detail {
+inline void require_comm(const PartitionedGraph& pg, const Comm* comm) {
+  if (!comm && pg.nparts() > 1) throw std::invalid_argument("gat_*_dist: nparts > 1 needs a Comm");
+  if (comm && comm->size() != pg.nparts()) throw std::invalid_argument("gat_*_dist: Comm size != nparts");
+}
+}  // namespace detail
+
+// GAT layer forward of one rank: H_local = the rank's rows of H; returns its rows of out.
+inline Tensor<float> gat_forward_dist(const PartitionedGraph& pg, const Comm* comm, const Tensor<float>& H_local,
+                                      const Tensor<float>& W, const Tensor<float>& a_l, const Tensor<float>& a_r,
+                                      const GatParams& p, DistStash* stash) {
+  detail::require_comm(pg, comm);
+  const std::int64_t n = pg.num_local(), h = p.heads, f = p.f, hf = h * f, Vp = pg.nparts() * pg.maxrows();
+  const std::int64_t base = pg.rank() * pg.maxrows();
+  detail::require_shape(H_local, n, H_local.cols, "gat_forward_dist H");
+  detail::require_shape(W, H_local.cols, hf, "gat_forward_dist W");
+  detail::require_shape(a_l, h, f, "gat_forward_dist a_l");
+  detail::require_shape(a_r, h, f, "gat_forward_dist a_r");
+  cudaStream_t s = pg.stream();
+  DistStash local;
+  DistStash& st = stash ? *stash : local;
+  DeviceBuffer dH = upload(H_local, s), dW = upload(W, s), dal = upload(a_l, s), dar = upload(a_r, s);
+  st.Ht_all = DeviceBuffer(std::max<std::int64_t>(Vp, 1) * hf * 4);
+  st.Al_all = DeviceBuffer(std::max<std::int64_t>(Vp, 1) * h * 4);
+  const std::int64_t nn = std::max<std::int64_t>(n, 1);
+  st.Ar = DeviceBuffer(nn * h * 4);
+  st.m = DeviceBuffer(nn * h * 4);
+  st.d = DeviceBuffer(nn * h * 4);
+  st.out = DeviceBuffer(nn * hf * 4);
+  if (n > 0) {  // K1 into this rank's block of the gather tables
+    DeviceBuffer& gws = pg.workspace(gnncg_gemm_workspace(0, 0, n, hf, H_local.cols));
+    check(gnncg_gat_transform(n, H_local.cols, h, f, dH.get<float>(), H_local.cols, dW.get<float>(),
+                              st.Ht_all.get<float>() + base * hf, dal.get<float>(), dar.get<float>(),
+                              st.Al_all.get<float>() + base * h, st.Ar.get<float>(), gws.get(), gws.bytes(), s),
+          "gnncg_gat_transform");
+  }
+  DeviceBuffer& ws = pg.workspace(gnncg_gat_dist_workspace(pg.part(), h, f));
+  check(gnncg_gat_fwd_dist(comm ? comm->get() : nullptr, pg.part(), h, f, p.slope, st.Ht_all.get<float>(),
+                           st.Al_all.get<float>(), st.Ar.get<float>(), st.out.get<float>(), st.m.get<float>(),
+                           st.d.get<float>(), ws.get(), ws.bytes(), s),
+        "gnncg_gat_fwd_dist");
+  return download(st.out, n, hf, s);
+}
+
+// GAT layer backward of one rank (fused fast mode): dW / da_l / da_r are summed over the ranks
+// (all-reduce); dH is the rank's rows.
+inline GatGrads gat_backward_dist(const PartitionedGraph& pg, const Comm* comm, const Tensor<float>& H_local,
+                                  const Tensor<float>& W, const Tensor<float>& a_l, const Tensor<float>& a_r,
+                                  const DistStash& st, const Tensor<float>& dOut_local, const GatParams& p,
+                                  bool need_dH) {
+  detail::require_comm(pg, comm);
+  const std::int64_t n = pg.num_local(), h = p.heads, f = p.f, hf = h * f, Fin = H_local.cols;
+  const std::int64_t Vp = pg.nparts() * pg.maxrows(), base = pg.rank() * pg.maxrows(), nn = std::max<std::int64_t>(n, 1);
+  detail::require_shape(dOut_local, n, hf, "gat_backward_dist dOut");
+  detail::require_shape(W, Fin, hf, "gat_backward_dist W");
+  cudaStream_t s = pg.stream();
+  DeviceBuffer dH_in = upload(H_local, s), dW_in = upload(W, s), dal = upload(a_l, s), dar = upload(a_r, s);
+  DeviceBuffer g_out = upload(dOut_local, s);
+  DeviceBuffer dHt(nn * hf * 4), dAl(nn * h * 4), dAr(nn * h * 4);
+  DeviceBuffer sendH(std::max<std::int64_t>(Vp, 1) * hf * 4), sendAl(std::max<std::int64_t>(Vp, 1) * h * 4);
+  DeviceBuffer packed((Fin * hf + 2 * hf) * 4);
+  float* dW = packed.get<float>();
+  float* da_l = dW + Fin * hf;
+  float* da_r = da_l + hf;
+  {
+    DeviceBuffer& ws = pg.workspace(gnncg_gat_dist_workspace(pg.part(), h, f));
+    check(gnncg_gat_bwd_dist(comm ? comm->get() : nullptr, pg.part(), h, f, p.slope, st.Ht_all.get<float>(),
+                             st.Al_all.get<float>(), st.Ar.get<float>(), st.m.get<float>(), st.d.get<float>(),
+                             st.out.get<float>(), g_out.get<float>(), dal.get<float>(), dar.get<float>(),
+                             dHt.get<float>(), dAl.get<float>(), dAr.get<float>(), sendH.get<float>(),
+                             sendAl.get<float>(), ws.get(), ws.bytes(), s),
+          "gnncg_gat_bwd_dist");
+  }
+  {
+    DeviceBuffer& ws = pg.workspace(gnncg_gat_attn_grad_workspace(n, h, f));
+    check(gnncg_gat_attn_grad(n, h, f, st.Ht_all.get<float>() + base * hf, dAl.get<float>(), dAr.get<float>(), da_l,
+                              da_r, ws.get(), ws.bytes(), s),
+          "gnncg_gat_attn_grad");
+  }
+  {
+    DeviceBuffer& ws = pg.workspace(gnncg_gemm_workspace(1, 0, Fin, hf, n));
+    check(gnncg_gemm(1, 0, Fin, hf, n, dH_in.get<float>(), Fin, dHt.get<float>(), hf, dW, hf, ws.get(), ws.bytes(), s),
+          "gnncg_gemm");
+  }
+  if (comm) check(gnncg_comm_allreduce(comm->get(), dW, Fin * hf + 2 * hf, s), "gnncg_comm_allreduce");
+  GatGrads out;
+  const Tensor<float> all = download(packed, 1, Fin * hf + 2 * hf, s);
+  out.dW = Tensor<float>(Fin, hf);
+  out.da_l = Tensor<float>(h, f);
+  out.da_r = Tensor<float>(h, f);
+  std::copy(all.data.begin(), all.data.begin() + Fin * hf, out.dW.data.begin());
+  std::copy(all.data.begin() + Fin * hf, all.data.begin() + Fin * hf + hf, out.da_l.data.begin());
+  std::copy(all.data.begin() + Fin * hf + hf, all.data.end(), out.da_r.data.begin());
+  if (need_dH) {
+    DeviceBuffer dHb(nn * Fin * 4);
+    DeviceBuffer& ws = pg.workspace(gnncg_gemm_workspace(0, 1, n, Fin, hf));
+    check(gnncg_gemm(0, 1, n, Fin, hf, dHt.get<float>(), hf, dW_in.get<float>(), hf, dHb.get<float>(), Fin, ws.get(),
+                     ws.bytes(), s),
+          "gnncg_gemm");
+    out.dH = download(dHb, n, Fin, s);
   }
   return out;
 }

@@ -66,11 +66,72 @@ int main() {
       }
     }
   }
-  // dW through a finite difference of the (double) loss on one entry, as a smoke of the backward.
-  std::printf("gat forward max rel_err = %.3e ; dW[0][0] = %.6f ; dH rows = %llu\n", worst, gr.dW.at(0, 0),
-              (unsigned long long)gr.dH.rows);
-  bool ok = worst < 1e-4 && gr.dW.rows == (std::uint64_t)Fin && gr.dH.rows == V && all_finite(gr.dW) &&
-            all_finite(gr.dH) && all_finite(gr.da_l);
+  // f64 restatement of the backward (stash-everything per-edge chain rule),
+  // loss = sum of exits: dOut = 1.  Compared elementwise with rel_err (tensor.hpp:153-156).
+  std::vector<double> dHt(V * hf, 0.0), dAl(V * h, 0.0), dAr(V * h, 0.0), c(V * h, 0.0);
+  {
+    std::vector<double> mxv(V * h), den(V * h);
+    auto z_of = [&](std::uint64_t u, std::uint64_t v, int k) { return Al[u * h + k] + Ar[v * h + k]; };
+    for (std::uint64_t v = 0; v < V; ++v)
+      for (int k = 0; k < h; ++k) {
+        double mx = -std::numeric_limits<double>::infinity(), dn = 0;
+        for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i) mx = std::max(mx, lrelu(z_of(in.entries[i].vertex, v, k)));
+        for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i) dn += std::exp(lrelu(z_of(in.entries[i].vertex, v, k)) - mx);
+        mxv[v * h + k] = mx;
+        den[v * h + k] = dn;
+      }
+    auto alpha = [&](std::uint64_t u, std::uint64_t v, int k) {
+      return std::exp(lrelu(z_of(u, v, k)) - mxv[v * h + k]) / den[v * h + k];
+    };
+    auto dalpha = [&](std::uint64_t u, std::uint64_t v, int k) {
+      double s = 0;
+      for (int j = 0; j < f; ++j) s += (double)dOut.at(v, k * f + j) * Ht.at(u, k * f + j);
+      return s;
+    };
+    for (std::uint64_t v = 0; v < V; ++v)
+      for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i)
+        for (int k = 0; k < h; ++k) c[v * h + k] += alpha(in.entries[i].vertex, v, k) * dalpha(in.entries[i].vertex, v, k);
+    for (std::uint64_t v = 0; v < V; ++v)
+      for (auto i = in.offsets[v]; i < in.offsets[v + 1]; ++i) {
+        const auto u = in.entries[i].vertex;
+        for (int k = 0; k < h; ++k) {
+          const double a = alpha(u, v, k), z = z_of(u, v, k);
+          const double dz = (z > 0 ? 1.0 : 0.2) * a * (dalpha(u, v, k) - c[v * h + k]);
+          dAl[u * h + k] += dz;
+          dAr[v * h + k] += dz;
+          for (int j = 0; j < f; ++j) dHt[u * hf + k * f + j] += a * dOut.at(v, k * f + j);
+        }
+      }
+    for (std::uint64_t u = 0; u < V; ++u)
+      for (int k = 0; k < h; ++k)
+        for (int j = 0; j < f; ++j)
+          dHt[u * hf + k * f + j] += dAl[u * h + k] * al.at(k, j) + dAr[u * h + k] * ar.at(k, j);
+  }
+  double worst_b = 0.0;
+  for (int i = 0; i < Fin; ++i)
+    for (int col = 0; col < hf; ++col) {
+      double s = 0;
+      for (std::uint64_t u = 0; u < V; ++u) s += Hd.at(u, i) * dHt[u * hf + col];
+      worst_b = std::max(worst_b, rel_err(s, (double)gr.dW.at(i, col)));
+    }
+  for (int k = 0; k < h; ++k)
+    for (int j = 0; j < f; ++j) {
+      double sl = 0, sr = 0;
+      for (std::uint64_t u = 0; u < V; ++u) {
+        sl += dAl[u * h + k] * Ht.at(u, k * f + j);
+        sr += dAr[u * h + k] * Ht.at(u, k * f + j);
+      }
+      worst_b = std::max({worst_b, rel_err(sl, (double)gr.da_l.at(k, j)), rel_err(sr, (double)gr.da_r.at(k, j))});
+    }
+  for (std::uint64_t u = 0; u < V; ++u)
+    for (int i = 0; i < Fin; ++i) {
+      double s = 0;
+      for (int col = 0; col < hf; ++col) s += dHt[u * hf + col] * W.at(i, col);
+      worst_b = std::max(worst_b, rel_err(s, (double)gr.dH.at(u, i)));
+    }
+  std::printf("gat forward max rel_err = %.3e ; backward (dW, da_l, da_r, dH) vs f64 max rel_err = %.3e\n", worst,
+              worst_b);
+  bool ok = worst < 1e-4 && worst_b < 1e-4 && gr.dW.rows == (std::uint64_t)Fin && gr.dH.rows == V;
   // error mapping: a shape error surfaces as the reference's TensorError
   try {
     TensorF bad(3, 3);
@@ -194,6 +255,32 @@ int main() {
     for (float v : g0r.dH.data) zero = zero && v == 0.f;
     std::printf("edge-less graph: outputs and gradients %s\n", zero ? "zero" : "NOT zero");
     ok = ok && zero;
+  }
+  // Multi-GPU API at world size 1 (one GPU per box here): the library's own NCCL communicator,
+  // the partitioned graph and the partitioned layer against the single-GPU fast path.
+  {
+    b200::Comm comm(1, 0, b200::Comm::unique_id());
+    b200::PartitionedGraph pg(g, 1, 0);
+    b200::GatParams q{h, f};
+    q.backward = b200::Backward::fast;
+    b200::GatStash sf;
+    TensorF of = b200::gat_forward(dg, H, W, al, ar, q, &sf);
+    b200::GatGrads gf = b200::gat_backward(dg, H, W, al, ar, sf, dOut, q, true);
+    b200::DistStash sd;
+    TensorF od = b200::gat_forward_dist(pg, &comm, H, W, al, ar, q, &sd);
+    b200::GatGrads gd = b200::gat_backward_dist(pg, &comm, H, W, al, ar, sd, dOut, q, true);
+    const double e = std::max({maxnorm(of, od), maxnorm(gf.dW, gd.dW), maxnorm(gf.dH, gd.dH),
+                               maxnorm(gf.da_l, gd.da_l), maxnorm(gf.da_r, gd.da_r)});
+    std::printf("gat partitioned (world 1, NCCL comm %d rank) vs single-GPU: max err %.3e\n", comm.size(), e);
+    ok = ok && comm.size() == 1 && pg.num_local() == (std::int64_t)V && e < 1e-5;
+    bool threw = false;
+    try {
+      b200::PartitionedGraph pg2(g, 2, 1);
+      b200::gat_forward_dist(pg2, nullptr, TensorF(pg2.num_local(), Fin), W, al, ar, q, nullptr);
+    } catch (const std::invalid_argument&) {
+      threw = true;  // P > 1 without a communicator
+    }
+    ok = ok && threw;
   }
   std::printf("%s\n", ok ? "OK" : "FAIL");
   return ok ? 0 : 1;
