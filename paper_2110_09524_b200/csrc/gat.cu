@@ -35,142 +35,6 @@ namespace {
 using namespace gat;
 
 // ---------------------------------------------------------------------------
-// K2: forward, single pass with a block-online softmax (RS1/RS2 folded into the
-// Aggregate): per 32-edge block the running max per head is updated once, the
-// accumulators rescaled by exp(m_old - m_new), and the block's unnormalised
-// weights exp(s - m_new) written to the per-warp table.
-// ---------------------------------------------------------------------------
-template <int VW, int NV, int OCC>
-__global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_fwd_kernel(GatParams p) {
-  __shared__ WarpSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  WarpSmem& sm = smem[w];
-  const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
-  if (wi >= p.num_items) return;
-  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
-  const int h = p.h, f = p.f, hf = h * f;
-  const float slope = p.slope;
-  constexpr int U = GatherDepth<NV, OCC>::U;
-
-  // Per-warp shared state (keeps registers for the gathers): stat[3] = A_r[v], stat[0] = running
-  // max per head (warp-uniform), t1[lane][k] = this lane's running exp-sum partial.
-  if (lane < h) {
-    sm.stat[3][lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);
-    sm.stat[0][lane] = -FLT_MAX;
-  }
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k) sm.t1[lane * TS + k] = 0.f;
-  const Cols<VW, NV> cols(lane, hf, f);
-  Vec<VW> acc[NV];
-  zero(acc);
-
-  const uint64_t e0 = it.e0, e1 = it.e1;
-  uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
-  uint32_t u_nxt = e0 + 32 + lane < e1 ? __ldg(p.nbr + e0 + 32 + lane) : 0u;
-  float al[MAXH];
-  load_heads(p.Al + (int64_t)u_cur * h, h, al);  // u_cur = 0 for idle lanes: a valid row, value unused
-  __syncwarp();
-
-  for (uint64_t base = e0; base < e1; base += 32) {
-    const int n = (int)min((uint64_t)32, e1 - base);
-    const bool valid = lane < n;
-    __syncwarp();
-#pragma unroll
-    for (int k = 0; k < MAXH; ++k) {
-      if (k < h) {
-        const float s = valid ? lrelu(al[k] + sm.stat[3][k], slope) : -FLT_MAX;
-        const float mold = sm.stat[0][k];
-        // the block max is only needed when some lane exceeds the running max
-        const float mnew = __any_sync(0xffffffffu, s > mold) ? fmaxf(mold, warp_max(s)) : mold;
-        const float sc = __expf(mold - mnew);
-        const float pk = valid ? __expf(s - mnew) : 0.f;
-        sm.t1[lane * TS + k] = fmaf(sm.t1[lane * TS + k], sc, pk);
-        sm.t0[lane * TS + k] = pk;
-        __syncwarp();
-        if (lane == 0) { sm.stat[2][k] = sc; sm.stat[0][k] = mnew; }
-      }
-    }
-    sm.nb[lane] = u_cur;
-    __syncwarp();
-    // prefetch: logits of the next block, ids of the block after
-    u_cur = u_nxt;
-    if (base + 32 + lane < e1) load_heads(p.Al + (int64_t)u_cur * h, h, al);
-    u_nxt = base + 64 + lane < e1 ? __ldg(p.nbr + base + 64 + lane) : 0u;
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      const float sc = sm.stat[2][cols.hd[i]];
-#pragma unroll
-      for (int q = 0; q < VW; ++q) acc[i].x[q] *= sc;
-    }
-    int j = 0;
-    for (; j + U <= n; j += U) {
-      Vec<VW> x[U][NV];
-#pragma unroll
-      for (int t = 0; t < U; ++t) gather_row<VW, NV>(p.Ht, sm.nb[j + t], hf, cols, x[t]);
-#pragma unroll
-      for (int t = 0; t < U; ++t)
-#pragma unroll
-        for (int i = 0; i < NV; ++i) {
-          const float a = sm.t0[(j + t) * TS + cols.hd[i]];
-#pragma unroll
-          for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[t][i].x[q], acc[i].x[q]);
-        }
-    }
-    for (; j < n; ++j) {
-      Vec<VW> x[NV];
-      gather_row<VW, NV>(p.Ht, sm.nb[j], hf, cols, x);
-#pragma unroll
-      for (int i = 0; i < NV; ++i) {
-        const float a = sm.t0[j * TS + cols.hd[i]];
-#pragma unroll
-        for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(a, x[i].x[q], acc[i].x[q]);
-      }
-    }
-    __syncwarp();
-  }
-
-  const bool empty = e0 == e1;
-  __syncwarp();
-#pragma unroll
-  for (int k = 0; k < MAXH; ++k) {
-    if (k < h) {
-      const float S = warp_sum(sm.t1[lane * TS + k]);
-      if (lane == 0) {
-        if (empty) sm.stat[0][k] = 0.f;
-        sm.stat[1][k] = S;
-      }
-    }
-  }
-  __syncwarp();
-  if (!it.split) {
-#pragma unroll
-    for (int i = 0; i < NV; ++i) {
-      if (cols.ok[i]) {
-        const float den = sm.stat[1][cols.hd[i]];
-        const float inv = den > 0.f ? 1.f / den : 0.f;
-        Vec<VW> o;
-#pragma unroll
-        for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
-        st_vec<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
-      }
-    }
-    if (lane < h) {
-      p.mo[(int64_t)it.row * h + lane] = sm.stat[0][lane];
-      p.dd[(int64_t)it.row * h + lane] = sm.stat[1][lane];
-    }
-  } else {
-    float* part = p.part + wi * fwd_stride(h, f);
-#pragma unroll
-    for (int i = 0; i < NV; ++i)
-      if (cols.ok[i]) st_vec<VW>(part + cols.col[i], acc[i]);
-    if (lane < h) {
-      part[hf + lane] = sm.stat[0][lane];
-      part[hf + h + lane] = sm.stat[1][lane];
-    }
-  }
-}
-
-// ---------------------------------------------------------------------------
 // K2 (overlapped edge phase): the block-synchronous forward with the edge phase moved
 // under the gathers.  At the start of every 32-edge block the warp first issues the loads of
 // the block's first U neighbour rows, and only then runs the edge phase (logits -> block
@@ -1163,9 +1027,8 @@ __global__ void __launch_bounds__(256) attn_grad_reduce_kernel(int nb, int hf, c
 // ---------------------------------------------------------------------------
 // Dispatch over the compiled (VW, NV) variants.
 // ---------------------------------------------------------------------------
-enum class Kind { Fwd, FwdOvl, BwdDst, BwdSrc, BwdSrcFast };
+enum class Kind { FwdOvl, BwdDst, BwdSrc, BwdSrcFast };
 int num_sms();
-bool ovl_enabled();
 bool pair_enabled();
 
 template <int VW, int NV, int PER, int OCC>
@@ -1200,7 +1063,6 @@ void launch_fast(const GatParams& p, dim3 grid, cudaStream_t s) {
 template <int VW, int NV, int OCC>
 void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
   switch (kind) {
-    case Kind::Fwd: gat_fwd_kernel<VW, NV, OCC><<<grid, THREADS, 0, s>>>(p); break;
     case Kind::FwdOvl: {
       constexpr int U = GatherDepth<NV, OCC>::U;
       constexpr int MINB = NV >= 8 ? 1 : OCC;
@@ -1218,8 +1080,7 @@ void launch_occ(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
 
 template <int VW, int NV>
 void launch_variant(Kind kind, const GatParams& p, dim3 grid, cudaStream_t s) {
-  if (gat_occupancy() >= 4) launch_occ<VW, NV, 4>(kind, p, grid, s);
-  else launch_occ<VW, NV, 2>(kind, p, grid, s);
+  launch_occ<VW, NV, 2>(kind, p, grid, s);  // 2 CTAs x 8 warps per SM (32 warps/SM measured slower)
 }
 
 template <int VW>
@@ -1322,31 +1183,10 @@ __global__ void pack_bf16_kernel(int64_t n, const float* __restrict__ src, uint1
 
 }  // namespace
 
-int gat::gat_occupancy() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNNCG_GAT_OCC");
-    v = (e && atoi(e) == 4) ? 4 : 2;
-  }
-  return v;
-}
 
 namespace {
 
-// GNNCG_GAT_TMA=1 selects the TMA-fed forward (gat_tma.cu).  Default off: measured slower
-// (17.9 vs 9.5 ms at the Reddit shape) -- the 8 persistent warps per SM it can host next
-// to its shared-memory ring do not issue enough independent row requests.
-bool tma_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNNCG_GAT_TMA");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
 
-// GNNCG_GAT_OVL=0 selects the block-synchronous forward (gat_fwd_kernel) instead of the
-// overlapped-edge-phase one (gat_fwd_ovl_kernel).
 // K2 / K4f pull work items from a counter in the workspace (behind the partials, where
 // gnncg_gat_workspace reserves 256 bytes) instead of a fixed stride: the items are ordered
 // largest first, so warps take them longest-first and finish together (with a fixed stride
@@ -1394,14 +1234,6 @@ int attach_counter(GatParams& p, uint64_t num_edges, void* ws, size_t ws_bytes, 
   return GNNCG_OK;
 }
 
-bool ovl_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNNCG_GAT_OVL");
-    v = (e && e[0] == '0') ? 0 : 1;
-  }
-  return v == 1;
-}
 
 // GNNCG_GAT_PAIR=0 disables K4f's paired-head column mapping.
 bool pair_enabled() {
@@ -1493,16 +1325,10 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
     rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
     if (rc) return rc;
     rc = dispatch_lp(Kind::FwdOvl, p, s);
-  } else if (tma_enabled() && tma_fwd_supported(h, f) && sched->num_items > 0) {
-    int* counter = reinterpret_cast<int*>(static_cast<char*>(ws) + align_up(need));
-    GNNCG_REQUIRE(ws_bytes >= align_up(need) + sizeof(int), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace too small");
-    rc = launch_fwd_tma(p, counter, s);
   } else {
-    if (ovl_enabled()) {
-      rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
-      if (rc) return rc;
-    }
-    rc = dispatch(ovl_enabled() ? Kind::FwdOvl : Kind::Fwd, p, s);
+    rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
+    if (rc) return rc;
+    rc = dispatch(Kind::FwdOvl, p, s);
   }
   if (rc) return rc;
   if (sched->num_split_rows > 0) {
@@ -1615,7 +1441,7 @@ int gnncg_gat_fast_supported(int h, int f) {
   if (h < 1 || h > MAXH || per < 1 || per > 16 || (per & (per - 1)) != 0 || h * f > 256 * vw) return 0;
   const int nvec = (int)ceil_div(h * f / vw, 32);
   const int nv = nvec <= 1 ? 1 : nvec <= 2 ? 2 : nvec <= 4 ? 4 : 8;
-  const int u = gat_occupancy() >= 4 ? (nv <= 2 ? 4 : (nv == 4 ? 2 : 1)) : (nv <= 2 ? 8 : (nv == 4 ? 4 : 2));
+  const int u = nv <= 2 ? 8 : (nv == 4 ? 4 : 2);
   return (u * nv) % per == 0;
 }
 

@@ -1,5 +1,5 @@
 // SPDX-License-Identifier: Apache-2.0
-// Device-side pieces shared by the fused GAT kernels (gat.cu, gat_tma.cu): work-item
+// Device-side pieces shared by the fused GAT kernels (gat.cu, gat_lean.cu): work-item
 // decoding, per-warp tables, lane/column mapping, split-row partial strides.
 #pragma once
 
@@ -107,16 +107,12 @@ struct GatParams {
 //     flight) before consuming any of them.
 // ---------------------------------------------------------------------------
 // OCC = CTAs per SM the kernel is built for (launch bound): 2 -> 16 warps/SM with deep
-// per-warp gathers; 4 -> 32 warps/SM (<= 64 registers) with shallower ones.  More warps
-// win for Zipf-distributed gathers (scripts/gather_bench.cu: 9 -> 16 TB/s from 16 to 32
-// warps/SM at equal bytes in flight).
+// per-warp gathers (U rows in flight).  32 warps/SM at <= 64 registers with half the depth
+// measured slower at the Reddit shape and is no longer built.
 template <int NV, int OCC = 2>
 struct GatherDepth {
-  static constexpr int U = OCC >= 4 ? (NV <= 2 ? 4 : (NV == 4 ? 2 : 1)) : (NV <= 2 ? 8 : (NV == 4 ? 4 : 2));
+  static constexpr int U = NV <= 2 ? 8 : (NV == 4 ? 4 : 2);
 };
-
-// Runtime choice of OCC (GNNCG_GAT_OCC=2|4, default 2: measured faster at the Reddit shape).
-int gat_occupancy();
 
 // Lane -> column mapping.  Default: vector i of lane l covers columns [(32 i + l) VW, +VW).
 // Paired (pl = lanes per head P > 0; rows that fill the warp exactly, hf = 32 NV VW): lane l
@@ -232,13 +228,6 @@ struct LpDepth {
   static constexpr int U = R > 16 ? 16 : (R < 1 ? 1 : R);
 };
 
-}  // namespace gat
-
-// TMA-fed kernels (gat_tma.cu)
-namespace gat {
-bool tma_fwd_supported(int h, int f);
-size_t tma_smem_bytes(int h, int f);
-int launch_fwd_tma(const GatParams& p, int* counter, cudaStream_t s);
 }  // namespace gat
 
 // Wavefront-lean K4f (gat_lean.cu): false when the shape is not one it takes.

@@ -26,6 +26,7 @@
 //   * the gathered rows' ids are read four at a time (LDS.128 broadcast);
 //   * (gate * alpha, c) per (edge, head) sit side by side: the dz stage reads one
 //     8-byte pair per output.
+#include <algorithm>
 #include <cfloat>
 
 #include "common.cuh"
@@ -74,15 +75,15 @@ __device__ __forceinline__ int tcidx(int e, int k) {
 
 __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-template <int H, int VW, int NV, int PER, int OCC, bool DYN>
-__global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParams p) {
+template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
+__global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(GatParams p) {
   constexpr int U = 8;  // rows in flight per warp
   constexpr int R = 4 / NV;
   constexpr int NVAL = U * NV, NOUT = NVAL / PER;
   constexpr bool PAIR = NV == 2;  // lane's vectors in heads (2g, 2g+1): one 16-byte dA_r reduction per edge
   static_assert(NV == 1 || NV == 2, "lean K4f: one or two vectors per lane");
   static_assert(NVAL % PER == 0 && (!PAIR || NOUT == 2), "lean K4f: outputs per lane");
-  __shared__ __align__(16) LeanSmem smem[WARPS];
+  __shared__ __align__(16) LeanSmem smem[WPC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   LeanSmem& sm = smem[w];
   constexpr int h = H;  // compile-time heads: the edge phase's pair indexing is shifts, not divides
@@ -97,7 +98,7 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParam
   const int kk = lane % h;        // edge phase: this lane's head
   unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, (unsigned)p.batch) : 0u;
   int64_t cur = 0, cend = 0;
-  for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
+  for (int64_t g = blockIdx.x; DYN || g * WPC < p.num_items; g += gridDim.x) {
     int64_t wi;
     if constexpr (DYN) {
       if (cur >= cend) {
@@ -108,7 +109,7 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_bwd_src_lean_kernel(GatParam
       wi = cur++;
       if (wi >= p.num_items) break;
     } else {
-      wi = g * WARPS + w;
+      wi = g * WPC + w;
       if (wi >= p.num_items) continue;
     }
     const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
@@ -265,11 +266,11 @@ struct LeanFwdSmem {
   float sc[MAXH];         // per head: rescale of the block, then 1 / exp-sum at the end
 };
 
-template <int H, int VW, int NV, int PER, int OCC, bool DYN>
-__global__ void __launch_bounds__(THREADS, OCC) gat_fwd_lean_kernel(GatParams p) {
+template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
+__global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatParams p) {
   constexpr int U = 8;
   constexpr int R = 4 / NV;
-  __shared__ __align__(16) LeanFwdSmem smem[WARPS];
+  __shared__ __align__(16) LeanFwdSmem smem[WPC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   LeanFwdSmem& sm = smem[w];
   constexpr int h = H;  // compile-time heads: the edge phase's pair indexing is shifts, not divides
@@ -280,14 +281,14 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_fwd_lean_kernel(GatParams p)
   constexpr int epi = kWarp / h;
   const int kk = lane % h;
   unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
-  for (int64_t g = blockIdx.x; DYN || g * WARPS < p.num_items; g += gridDim.x) {
+  for (int64_t g = blockIdx.x; DYN || g * WPC < p.num_items; g += gridDim.x) {
     int64_t wi;
     if constexpr (DYN) {
       wi = __shfl_sync(0xffffffffu, nx, 0);
       if (wi >= p.num_items) break;
       if (lane == 0) nx = atomicAdd(p.ctr, 1u);
     } else {
-      wi = g * WARPS + w;
+      wi = g * WPC + w;
       if (wi >= p.num_items) continue;
     }
     const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
@@ -403,16 +404,55 @@ __global__ void __launch_bounds__(THREADS, OCC) gat_fwd_lean_kernel(GatParams p)
   }  // work items
 }
 
-template <int VW, int NV, int PER>
-void launch_fwd(const GatParams& p, unsigned grid, cudaStream_t s) {
-  if (p.ctr) gat_fwd_lean_kernel<8, VW, NV, PER, 2, true><<<grid, THREADS, 0, s>>>(p);
-  else gat_fwd_lean_kernel<8, VW, NV, PER, 2, false><<<grid, THREADS, 0, s>>>(p);
+// CTA shape of the lean kernels: warps per CTA and CTAs per SM (the launch bound caps the
+// registers at 65536 / (MINB * WPC * 32)).  Overridable at build time for A/B runs.
+// Measured on B200 (two boxes, ms per launch at C2, K4f / K2): 8 warps x 2 CTAs (128
+// registers, 16 warps/SM) 11.49-11.62 / 7.94-8.03; 4 x 5 (96 registers, no spill, 20
+// warps/SM) 10.78-10.92 / 7.71-7.81; 2 x 10 (96) 11.15-11.26 / 7.86-7.95; 2 x 12 (80, 24
+// warps) 10.92-10.95 / 8.15-8.16; 2 x 16 (64, 32 warps) 11.95 / 7.68-7.75.  At C5: 4 x 5
+// K4f 105.6 vs 113.0 ms, K2 82.5 vs 81.4 ms.
+#ifndef GNNCG_LEAN_FWD_WPC
+#define GNNCG_LEAN_FWD_WPC 4
+#endif
+#ifndef GNNCG_LEAN_FWD_MINB
+#define GNNCG_LEAN_FWD_MINB 5
+#endif
+#ifndef GNNCG_LEAN_BWD_WPC
+#define GNNCG_LEAN_BWD_WPC 4
+#endif
+#ifndef GNNCG_LEAN_BWD_MINB
+#define GNNCG_LEAN_BWD_MINB 5
+#endif
+constexpr int kFwdWpc = GNNCG_LEAN_FWD_WPC, kFwdMinb = GNNCG_LEAN_FWD_MINB;
+constexpr int kBwdWpc = GNNCG_LEAN_BWD_WPC, kBwdMinb = GNNCG_LEAN_BWD_MINB;
+
+int lean_num_sms() {
+  static int v = 0;
+  if (v == 0) {
+    int dev = 0;
+    cudaGetDevice(&dev);
+    if (cudaDeviceGetAttribute(&v, cudaDevAttrMultiProcessorCount, dev) != cudaSuccess || v <= 0) v = 148;
+  }
+  return v;
+}
+
+// persistent grid: MINB CTAs per SM, no more than the items need
+unsigned lean_grid(int64_t items, int wpc, int minb) {
+  return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, wpc), (int64_t)lean_num_sms() * minb));
 }
 
 template <int VW, int NV, int PER>
-void launch(const GatParams& p, unsigned grid, cudaStream_t s) {
-  if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, 2, true><<<grid, THREADS, 0, s>>>(p);
-  else gat_bwd_src_lean_kernel<8, VW, NV, PER, 2, false><<<grid, THREADS, 0, s>>>(p);
+void launch_fwd(const GatParams& p, cudaStream_t s) {
+  const unsigned grid = lean_grid(p.num_items, kFwdWpc, kFwdMinb);
+  if (p.ctr) gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, true><<<grid, kFwdWpc * kWarp, 0, s>>>(p);
+  else gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, false><<<grid, kFwdWpc * kWarp, 0, s>>>(p);
+}
+
+template <int VW, int NV, int PER>
+void launch(const GatParams& p, cudaStream_t s) {
+  const unsigned grid = lean_grid(p.num_items, kBwdWpc, kBwdMinb);
+  if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
+  else gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
 }
 
 }  // namespace
@@ -434,17 +474,17 @@ bool lean_enabled() {
   return v == 1;
 }
 
-bool launch_fwd_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
+bool launch_fwd_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-  if (p.f == 32) launch_fwd<4, 2, 8>(p, grid, s);
-  else launch_fwd<4, 1, 4>(p, grid, s);
+  if (p.f == 32) launch_fwd<4, 2, 8>(p, s);
+  else launch_fwd<4, 1, 4>(p, s);
   return true;
 }
 
-bool launch_bwd_src_lean(const GatParams& p, unsigned grid, cudaStream_t s) {
+bool launch_bwd_src_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-  if (p.f == 32) launch<4, 2, 8>(p, grid, s);
-  else launch<4, 1, 4>(p, grid, s);
+  if (p.f == 32) launch<4, 2, 8>(p, s);
+  else launch<4, 1, 4>(p, s);
   return true;
 }
 
