@@ -89,6 +89,16 @@ const char* gnncg_version(void);
 int gnncg_device_check(void);
 /* Number of kernels this library has launched in the process (instrumentation). */
 uint64_t gnncg_launch_count(void);
+/* Cost counters (instrumentation; "measured flops / io_units == predicted").
+ * `counters` = a zeroed DEVICE array of 10 uint64 (NULL turns counting off).  While set, every
+ * GAT kernel adds the edges each work item walks and the rows it completes to its pair
+ * (edges, rows):
+ *   [0,1] K2 (fwd, fp32 or bf16)  [2,3] K3  [4,5] K4  [6,7] K4f (fused fast backward)
+ *   [8,9] the attention LPs (gnncg_gat_transform's epilogue / gnncg_gat_attn_dots): rows, calls.
+ * The sums equal (|E|, rows) per call iff every edge was aggregated exactly once and every row
+ * written once; the flops / io units follow from each kernel's fixed per-edge and per-row work
+ * (paper_2110_09524_b200/cost.py).  Process-wide; not for concurrent measurement. */
+int gnncg_cost_counters(uint64_t* counters);
 
 /* ------------------------------------------------------- graph store (K9)
  * Replaces build_index (graph.cpp:14-28) and the Graph ctor (graph.cpp:32-45).

@@ -95,6 +95,7 @@ _SIGS = {
     "gnncg_version": ([], C.c_char_p),
     "gnncg_device_check": ([], i32),
     "gnncg_launch_count": ([], u64),
+    "gnncg_cost_counters": ([vp], i32),
     "gnncg_csr_build_workspace": ([i64, i64], sz),
     "gnncg_csr_build": ([i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_csr_build_rect": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),

@@ -32,6 +32,12 @@ int require_device();
 // Counts every kernel this library launches (gnncg_launch_count()).
 void note_launch();
 
+// Device cost counters of one kernel kind (gnncg_cost_counters), null when off.
+enum CostKind { kCostK2 = 0, kCostK3 = 1, kCostK4 = 2, kCostK4f = 3, kCostLp = 4 };
+unsigned long long* cost_slot(int kind);
+// slot[0] += a, slot[1] += b on the stream (host-side counts, e.g. the LP rows of K1)
+void cost_add(int kind, uint64_t a, uint64_t b, cudaStream_t s);
+
 #define GNNCG_LAUNCH_CHECK()                     \
   do {                                           \
     ::gnncg_b200::note_launch();                 \

@@ -145,6 +145,7 @@ __global__ void __launch_bounds__(CW * kWarp) __maxnreg__(MINB >= 2 ? ((65536 / 
     if (wi >= p.num_items) continue;
   }
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  count_item(p, it, lane);
 
   if (lane < h) {
     sm.ar[lane] = __ldg(p.Ar + (int64_t)it.row * h + lane);
@@ -257,6 +258,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_dst_kernel
   const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
   if (wi >= p.num_items) return;
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  count_item(p, it, lane);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
   constexpr int U = GatherDepth<NV, OCC>::U;
@@ -384,6 +386,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_kernel
   const int64_t wi = (int64_t)blockIdx.x * WARPS + w;
   if (wi >= p.num_items) return;
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  count_item(p, it, lane);
   const int h = p.h, f = p.f, hf = h * f;
   const float slope = p.slope;
   const int64_t u = it.row;
@@ -561,6 +564,7 @@ __global__ void __launch_bounds__(THREADS, NV >= 8 ? 1 : OCC) gat_bwd_src_fast_k
     if (wi >= p.num_items) continue;
   }
   const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  count_item(p, it, lane);
   const int64_t u = it.row;
 
   if (lane < h) sm.stat[3][lane] = __ldg(p.Al + u * h + lane);
@@ -820,6 +824,7 @@ __global__ void gat_fwd_merge_kernel(GatParams p, const uint32_t* __restrict__ s
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
   if (sr >= num_split_rows) return;
+  if (p.cnt != nullptr && lane == 0) atomicAdd(p.cnt + 1, 1ull);  // a split row completed
   const int h = p.h, f = p.f, hf = h * f;
   const int64_t stride = fwd_stride(h, f);
   const uint32_t row = split_rows[sr];
@@ -852,6 +857,7 @@ __global__ void gat_bwd_dst_merge_kernel(GatParams p, const uint32_t* __restrict
   if (sr >= num_split_rows * h) return;
   const int64_t r = sr / h;
   const int k = (int)(sr % h);
+  if (p.cnt != nullptr && k == 0) atomicAdd(p.cnt + 1, 1ull);  // a split row completed
   const uint32_t row = split_rows[r];
   float c = 0.f, P = 0.f, Q = 0.f;
   for (int64_t it = split_first[r]; it < split_first[r + 1]; ++it) {
@@ -869,6 +875,7 @@ __global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t sr = (int64_t)blockIdx.x * WARPS + w;
   if (sr >= num_split_rows) return;
+  if (p.cnt != nullptr && lane == 0) atomicAdd(p.cnt + 1, 1ull);  // a split row completed
   const int h = p.h, f = p.f, hf = h * f;
   const int64_t stride = src_stride(h, f);
   const int64_t u = split_rows[sr];
@@ -1290,6 +1297,7 @@ int gnncg_gat_attn_dots(int64_t rows, int h, int f, const float* Ht, const float
   GNNCG_REQUIRE(Ht && a_l && a_r && Al && Ar, GNNCG_ERR_ARG, "attn_dots: null pointer");
   const int64_t n = rows * h;
   const int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 32);
+  cost_add(kCostLp, (uint64_t)rows, 1, as_stream(stream));
   attn_dots_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, Ht, a_l, a_r, Al, Ar);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
@@ -1316,6 +1324,7 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_fwd: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
+  p.cnt = cost_slot(kCostK2);
   p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -1385,6 +1394,7 @@ int gnncg_gat_bwd_dst(const gnncg_index_t* csr_dst, const gnncg_sched_t* sched, 
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_dst: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
+  p.cnt = cost_slot(kCostK3);
   p.off = csr_dst->off; p.nbr = csr_dst->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -1418,6 +1428,7 @@ int gnncg_gat_bwd_src(const gnncg_index_t* csc_src, const gnncg_sched_t* sched, 
   GNNCG_REQUIRE(ws_bytes >= need && (need == 0 || ws), GNNCG_ERR_WORKSPACE, "gat_bwd_src: workspace %zu < %zu",
                 ws_bytes, need);
   GatParams p{};
+  p.cnt = cost_slot(kCostK4);
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
@@ -1485,6 +1496,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   cudaStream_t s = as_stream(stream);
   if (!(flags & kFusedKeepDar)) GNNCG_CUDA_TRY(cudaMemsetAsync(dAr, 0, sizeof(float) * (size_t)num_local * h, s));
   GatParams p{};
+  p.cnt = cost_slot(kCostK4f);
   p.off = csc_src->off; p.nbr = csc_src->nbr; p.items = sched->items;
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;

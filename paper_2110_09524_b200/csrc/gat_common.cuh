@@ -94,7 +94,20 @@ struct GatParams {
   int fast;  // K4 fused with K3: dA_r accumulated atomically, its LP term added by gat_lp_dar_kernel
   unsigned* ctr;  // dynamic item fetch (DYN kernels): zeroed work counter in the workspace
   int batch;      // items taken per counter request
+  unsigned long long* cnt;  // cost counters of this kernel kind (gnncg_cost_counters), or null
 };
+
+// Cost counters (gnncg_cost_counters; "measured == predicted"): per work item
+// the warp adds the edges it walks, and one completed row for an unsplit item (the split-row
+// merge kernels add theirs), so the host can check that every edge was aggregated exactly
+// once and every row written once (split rows, the work counter's batches) and derive the
+// measured flops / io units from the kernel's fixed per-edge and per-row work.
+__device__ __forceinline__ void count_item(const GatParams& p, const Item& it, int lane) {
+  if (p.cnt != nullptr && lane == 0) {
+    atomicAdd(p.cnt, (unsigned long long)(it.e1 - it.e0));
+    if (!it.split) atomicAdd(p.cnt + 1, 1ull);
+  }
+}
 
 // ---------------------------------------------------------------------------
 // Shared pieces of the three fused kernels.

@@ -113,6 +113,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
       if (wi >= p.num_items) continue;
     }
     const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+    count_item(p, it, lane);
     const int64_t u = it.row;
     const float alu = __ldg(p.Al + u * h + kk);
     Vec<VW> x[NV], acc[NV];
@@ -292,6 +293,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
       if (wi >= p.num_items) continue;
     }
     const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+    count_item(p, it, lane);
     const float arv = __ldg(p.Ar + (int64_t)it.row * h + kk);
     float m_run = -FLT_MAX, S = 0.f;  // this lane's head kk: running max, exp-sum partial
     Vec<VW> acc[NV];

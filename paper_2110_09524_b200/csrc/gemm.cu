@@ -307,6 +307,7 @@ int gnncg_gat_transform(int64_t M, int64_t K, int heads, int f, const float* H, 
       GNNCG_LAUNCH_CHECK();
       W_lo = static_cast<const float*>(ws);
     }
+    cost_add(kCostLp, (uint64_t)M, 1, s);  // the epilogue forms A_l / A_r of all M rows
     return tc_gemm(0, 0, M, N, K, H, ldh, W, N, Ht, N, 1, K, nullptr, s, epi, W_lo, N);
   }
   // unfused: the GEMM, then the LP kernel

@@ -12,8 +12,26 @@ namespace gnncg_b200 {
 
 static thread_local char g_err[1024] = "";
 static std::atomic<unsigned long long> g_launches{0};
+static std::atomic<unsigned long long*> g_cost{nullptr};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+unsigned long long* cost_slot(int kind) {
+  unsigned long long* c = g_cost.load(std::memory_order_acquire);
+  return c ? c + 2 * kind : nullptr;
+}
+
+__global__ void cost_add_kernel(unsigned long long* c, unsigned long long a, unsigned long long b) {
+  c[0] += a;
+  c[1] += b;
+}
+
+void cost_add(int kind, uint64_t a, uint64_t b, cudaStream_t s) {
+  unsigned long long* c = cost_slot(kind);
+  if (!c) return;
+  cost_add_kernel<<<1, 1, 0, s>>>(c, a, b);
+  note_launch();
+}
 
 void set_error(const char* fmt, ...) {
   va_list ap;
@@ -65,6 +83,11 @@ const char* gnncg_version(void) { return "gnncg_b200 0.1.0 (sm_100a)"; }
 int gnncg_device_check(void) { return require_device(); }
 
 uint64_t gnncg_launch_count(void) { return g_launches.load(std::memory_order_relaxed); }
+
+int gnncg_cost_counters(uint64_t* counters) {
+  g_cost.store(reinterpret_cast<unsigned long long*>(counters), std::memory_order_release);
+  return GNNCG_OK;
+}
 
 // Partitioner: bound[p] = lower_bound(off, ceil(p*E/P)).  Bit-exact with
 // oracle/oracle.cpp:orc_partition_rows.

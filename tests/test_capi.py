@@ -107,3 +107,31 @@ def test_binding_arity_matches_header():
         params = protos[name].strip()
         n = 0 if params in ("", "void") else params.count(",") + 1
         assert n == len(args), f"{name}: header has {n} parameters, binding declares {len(args)}"
+
+
+def test_bench_spawns_one_rank_per_gpu(monkeypatch):
+    """`bench.py --gpus N` outside torchrun launches N ranks through torch.distributed.run on
+    127.0.0.1 (the driver's N-GPU invocation), passing its own arguments through."""
+    import subprocess
+    import sys
+
+    import bench
+
+    seen = {}
+
+    class R:
+        returncode = 0
+
+    def fake_run(cmd, env=None, **kw):
+        seen["cmd"], seen["env"] = cmd, env
+        return R()
+
+    monkeypatch.setattr(subprocess, "run", fake_run)
+    monkeypatch.setattr(sys, "argv", ["bench.py", "--gpus", "4", "--config", "c5", "--steps", "2"])
+    args = bench.parse()
+    assert bench.spawn_ranks(args) == 0
+    cmd = seen["cmd"]
+    assert cmd[1:3] == ["-m", "torch.distributed.run"] and "--nproc-per-node=4" in cmd
+    assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
+    assert cmd[-6:] == ["--gpus", "4", "--config", "c5", "--steps", "2"]
+    assert seen["env"]["NCCL_DEBUG"] == "INFO"
