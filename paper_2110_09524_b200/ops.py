@@ -93,8 +93,14 @@ def _f32_rows(t: torch.Tensor, name: str) -> torch.Tensor:
 def _shape(t: torch.Tensor, shape, name: str):
     if tuple(t.shape) != tuple(shape):
         raise TensorError(f"{name}: shape {tuple(t.shape)} != expected {tuple(shape)}")
-    if t.dtype != torch.float32 or not t.is_contiguous():
-        raise TensorError(f"{name}: expected a contiguous float32 tensor")
+    return t
+
+
+def _out(t: torch.Tensor, shape, name: str) -> torch.Tensor:
+    """A caller-provided output buffer: exact shape, contiguous fp32 CUDA (written by pointer)."""
+    _shape(t, shape, name)
+    if t.dtype != torch.float32 or not t.is_cuda or not t.is_contiguous():
+        raise TensorError(f"{name}: expected a contiguous float32 CUDA tensor")
     return t
 
 
@@ -244,9 +250,9 @@ def gat_transform(H, W, a_l, a_r, heads, f, ws=None, Ht=None, Al=None, Ar=None):
     M, K = H.shape
     hf = heads * f
     dev = H.device
-    Ht = torch.empty(M, hf, device=dev) if Ht is None else _shape(Ht, (M, hf), "Ht")
-    Al = torch.empty(M, heads, device=dev) if Al is None else _shape(Al, (M, heads), "Al")
-    Ar = torch.empty(M, heads, device=dev) if Ar is None else _shape(Ar, (M, heads), "Ar")
+    Ht = torch.empty(M, hf, device=dev) if Ht is None else _out(Ht, (M, hf), "Ht")
+    Al = torch.empty(M, heads, device=dev) if Al is None else _out(Al, (M, heads), "Al")
+    Ar = torch.empty(M, heads, device=dev) if Ar is None else _out(Ar, (M, heads), "Ar")
     need = _lib.lib().gnncg_gemm_workspace(0, 0, M, hf, K)
     if ws is None:
         buf = torch.empty(max(need, 1), dtype=torch.uint8, device=dev)
