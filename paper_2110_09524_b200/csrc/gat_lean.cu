@@ -28,7 +28,6 @@
 //     8-byte pair per output.
 #include <algorithm>
 #include <cfloat>
-#include <type_traits>
 
 #include "common.cuh"
 #include "gat_common.cuh"
@@ -57,10 +56,6 @@ struct LeanSmem {
   float2 tc[kWarp * MAXH];     // (LReLU'(z) alpha, c) per (edge, head), tcidx order
   float dl[MAXH];              // dA_l[u] per head (item end)
 };
-// + the next block's destination records, prefetched by cp.async (RPF kernels, h = 8)
-struct LeanSmemR : LeanSmem {
-  float4 rs[kWarp * 8];
-};
 
 // index of alpha(e, k) in LeanSmem::w: rows grouped by R = 4 / NV, heads by NV
 template <int NV, int h>
@@ -80,7 +75,7 @@ __device__ __forceinline__ int tcidx(int e, int k) {
 
 __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
-template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN, bool RPF = false>
+template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
 __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(GatParams p) {
   constexpr int U = 8;  // rows in flight per warp
   constexpr int R = 4 / NV;
@@ -88,11 +83,9 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
   constexpr bool PAIR = NV == 2;  // lane's vectors in heads (2g, 2g+1): one 16-byte dA_r reduction per edge
   static_assert(NV == 1 || NV == 2, "lean K4f: one or two vectors per lane");
   static_assert(NVAL % PER == 0 && (!PAIR || NOUT == 2), "lean K4f: outputs per lane");
-  using Sm = std::conditional_t<RPF, LeanSmemR, LeanSmem>;
-  static_assert(!RPF || H == 8, "record prefetch: 8 heads");
-  __shared__ __align__(16) Sm smem[WPC];
+  __shared__ __align__(16) LeanSmem smem[WPC];
   const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
-  Sm& sm = smem[w];
+  LeanSmem& sm = smem[w];
   constexpr int h = H;  // compile-time heads: the edge phase's pair indexing is shifts, not divides
   const int f = p.f, hf = h * f;
   const float slope = p.slope;
@@ -133,7 +126,6 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
     const uint64_t e0 = it.e0, e1 = it.e1;
     uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
     const float* tab = p.dOut;
-    bool have_rs = false;  // RPF: this block's records already sit in sm.rs
     for (uint64_t base = e0; base < e1; base += 32) {
       const int n = (int)min((uint64_t)32, e1 - base);
       sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
@@ -149,22 +141,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
       {
         // edge phase, lanes = (edge, head) pairs: one {A_r, lse, c, 0} record load each
         float4 q[MAXH];
-        if constexpr (RPF) {
-          if (have_rs) {
-            cp_async_wait_all();
-            __syncwarp();
-          }
-        }
 #pragma unroll
         for (int i = 0; i < MAXH; ++i) {
           if (i < h) {
             const int e = i * epi + lane / h;
-            if constexpr (RPF) {
-              if (have_rs) {
-                q[i] = sm.rs[i * kWarp + lane];  // = record (edge e, head kk): rs[e * 8 + kk]
-                continue;
-              }
-            }
             q[i] = __ldg(reinterpret_cast<const float4*>(p.rec + (int64_t)sm.nb[e] * (4 * h)) + kk);
           }
         }
@@ -201,16 +181,6 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
               axpy_vec<VW>(wa[rr * NV + i], gv[t + rr][i].x, acc[i].x);
               pd[(t + rr) * NV + i] = dot_vec<VW>(x[i].x, gv[t + rr][i].x);
             }
-        }
-        if constexpr (RPF) {
-          // the next block's records go to shared memory while this block computes (its ids
-          // arrived during the first row group; this block's records are in registers)
-          if (j == 0 && base + 32 < e1) {
-            const float4* src = reinterpret_cast<const float4*>(p.rec + (int64_t)v_cur * (4 * h));
-#pragma unroll
-            for (int k = 0; k < 8; ++k) cp_async16_cg(&sm.rs[lane * 8 + k], src + k);
-            cp_async_commit();
-          }
         }
         bfly<NVAL, PER / 2>(pd, lane);
         float dzp[NOUT];
@@ -252,7 +222,6 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
         }
       }
       __syncwarp();
-      if constexpr (RPF) have_rs = base + 32 < e1;
     }
 #pragma unroll
     for (int i = 0; i < NV; ++i) {
@@ -481,24 +450,9 @@ void launch_fwd(const GatParams& p, cudaStream_t s) {
   else gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, false><<<grid, kFwdWpc * kWarp, 0, s>>>(p);
 }
 
-// GNNCG_GAT_RPF=1: K4f prefetches the next block's destination records into shared memory
-bool rpf_enabled() {
-  static int v = -1;
-  if (v < 0) {
-    const char* e = getenv("GNNCG_GAT_RPF");
-    v = (e && e[0] == '1') ? 1 : 0;
-  }
-  return v == 1;
-}
-
 template <int VW, int NV, int PER>
 void launch(const GatParams& p, cudaStream_t s) {
   const unsigned grid = lean_grid(p.num_items, kBwdWpc, kBwdMinb);
-  if (rpf_enabled()) {
-    if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true, true><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
-    else gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false, true><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
-    return;
-  }
   if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
   else gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
 }
