@@ -65,15 +65,41 @@ __device__ __forceinline__ int widx(int e, int k) {
 }
 
 // index of (gate * alpha, c)(e, k) in LeanSmem::tc, laid out so that the two outputs of a
-// lane in the dz stage are one conflict-free 16-byte read: NV = 2 -> heads (2g, 2g+1) of one
-// edge are adjacent; NV = 1 -> edges (2r, 2r+1) of one head are adjacent
+// lane in the dz stage are one 16-byte read: NV = 2 -> heads (2g, 2g+1) of one edge are
+// adjacent; NV = 1 -> edges (2r, 2r+1) of one head are adjacent.  The 16-byte chunks are
+// XOR-swizzled so that both the dz stage's reads (a quarter warp: 8 edges x one head pair, or
+// 4 edge pairs x 2 heads) and the edge phase's 8-byte writes (a half warp: 2 edges x 8 heads)
+// hit 8 distinct bank groups.  Unswizzled, the reads were 16-way conflicts: 16 wavefronts per
+// 8-row group instead of 4 (ncu source page, profiles/r02_k4f_smem.md), 12 of K4f's ~55
+// shared-pipe wavefronts per group.  h = 8 (lean kernels).
 template <int NV, int h>
 __device__ __forceinline__ int tcidx(int e, int k) {
-  if constexpr (NV == 2) return e * h + k;
-  else return ((e >> 1) * h + k) * 2 + (e & 1);
+  static_assert(h == 8, "tc swizzle: 8 heads");
+  if constexpr (NV == 2) return (e * 4 + ((k >> 1) ^ ((e >> 1) & 3))) * 2 + (k & 1);
+  else return ((e >> 1) * h + (k ^ (2 * ((e >> 1) & 3)))) * 2 + (e & 1);
 }
 
 __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
+
+// K2's row gathers of a [*, 8 F] table at this lane's paired columns (Cols with pl = F / VW:
+// vector i sits F floats after vector i - 1).  The lane's base + column pointer is formed once
+// and made opaque, so each row costs a 64-bit row * row_bytes + pointer (LEA + LEA.HI.X) and NV
+// loads with immediate offsets; the plain (base + column) + row * row_bytes form compiles to 3
+// IMADs and a MOV per row (the uniform table base folded into every address and the column
+// re-added).  Measured at C2: K2 7.84 -> 7.62 ms; the same change made K4f slower (10.9 ->
+// 11.4 ms: its loads issue later in the schedule), so K4f keeps gather_row.
+template <int VW, int NV, int F>
+struct LaneRows {
+  const char* lb;
+  __device__ __forceinline__ LaneRows(const float* base, int col0) {
+    asm("mov.b64 %0, %1;" : "=l"(lb) : "l"(base + col0));
+  }
+  __device__ __forceinline__ void gather(uint32_t r, Vec<VW> (&x)[NV]) const {
+    const char* a = lb + (uint64_t)r * (8u * F * 4u);
+#pragma unroll
+    for (int i = 0; i < NV; ++i) x[i] = ldg_vec<VW>(reinterpret_cast<const float*>(a + i * F * 4));
+  }
+};
 
 template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
 __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(GatParams p) {
@@ -281,6 +307,8 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
   const int hd0 = cols.hd[0];
   constexpr int epi = kWarp / h;
   const int kk = lane % h;
+  constexpr int F = PER * VW;  // = f: the shapes this kernel takes fill the warp
+  const LaneRows<VW, NV, F> hrows(p.Ht, cols.col[0]);
   unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
   for (int64_t g = blockIdx.x; DYN || g * WPC < p.num_items; g += gridDim.x) {
     int64_t wi;
@@ -309,10 +337,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #pragma unroll
       for (int t = 0; t < U; t += 4) {
         const uint4 id4 = lds_u4(sm.nb + t);
-        gather_row<VW, NV>(p.Ht, id4.x, hf, cols, x[t]);
-        gather_row<VW, NV>(p.Ht, id4.y, hf, cols, x[t + 1]);
-        gather_row<VW, NV>(p.Ht, id4.z, hf, cols, x[t + 2]);
-        gather_row<VW, NV>(p.Ht, id4.w, hf, cols, x[t + 3]);
+        hrows.gather(id4.x, x[t]);
+        hrows.gather(id4.y, x[t + 1]);
+        hrows.gather(id4.z, x[t + 2]);
+        hrows.gather(id4.w, x[t + 3]);
       }
       // edge phase on (edge, head) pairs: logits of this lane's head for edges i*epi + lane/h
       float s[MAXH];
@@ -368,10 +396,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #pragma unroll
         for (int t = 0; t < U; t += 4) {
           const uint4 id4 = lds_u4(sm.nb + j + t);
-          gather_row<VW, NV>(p.Ht, id4.x, hf, cols, x[t]);
-          gather_row<VW, NV>(p.Ht, id4.y, hf, cols, x[t + 1]);
-          gather_row<VW, NV>(p.Ht, id4.z, hf, cols, x[t + 2]);
-          gather_row<VW, NV>(p.Ht, id4.w, hf, cols, x[t + 3]);
+          hrows.gather(id4.x, x[t]);
+          hrows.gather(id4.y, x[t + 1]);
+          hrows.gather(id4.z, x[t + 2]);
+          hrows.gather(id4.w, x[t + 3]);
         }
       }
       __syncwarp();
