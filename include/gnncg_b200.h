@@ -80,6 +80,13 @@ typedef struct gnncg_sched {
   const uint32_t* items;       /* 2*num_items: (row, chunk index) pairs */
   const uint32_t* split_rows;  /* num_split_rows row ids */
   const uint32_t* split_first; /* num_split_rows+1 item offsets into [0, num_split_items) */
+  /* Optional L2 hint (NULL / 0 = none): HOST prefix sums of how often each row of the table the
+   * kernel GATHERS is read, i.e. the offsets of the other index (csc_src's for a csr_dst schedule:
+   * K2 gathers source rows; csr_dst's for a csc_src schedule: K4f gathers destination rows), and
+   * their row count.  With gnncg_l2_persist() on, the fp32 fused kernels mark the contiguous row
+   * range carrying the most gathers as L2-persisting (gnncg_hot_window_host).  Caller-owned. */
+  const uint64_t* gather_off;
+  int64_t gather_rows;
 } gnncg_sched_t;
 
 /* ---------------------------------------------------------------- runtime */
@@ -99,6 +106,16 @@ uint64_t gnncg_launch_count(void);
  * written once; the flops / io units follow from each kernel's fixed per-edge and per-row work
  * (paper_2110_09524_b200/cost.py).  Process-wide; not for concurrent measurement. */
 int gnncg_cost_counters(uint64_t* counters);
+/* L2 residency for the gathered tables (opt-in, process-wide).  Sets the device's persisting-L2
+ * set-aside to min(bytes, cudaDevAttrMaxPersistingL2CacheSize) (0 turns it off and resets the
+ * persisting lines); *granted_host (may be NULL) receives the size set.  While on, the fp32
+ * fused GAT kernels (K2, K4f) launch with an access-policy window over the hottest rows of the
+ * table they gather (schedules carrying gather_off): those rows stay in L2, the rest streams.
+ * Results do not change (cache policy only). */
+int gnncg_l2_persist(size_t bytes, size_t* granted_host);
+/* The window: the start row b maximising off[b+n] - off[b] (the gathers of rows [b, b+n)) over
+ * 0 <= b <= num_rows - n, lowest b on ties; n is clamped to num_rows. */
+int gnncg_hot_window_host(int64_t num_rows, const uint64_t* off_host, int64_t n, int64_t* begin_host);
 
 /* ------------------------------------------------------- graph store (K9)
  * Replaces build_index (graph.cpp:14-28) and the Graph ctor (graph.cpp:32-45).

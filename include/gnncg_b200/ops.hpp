@@ -98,6 +98,7 @@ struct DeviceIndex {
   std::int64_t rows = 0, edges = 0;
   DeviceBuffer off, nbr, eid;
   DeviceBuffer items, split_rows, split_first;
+  std::vector<std::uint64_t> host_off;  // host copy of off (the other index's L2 gather hint)
   gnncg_sched_t sched{};
 
   gnncg_index_t view() const {
@@ -122,6 +123,12 @@ class DeviceGraph {
     DeviceBuffer ws(gnncg_csr_build_workspace(V_, E_));
     build(dst_, edge_dst_, edge_src_, ws, chunk);
     build(src_, edge_src_, edge_dst_, ws, chunk);
+    // L2 hint (gnncg_l2_persist): K2 over csr_dst gathers source rows, read out-degree times;
+    // K4f over csc_src gathers destination rows, read in-degree times
+    dst_.sched.gather_off = src_.host_off.data();
+    dst_.sched.gather_rows = V_;
+    src_.sched.gather_off = dst_.host_off.data();
+    src_.sched.gather_rows = V_;
   }
 
   std::int64_t num_vertices() const { return V_; }
@@ -165,6 +172,7 @@ class DeviceGraph {
     std::vector<std::uint32_t> items(2 * n + 2), srows(nr + 1), first(nr + 1);
     check(gnncg_sched_build_host(rows, off.data(), chunk, &n, &ns, &nr, items.data(), srows.data(), first.data()),
           "sched");
+    idx.host_off = std::move(off);
     idx.items = upload(items.data(), items.size(), s);
     idx.split_rows = upload(srows.data(), srows.size(), s);
     idx.split_first = upload(first.data(), first.size(), s);

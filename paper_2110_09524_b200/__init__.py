@@ -6,7 +6,7 @@ compute runs in the in-tree ``libgnncg_b200.so`` (C ABI: include/gnncg_b200.h);
 there is no CPU fallback.
 """
 from ._lib import (ArgumentError, CudaError, DeviceError, GnncgError, GraphError, TensorError,  # noqa: F401
-                   UnsupportedError, WorkspaceError)
+                   UnsupportedError, WorkspaceError, hot_window, l2_persist)
 from .graph import DeviceGraph, DeviceIndex, DeviceSched, chung_lu_cdf, knn_edges, partition_rows, uniform_edges  # noqa: F401
 from .ops import (GatGrads, GatParams, GatStash, edgeconv_backward, edgeconv_forward, gat_backward,  # noqa: F401
                   gat_forward, gat_region_backward, gat_region_forward, gcn_backward, gcn_forward, gcn_norm, gemm,

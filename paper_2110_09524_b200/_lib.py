@@ -75,7 +75,8 @@ class Sched(C.Structure):
     """gnncg_sched_t -- edge-balance work items of the unified thread mapping."""
 
     _fields_ = [("num_items", i64), ("num_split_items", i64), ("num_split_rows", i64), ("chunk", i32),
-                ("reserved", i32), ("items", vp), ("split_rows", vp), ("split_first", vp)]
+                ("reserved", i32), ("items", vp), ("split_rows", vp), ("split_first", vp),
+                ("gather_off", vp), ("gather_rows", i64)]
 
 
 P = C.POINTER
@@ -96,6 +97,8 @@ _SIGS = {
     "gnncg_device_check": ([], i32),
     "gnncg_launch_count": ([], u64),
     "gnncg_cost_counters": ([vp], i32),
+    "gnncg_l2_persist": ([sz, P(sz)], i32),
+    "gnncg_hot_window_host": ([i64, vp, i64, P(i64)], i32),
     "gnncg_csr_build_workspace": ([i64, i64], sz),
     "gnncg_csr_build": ([i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_csr_build_rect": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
@@ -198,3 +201,22 @@ def call(name: str, *args):
 
 def require_device():
     check(lib().gnncg_device_check(), "gnncg_device_check")
+
+
+def l2_persist(nbytes: int) -> int:
+    """gnncg_l2_persist: opt in to L2-persisting windows over the hottest gathered rows of the
+    fused GAT kernels (0 turns it off).  Returns the set-aside granted (clamped to the device)."""
+    got = sz()
+    call("gnncg_l2_persist", int(nbytes), C.byref(got))
+    return int(got.value)
+
+
+def hot_window(off, n: int) -> int:
+    """gnncg_hot_window_host: start row of the n-row window with the most gathers (off = the
+    gathered table's per-row read counts as prefix sums, uint64)."""
+    import numpy as np
+
+    off = np.ascontiguousarray(off, dtype=np.uint64)
+    b = i64()
+    call("gnncg_hot_window_host", off.size - 1, off.ctypes.data, int(n), C.byref(b))
+    return int(b.value)

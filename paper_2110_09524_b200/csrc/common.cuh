@@ -32,6 +32,14 @@ int require_device();
 // Counts every kernel this library launches (gnncg_launch_count()).
 void note_launch();
 
+// L2 access-policy window over the hottest rows of a gathered table (gnncg_l2_persist).
+struct L2Window {
+  const void* base = nullptr;
+  size_t bytes = 0;
+};
+size_t l2_persist_bytes();
+L2Window l2_window(const gnncg_sched_t* sched, const void* table, size_t row_bytes);
+
 // Device cost counters of one kernel kind (gnncg_cost_counters), null when off.
 enum CostKind { kCostK2 = 0, kCostK3 = 1, kCostK4 = 2, kCostK4f = 3, kCostLp = 4 };
 unsigned long long* cost_slot(int kind);

@@ -1329,6 +1329,7 @@ static int gat_fwd_impl(bool lp, const gnncg_index_t* csr_dst, const gnncg_sched
   p.num_items = sched->num_items; p.num_split_items = sched->num_split_items; p.chunk = sched->chunk;
   p.h = h; p.f = f; p.slope = slope;
   p.Ht = Ht; p.lp = Ht_lp; p.Al = Al; p.Ar = Ar; p.out = out; p.mo = m; p.dd = d; p.part = static_cast<float*>(ws);
+  if (!lp) p.win = l2_window(sched, Ht, (size_t)h * f * 4);  // source rows of Ht (csc_src offsets)
   cudaStream_t s = as_stream(stream);
   if (lp) {
     rc = attach_counter(p, csr_dst->num_edges, ws, ws_bytes, need, s);
@@ -1504,6 +1505,7 @@ static int gat_bwd_src_fused_impl(bool lp, const gnncg_index_t* csc_src, const g
   p.a_l = a_l; p.a_r = a_r; p.dHt = dHt; p.dAl = dAl; p.row_base = row_base; p.num_local = num_local;
   p.part = static_cast<float*>(ws);
   p.fast = 1;
+  if (!lp) p.win = l2_window(sched, dOut, (size_t)h * f * 4);  // destination rows of dOut (csr_dst offsets)
   // (C5's ~100-edge items: one item per request was slower than the fixed stride, 132.5 ->
   // 134.6 ms, the counter address being the limit; 5 per request: 115.8 ms)
   rc = attach_counter(p, csc_src->num_edges, ws, ws_bytes, need, s);

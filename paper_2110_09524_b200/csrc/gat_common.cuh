@@ -95,6 +95,7 @@ struct GatParams {
   unsigned* ctr;  // dynamic item fetch (DYN kernels): zeroed work counter in the workspace
   int batch;      // items taken per counter request
   unsigned long long* cnt;  // cost counters of this kernel kind (gnncg_cost_counters), or null
+  L2Window win;             // launch attribute only: L2-persisting rows of the gathered table
 };
 
 // Cost counters (gnncg_cost_counters; "measured == predicted"): per work item

@@ -471,18 +471,44 @@ unsigned lean_grid(int64_t items, int wpc, int minb) {
   return (unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(items, wpc), (int64_t)lean_num_sms() * minb));
 }
 
+// Launch with the L2 access-policy window of p.win (gnncg_l2_persist): the hottest rows of the
+// gathered table are marked persisting, every other access streams.  Measured at C2 (same box,
+// set-aside 30 / 60 MB vs off): K4f 10.56-10.76 vs 10.92-11.20 ms, K2 7.43-7.59 vs 7.67-7.87
+// ms; 90+ MB slows the kernels between them (profiles/r02_l2_persist.txt).
+template <typename... KArgs>
+void launch_win(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t s, const GatParams& p) {
+  if (p.win.bytes == 0) {
+    k<<<grid, block, 0, s>>>(p);
+    return;
+  }
+  cudaLaunchConfig_t cfg = {};
+  cfg.gridDim = dim3(grid);
+  cfg.blockDim = dim3(block);
+  cfg.stream = s;
+  cudaLaunchAttribute at[1];
+  at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+  at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(p.win.base);
+  at[0].val.accessPolicyWindow.num_bytes = p.win.bytes;
+  at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+  at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+  at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+  cfg.attrs = at;
+  cfg.numAttrs = 1;
+  cudaLaunchKernelEx(&cfg, k, p);
+}
+
 template <int VW, int NV, int PER>
 void launch_fwd(const GatParams& p, cudaStream_t s) {
   const unsigned grid = lean_grid(p.num_items, kFwdWpc, kFwdMinb);
-  if (p.ctr) gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, true><<<grid, kFwdWpc * kWarp, 0, s>>>(p);
-  else gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, false><<<grid, kFwdWpc * kWarp, 0, s>>>(p);
+  if (p.ctr) launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, true>, grid, kFwdWpc * kWarp, s, p);
+  else launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, false>, grid, kFwdWpc * kWarp, s, p);
 }
 
 template <int VW, int NV, int PER>
 void launch(const GatParams& p, cudaStream_t s) {
   const unsigned grid = lean_grid(p.num_items, kBwdWpc, kBwdMinb);
-  if (p.ctr) gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
-  else gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false><<<grid, kBwdWpc * kWarp, 0, s>>>(p);
+  if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true>, grid, kBwdWpc * kWarp, s, p);
+  else launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false>, grid, kBwdWpc * kWarp, s, p);
 }
 
 }  // namespace

@@ -1,6 +1,7 @@
 // SPDX-License-Identifier: Apache-2.0
 // Runtime plumbing of the C ABI: errors, device check, host-side schedule and
 // partition construction (no device work here).
+#include <algorithm>
 #include <atomic>
 #include <cstdarg>
 #include <cstring>
@@ -15,6 +16,39 @@ static std::atomic<unsigned long long> g_launches{0};
 static std::atomic<unsigned long long*> g_cost{nullptr};
 
 void note_launch() { g_launches.fetch_add(1, std::memory_order_relaxed); }
+
+static std::atomic<size_t> g_l2_persist{0};
+size_t l2_persist_bytes() { return g_l2_persist.load(std::memory_order_relaxed); }
+
+// argmax_b off[b+n] - off[b] (lowest b on ties), cached for the last few (off, rows, n): the
+// scan is O(rows) on the host and a schedule is reused for every layer and step.
+int64_t hot_window_begin(const uint64_t* off, int64_t rows, int64_t n) {
+  if (!off || rows <= 0 || n <= 0 || n >= rows) return 0;
+  struct Hit { const uint64_t* off; int64_t rows, n, b; };
+  static thread_local Hit cache[4] = {};
+  static thread_local int next = 0;
+  for (const Hit& c : cache)
+    if (c.off == off && c.rows == rows && c.n == n) return c.b;
+  int64_t best = 0;
+  uint64_t bv = off[n] - off[0];
+  for (int64_t b = 1; b + n <= rows; ++b) {
+    const uint64_t v = off[b + n] - off[b];
+    if (v > bv) { bv = v; best = b; }
+  }
+  cache[next] = Hit{off, rows, n, best};
+  next = (next + 1) % 4;
+  return best;
+}
+
+// The window for a gather of `table` (rows of row_bytes) under schedule `sched`, or {null, 0}.
+L2Window l2_window(const gnncg_sched_t* sched, const void* table, size_t row_bytes) {
+  const size_t pb = l2_persist_bytes();
+  if (pb == 0 || !sched || !sched->gather_off || sched->gather_rows <= 0 || !table || row_bytes == 0) return {};
+  const int64_t n = std::min<int64_t>((int64_t)(pb / row_bytes), sched->gather_rows);
+  if (n <= 0) return {};
+  const int64_t b = hot_window_begin(sched->gather_off, sched->gather_rows, n);
+  return {static_cast<const char*>(table) + (size_t)b * row_bytes, (size_t)n * row_bytes};
+}
 
 unsigned long long* cost_slot(int kind) {
   unsigned long long* c = g_cost.load(std::memory_order_acquire);
@@ -86,6 +120,30 @@ uint64_t gnncg_launch_count(void) { return g_launches.load(std::memory_order_rel
 
 int gnncg_cost_counters(uint64_t* counters) {
   g_cost.store(reinterpret_cast<unsigned long long*>(counters), std::memory_order_release);
+  return GNNCG_OK;
+}
+
+int gnncg_l2_persist(size_t bytes, size_t* granted) {
+  GNNCG_DEVICE_GUARD();
+  int dev = 0, mx = 0;
+  cudaGetDevice(&dev);
+  cudaDeviceGetAttribute(&mx, cudaDevAttrMaxPersistingL2CacheSize, dev);
+  const size_t want = std::min<size_t>(bytes, (size_t)std::max(mx, 0));
+  cudaError_t e = cudaDeviceSetLimit(cudaLimitPersistingL2CacheSize, want);
+  if (e == cudaSuccess && want == 0) e = cudaCtxResetPersistingL2Cache();
+  if (e != cudaSuccess) {
+    cudaGetLastError();
+    return fail(GNNCG_ERR_CUDA, "l2_persist: %s", cudaGetErrorString(e));
+  }
+  g_l2_persist.store(want, std::memory_order_relaxed);
+  if (granted) *granted = want;
+  return GNNCG_OK;
+}
+
+int gnncg_hot_window_host(int64_t num_rows, const uint64_t* off, int64_t n, int64_t* begin) {
+  GNNCG_REQUIRE(off && begin, GNNCG_ERR_ARG, "hot_window: null pointer");
+  GNNCG_REQUIRE(num_rows >= 0 && n >= 0, GNNCG_ERR_ARG, "hot_window: negative size");
+  *begin = hot_window_begin(off, num_rows, std::min(n, num_rows));
   return GNNCG_OK;
 }
 

@@ -50,6 +50,9 @@ class DeviceIndex:
     eid: torch.Tensor | None
     _struct: Index | None = field(default=None, repr=False)
     _sched: dict = field(default_factory=dict, repr=False)
+    # host uint64 offsets of the other index of the same graph: how often the fused kernel over
+    # THIS index reads each row of the table it gathers (gnncg_sched_t.gather_off, L2 hint)
+    gather_off: np.ndarray | None = field(default=None, repr=False)
 
     @property
     def num_rows(self) -> int:
@@ -66,7 +69,9 @@ class DeviceIndex:
 
     def sched(self, chunk: int = DEFAULT_CHUNK) -> "DeviceSched":
         if chunk not in self._sched:
-            self._sched[chunk] = DeviceSched.build(self.off.cpu().numpy().view(np.uint64), chunk, self.off.device)
+            sc = DeviceSched.build(self.off.cpu().numpy().view(np.uint64), chunk, self.off.device)
+            sc.gather_off = self.gather_off
+            self._sched[chunk] = sc
         return self._sched[chunk]
 
     def max_degree(self) -> int:
@@ -93,6 +98,7 @@ class DeviceSched:
     items: torch.Tensor
     split_rows: torch.Tensor
     split_first: torch.Tensor
+    gather_off: np.ndarray | None = None
     _struct: Sched | None = field(default=None, repr=False)
 
     @staticmethod
@@ -119,8 +125,10 @@ class DeviceSched:
 
     def struct(self) -> Sched:
         if self._struct is None:
+            go = self.gather_off
             self._struct = Sched(self.num_items, self.num_split_items, self.num_split_rows, self.chunk, 0,
-                                 _ptr(self.items), _ptr(self.split_rows), _ptr(self.split_first))
+                                 _ptr(self.items), _ptr(self.split_rows), _ptr(self.split_first),
+                                 None if go is None else go.ctypes.data, 0 if go is None else go.size - 1)
         return self._struct
 
 
@@ -184,6 +192,10 @@ class DeviceGraph:
         ws = Workspace(src.device)
         csr = cls.build_index(V, dst, src, ws)
         csc = cls.build_index(V, src, dst, ws)
+        # L2 hint: K2 over csr_dst gathers source rows (read out-degree times), K4f over csc_src
+        # gathers destination rows (read in-degree times)
+        csr.gather_off = np.ascontiguousarray(csc.off.cpu().numpy().view(np.uint64))
+        csc.gather_off = np.ascontiguousarray(csr.off.cpu().numpy().view(np.uint64))
         g = cls(V, src, dst, csr, csc)
         g.ws = ws
         return g

@@ -135,3 +135,33 @@ def test_bench_spawns_one_rank_per_gpu(monkeypatch):
     assert cmd[cmd.index("--master-addr") + 1] == "127.0.0.1"
     assert cmd[-6:] == ["--gpus", "4", "--config", "c5", "--steps", "2"]
     assert seen["env"]["NCCL_DEBUG"] == "INFO"
+
+
+def _hot_window_reference(off, n):
+    """argmax_b off[b+n] - off[b], lowest b on ties (runtime.cu:hot_window_begin)."""
+    rows = off.size - 1
+    if n <= 0 or n >= rows:
+        return 0
+    sums = off[n:].astype(np.int64) - off[:rows - n + 1].astype(np.int64)
+    return int(np.argmax(sums))
+
+
+@pytest.mark.parametrize("seed", [0, 1, 2])
+def test_hot_window_host(seed):
+    rng = np.random.default_rng(seed)
+    deg = rng.integers(0, 50, 3000)
+    deg[rng.integers(0, 3000, 5)] += 10_000  # a few hubs somewhere
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    for n in (0, 1, 7, 100, 2999, 3000, 5000):
+        assert _lib.hot_window(off, n) == _hot_window_reference(off, n), n
+    # degree-descending ids (the Chung-Lu generator): the window starts at row 0
+    off = np.concatenate([[0], np.cumsum(np.sort(deg)[::-1])]).astype(np.uint64)
+    assert _lib.hot_window(off, 250) == 0
+    with pytest.raises(_lib.ArgumentError):
+        _lib.call("gnncg_hot_window_host", 10, None, 2, C.byref(_lib.i64()))
+
+
+@pytest.mark.skipif(torch.cuda.is_available(), reason="checks the no-device path")
+def test_l2_persist_needs_device():
+    with pytest.raises(_lib.DeviceError):
+        _lib.l2_persist(32 << 20)
