@@ -81,6 +81,16 @@ __device__ __forceinline__ int tcidx(int e, int k) {
 
 __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret_cast<const uint4*>(p); }
 
+// Streaming accesses (read / written once per launch: the neighbour ids, the output rows) are
+// marked evict-first so they do not displace the gathered rows in L2.  Measured (same box):
+// C5 K2 73.4 vs 75.3 ms; C2 within noise (38.1-38.8 vs 38.3-38.7 ms per step).
+__device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
+template <int VW>
+__device__ __forceinline__ void st_stream(float* p, const Vec<VW>& v) {
+  static_assert(VW == 4, "streaming store: 16-byte vectors");
+  __stcs(reinterpret_cast<float4*>(p), make_float4(v.x[0], v.x[1], v.x[2], v.x[3]));
+}
+
 // K2's row gathers of a [*, 8 F] table at this lane's paired columns (Cols with pl = F / VW:
 // vector i sits F floats after vector i - 1).  The lane's base + column pointer is formed once
 // and made opaque, so each row costs a 64-bit row * row_bytes + pointer (LEA + LEA.HI.X) and NV
@@ -150,7 +160,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
     for (int i = 0; i < NV; ++i) dal[i] = 0.f;
 
     const uint64_t e0 = it.e0, e1 = it.e1;
-    uint32_t v_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+    uint32_t v_cur = e0 + lane < e1 ? ld_stream(p.nbr + e0 + lane) : 0u;
     const float* tab = p.dOut;
     for (uint64_t base = e0; base < e1; base += 32) {
       const int n = (int)min((uint64_t)32, e1 - base);
@@ -186,7 +196,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
         }
       }
       __syncwarp();
-      v_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+      v_cur = base + 32 + lane < e1 ? ld_stream(p.nbr + base + 32 + lane) : 0u;
       {
         const uint4 id4 = lds_u4(sm.nb + 4);
         gather_row<VW, NV>(tab, id4.x, hf, cols, gv[4]);
@@ -265,7 +275,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
         Vec<VW> o;
 #pragma unroll
         for (int q = 0; q < VW; ++q) o.x[q] = fmaf(dl, al.x[q], acc[i].x[q]);
-        st_vec<VW>(p.dHt + u * hf + cols.col[i], o);
+        st_stream<VW>(p.dHt + u * hf + cols.col[i], o);
       }
     } else {
       float* part = p.part + wi * src_stride(h, f);
@@ -327,7 +337,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
     Vec<VW> acc[NV];
     zero(acc);
     const uint64_t e0 = it.e0, e1 = it.e1;
-    uint32_t u_cur = e0 + lane < e1 ? __ldg(p.nbr + e0 + lane) : 0u;
+    uint32_t u_cur = e0 + lane < e1 ? ld_stream(p.nbr + e0 + lane) : 0u;
     for (uint64_t base = e0; base < e1; base += 32) {
       const int n = (int)min((uint64_t)32, e1 - base);
       const uint32_t u_last = __shfl_sync(0xffffffffu, u_cur, n - 1);
@@ -347,7 +357,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #pragma unroll
       for (int i = 0; i < MAXH; ++i)
         if (i < h) s[i] = __ldg(p.Al + (int64_t)sm.nb[i * epi + lane / h] * h + kk);
-      u_cur = base + 32 + lane < e1 ? __ldg(p.nbr + base + 32 + lane) : 0u;
+      u_cur = base + 32 + lane < e1 ? ld_stream(p.nbr + base + 32 + lane) : 0u;
       float mx = -FLT_MAX;
 #pragma unroll
       for (int i = 0; i < MAXH; ++i) {
@@ -415,7 +425,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
         Vec<VW> o;
 #pragma unroll
         for (int q = 0; q < VW; ++q) o.x[q] = acc[i].x[q] * inv;
-        st_vec<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
+        st_stream<VW>(p.out + (int64_t)it.row * hf + cols.col[i], o);
       }
       if (lane < h) {
         p.mo[(int64_t)it.row * h + lane] = mk;
