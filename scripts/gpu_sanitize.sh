@@ -26,4 +26,5 @@ for tool in memcheck racecheck synccheck; do
     -k "G3 or ER16 or cora or edgeless or star" > gpurun_out/san_dyn_${tool}_$TAG.log 2>&1
   echo "rc=$?" >> gpurun_out/san_dyn_${tool}_$TAG.log
 done
+timeout 1200 compute-sanitizer --tool memcheck --error-exitcode 99 --print-limit 20 python -m pytest tests/test_gpu_l2.py -q -x -p no:cacheprovider > gpurun_out/san_l2_$TAG.log 2>&1; echo "rc=$?" >> gpurun_out/san_l2_$TAG.log
 echo done
