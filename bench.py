@@ -445,9 +445,10 @@ KERNEL_REGEX = {"gat_fwd": "gat_fwd", "gat_bwd_src_fused": "gat_bwd_src_(lean|fa
                 "gat_bwd_src": "gat_bwd_src_kernel", "gat_bwd_dst": "gat_bwd_dst"}
 
 
-def ncu_dram_bytes(args, kernel: str):
-    """DRAM bytes of one launch of `kernel` in this configuration, from an ncu replay of a
-    one-step child run (the second launch: a warm one).  Returns (bytes, ncu_ms, note)."""
+def ncu_dram_bytes(args, kernel: str, per_step: int = 1):
+    """DRAM bytes per launch of `kernel` in this configuration: an ncu replay of a child run (one
+    warm-up step, then one profiled step) captures the `per_step` launches of the profiled step
+    and averages them (layers differ in width, e.g. GCN).  Returns (bytes, ncu_ms, note)."""
     import csv
     import io
     import shutil
@@ -459,15 +460,17 @@ def ncu_dram_bytes(args, kernel: str):
     regex = KERNEL_REGEX.get(kernel, kernel)
     with tempfile.TemporaryDirectory() as td:
         log = os.path.join(td, "ncu.csv")
-        cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", f"regex:{regex}", "-s", "1", "-c", "1",
-               "--csv", "--log-file", log, sys.executable, os.path.abspath(__file__), "--steps", "1", "--warmup", "0",
+        n = max(1, int(per_step))
+        cmd = [ncu, "--metrics", NCU_METRICS, "--clock-control", "none", "-k", f"regex:{regex}", "-s", str(n),
+               "-c", str(n), "--csv", "--log-file", log, sys.executable, os.path.abspath(__file__), "--steps", "1",
+               "--warmup", "1",
                "--config", args.config, "--gather", args.gather, "--no-cpu-baseline", "--no-e2e", "--no-ncu",
                "--no-parity", "--ncu-probe"]
         if args.chunk:
             cmd += ["--chunk", str(args.chunk)]
         cmd += ["--l2-persist-mb", str(args.l2_persist_mb)]
         try:
-            subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=600, check=False,
+            subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=900, check=False,
                            env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})
             with open(log) as fh:
                 text = fh.read()
@@ -480,16 +483,21 @@ def ncu_dram_bytes(args, kernel: str):
     mi, ui, vi = hdr.index("Metric Name"), hdr.index("Metric Unit"), hdr.index("Metric Value")
     scale = {"byte": 1, "Kbyte": 1e3, "Mbyte": 1e6, "Gbyte": 1e9, "Tbyte": 1e12, "ns": 1e-6, "us": 1e-3, "ms": 1.0,
              "usecond": 1e-3, "msecond": 1.0, "nsecond": 1e-6}
-    vals = {}
+    ii = hdr.index("ID")
+    vals = {}  # metric -> {launch id: value}
     for r in rows[1:]:
         try:
-            vals[r[mi]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
+            vals.setdefault(r[mi], {})[r[ii]] = float(r[vi].replace(",", "")) * scale.get(r[ui], 1.0)
         except (ValueError, IndexError):
             continue
-    if "dram__bytes_read.sum" not in vals:
+    rd = vals.get("dram__bytes_read.sum", {})
+    if not rd:
         return None, None, "ncu capture lacks dram__bytes"
-    return (vals["dram__bytes_read.sum"] + vals.get("dram__bytes_write.sum", 0.0), vals.get("gpu__time_duration.sum"),
-            f"ncu --metrics {NCU_METRICS} on one warm launch (regex {regex}) of a child run of this config")
+    wr, tm = vals.get("dram__bytes_write.sum", {}), vals.get("gpu__time_duration.sum", {})
+    k = len(rd)
+    return ((sum(rd.values()) + sum(wr.values())) / k, (sum(tm.values()) / k) if tm else None,
+            f"ncu --metrics {NCU_METRICS}, mean over the {k} launch(es) (regex {regex}) of one warm step of a child "
+            "run of this config (run after this process freed its device memory)")
 
 
 # ----------------------------------------------------------------------------- GPU arm
@@ -692,11 +700,42 @@ def run_ours(args):
 
     mem = memory_block(model, H, 0.0, wl)
 
+    # --- checker leg (oracle/: never the measured path) ---------------------------------
+    cpu = parity = None
+    if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
+        from oracle.sampled import gat_model_sampled_check
+
+        for p, p0 in zip(model_params(model), init_params):  # the benchmarked model at its initial parameters
+            p.copy_(p0)
+        t0 = time.perf_counter()
+        parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0, hub_src=args.config == "reddit")
+        e_out = max(parity["max_rel_err"].get("out_layer1", 0), parity["max_rel_err"].get("out_last", 0))
+        e_grad = parity.get("max_norm_err", {}).get("dH_last")
+        parity.update({"comparator": {"outputs": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
+                                      "gradients": "|a-b| / max(1, max|ref|) over the checked rows (DESIGN.md §2: "
+                                                   "stated deviation; fp32 sums cannot meet the elementwise bound "
+                                                   "where entries cancel)"},
+                       "bound": 1e-4, "pass": e_out < 1e-4 and (e_grad is None or e_grad < 1e-4),
+                       "max_rel_err_out": e_out, "max_rel_err_grads": e_grad,
+                       "oracle": "oracle/sampled.py: f64 local-neighbourhood restatement on the GPU model's own "
+                                 "layer inputs (one extra fwd+bwd after the timed steps)",
+                       "check_s": time.perf_counter() - t0})
     # --- roofline: DRAM bytes of the dominant kernel (ncu, this configuration) ----------
-    traffic, ncu_ms, tnote = (None, None, "skipped (--no-ncu)")
+    # The ncu child rebuilds the whole workload: free this process's device memory first (C5's
+    # graph and tables do not fit twice).
     single = rank == 0 and world == 1 and not dmode
     if single and not args.no_ncu:
-        traffic, ncu_ms, tnote = ncu_dram_bytes(args, dominant)
+        import gc
+
+        model = H = H_buf = graphed = step = init_params = None  # noqa: F841
+        for key in list(wl):
+            if key not in ("config", "cost", "scaling"):
+                wl[key] = None
+        gc.collect()
+        torch.cuda.empty_cache()
+    traffic, ncu_ms, tnote = (None, None, "skipped (--no-ncu)")
+    if single and not args.no_ncu:
+        traffic, ncu_ms, tnote = ncu_dram_bytes(args, dominant, kernels[dominant]["launches"] // max(1, args.steps))
     if traffic is None and args.config == "reddit" and args.gather == "fp32":
         tpath = os.path.join(ROOT, "profiles", "ncu_traffic.json")
         if os.path.exists(tpath):
@@ -726,26 +765,6 @@ def run_ours(args):
         roofline.update({"gather_ceiling_GBps": ceil, "gather_frac": roofline["l2_gather_rate_GBps"] / ceil,
                          "gather_ceiling_source": "profiles/r01_gather_ceiling.json (scripts/gather_bench2.cu)"})
 
-    # --- checker leg (oracle/: never the measured path) ---------------------------------
-    cpu = parity = None
-    if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
-        from oracle.sampled import gat_model_sampled_check
-
-        for p, p0 in zip(model_params(model), init_params):  # the benchmarked model at its initial parameters
-            p.copy_(p0)
-        t0 = time.perf_counter()
-        parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0, hub_src=args.config == "reddit")
-        e_out = max(parity["max_rel_err"].get("out_layer1", 0), parity["max_rel_err"].get("out_last", 0))
-        e_grad = parity.get("max_norm_err", {}).get("dH_last")
-        parity.update({"comparator": {"outputs": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
-                                      "gradients": "|a-b| / max(1, max|ref|) over the checked rows (DESIGN.md §2: "
-                                                   "stated deviation; fp32 sums cannot meet the elementwise bound "
-                                                   "where entries cancel)"},
-                       "bound": 1e-4, "pass": e_out < 1e-4 and (e_grad is None or e_grad < 1e-4),
-                       "max_rel_err_out": e_out, "max_rel_err_grads": e_grad,
-                       "oracle": "oracle/sampled.py: f64 local-neighbourhood restatement on the GPU model's own "
-                                 "layer inputs (one extra fwd+bwd after the timed steps)",
-                       "check_s": time.perf_counter() - t0})
     if single and not args.no_cpu_baseline and args.config == "reddit":
         cpu = cpu_baseline_for_gpu_arm()
 
