@@ -701,6 +701,7 @@ def run_ours(args):
     mem = memory_block(model, H, 0.0, wl)
 
     # --- checker leg (oracle/: never the measured path) ---------------------------------
+    single = rank == 0 and world == 1 and not dmode
     cpu = parity = None
     if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
         from oracle.sampled import gat_model_sampled_check
@@ -723,7 +724,6 @@ def run_ours(args):
     # --- roofline: DRAM bytes of the dominant kernel (ncu, this configuration) ----------
     # The ncu child rebuilds the whole workload: free this process's device memory first (C5's
     # graph and tables do not fit twice).
-    single = rank == 0 and world == 1 and not dmode
     if single and not args.no_ncu:
         import gc
 
