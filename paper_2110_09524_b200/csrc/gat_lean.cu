@@ -26,6 +26,13 @@
 //   * the gathered rows' ids are read four at a time (LDS.128 broadcast);
 //   * (gate * alpha, c) per (edge, head) sit side by side: the dz stage reads one
 //     8-byte pair per output.
+// Lane layout at the Reddit shape (8 x 32): each lane owns 8 consecutive columns of ONE head
+// (VW = 8, NV = 1, 4 lanes per head) and gathers them with one 256-bit load (LDG.E.ENL2.256):
+// half the load instructions of the paired 2 x 128-bit layout (VW = 4, NV = 2, 8 lanes per
+// head), and the per-edge head dots reduce over 4 lanes instead of 8 (6 shuffles and 12
+// selects per 8-row group instead of 14 and 28).  Measured (same box, 3 rounds): K4f 9.9-10.0
+// vs 10.6-10.7 ms, step 37.5-37.6 vs 38.8-39.3 ms; K2 unchanged (7.50-7.57 vs 7.57-7.65).
+// The paired layout stays buildable for A/B (-DGNNCG_LEAN_PAIRED).
 #include <algorithm>
 #include <cfloat>
 
@@ -87,8 +94,35 @@ __device__ __forceinline__ uint4 lds_u4(const uint32_t* p) { return *reinterpret
 __device__ __forceinline__ uint32_t ld_stream(const uint32_t* p) { return __ldcs(p); }
 template <int VW>
 __device__ __forceinline__ void st_stream(float* p, const Vec<VW>& v) {
-  static_assert(VW == 4, "streaming store: 16-byte vectors");
+  static_assert(VW == 4 || VW == 8, "streaming store: 16- or 32-byte vectors");
   __stcs(reinterpret_cast<float4*>(p), make_float4(v.x[0], v.x[1], v.x[2], v.x[3]));
+  if constexpr (VW == 8) __stcs(reinterpret_cast<float4*>(p) + 1, make_float4(v.x[4], v.x[5], v.x[6], v.x[7]));
+}
+
+// One gathered lane vector: VW = 8 is a single 256-bit load (LDG.E.ENL2.256, sm_100; the
+// address is 32-byte aligned: 1 KB rows, 8-float lane columns), VW = 4 a 128-bit one.
+template <int VW>
+__device__ __forceinline__ Vec<VW> ldg_row(const float* p) {
+  if constexpr (VW == 8) {
+    Vec<8> r;
+    asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+        : "=f"(r.x[0]), "=f"(r.x[1]), "=f"(r.x[2]), "=f"(r.x[3]), "=f"(r.x[4]), "=f"(r.x[5]), "=f"(r.x[6]),
+          "=f"(r.x[7])
+        : "l"(p));
+    return r;
+  } else {
+    return ldg_vec<VW>(p);
+  }
+}
+
+// gather_row (gat_common.cuh) with ldg_row: row r of a [*, hf] table at this lane's columns.
+template <int VW, int NV>
+__device__ __forceinline__ void lean_gather(const float* __restrict__ base, uint32_t r, int hf,
+                                            const Cols<VW, NV>& c, Vec<VW> (&x)[NV]) {
+  const uint64_t off = (uint64_t)r * (uint32_t)(hf * 4);
+#pragma unroll
+  for (int i = 0; i < NV; ++i)
+    x[i] = ldg_row<VW>(reinterpret_cast<const float*>(reinterpret_cast<const char*>(base + c.col[i]) + off));
 }
 
 // K2's row gathers of a [*, 8 F] table at this lane's paired columns (Cols with pl = F / VW:
@@ -107,7 +141,7 @@ struct LaneRows {
   __device__ __forceinline__ void gather(uint32_t r, Vec<VW> (&x)[NV]) const {
     const char* a = lb + (uint64_t)r * (8u * F * 4u);
 #pragma unroll
-    for (int i = 0; i < NV; ++i) x[i] = ldg_vec<VW>(reinterpret_cast<const float*>(a + i * F * 4));
+    for (int i = 0; i < NV; ++i) x[i] = ldg_row<VW>(reinterpret_cast<const float*>(a + i * F * 4));
   }
 };
 
@@ -169,10 +203,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
       Vec<VW> gv[U][NV];
       {  // the first half of the first row group goes out before the record loads
         const uint4 id4 = lds_u4(sm.nb);
-        gather_row<VW, NV>(tab, id4.x, hf, cols, gv[0]);
-        gather_row<VW, NV>(tab, id4.y, hf, cols, gv[1]);
-        gather_row<VW, NV>(tab, id4.z, hf, cols, gv[2]);
-        gather_row<VW, NV>(tab, id4.w, hf, cols, gv[3]);
+        lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[0]);
+        lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[1]);
+        lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[2]);
+        lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[3]);
       }
       {
         // edge phase, lanes = (edge, head) pairs: one {A_r, lse, c, 0} record load each
@@ -199,10 +233,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
       v_cur = base + 32 + lane < e1 ? ld_stream(p.nbr + base + 32 + lane) : 0u;
       {
         const uint4 id4 = lds_u4(sm.nb + 4);
-        gather_row<VW, NV>(tab, id4.x, hf, cols, gv[4]);
-        gather_row<VW, NV>(tab, id4.y, hf, cols, gv[5]);
-        gather_row<VW, NV>(tab, id4.z, hf, cols, gv[6]);
-        gather_row<VW, NV>(tab, id4.w, hf, cols, gv[7]);
+        lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[4]);
+        lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[5]);
+        lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[6]);
+        lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[7]);
       }
       for (int j = 0;;) {
         float pd[NVAL];
@@ -235,8 +269,11 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
           for (int ii = 0; ii < NV; ++ii)
             if (i == ii) dal[ii] += dz;
           dzp[q] = dz;
+          // NV = 1: one 4-byte reduction per (edge, head).  Pairing heads into 8- / 16-byte
+          // reductions through shuffles measured slower (C2 K4f 10.1 / 10.4 vs 10.0 ms)
           if (!PAIR && e < n) atomicAdd(p.dAro + (int64_t)sm.nb[e] * h + hd, dz);
         }
+
         if constexpr (PAIR) {
           // outputs (edge j + r, heads hd0, hd0 + 1); the next two heads of the same edge
           // are PER lanes up: even lane groups add four adjacent heads at once
@@ -251,10 +288,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
 #pragma unroll
         for (int t = 0; t < U; t += 4) {
           const uint4 id4 = lds_u4(sm.nb + j + t);
-          gather_row<VW, NV>(tab, id4.x, hf, cols, gv[t]);
-          gather_row<VW, NV>(tab, id4.y, hf, cols, gv[t + 1]);
-          gather_row<VW, NV>(tab, id4.z, hf, cols, gv[t + 2]);
-          gather_row<VW, NV>(tab, id4.w, hf, cols, gv[t + 3]);
+          lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[t]);
+          lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[t + 1]);
+          lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[t + 2]);
+          lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[t + 3]);
         }
       }
       __syncwarp();
@@ -542,14 +579,22 @@ bool lean_enabled() {
 
 bool launch_fwd_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
+#ifdef GNNCG_LEAN_PAIRED
   if (p.f == 32) launch_fwd<4, 2, 8>(p, s);
+#else
+  if (p.f == 32) launch_fwd<8, 1, 4>(p, s);
+#endif
   else launch_fwd<4, 1, 4>(p, s);
   return true;
 }
 
 bool launch_bwd_src_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
+#ifdef GNNCG_LEAN_PAIRED
   if (p.f == 32) launch<4, 2, 8>(p, s);
+#else
+  if (p.f == 32) launch<8, 1, 4>(p, s);
+#endif
   else launch<4, 1, 4>(p, s);
   return true;
 }
