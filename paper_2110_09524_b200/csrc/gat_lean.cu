@@ -487,7 +487,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 // registers, 16 warps/SM) 11.49-11.62 / 7.94-8.03; 4 x 5 (96 registers, no spill, 20
 // warps/SM) 10.78-10.92 / 7.71-7.81; 2 x 10 (96) 11.15-11.26 / 7.86-7.95; 2 x 12 (80, 24
 // warps) 10.92-10.95 / 8.15-8.16; 2 x 16 (64, 32 warps) 11.95 / 7.68-7.75.  At C5: 4 x 5
-// K4f 105.6 vs 113.0 ms, K2 82.5 vs 81.4 ms.
+// K4f 105.6 vs 113.0 ms, K2 82.5 vs 81.4 ms.  With the 256-bit lane rows (K4f needs fewer
+// registers at 8 x 32) K4f moved to 4 x 7 (72 registers, 28 warps/SM): C2 9.23-9.35 vs 9.94-10.02
+// ms (4 x 6: 9.47-9.54, 8 x 3: 9.46-9.52, 2 x 12: 9.45-9.57, 8 x 4: 9.64-9.70), C5 99.6 vs
+// 100.6 ms (profiles/r02_cta.txt).
 #ifndef GNNCG_LEAN_FWD_WPC
 #define GNNCG_LEAN_FWD_WPC 4
 #endif
@@ -498,7 +501,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #define GNNCG_LEAN_BWD_WPC 4
 #endif
 #ifndef GNNCG_LEAN_BWD_MINB
-#define GNNCG_LEAN_BWD_MINB 5
+#define GNNCG_LEAN_BWD_MINB 7
 #endif
 constexpr int kFwdWpc = GNNCG_LEAN_FWD_WPC, kFwdMinb = GNNCG_LEAN_FWD_MINB;
 constexpr int kBwdWpc = GNNCG_LEAN_BWD_WPC, kBwdMinb = GNNCG_LEAN_BWD_MINB;
