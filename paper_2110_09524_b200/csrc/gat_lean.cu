@@ -490,12 +490,20 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 // K4f 105.6 vs 113.0 ms, K2 82.5 vs 81.4 ms.  With the 256-bit lane rows (K4f needs fewer
 // registers at 8 x 32) K4f moved to 4 x 7 (72 registers, 28 warps/SM): C2 9.23-9.35 vs 9.94-10.02
 // ms (4 x 6: 9.47-9.54, 8 x 3: 9.46-9.52, 2 x 12: 9.45-9.57, 8 x 4: 9.64-9.70), C5 99.6 vs
-// 100.6 ms (profiles/r02_cta.txt).
+// 100.6 ms (profiles/r02_cta.txt).  K2 at 8 x 32 (VW = 8) moved to 8 x 4 (64 registers, 32
+// warps/SM): 7.53-7.58 vs 7.80 ms; at 8 x 16 (C5, VW = 4) it stays 4 x 5 (4 x 7
+// there: 81.0 vs 75.6 ms).
 #ifndef GNNCG_LEAN_FWD_WPC
 #define GNNCG_LEAN_FWD_WPC 4
 #endif
 #ifndef GNNCG_LEAN_FWD_MINB
 #define GNNCG_LEAN_FWD_MINB 5
+#endif
+#ifndef GNNCG_LEAN_FWD8_WPC
+#define GNNCG_LEAN_FWD8_WPC 8
+#endif
+#ifndef GNNCG_LEAN_FWD8_MINB
+#define GNNCG_LEAN_FWD8_MINB 4
 #endif
 #ifndef GNNCG_LEAN_BWD_WPC
 #define GNNCG_LEAN_BWD_WPC 4
@@ -503,7 +511,12 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #ifndef GNNCG_LEAN_BWD_MINB
 #define GNNCG_LEAN_BWD_MINB 7
 #endif
-constexpr int kFwdWpc = GNNCG_LEAN_FWD_WPC, kFwdMinb = GNNCG_LEAN_FWD_MINB;
+// K2's shape per lane width: VW = 8 (8 x 32 rows) / VW = 4 (8 x 16 rows)
+template <int VW>
+struct FwdShape {
+  static constexpr int WPC = VW == 8 ? GNNCG_LEAN_FWD8_WPC : GNNCG_LEAN_FWD_WPC;
+  static constexpr int MINB = VW == 8 ? GNNCG_LEAN_FWD8_MINB : GNNCG_LEAN_FWD_MINB;
+};
 constexpr int kBwdWpc = GNNCG_LEAN_BWD_WPC, kBwdMinb = GNNCG_LEAN_BWD_MINB;
 
 int lean_num_sms() {
@@ -549,9 +562,10 @@ void launch_win(void (*k)(KArgs...), unsigned grid, unsigned block, cudaStream_t
 
 template <int VW, int NV, int PER>
 void launch_fwd(const GatParams& p, cudaStream_t s) {
-  const unsigned grid = lean_grid(p.num_items, kFwdWpc, kFwdMinb);
-  if (p.ctr) launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, true>, grid, kFwdWpc * kWarp, s, p);
-  else launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, kFwdWpc, kFwdMinb, false>, grid, kFwdWpc * kWarp, s, p);
+  constexpr int W = FwdShape<VW>::WPC, M = FwdShape<VW>::MINB;
+  const unsigned grid = lean_grid(p.num_items, W, M);
+  if (p.ctr) launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, W, M, true>, grid, W * kWarp, s, p);
+  else launch_win(gat_fwd_lean_kernel<8, VW, NV, PER, W, M, false>, grid, W * kWarp, s, p);
 }
 
 template <int VW, int NV, int PER>
