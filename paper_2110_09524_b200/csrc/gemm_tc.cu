@@ -12,8 +12,8 @@
 // Default kernel (gemm_tf32x3_persist_kernel): one CTA per SM walks the output tiles;
 //   warp 0       TMA producer: cp.async.bulk.tensor 2D boxes of A and B
 //   warp 1       TMEM allocator + single-thread tcgen05.mma issuer (kind::tf32)
-//   warps 2..7   split warps: lo of each landed stage in shared memory
-//   warps 8..11  epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
+//   warps 2..11  split warps: lo of each landed stage in shared memory
+//   warps 12..15 epilogue: tcgen05.ld 32x32b.x32 from TMEM -> registers -> global
 // mbarrier pipeline: full (TMA bytes) -> split -> MMA -> empty (tcgen05.commit); the
 // accumulator is double-buffered in TMEM (accfull / accempty), so tile i's epilogue overlaps
 // tile i+1's main loop.  gemm_tf32x3_kernel (GNNCG_TC_PERSIST=0) is the one-tile-per-CTA form.
@@ -346,8 +346,15 @@ __global__ void __launch_bounds__(THREADS, 1)
 // (2 x BN columns), so the epilogue of tile i (its own 4 warps, one per TMEM lane quadrant)
 // overlaps the TMA / split / MMA work of tile i+1, and no CTA pays the TMEM allocation and
 // pipeline fill per tile.
-//   warp 0 TMA producer | warp 1 MMA issuer | warps 2..7 split | warps 8..11 epilogue
-constexpr int P_SPLIT_WARPS = 6;
+//   warp 0 TMA producer | warp 1 MMA issuer | warps 2..11 split | warps 12..15 epilogue
+// Split warps (lo = x - tf32(x) of each landed stage): 10 measured best where both operands are
+// split per stage (dW = H^T dHt: C2 0.337 vs 0.373 ms, C5 5.18 vs 6.19 ms); the GEMMs whose B
+// (the weight) is pre-split are unchanged (profiles/r02_gemm_split.txt).  P_EPI_WARP0 must stay
+// a multiple of 4 (the epilogue warps' TMEM lane quadrants): 2, 6, 10, ...
+#ifndef GNNCG_TC_SPLIT_WARPS
+#define GNNCG_TC_SPLIT_WARPS 10
+#endif
+constexpr int P_SPLIT_WARPS = GNNCG_TC_SPLIT_WARPS;
 constexpr int P_EPI_WARP0 = 2 + P_SPLIT_WARPS;  // 8: warp % 4 == TMEM lane quadrant
 constexpr int P_THREADS = 32 * (P_EPI_WARP0 + 4);
 
