@@ -3,7 +3,7 @@
 # the bf16 mode and the tcgen05 GEMM.  usage: scripts/gpu_sanitize.sh tag
 cd "$GRAFT_REPO_ROOT"; TAG=${1:-san}; mkdir -p gpurun_out
 SEL='tests/test_gpu_gat.py::test_region_forward_and_backward tests/test_gpu_gat.py::test_edgeless_graph tests/test_gpu_gat_bf16.py::test_bf16_region tests/test_gpu_edgeconv_gmm.py tests/test_gpu_gcn.py tests/test_gpu_graph.py'
-K='G3 or ER16 or cora or edgeless or empty or small or golden'
+K='G3 or ER16 or cora or star or edgeless or empty or small or golden'
 for tool in memcheck racecheck synccheck; do
   timeout 1500 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
     python -m pytest $SEL -q -x -p no:cacheprovider -k "$K" > gpurun_out/san_${tool}_$TAG.log 2>&1
