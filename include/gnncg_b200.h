@@ -84,7 +84,8 @@ typedef struct gnncg_sched {
    * kernel GATHERS is read, i.e. the offsets of the other index (csc_src's for a csr_dst schedule:
    * K2 gathers source rows; csr_dst's for a csc_src schedule: K4f gathers destination rows), and
    * their row count.  With gnncg_l2_persist() on, the fp32 fused kernels mark the contiguous row
-   * range carrying the most gathers as L2-persisting (gnncg_hot_window_host).  Caller-owned. */
+   * range carrying the most gathers as L2-persisting (gnncg_hot_window_host).  Caller-owned and
+ * not modified while in use: the window is computed once per (gather_off, gather_rows, size). */
   const uint64_t* gather_off;
   int64_t gather_rows;
 } gnncg_sched_t;

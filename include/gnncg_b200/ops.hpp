@@ -214,7 +214,16 @@ struct GatGrads {
   Tensor<float> dH, dW, da_l, da_r;
 };
 
+// Opt in to L2-persisting windows over the hottest gathered rows of the fused GAT kernels
+// (gnncg_l2_persist; DeviceGraph's schedules carry the hint).  Returns the set-aside granted.
+inline size_t l2_persist(size_t bytes) {
+  size_t got = 0;
+  check(gnncg_l2_persist(bytes, &got), "gnncg_l2_persist");
+  return got;
+}
+
 namespace detail {
+
 inline void require_shape(const Tensor<float>& t, std::uint64_t r, std::uint64_t c, const char* name) {
   if (t.rows != r || t.cols != c)
     throw TensorError(std::string(name) + ": shape mismatch (" + std::to_string(t.rows) + "x" +

@@ -161,6 +161,22 @@ int main() {
                 bound);
     ok = ok && e < bound;
   }
+  // The L2-persisting window (b200::l2_persist) is a cache policy: the 8 x 32 forward (the lean
+  // kernel the window applies to) is bitwise the same with it on.
+  {
+    const b200::GatParams q{8, 32};
+    const TensorF W8 = init_seeded<float>(Fin, 256, 7);
+    const TensorF al8 = init_seeded<float>(8, 32, 8), ar8 = init_seeded<float>(8, 32, 9);
+    b200::GatStash s0, s1;
+    const TensorF o0 = b200::gat_forward(dg, H, W8, al8, ar8, q, &s0);
+    const size_t got = b200::l2_persist(4u << 20);
+    const TensorF o1 = b200::gat_forward(dg, H, W8, al8, ar8, q, &s1);
+    b200::l2_persist(0);
+    bool same = got > 0 && o0.size() == o1.size();
+    for (std::uint64_t i = 0; same && i < o0.size(); ++i) same = o0.data[i] == o1.data[i];
+    std::printf("gat 8x32 forward with the L2 window (%zu MB): bitwise %s\n", got >> 20, same ? "equal" : "DIFFERENT");
+    ok = ok && same;
+  }
   // EdgeConv argmax returns edge ids of the same Graph
   std::vector<std::uint32_t> amax;
   const TensorF Th = init_seeded<float>(Fin, 16, 5), Ph = init_seeded<float>(Fin, 16, 6);
