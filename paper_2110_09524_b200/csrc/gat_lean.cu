@@ -32,8 +32,9 @@
 // head), and the per-edge head dots reduce over 4 lanes instead of 8 (6 shuffles and 12
 // selects per 8-row group instead of 14 and 28).  Measured (same box, 3 rounds): K4f 9.9-10.0
 // vs 10.6-10.7 ms, step 37.5-37.6 vs 38.8-39.3 ms; K2 unchanged (7.50-7.57 vs 7.57-7.65).
-// The paired layout stays buildable for A/B (-DGNNCG_LEAN_PAIRED).
+// The paired layout remains the path for tables that are only 16-byte aligned.
 #include <algorithm>
+#include <cstdint>
 #include <cfloat>
 
 #include "common.cuh"
@@ -517,7 +518,13 @@ struct FwdShape {
   static constexpr int WPC = VW == 8 ? GNNCG_LEAN_FWD8_WPC : GNNCG_LEAN_FWD_WPC;
   static constexpr int MINB = VW == 8 ? GNNCG_LEAN_FWD8_MINB : GNNCG_LEAN_FWD_MINB;
 };
-constexpr int kBwdWpc = GNNCG_LEAN_BWD_WPC, kBwdMinb = GNNCG_LEAN_BWD_MINB;
+// K4f's shape: the one-head-per-lane layouts (NV = 1) at 4 x 7; the paired fallback (NV = 2,
+// 16-byte aligned tables) keeps the 96-register 4 x 5 it was tuned at
+template <int NV>
+struct BwdShape {
+  static constexpr int WPC = NV == 1 ? GNNCG_LEAN_BWD_WPC : 4;
+  static constexpr int MINB = NV == 1 ? GNNCG_LEAN_BWD_MINB : 5;
+};
 
 int lean_num_sms() {
   static int v = 0;
@@ -570,9 +577,10 @@ void launch_fwd(const GatParams& p, cudaStream_t s) {
 
 template <int VW, int NV, int PER>
 void launch(const GatParams& p, cudaStream_t s) {
-  const unsigned grid = lean_grid(p.num_items, kBwdWpc, kBwdMinb);
-  if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, true>, grid, kBwdWpc * kWarp, s, p);
-  else launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, kBwdWpc, kBwdMinb, false>, grid, kBwdWpc * kWarp, s, p);
+  constexpr int W = BwdShape<NV>::WPC, M = BwdShape<NV>::MINB;
+  const unsigned grid = lean_grid(p.num_items, W, M);
+  if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, W, M, true>, grid, W * kWarp, s, p);
+  else launch_win(gat_bwd_src_lean_kernel<8, VW, NV, PER, W, M, false>, grid, W * kWarp, s, p);
 }
 
 }  // namespace
@@ -594,25 +602,29 @@ bool lean_enabled() {
   return v == 1;
 }
 
+// The 256-bit lane rows need 32-byte aligned tables (rows are 1 KB): a caller's table that is
+// only 16-byte aligned (a column view, an offset pointer) takes the paired 2 x 128-bit layout.
+bool aligned32(const void* q) { return (reinterpret_cast<uintptr_t>(q) & 31u) == 0; }
+
 bool launch_fwd_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-#ifdef GNNCG_LEAN_PAIRED
-  if (p.f == 32) launch_fwd<4, 2, 8>(p, s);
-#else
-  if (p.f == 32) launch_fwd<8, 1, 4>(p, s);
-#endif
-  else launch_fwd<4, 1, 4>(p, s);
+  if (p.f == 32) {
+    if (aligned32(p.Ht)) launch_fwd<8, 1, 4>(p, s);
+    else launch_fwd<4, 2, 8>(p, s);
+  } else {
+    launch_fwd<4, 1, 4>(p, s);
+  }
   return true;
 }
 
 bool launch_bwd_src_lean(const GatParams& p, unsigned, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f)) return false;
-#ifdef GNNCG_LEAN_PAIRED
-  if (p.f == 32) launch<4, 2, 8>(p, s);
-#else
-  if (p.f == 32) launch<8, 1, 4>(p, s);
-#endif
-  else launch<4, 1, 4>(p, s);
+  if (p.f == 32) {
+    if (aligned32(p.dOut)) launch<8, 1, 4>(p, s);
+    else launch<4, 2, 8>(p, s);
+  } else {
+    launch<4, 1, 4>(p, s);
+  }
   return true;
 }
 
