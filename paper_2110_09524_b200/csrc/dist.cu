@@ -155,6 +155,26 @@ __global__ void __launch_bounds__(256) gat_dist_combine_kernel(int64_t rows, int
                                                                float* __restrict__ dAl) {
   const int hf = h * f;
   const int64_t n1 = rows * hf, n2 = rows * h;
+  if ((f & 3) == 0 && (hf >> 2) <= (int)blockDim.x) {
+    // threads = (row slot, column quad), 16-byte accesses, no per-element 64-bit divide
+    const int q4 = hf >> 2, rpb = blockDim.x / q4;
+    const int slot = threadIdx.x / q4, c4 = threadIdx.x - slot * q4;
+    if (slot < rpb) {
+      const float4 ar = __ldg(reinterpret_cast<const float4*>(a_r) + c4);
+      const int k = (c4 * 4) / f;
+      for (int64_t r = (int64_t)blockIdx.x * rpb + slot; r < rows; r += (int64_t)gridDim.x * rpb) {
+        const float g = dAr[r * h + k];
+        const float4 x = reinterpret_cast<const float4*>(recvH + r * hf)[c4];
+        float4* o = reinterpret_cast<float4*>(dHt + r * hf) + c4;
+        float4 v = *o;
+        v.x += x.x + g * ar.x; v.y += x.y + g * ar.y; v.z += x.z + g * ar.z; v.w += x.w + g * ar.w;
+        *o = v;
+      }
+    }
+    for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n2; i += (int64_t)gridDim.x * blockDim.x)
+      dAl[i] += recvAl[i];
+    return;
+  }
   for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n1 + n2; i += (int64_t)gridDim.x * blockDim.x) {
     if (i < n1) {
       const int64_t r = i / hf;

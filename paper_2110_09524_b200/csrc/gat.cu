@@ -733,12 +733,13 @@ __global__ void gat_bwd_prep_kernel(int64_t rows, int h, int f, const float* __r
                                     const float* __restrict__ out, const float* __restrict__ Ar,
                                     const float* __restrict__ m, const float* __restrict__ d,
                                     float* __restrict__ rec) {
-  const int64_t n = rows * h;
+  const int rpb = blockDim.x / h;  // rows per block step (h <= blockDim.x): no per-element 64-bit divide
+  const int rr = threadIdx.x / h, k = threadIdx.x - rr * h;
+  if (rr >= rpb) return;
   const bool vec = (f % 4) == 0;
   const int rs = rec_stride(h);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / h;
-    const int k = (int)(i % h);
+  for (int64_t v = (int64_t)blockIdx.x * rpb + rr; v < rows; v += (int64_t)gridDim.x * rpb) {
+    const int64_t i = v * h + k;
     const float* g = dOut + i * f;
     const float* o = out + i * f;
     float s = 0.f;
@@ -763,11 +764,12 @@ __global__ void gat_bwd_prep_bf16_kernel(int64_t rows, int h, int f, const float
                                          const float* __restrict__ out, const float* __restrict__ Ar,
                                          const float* __restrict__ m, const float* __restrict__ d,
                                          float* __restrict__ rec, uint16_t* __restrict__ dOut_lp) {
-  const int64_t n = rows * h;
+  const int rpb = blockDim.x / h;  // rows per block step (h <= blockDim.x): no per-element 64-bit divide
+  const int rr = threadIdx.x / h, k = threadIdx.x - rr * h;
+  if (rr >= rpb) return;
   const int rs = rec_stride(h);
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / h;
-    const int k = (int)(i % h);
+  for (int64_t v = (int64_t)blockIdx.x * rpb + rr; v < rows; v += (int64_t)gridDim.x * rpb) {
+    const int64_t i = v * h + k;
     const float* g = dOut + i * f;
     const float* o = out + i * f;
     uint2* gl = reinterpret_cast<uint2*>(dOut_lp + i * f);
@@ -900,17 +902,22 @@ __global__ void gat_bwd_src_merge_kernel(GatParams p, const uint32_t* __restrict
 // ---------------------------------------------------------------------------
 // Reorganized LPs and their parameter gradients.
 // ---------------------------------------------------------------------------
+// A_l[v, k] = <Ht[v, k f : (k+1) f], a_l[k]> (A_r likewise), one thread per (row, head), columns
+// summed in order (bitwise the same as K1's LP epilogue).  A block covers 256 / h rows at a time
+// and strides over rows, so the (row, head) split is one division per thread, not a 64-bit
+// divide and modulo per element (which made the kernel ~3x slower than its bytes at C5).
 __global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __restrict__ Ht,
                                  const float* __restrict__ a_l, const float* __restrict__ a_r, float* __restrict__ Al,
                                  float* __restrict__ Ar) {
-  const int64_t n = rows * h;
   const bool vec = (f % 4) == 0;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < n; i += (int64_t)gridDim.x * blockDim.x) {
-    const int64_t v = i / h;
-    const int k = (int)(i % h);
-    const float* x = Ht + v * h * f + (int64_t)k * f;
-    const float* pl = a_l + k * f;
-    const float* pr = a_r + k * f;
+  const int rpb = blockDim.x / h;  // rows per block step (h <= blockDim.x)
+  const int rr = threadIdx.x / h, k = threadIdx.x - rr * h;
+  if (rr >= rpb) return;
+  const float* pl = a_l + k * f;
+  const float* pr = a_r + k * f;
+  const int64_t hf = (int64_t)h * f;
+  for (int64_t v = (int64_t)blockIdx.x * rpb + rr; v < rows; v += (int64_t)gridDim.x * rpb) {
+    const float* x = Ht + v * hf + (int64_t)k * f;
     float sl = 0.f, sr = 0.f;
     if (vec) {
       for (int j = 0; j < f; j += 4) {
@@ -927,8 +934,8 @@ __global__ void attn_dots_kernel(int64_t rows, int h, int f, const float* __rest
         sr = fmaf(xv, __ldg(pr + j), sr);
       }
     }
-    Al[i] = sl;
-    Ar[i] = sr;
+    Al[v * h + k] = sl;
+    Ar[v * h + k] = sr;
   }
 }
 
@@ -1295,8 +1302,9 @@ int gnncg_gat_attn_dots(int64_t rows, int h, int f, const float* Ht, const float
   GNNCG_REQUIRE(rows >= 0 && h >= 1 && f >= 1, GNNCG_ERR_SHAPE, "attn_dots: bad shape");
   if (rows == 0) return GNNCG_OK;
   GNNCG_REQUIRE(Ht && a_l && a_r && Al && Ar, GNNCG_ERR_ARG, "attn_dots: null pointer");
-  const int64_t n = rows * h;
-  const int g = (int)std::min<int64_t>(ceil_div(n, 256), 148 * 32);
+  GNNCG_REQUIRE(h <= 256, GNNCG_ERR_UNSUPPORTED, "attn_dots: heads=%d > 256", h);
+  const int rpb = 256 / h;
+  const int g = (int)std::min<int64_t>(ceil_div(rows, (int64_t)rpb), 148 * 32);
   cost_add(kCostLp, (uint64_t)rows, 1, as_stream(stream));
   attn_dots_kernel<<<g, 256, 0, as_stream(stream)>>>(rows, h, f, Ht, a_l, a_r, Al, Ar);
   GNNCG_LAUNCH_CHECK();
