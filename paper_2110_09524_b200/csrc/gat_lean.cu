@@ -11,7 +11,7 @@
 // (+ LP terms), dA_l[u] = sum dz, dA_r[v] += dz (global reduction)
 // (PAPER.md:615-662 ).
 //
-// Why a second kernel: ncu on B200 (profiles/r02_k4_lsu.md) shows the previous one
+// Why a second kernel: ncu on B200 (profiles/r01_v12_ncu_full.json) shows the previous one
 // bound by the L1 data pipe (l1tex__data_pipe_lsu_wavefronts 82% of peak), not by
 // DRAM (54%) or L2 (52%).  22 wavefronts per edge: 15.4 global (8 of them the gathered
 // 1 KB row, 6 the per-lane 96-byte destination records: 32 scattered 16-byte loads per
