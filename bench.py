@@ -68,6 +68,9 @@ def parse():
                     help="replay the step as a CUDA graph (auto: on for the small, launch-bound configs)")
     ap.add_argument("--config", default="reddit", choices=["reddit", "cora", "edgeconv20", "edgeconv40", "monet", "c5", "gcn"],
                     help="reddit = the headline (BASELINE configs[1]); the others are configs[0,2,3,4]")
+    ap.add_argument("--relabel", choices=["none", "random", "degree"], default="none",
+                    help="GAT graphs: keep the generator's ids (degree-descending), shuffle them (an arbitrary "
+                         "input labelling), or shuffle then relabel by degree (DeviceGraph.degree_order)")
     ap.add_argument("--l2-persist-mb", type=int, default=48,
                     help="L2 set-aside for the fused GAT kernels' hottest gathered rows (gnncg_l2_persist; 0 = off)")
     ap.add_argument("--no-ncu", action="store_true", help="skip the one-launch ncu DRAM-byte capture")
@@ -194,6 +197,12 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
             V_loc, E_loc = lg.num_local, lg.num_edges
         else:
             g = DeviceGraph.chung_lu(V, E, offset=offset, seed=0, device=dev)
+            if args.relabel != "none":
+                shuffle = torch.randperm(V, generator=torch.Generator().manual_seed(7)).to(dev)
+                g = g.relabel(shuffle)
+                if args.relabel == "degree":
+                    g = g.relabel(g.degree_order())
+                torch.cuda.empty_cache()
             model = GAT(g, dims, seed=1, chunk=args.chunk, gather=args.gather)
             V_loc, E_loc = V, E
         h, f = dims[0][1], dims[0][2]
@@ -206,7 +215,8 @@ def build_workload(args, dev, world: int, rank: int) -> dict:
                   config={"workload": desc, "V": V, "E": E, "layers": len(dims),
                           "gather": args.gather,
                           "dims": ", ".join(f"{a}->{b}x{c}" for a, b, c in dims),
-                          "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0",
+                          "graph": f"Chung-Lu w_i=2^40/(i+{offset}), seed 0"
+                                   + ("" if args.relabel == "none" else f", ids {args.relabel}-relabeled"),
                           "l2": "inputs larger than L2 (features and index exceed 126 MB)"})
     elif cfg == "cora":
         V, E, dims = 2708, 10556, [(1433, 8, 8)]
@@ -468,7 +478,7 @@ def ncu_dram_bytes(args, kernel: str, per_step: int = 1):
                "--no-parity", "--ncu-probe"]
         if args.chunk:
             cmd += ["--chunk", str(args.chunk)]
-        cmd += ["--l2-persist-mb", str(args.l2_persist_mb)]
+        cmd += ["--l2-persist-mb", str(args.l2_persist_mb), "--relabel", args.relabel]
         try:
             subprocess.run(cmd, stdout=subprocess.DEVNULL, stderr=subprocess.DEVNULL, timeout=900, check=False,
                            env={k: v for k, v in os.environ.items() if k not in ("RANK", "WORLD_SIZE", "LOCAL_RANK")})

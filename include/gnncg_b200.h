@@ -112,7 +112,9 @@ int gnncg_cost_counters(uint64_t* counters);
  * persisting lines); *granted_host (may be NULL) receives the size set.  While on, the fp32
  * fused GAT kernels (K2, K4f) launch with an access-policy window over the hottest rows of the
  * table they gather (schedules carrying gather_off): those rows stay in L2, the rest streams.
- * Results do not change (cache policy only). */
+ * The window is used only when its rows carry at least twice their share of the reads (row ids
+ * clustered by degree, e.g. after DeviceGraph.relabel(degree_order())); otherwise the launch is
+ * plain.  Results do not change (cache policy only). */
 int gnncg_l2_persist(size_t bytes, size_t* granted_host);
 /* The window: the start row b maximising off[b+n] - off[b] (the gathers of rows [b, b+n)) over
  * 0 <= b <= num_rows - n, lowest b on ties; n is clamped to num_rows. */

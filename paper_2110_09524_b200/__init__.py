@@ -7,7 +7,8 @@ there is no CPU fallback.
 """
 from ._lib import (ArgumentError, CudaError, DeviceError, GnncgError, GraphError, TensorError,  # noqa: F401
                    UnsupportedError, WorkspaceError, hot_window, l2_persist)
-from .graph import DeviceGraph, DeviceIndex, DeviceSched, chung_lu_cdf, knn_edges, partition_rows, uniform_edges  # noqa: F401
+from .graph import (DeviceGraph, DeviceIndex, DeviceSched, chung_lu_cdf, knn_edges, partition_rows,  # noqa: F401
+                    permute_rows, uniform_edges, unpermute_rows)
 from .ops import (GatGrads, GatParams, GatStash, edgeconv_backward, edgeconv_forward, gat_backward,  # noqa: F401
                   gat_forward, gat_region_backward, gat_region_forward, gcn_backward, gcn_forward, gcn_norm, gemm,
                   gmm_backward, gmm_forward, matmul, matmul_nt, matmul_tn, spmm)

@@ -47,6 +47,12 @@ L2Window l2_window(const gnncg_sched_t* sched, const void* table, size_t row_byt
   const int64_t n = std::min<int64_t>((int64_t)(pb / row_bytes), sched->gather_rows);
   if (n <= 0) return {};
   const int64_t b = hot_window_begin(sched->gather_off, sched->gather_rows, n);
+  // only where the window concentrates the reads: at least twice its share of the rows.  A
+  // shuffled labelling has no such range, and persisting an arbitrary slice of it was measured
+  // slower than no window (C2: 39.6 vs 37.4 ms; degree-ordered ids: 35.0 ms with the window).
+  const uint64_t* off = sched->gather_off;
+  const double reads = (double)(off[b + n] - off[b]), total = (double)off[sched->gather_rows];
+  if (total <= 0.0 || reads < 2.0 * total * (double)n / (double)sched->gather_rows) return {};
   return {static_cast<const char*>(table) + (size_t)b * row_bytes, (size_t)n * row_bytes};
 }
 

@@ -226,6 +226,30 @@ class DeviceGraph:
         call("gnncg_gen_chung_lu", V, E, _ptr(tcdf), seed, _ptr(src), _ptr(dst), _stream())
         return cls.from_device_edges(V, src, dst)
 
+    # -- relabeling ---------------------------------------------------------
+    def degree_order(self) -> torch.Tensor:
+        """perm (int64, device): perm[new] = old id, vertices by descending in + out degree (ties:
+        lower old id first).  Relabeling with it puts the rows the fused kernels gather most often
+        at the low ids, where the L2-persisting window (gnncg_l2_persist) can cover them for any
+        input labelling.  Preprocessing on torch, outside any training step."""
+        deg = (self.csr_dst.off[1:] - self.csr_dst.off[:-1]) + (self.csc_src.off[1:] - self.csc_src.off[:-1])
+        return torch.sort(-deg, stable=True).indices
+
+    def relabel(self, perm: torch.Tensor) -> "DeviceGraph":
+        """The same graph with vertex old = perm[new] renamed new (edge ids unchanged: edge i is
+        still edge i, so per-row edge order, EdgeConv argmax ids and results are unchanged up to
+        the renaming).  Inputs follow with permute_rows(X, perm); outputs map back with
+        unpermute_rows(Y, perm)."""
+        V = self.num_vertices
+        perm = perm.to(device=self.device, dtype=torch.int64)
+        if perm.numel() != V:
+            raise _lib.TensorError("relabel: perm must have num_vertices entries")
+        inv = torch.empty_like(perm)
+        inv[perm] = torch.arange(V, device=self.device)
+        src = inv[self.edge_src.to(torch.int64) & 0xFFFFFFFF].to(torch.int32)
+        dst = inv[self.edge_dst.to(torch.int64) & 0xFFFFFFFF].to(torch.int32)
+        return DeviceGraph.from_device_edges(V, src, dst)
+
     # -- queries -----------------------------------------------------------
     def index(self, which: str) -> DeviceIndex:
         return self.csr_dst if which == "dst" else self.csc_src
@@ -243,6 +267,18 @@ class DeviceGraph:
         return dict(V=self.num_vertices, src=self.edge_src.cpu().numpy().view(np.uint32),
                     dst=self.edge_dst.cpu().numpy().view(np.uint32), dst_off=d[0], dst_src=d[1], dst_eid=d[2],
                     src_off=s[0], src_dst=s[1], src_eid=s[2])
+
+
+def permute_rows(X: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    """Rows of X in the relabeled order: out[new] = X[perm[new]] (DeviceGraph.relabel)."""
+    return X.index_select(0, perm.to(device=X.device, dtype=torch.int64))
+
+
+def unpermute_rows(Y: torch.Tensor, perm: torch.Tensor) -> torch.Tensor:
+    """Rows of a relabeled result back in the original order: out[perm[new]] = Y[new]."""
+    out = torch.empty_like(Y)
+    out.index_copy_(0, perm.to(device=Y.device, dtype=torch.int64), Y)
+    return out
 
 
 # ---------------------------------------------------------------------------

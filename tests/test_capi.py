@@ -165,3 +165,12 @@ def test_hot_window_host(seed):
 def test_l2_persist_needs_device():
     with pytest.raises(_lib.DeviceError):
         _lib.l2_persist(32 << 20)
+
+
+def test_permute_rows_roundtrip():
+    from paper_2110_09524_b200.graph import permute_rows, unpermute_rows
+
+    X = torch.arange(20.0).reshape(10, 2)
+    perm = torch.tensor([3, 0, 9, 1, 2, 8, 7, 4, 6, 5])
+    Y = permute_rows(X, perm)
+    assert torch.equal(Y[0], X[3]) and torch.equal(unpermute_rows(Y, perm), X)

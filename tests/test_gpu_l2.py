@@ -43,3 +43,39 @@ def test_l2_window_is_cache_policy_only(cuda, h, f):
     for x, y in zip(a[3:], b[3:]):  # K4f: dA_r sums arrive in any order
         s = max(1.0, float(np.abs(x).max()))
         assert float(np.abs(x - y).max()) / s < 1e-6
+
+
+def test_degree_relabel_is_a_renaming(cuda):
+    """DeviceGraph.relabel(degree_order()) renames vertices only: the GAT region on the relabeled
+    graph with permuted inputs gives the permuted outputs (bitwise forward: edge ids and per-row
+    edge order are unchanged), and the hottest rows land at the low ids."""
+    from paper_2110_09524_b200 import permute_rows, unpermute_rows
+
+    g0 = DeviceGraph.chung_lu(20_000, 1_000_000, offset=100, seed=4, device="cuda")
+    shuffle = torch.randperm(20_000, generator=torch.Generator().manual_seed(1)).to("cuda")
+    g = g0.relabel(shuffle)  # an arbitrary labelling
+    perm = g.degree_order()
+    gr = g.relabel(perm)
+    deg = lambda x: (x.csr_dst.off[1:] - x.csr_dst.off[:-1]) + (x.csc_src.off[1:] - x.csc_src.off[:-1])  # noqa: E731
+    d = deg(gr)
+    assert bool((d[:-1] >= d[1:]).all())  # descending
+    assert torch.equal(torch.sort(deg(g)).values, torch.sort(d).values)
+    h, f = 8, 32
+    gen = torch.Generator(device="cuda").manual_seed(3)
+    u = lambda *s: torch.rand(*s, device="cuda", generator=gen) * 2 - 1  # noqa: E731
+    Ht, Al, Ar, dOut = u(20_000, h * f), u(20_000, h), u(20_000, h), u(20_000, h * f)
+    al, ar = u(h, f), u(h, f)
+    p = GatParams(h, f)
+    out, m, dd = gat_region_forward(g, Ht, Al, Ar, p)
+    P = lambda x: permute_rows(x, perm)  # noqa: E731
+    out2, m2, d2 = gat_region_forward(gr, P(Ht), P(Al), P(Ar), p)
+    for x, y in ((out, out2), (m, m2), (dd, d2)):
+        assert torch.equal(x, unpermute_rows(y, perm))
+    st = GatStash(Ht, Al, Ar, m, dd, out)
+    st2 = GatStash(P(Ht), P(Al), P(Ar), m2, d2, out2)
+    a = gat_region_backward(g, st, al, ar, dOut, p, mode="fast")
+    b = gat_region_backward(gr, st2, al, ar, P(dOut), p, mode="fast")
+    for x, y in zip(a[:3], b[:3]):  # dHt, dA_l, dA_r
+        y = unpermute_rows(y, perm)
+        s = max(1.0, float(x.abs().max()))
+        assert float((x - y).abs().max()) / s < 1e-5
