@@ -323,7 +323,8 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr_dst, const gnncg_index_t* csc_src, in
  *   Y[r,:] = act(bias + sum_{i in row r} w[eid_i] X[nbr_i,:])
  * edge_w is indexed by edge id (NULL = all ones; non-NULL needs idx->eid); bias may be
  * NULL; relu != 0 applies max(0,.).  Rows of idx are local (Y has idx->num_rows rows),
- * neighbours global.  Deterministic (fixed-order split-row merge). */
+ * neighbours global.  Deterministic (fixed-order split-row merge).  The workspace holds the
+ * split-row partials and a work counter: one workspace per concurrently running call. */
 size_t gnncg_spmm_workspace(const gnncg_sched_t* sched, int cols);
 int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, const float* edge_w, const float* X,
                const float* bias, int relu, float* Y, void* workspace, size_t workspace_bytes, void* stream);

@@ -13,6 +13,8 @@
 #include "common.cuh"
 #include "gat_common.cuh"
 
+#include <algorithm>
+#include <cstdint>
 #include <cstdlib>
 
 namespace gnncg_b200 {
@@ -123,6 +125,103 @@ __global__ void __launch_bounds__(THREADS, OCC) spmm_kernel(SpmmParams p) {
   }
 }
 
+// Lean weighted aggregate for 256-column rows (the GCN hidden width; K2's layout without the
+// softmax): each lane owns 8 consecutive columns and gathers them with one 256-bit load; the
+// block's ids and weights sit in shared memory (one broadcast LDS.128 per 4 rows instead of two
+// shuffles per row); 8 rows in flight per warp; ids read evict-first; the next block's weight
+// (a dependent load through eid) goes out after the first row group's gathers.
+struct SpmmLeanSmem {
+  uint32_t nb[32];
+  float w[32];
+};
+
+template <int WPC, int MINB>
+__global__ void __launch_bounds__(WPC * 32, MINB) spmm_lean_kernel(SpmmParams p, unsigned* __restrict__ ctr) {
+  constexpr int U = 8, F = 256;
+  __shared__ __align__(16) SpmmLeanSmem smem[WPC];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
+  SpmmLeanSmem& sm = smem[w];
+  // persistent warps pull items from a counter (largest first): no warp of a CTA idles while
+  // its neighbours finish longer rows
+  unsigned nxt = lane == 0 ? atomicAdd(ctr, 1u) : 0u;
+  for (;;) {
+  const int64_t wi = __shfl_sync(0xffffffffu, nxt, 0);
+  if (wi >= p.num_items) break;
+  if (lane == 0) nxt = atomicAdd(ctr, 1u);
+  const Item it = decode_item(p.items, p.off, wi, p.num_split_items, p.chunk);
+  const float* xl = p.X + lane * 8;
+  float acc[8];
+#pragma unroll
+  for (int q = 0; q < 8; ++q) acc[q] = 0.f;
+  uint32_t nb = 0;
+  float a = 0.f;
+  if (it.e0 + lane < it.e1) {
+    nb = __ldcs(p.nbr + it.e0 + lane);
+    a = p.w ? __ldg(p.w + __ldcs(p.eid + it.e0 + lane)) : 1.f;
+  }
+  for (uint64_t base = it.e0; base < it.e1; base += 32) {
+    const int n = (int)min((uint64_t)32, it.e1 - base);
+    const uint32_t nb_last = __shfl_sync(0xffffffffu, nb, n - 1);
+    sm.nb[lane] = lane < n ? nb : nb_last;  // rows past n repeat the last one with weight 0
+    sm.w[lane] = lane < n ? a : 0.f;
+    __syncwarp();
+    const uint64_t nx = base + 32 + lane;
+    const bool has_next = nx < it.e1;
+    const uint32_t nb_n = has_next ? __ldcs(p.nbr + nx) : 0u;
+    const uint32_t eid_n = has_next && p.w ? __ldcs(p.eid + nx) : 0u;
+    float a_n = 0.f;
+    for (int j = 0;;) {
+      float x[U][8];
+#pragma unroll
+      for (int t = 0; t < U; t += 4) {
+        const uint4 id4 = *reinterpret_cast<const uint4*>(sm.nb + j + t);
+        const uint32_t ids[4] = {id4.x, id4.y, id4.z, id4.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k) {
+          const float* src = xl + (uint64_t)ids[k] * F;
+          asm("ld.global.nc.v8.f32 {%0, %1, %2, %3, %4, %5, %6, %7}, [%8];"
+              : "=f"(x[t + k][0]), "=f"(x[t + k][1]), "=f"(x[t + k][2]), "=f"(x[t + k][3]), "=f"(x[t + k][4]),
+                "=f"(x[t + k][5]), "=f"(x[t + k][6]), "=f"(x[t + k][7])
+              : "l"(src));
+        }
+      }
+      if (j == 0) a_n = has_next ? (p.w ? __ldg(p.w + eid_n) : 1.f) : 0.f;
+#pragma unroll
+      for (int t = 0; t < U; t += 4) {
+        const float4 wv = *reinterpret_cast<const float4*>(sm.w + j + t);
+        const float wa[4] = {wv.x, wv.y, wv.z, wv.w};
+#pragma unroll
+        for (int k = 0; k < 4; ++k)
+#pragma unroll
+          for (int q = 0; q < 8; ++q) acc[q] = fmaf(wa[k], x[t + k][q], acc[q]);
+      }
+      j += U;
+      if (j >= n) break;
+    }
+    __syncwarp();
+    nb = nb_n;
+    a = a_n;
+  }
+  const int c = lane * 8;
+  if (!it.split) {
+    float o[8];
+#pragma unroll
+    for (int q = 0; q < 8; ++q) {
+      const float z = acc[q] + (p.bias ? __ldg(p.bias + c + q) : 0.f);
+      o[q] = p.relu ? fmaxf(z, 0.f) : z;
+    }
+    float4* y = reinterpret_cast<float4*>(p.Y + (int64_t)it.row * F + c);
+    __stcs(y, make_float4(o[0], o[1], o[2], o[3]));
+    __stcs(y + 1, make_float4(o[4], o[5], o[6], o[7]));
+  } else {
+    float4* q4 = reinterpret_cast<float4*>(p.part + wi * (int64_t)F + c);
+    q4[0] = make_float4(acc[0], acc[1], acc[2], acc[3]);
+    q4[1] = make_float4(acc[4], acc[5], acc[6], acc[7]);
+  }
+  __syncwarp();
+  }  // items
+}
+
 __global__ void spmm_merge_kernel(SpmmParams p, const uint32_t* __restrict__ split_rows,
                                   const uint32_t* __restrict__ split_first, int64_t num_split_rows) {
   const int64_t sr = blockIdx.x;
@@ -197,6 +296,16 @@ SpmmShape spmm_shape() {
   return s;
 }
 
+// GNNCG_SPMM_LEAN=0: the general kernel for 256-column rows too (A/B)
+bool spmm_lean_enabled() {
+  static int v = -1;
+  if (v < 0) {
+    const char* e = getenv("GNNCG_SPMM_LEAN");
+    v = (e && e[0] == '0') ? 0 : 1;
+  }
+  return v == 1;
+}
+
 template <int VW, int OCC>
 int launch_spmm_occ(SpmmParams p, dim3 grid, int max_nv, cudaStream_t s) {
   // split the columns into the fewest slices of <= max_nv vectors per lane, evenly
@@ -227,7 +336,8 @@ using namespace gnncg_b200;
 extern "C" {
 
 size_t gnncg_spmm_workspace(const gnncg_sched_t* sched, int cols) {
-  return sched ? align_up((size_t)sched->num_split_items * cols * sizeof(float)) : 0;
+  // split-row partials, + the lean kernel's work counter
+  return sched ? align_up((size_t)sched->num_split_items * cols * sizeof(float)) + 256 : 0;
 }
 
 int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, const float* edge_w, const float* X,
@@ -246,10 +356,50 @@ int gnncg_spmm(const gnncg_index_t* idx, const gnncg_sched_t* sched, int cols, c
   SpmmParams p{idx->off, idx->nbr, idx->eid, sched->items, sched->num_items, sched->num_split_items, sched->chunk,
                cols, 0, edge_w, X, bias, Y, static_cast<float*>(ws), relu};
   cudaStream_t s = as_stream(stream);
-  dim3 grid((unsigned)ceil_div(sched->num_items, WARPS));
-  int rc = cols % 4 == 0 ? launch_spmm<4>(p, grid, s) : (cols % 2 == 0 ? launch_spmm<2>(p, grid, s)
-                                                                         : launch_spmm<1>(p, grid, s));
-  if (rc) return rc;
+  if (cols == 256 && spmm_lean_enabled() && ((reinterpret_cast<uintptr_t>(X) | reinterpret_cast<uintptr_t>(Y)) & 31) == 0) {
+    // 256-column rows (32-byte aligned): the lean kernel, 8 warps x 4 CTAs per SM (64 registers)
+#ifndef GNNCG_SPMM_LEAN_WPC
+#define GNNCG_SPMM_LEAN_WPC 8
+#endif
+#ifndef GNNCG_SPMM_LEAN_MINB
+#define GNNCG_SPMM_LEAN_MINB 4
+#endif
+    constexpr int W = GNNCG_SPMM_LEAN_WPC, M = GNNCG_SPMM_LEAN_MINB;
+    p.tile = 256;
+    unsigned* ctr = reinterpret_cast<unsigned*>(static_cast<char*>(ws) + align_up((size_t)sched->num_split_items * cols * sizeof(float)));
+    GNNCG_CUDA_TRY(cudaMemsetAsync(ctr, 0, sizeof(unsigned), s));
+    const L2Window win = l2_window(sched, X, 256 * sizeof(float));
+    int sms = 148;
+    {
+      int dev = 0;
+      cudaGetDevice(&dev);
+      cudaDeviceGetAttribute(&sms, cudaDevAttrMultiProcessorCount, dev);
+    }
+    const dim3 g((unsigned)std::max<int64_t>(1, std::min<int64_t>(ceil_div(sched->num_items, W), (int64_t)sms * M)));
+    if (win.bytes == 0) {
+      spmm_lean_kernel<W, M><<<g, W * 32, 0, s>>>(p, ctr);
+    } else {
+      cudaLaunchConfig_t cfg = {};
+      cfg.gridDim = g;
+      cfg.blockDim = dim3(W * 32);
+      cfg.stream = s;
+      cudaLaunchAttribute at[1];
+      at[0].id = cudaLaunchAttributeAccessPolicyWindow;
+      at[0].val.accessPolicyWindow.base_ptr = const_cast<void*>(win.base);
+      at[0].val.accessPolicyWindow.num_bytes = win.bytes;
+      at[0].val.accessPolicyWindow.hitRatio = 1.0f;
+      at[0].val.accessPolicyWindow.hitProp = cudaAccessPropertyPersisting;
+      at[0].val.accessPolicyWindow.missProp = cudaAccessPropertyStreaming;
+      cfg.attrs = at;
+      cfg.numAttrs = 1;
+      cudaLaunchKernelEx(&cfg, spmm_lean_kernel<W, M>, p, ctr);
+    }
+  } else {
+    dim3 grid((unsigned)ceil_div(sched->num_items, WARPS));
+    int rc = cols % 4 == 0 ? launch_spmm<4>(p, grid, s) : (cols % 2 == 0 ? launch_spmm<2>(p, grid, s)
+                                                                           : launch_spmm<1>(p, grid, s));
+    if (rc) return rc;
+  }
   GNNCG_LAUNCH_CHECK();
   if (sched->num_split_rows > 0) {
     spmm_merge_kernel<<<(unsigned)sched->num_split_rows, 256, 0, s>>>(p, sched->split_rows, sched->split_first,
