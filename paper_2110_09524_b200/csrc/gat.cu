@@ -1149,6 +1149,9 @@ void launch_lp_fast_per(const GatParams& p, unsigned g, cudaStream_t s) {
 template <int VW, int NV>
 void launch_lp(Kind kind, const GatParams& p, cudaStream_t s) {
   const unsigned g = (unsigned)std::min<int64_t>(ceil_div(p.num_items, WARPS), (int64_t)num_sms() * 2);
+  // gat_lean.cu: the 8 x 32 / 8 x 16 shapes
+  if (kind == Kind::FwdOvl && launch_fwd_lean_lp(p, s)) return;
+  if (kind == Kind::BwdSrcFast && launch_bwd_src_lean_lp(p, s)) return;
   if (kind == Kind::FwdOvl) {
     if (p.ctr) gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true, true><<<g, THREADS, 0, s>>>(p);
     else gat_fwd_ovl_kernel<VW, NV, LpDepth<VW, NV>::U, WARPS, 2, true><<<g, THREADS, 0, s>>>(p);

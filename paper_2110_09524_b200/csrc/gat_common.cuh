@@ -249,5 +249,7 @@ namespace gat {
 bool lean_supported(int h, int f);
 bool launch_bwd_src_lean(const GatParams& p, unsigned grid, cudaStream_t s);
 bool launch_fwd_lean(const GatParams& p, unsigned grid, cudaStream_t s);
+bool launch_fwd_lean_lp(const GatParams& p, cudaStream_t s);
+bool launch_bwd_src_lean_lp(const GatParams& p, cudaStream_t s);
 }  // namespace gat
 }  // namespace gnncg_b200

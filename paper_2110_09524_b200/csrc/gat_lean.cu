@@ -116,14 +116,38 @@ __device__ __forceinline__ Vec<VW> ldg_row(const float* p) {
   }
 }
 
-// gather_row (gat_common.cuh) with ldg_row: row r of a [*, hf] table at this lane's columns.
-template <int VW, int NV>
-__device__ __forceinline__ void lean_gather(const float* __restrict__ base, uint32_t r, int hf,
-                                            const Cols<VW, NV>& c, Vec<VW> (&x)[NV]) {
-  const uint64_t off = (uint64_t)r * (uint32_t)(hf * 4);
+// One lane vector of the bf16 gather table (the bf16 mode): VW bf16 = 8 or 16 bytes, kept packed.
+template <int VW>
+__device__ __forceinline__ Row<VW, true> ldg_row_lp(const char* p) {
+  Row<VW, true> r;
+  if constexpr (VW == 8) {
+    const uint4 t = __ldg(reinterpret_cast<const uint4*>(p));
+    r.w[0] = t.x; r.w[1] = t.y; r.w[2] = t.z; r.w[3] = t.w;
+  } else {
+    static_assert(VW == 4, "lean bf16 rows: 4 or 8 columns per lane");
+    const uint2 t = __ldg(reinterpret_cast<const uint2*>(p));
+    r.w[0] = t.x; r.w[1] = t.y;
+  }
+  return r;
+}
+
+// gather_row (gat_common.cuh) with ldg_row: row r of a [*, hf] table at this lane's columns,
+// fp32 (LP = false) or bf16 (LP = true, the bf16 mode's gather table).
+template <int VW, int NV, bool LP>
+__device__ __forceinline__ void lean_gather(const void* __restrict__ base, uint32_t r, int hf,
+                                            const Cols<VW, NV>& c, Row<VW, LP> (&x)[NV]) {
+  if constexpr (LP) {
+    const uint64_t off = (uint64_t)r * (uint32_t)(hf * 2);
 #pragma unroll
-  for (int i = 0; i < NV; ++i)
-    x[i] = ldg_row<VW>(reinterpret_cast<const float*>(reinterpret_cast<const char*>(base + c.col[i]) + off));
+    for (int i = 0; i < NV; ++i)
+      x[i] = ldg_row_lp<VW>(reinterpret_cast<const char*>(static_cast<const uint16_t*>(base) + c.col[i]) + off);
+  } else {
+    const uint64_t off = (uint64_t)r * (uint32_t)(hf * 4);
+#pragma unroll
+    for (int i = 0; i < NV; ++i)
+      x[i].v = ldg_row<VW>(
+          reinterpret_cast<const float*>(reinterpret_cast<const char*>(static_cast<const float*>(base) + c.col[i]) + off));
+  }
 }
 
 // K2's row gathers of a [*, 8 F] table at this lane's paired columns (Cols with pl = F / VW:
@@ -133,20 +157,27 @@ __device__ __forceinline__ void lean_gather(const float* __restrict__ base, uint
 // IMADs and a MOV per row (the uniform table base folded into every address and the column
 // re-added).  Measured at C2: K2 7.84 -> 7.62 ms; the same change made K4f slower (10.9 ->
 // 11.4 ms: its loads issue later in the schedule), so K4f keeps gather_row.
-template <int VW, int NV, int F>
+template <int VW, int NV, int F, bool LP = false>
 struct LaneRows {
+  static constexpr uint32_t EB = LP ? 2u : 4u;  // bytes per element of the table
   const char* lb;
-  __device__ __forceinline__ LaneRows(const float* base, int col0) {
-    asm("mov.b64 %0, %1;" : "=l"(lb) : "l"(base + col0));
+  __device__ __forceinline__ LaneRows(const void* base, int col0) {
+    const void* b;
+    if constexpr (LP) b = static_cast<const uint16_t*>(base) + col0;
+    else b = static_cast<const float*>(base) + col0;
+    asm("mov.b64 %0, %1;" : "=l"(lb) : "l"(b));
   }
-  __device__ __forceinline__ void gather(uint32_t r, Vec<VW> (&x)[NV]) const {
-    const char* a = lb + (uint64_t)r * (8u * F * 4u);
+  __device__ __forceinline__ void gather(uint32_t r, Row<VW, LP> (&x)[NV]) const {
+    const char* a = lb + (uint64_t)r * (8u * F * EB);
 #pragma unroll
-    for (int i = 0; i < NV; ++i) x[i] = ldg_row<VW>(reinterpret_cast<const float*>(a + i * F * 4));
+    for (int i = 0; i < NV; ++i) {
+      if constexpr (LP) x[i] = ldg_row_lp<VW>(a + i * F * EB);
+      else x[i].v = ldg_row<VW>(reinterpret_cast<const float*>(a + i * F * EB));
+    }
   }
 };
 
-template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
+template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN, bool LP = false>
 __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(GatParams p) {
   constexpr int U = 8;  // rows in flight per warp
   constexpr int R = 4 / NV;
@@ -187,8 +218,16 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
     count_item(p, it, lane);
     const int64_t u = it.row;
     const float alu = __ldg(p.Al + u * h + kk);
-    Vec<VW> x[NV], acc[NV];
-    gather_row<VW, NV>(p.Ht, (uint32_t)u, hf, cols, x);
+    Row<VW, LP> x[NV];  // the own row, as the forward aggregated it (bf16 mode: the bf16 Ht)
+    Vec<VW> acc[NV];
+    if constexpr (LP) {
+      lean_gather<VW, NV, true>(p.lp_x, (uint32_t)u, hf, cols, x);
+    } else {
+      Vec<VW> xv[NV];
+      gather_row<VW, NV>(p.Ht, (uint32_t)u, hf, cols, xv);
+#pragma unroll
+      for (int i = 0; i < NV; ++i) x[i].v = xv[i];
+    }
     zero(acc);
     float dal[NV];
 #pragma unroll
@@ -196,18 +235,18 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
 
     const uint64_t e0 = it.e0, e1 = it.e1;
     uint32_t v_cur = e0 + lane < e1 ? ld_stream(p.nbr + e0 + lane) : 0u;
-    const float* tab = p.dOut;
+    const void* tab = LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.dOut);
     for (uint64_t base = e0; base < e1; base += 32) {
       const int n = (int)min((uint64_t)32, e1 - base);
       sm.nb[lane] = v_cur;  // idle lanes hold row 0: a valid row whose weights are 0
       __syncwarp();
-      Vec<VW> gv[U][NV];
+      Row<VW, LP> gv[U][NV];
       {  // the first half of the first row group goes out before the record loads
         const uint4 id4 = lds_u4(sm.nb);
-        lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[0]);
-        lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[1]);
-        lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[2]);
-        lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[3]);
+        lean_gather<VW, NV, LP>(tab, id4.x, hf, cols, gv[0]);
+        lean_gather<VW, NV, LP>(tab, id4.y, hf, cols, gv[1]);
+        lean_gather<VW, NV, LP>(tab, id4.z, hf, cols, gv[2]);
+        lean_gather<VW, NV, LP>(tab, id4.w, hf, cols, gv[3]);
       }
       {
         // edge phase, lanes = (edge, head) pairs: one {A_r, lse, c, 0} record load each
@@ -234,10 +273,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
       v_cur = base + 32 + lane < e1 ? ld_stream(p.nbr + base + 32 + lane) : 0u;
       {
         const uint4 id4 = lds_u4(sm.nb + 4);
-        lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[4]);
-        lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[5]);
-        lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[6]);
-        lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[7]);
+        lean_gather<VW, NV, LP>(tab, id4.x, hf, cols, gv[4]);
+        lean_gather<VW, NV, LP>(tab, id4.y, hf, cols, gv[5]);
+        lean_gather<VW, NV, LP>(tab, id4.z, hf, cols, gv[6]);
+        lean_gather<VW, NV, LP>(tab, id4.w, hf, cols, gv[7]);
       }
       for (int j = 0;;) {
         float pd[NVAL];
@@ -249,8 +288,8 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
           for (int rr = 0; rr < R; ++rr)
 #pragma unroll
             for (int i = 0; i < NV; ++i) {
-              axpy_vec<VW>(wa[rr * NV + i], gv[t + rr][i].x, acc[i].x);
-              pd[(t + rr) * NV + i] = dot_vec<VW>(x[i].x, gv[t + rr][i].x);
+              axpy_vec<VW>(wa[rr * NV + i], gv[t + rr][i], acc[i].x);
+              pd[(t + rr) * NV + i] = dot_vec<VW>(x[i], gv[t + rr][i]);
             }
         }
         bfly<NVAL, PER / 2>(pd, lane);
@@ -289,10 +328,10 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_bwd_src_lean_kernel(Gat
 #pragma unroll
         for (int t = 0; t < U; t += 4) {
           const uint4 id4 = lds_u4(sm.nb + j + t);
-          lean_gather<VW, NV>(tab, id4.x, hf, cols, gv[t]);
-          lean_gather<VW, NV>(tab, id4.y, hf, cols, gv[t + 1]);
-          lean_gather<VW, NV>(tab, id4.z, hf, cols, gv[t + 2]);
-          lean_gather<VW, NV>(tab, id4.w, hf, cols, gv[t + 3]);
+          lean_gather<VW, NV, LP>(tab, id4.x, hf, cols, gv[t]);
+          lean_gather<VW, NV, LP>(tab, id4.y, hf, cols, gv[t + 1]);
+          lean_gather<VW, NV, LP>(tab, id4.z, hf, cols, gv[t + 2]);
+          lean_gather<VW, NV, LP>(tab, id4.w, hf, cols, gv[t + 3]);
         }
       }
       __syncwarp();
@@ -341,7 +380,7 @@ struct LeanFwdSmem {
   float sc[MAXH];         // per head: rescale of the block, then 1 / exp-sum at the end
 };
 
-template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN>
+template <int H, int VW, int NV, int PER, int WPC, int MINB, bool DYN, bool LP = false>
 __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatParams p) {
   constexpr int U = 8;
   constexpr int R = 4 / NV;
@@ -356,7 +395,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
   constexpr int epi = kWarp / h;
   const int kk = lane % h;
   constexpr int F = PER * VW;  // = f: the shapes this kernel takes fill the warp
-  const LaneRows<VW, NV, F> hrows(p.Ht, cols.col[0]);
+  const LaneRows<VW, NV, F, LP> hrows(LP ? static_cast<const void*>(p.lp) : static_cast<const void*>(p.Ht), cols.col[0]);
   unsigned nx = DYN && lane == 0 ? atomicAdd(p.ctr, 1u) : 0u;
   for (int64_t g = blockIdx.x; DYN || g * WPC < p.num_items; g += gridDim.x) {
     int64_t wi;
@@ -381,7 +420,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
       const uint32_t u_last = __shfl_sync(0xffffffffu, u_cur, n - 1);
       sm.nb[lane] = lane < n ? u_cur : u_last;  // rows past n repeat the last one (weight 0)
       __syncwarp();
-      Vec<VW> x[U][NV];
+      Row<VW, LP> x[U][NV];
 #pragma unroll
       for (int t = 0; t < U; t += 4) {
         const uint4 id4 = lds_u4(sm.nb + t);
@@ -437,7 +476,7 @@ __global__ void __launch_bounds__(WPC * kWarp, MINB) gat_fwd_lean_kernel(GatPara
 #pragma unroll
             for (int i = 0; i < NV; ++i)
 #pragma unroll
-              for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(wa[rr * NV + i], x[t + rr][i].x[q], acc[i].x[q]);
+              for (int q = 0; q < VW; ++q) acc[i].x[q] = fmaf(wa[rr * NV + i], x[t + rr][i][q], acc[i].x[q]);
         }
         j += U;
         if (j >= n) break;
@@ -624,6 +663,41 @@ bool launch_bwd_src_lean(const GatParams& p, unsigned, cudaStream_t s) {
     else launch<4, 2, 8>(p, s);
   } else {
     launch<4, 1, 4>(p, s);
+  }
+  return true;
+}
+
+// The bf16 mode (gnncg_gat_fwd_bf16 / gnncg_gat_bwd_src_fused_bf16) at the same shapes: the
+// lean kernels with bf16 gather tables (8 or 4 columns of one head per lane: one 16- or 8-byte
+// load per lane-row), all arithmetic fp32.
+bool launch_fwd_lean_lp(const GatParams& p, cudaStream_t s) {
+  if (!lean_enabled() || !lean_supported(p.h, p.f) || (reinterpret_cast<uintptr_t>(p.lp) & 15)) return false;
+  if (p.f == 32) {
+    constexpr int W = FwdShape<8>::WPC, M = FwdShape<8>::MINB;
+    const unsigned grid = lean_grid(p.num_items, W, M);
+    if (p.ctr) launch_win(gat_fwd_lean_kernel<8, 8, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
+    else launch_win(gat_fwd_lean_kernel<8, 8, 1, 4, W, M, false, true>, grid, W * kWarp, s, p);
+  } else {
+    constexpr int W = FwdShape<4>::WPC, M = FwdShape<4>::MINB;
+    const unsigned grid = lean_grid(p.num_items, W, M);
+    if (p.ctr) launch_win(gat_fwd_lean_kernel<8, 4, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
+    else launch_win(gat_fwd_lean_kernel<8, 4, 1, 4, W, M, false, true>, grid, W * kWarp, s, p);
+  }
+  return true;
+}
+
+bool launch_bwd_src_lean_lp(const GatParams& p, cudaStream_t s) {
+  if (!lean_enabled() || !lean_supported(p.h, p.f) || ((reinterpret_cast<uintptr_t>(p.lp) |
+                                                        reinterpret_cast<uintptr_t>(p.lp_x)) & 15))
+    return false;
+  constexpr int W = BwdShape<1>::WPC, M = BwdShape<1>::MINB;
+  const unsigned grid = lean_grid(p.num_items, W, M);
+  if (p.f == 32) {
+    if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, 8, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
+    else launch_win(gat_bwd_src_lean_kernel<8, 8, 1, 4, W, M, false, true>, grid, W * kWarp, s, p);
+  } else {
+    if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, 4, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
+    else launch_win(gat_bwd_src_lean_kernel<8, 4, 1, 4, W, M, false, true>, grid, W * kWarp, s, p);
   }
   return true;
 }
