@@ -670,10 +670,23 @@ bool launch_bwd_src_lean(const GatParams& p, unsigned, cudaStream_t s) {
 // The bf16 mode (gnncg_gat_fwd_bf16 / gnncg_gat_bwd_src_fused_bf16) at the same shapes: the
 // lean kernels with bf16 gather tables (8 or 4 columns of one head per lane: one 16- or 8-byte
 // load per lane-row), all arithmetic fp32.
+#ifndef GNNCG_LEAN_FWDLP_WPC
+#define GNNCG_LEAN_FWDLP_WPC 8
+#endif
+#ifndef GNNCG_LEAN_FWDLP_MINB
+#define GNNCG_LEAN_FWDLP_MINB 4
+#endif
+#ifndef GNNCG_LEAN_BWDLP_WPC
+#define GNNCG_LEAN_BWDLP_WPC 4
+#endif
+#ifndef GNNCG_LEAN_BWDLP_MINB
+#define GNNCG_LEAN_BWDLP_MINB 7
+#endif
+
 bool launch_fwd_lean_lp(const GatParams& p, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f) || (reinterpret_cast<uintptr_t>(p.lp) & 15)) return false;
   if (p.f == 32) {
-    constexpr int W = FwdShape<8>::WPC, M = FwdShape<8>::MINB;
+    constexpr int W = GNNCG_LEAN_FWDLP_WPC, M = GNNCG_LEAN_FWDLP_MINB;
     const unsigned grid = lean_grid(p.num_items, W, M);
     if (p.ctr) launch_win(gat_fwd_lean_kernel<8, 8, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
     else launch_win(gat_fwd_lean_kernel<8, 8, 1, 4, W, M, false, true>, grid, W * kWarp, s, p);
@@ -690,7 +703,7 @@ bool launch_bwd_src_lean_lp(const GatParams& p, cudaStream_t s) {
   if (!lean_enabled() || !lean_supported(p.h, p.f) || ((reinterpret_cast<uintptr_t>(p.lp) |
                                                         reinterpret_cast<uintptr_t>(p.lp_x)) & 15))
     return false;
-  constexpr int W = BwdShape<1>::WPC, M = BwdShape<1>::MINB;
+  constexpr int W = GNNCG_LEAN_BWDLP_WPC, M = GNNCG_LEAN_BWDLP_MINB;
   const unsigned grid = lean_grid(p.num_items, W, M);
   if (p.f == 32) {
     if (p.ctr) launch_win(gat_bwd_src_lean_kernel<8, 8, 1, 4, W, M, true, true>, grid, W * kWarp, s, p);
