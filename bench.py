@@ -713,20 +713,22 @@ def run_ours(args):
     # --- checker leg (oracle/: never the measured path) ---------------------------------
     single = rank == 0 and world == 1 and not dmode
     cpu = parity = None
-    if single and args.config in ("reddit", "c5") and not args.no_parity and args.gather == "fp32":
+    if single and args.config in ("reddit", "c5") and not args.no_parity:
         from oracle.sampled import gat_model_sampled_check
 
         for p, p0 in zip(model_params(model), init_params):  # the benchmarked model at its initial parameters
             p.copy_(p0)
         t0 = time.perf_counter()
         parity = gat_model_sampled_check(model, H, n_rows=16, n_src=4, seed=0, hub_src=args.config == "reddit")
+        # fp32 gathers: the 1e-4 contract; bf16 gather tables: the stated looser bound
+        bound = 1e-4 if args.gather == "fp32" else 2e-2
         e_out = max(parity["max_rel_err"].get("out_layer1", 0), parity["max_rel_err"].get("out_last", 0))
         e_grad = parity.get("max_norm_err", {}).get("dH_last")
         parity.update({"comparator": {"outputs": "rel_err = |a-b| / max(1,|a|,|b|) elementwise (tensor.hpp:153-156)",
                                       "gradients": "|a-b| / max(1, max|ref|) over the checked rows (DESIGN.md §2: "
                                                    "stated deviation; fp32 sums cannot meet the elementwise bound "
                                                    "where entries cancel)"},
-                       "bound": 1e-4, "pass": e_out < 1e-4 and (e_grad is None or e_grad < 1e-4),
+                       "bound": bound, "pass": e_out < bound and (e_grad is None or e_grad < bound),
                        "max_rel_err_out": e_out, "max_rel_err_grads": e_grad,
                        "oracle": "oracle/sampled.py: f64 local-neighbourhood restatement on the GPU model's own "
                                  "layer inputs (one extra fwd+bwd after the timed steps)",
