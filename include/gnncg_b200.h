@@ -145,6 +145,14 @@ int gnncg_max_degree(const gnncg_index_t* idx, uint64_t* max_degree_host, void* 
  * balanced edge counts, bound[p] = lower_bound(off, ceil(p*E/P)), bound[P] = V.
  * off_host/bound_host are host arrays. */
 int gnncg_partition_rows(int64_t num_rows, const uint64_t* off_host, int32_t parts, uint64_t* bound_host);
+/* Cost-balanced variant: row v costs its edges plus row_weight (the per-row work of a layer in
+ * edge units: the row's share of the transform / gradient GEMMs, records, per-item overheads),
+ *   cost(v) = off[v] + row_weight * v,  bound[p] = lower_bound(cost, ceil(p * cost(V) / P)).
+ * row_weight = 0 is gnncg_partition_rows.  Edge-balanced blocks of a power-law graph give the
+ * rank with the low-degree tail ~45x the rows of the hub rank and ~2x its step time (C5, P = 8,
+ * scripts/emulate_ranks.py). */
+int gnncg_partition_rows_weighted(int64_t num_rows, const uint64_t* off_host, int32_t parts, uint64_t row_weight,
+                                  uint64_t* bound_host);
 
 /* Deterministic Chung-Lu edge generator (device): edge e draws its destination
  * and source independently from the integer weight CDF `cdf` (device, V entries,

@@ -611,18 +611,22 @@ class Comm {
 };
 
 // Rank `rank`'s share of a P-way destination-row partition of a gnncg::Graph: rows
-// [row_begin, row_end) = gnncg_partition_rows over the csr_dst offsets (edge-balanced), and
+// [row_begin, row_end) = gnncg_partition_rows_weighted over the csr_dst offsets (cost-balanced), and
 // the rank's in-edges split by the owner of their source (see gnncg_part_t).
 class PartitionedGraph {
  public:
-  PartitionedGraph(const Graph& g, int nparts, int rank, std::int32_t chunk = 2048, cudaStream_t stream = nullptr)
+  // row_weight: the cost-balanced partitioner's per-row weight in edge units
+  // (gnncg_partition_rows_weighted; 0 = edge-balanced blocks)
+  PartitionedGraph(const Graph& g, int nparts, int rank, std::int32_t chunk = 2048, cudaStream_t stream = nullptr,
+                   std::uint64_t row_weight = 64)
       : P_(nparts), rank_(rank), s_(stream) {
     check(gnncg_device_check(), "gnncg_device_check");
     if (nparts < 1 || rank < 0 || rank >= nparts) throw std::invalid_argument("PartitionedGraph: bad rank / nparts");
     const AdjIndex& in = g.csr_dst();
     const std::int64_t V = (std::int64_t)g.num_vertices();
     bounds_.resize(P_ + 1);
-    check(gnncg_partition_rows(V, in.offsets.data(), P_, bounds_.data()), "gnncg_partition_rows");
+    check(gnncg_partition_rows_weighted(V, in.offsets.data(), P_, row_weight, bounds_.data()),
+          "gnncg_partition_rows_weighted");
     for (int q = 0; q < P_; ++q) maxrows_ = std::max<std::int64_t>(maxrows_, bounds_[q + 1] - bounds_[q]);
     r0_ = (std::int64_t)bounds_[rank];
     n_ = (std::int64_t)bounds_[rank + 1] - r0_;

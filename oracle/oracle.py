@@ -214,6 +214,25 @@ def partition_rows(off: np.ndarray, P: int) -> np.ndarray:
     return bound
 
 
+def partition_rows_weighted(off: np.ndarray, P: int, row_weight: int) -> np.ndarray:
+    """Cost-balanced row blocks (restatement of gnncg_partition_rows_weighted, include/gnncg_b200.h):
+    cost(v) = off[v] + row_weight * v, bound[p] = lower_bound(cost, ceil(p * cost(V) / P)), exact
+    integer arithmetic (Python ints)."""
+    off = [int(x) for x in np.asarray(off, dtype=np.uint64)]
+    V = len(off) - 1
+    cost = [off[v] + row_weight * v for v in range(V + 1)]
+    total = cost[V]
+    import bisect
+
+    bound = [0] * (P + 1)
+    for p in range(1, P):
+        target = -(-(p * total) // P)
+        b = min(bisect.bisect_left(cost, target), V)
+        bound[p] = max(b, bound[p - 1])
+    bound[P] = V
+    return np.array(bound, np.uint64)
+
+
 # ----------------------------------------------------------------------------
 # GAT
 # ----------------------------------------------------------------------------

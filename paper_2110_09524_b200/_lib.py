@@ -104,6 +104,7 @@ _SIGS = {
     "gnncg_csr_build_rect": ([i64, i64, i64, vp, vp, vp, vp, vp, vp, sz, vp], i32),
     "gnncg_max_degree": ([P(Index), P(u64), vp], i32),
     "gnncg_partition_rows": ([i64, vp, i32, vp], i32),
+    "gnncg_partition_rows_weighted": ([i64, vp, i32, u64, vp], i32),
     "gnncg_gen_chung_lu": ([i64, i64, vp, u64, vp, vp, vp], i32),
     "gnncg_gen_chung_lu_degrees": ([i64, i64, vp, u64, vp, vp], i32),
     "gnncg_gen_chung_lu_rows_workspace": ([i64], sz),

@@ -174,6 +174,28 @@ int gnncg_partition_rows(int64_t num_rows, const uint64_t* off, int32_t parts, u
   return GNNCG_OK;
 }
 
+int gnncg_partition_rows_weighted(int64_t num_rows, const uint64_t* off, int32_t parts, uint64_t row_weight,
+                                  uint64_t* bound) {
+  GNNCG_REQUIRE(off && bound, GNNCG_ERR_ARG, "partition_rows_weighted: null pointer");
+  GNNCG_REQUIRE(parts >= 1, GNNCG_ERR_ARG, "partition_rows_weighted: parts must be >= 1");
+  const uint64_t V = (uint64_t)num_rows;
+  const auto cost = [&](uint64_t v) { return off[v] + row_weight * v; };
+  const uint64_t total = cost(V);
+  bound[0] = 0;
+  for (int p = 1; p < parts; ++p) {
+    const uint64_t target = (uint64_t)(((unsigned __int128)p * total + (uint64_t)parts - 1) / (uint64_t)parts);
+    uint64_t lo = 0, hi = V + 1;  // lower_bound over cost[0..V] (non-decreasing)
+    while (lo < hi) {
+      const uint64_t mid = (lo + hi) / 2;
+      if (cost(mid) < target) lo = mid + 1; else hi = mid;
+    }
+    bound[p] = lo > V ? V : lo;
+    if (bound[p] < bound[p - 1]) bound[p] = bound[p - 1];
+  }
+  bound[parts] = V;
+  return GNNCG_OK;
+}
+
 // Work items of the unified thread mapping (one warp per item):
 //   * split rows (deg > chunk) first, each as ceil(deg/chunk) consecutive items
 //     (hub rows start first: longest-processing-time order);

@@ -1,7 +1,8 @@
 """Multi-GPU GAT: destination-row partitioning with one all-gather per layer (north_star).
 
 Destination vertices are split into P contiguous row blocks of csr_dst with balanced
-edge counts (``gnncg_partition_rows``: bound[p] = lower_bound(off, ceil(p E / P))).
+costs (``gnncg_partition_rows_weighted``: edges + DEFAULT_ROW_WEIGHT per row; weight 0 is the
+edge-balanced ``gnncg_partition_rows``, bound[p] = lower_bound(off, ceil(p E / P))).
 Rank p owns rows [r_p, r_{p+1}) and every tensor indexed by them (H, out, m, d, A_r, dOut).
 Source-side tables (Ht, A_l) live in the PADDED all-gather layout: rank q's rows at
 [q*maxrows, q*maxrows + n_q), so the kernels index the gathered tables directly.
@@ -74,10 +75,10 @@ class PartitionPlan:
         return p * self.maxrows + (u - b[p])
 
     @classmethod
-    def from_dst(cls, V: int, dst: torch.Tensor, P: int) -> "PartitionPlan":
+    def from_dst(cls, V: int, dst: torch.Tensor, P: int, row_weight: int = 0) -> "PartitionPlan":
         deg = torch.bincount(dst.to(torch.int64), minlength=V).cpu().numpy()
         off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
-        return cls(partition_rows(off, P))
+        return cls(partition_rows(off, P, row_weight))
 
 
 @dataclass
@@ -344,7 +345,14 @@ class PartitionedGAT:
         return self.loss[:1], grads
 
 
-def partitioned_chung_lu(V: int, E: int, *, offset: int, seed: int, rank: int, world: int, device) -> LocalGraph:
+# Per-row work of a layer in edge units for the cost-balanced partitioner (gnncg_partition_rows_weighted):
+# the slowest rank's step (per-rank emulation, scripts/emulate_ranks.py, profiles/r02_partition.txt)
+# at P = 8 is lowest near 64 for both C5 (175 -> 104 ms, mean 90) and the Reddit shape (11.0 -> 8.4 ms).
+DEFAULT_ROW_WEIGHT = 64
+
+
+def partitioned_chung_lu(V: int, E: int, *, offset: int, seed: int, rank: int, world: int, device,
+                         row_weight: int = DEFAULT_ROW_WEIGHT) -> LocalGraph:
     """This rank's share of the Chung-Lu graph gnncg_gen_chung_lu would produce, without the
     global edge list: the in-degree histogram gives the offsets the partitioner splits
     (bit-exact, gnncg_partition_rows), then gnncg_gen_chung_lu_rows regenerates the edge
@@ -357,7 +365,7 @@ def partitioned_chung_lu(V: int, E: int, *, offset: int, seed: int, rank: int, w
     off = np.zeros(V + 1, np.uint64)
     off[1:] = np.cumsum(deg.cpu().numpy().view(np.uint32), dtype=np.uint64)
     del deg
-    plan = PartitionPlan(partition_rows(off, world))
+    plan = PartitionPlan(partition_rows(off, world, row_weight))
     r0, r1 = int(plan.bounds[rank]), int(plan.bounds[rank + 1])
     n = int(off[r1] - off[r0])
     src = torch.empty(max(n, 1), dtype=torch.int32, device=device)

@@ -356,9 +356,13 @@ def knn_edges(clouds: int, points: int, k: int, seed: int):
     return (np.concatenate(src_all).astype(np.uint32), np.concatenate(dst_all).astype(np.uint32))
 
 
-def partition_rows(off: np.ndarray, parts: int) -> np.ndarray:
-    """Row-block partitioner: bound[p] = lower_bound(off, ceil(p*E/P)) (bit-exact, host)."""
+def partition_rows(off: np.ndarray, parts: int, row_weight: int = 0) -> np.ndarray:
+    """Row-block partitioner: bound[p] = lower_bound(off, ceil(p*E/P)) (bit-exact, host); with
+    row_weight > 0 the cost-balanced variant, cost(v) = off[v] + row_weight * v."""
     off = np.ascontiguousarray(off, dtype=np.uint64)
     bound = np.zeros(parts + 1, np.uint64)
-    call("gnncg_partition_rows", off.size - 1, off.ctypes.data, parts, bound.ctypes.data)
+    if row_weight:
+        call("gnncg_partition_rows_weighted", off.size - 1, off.ctypes.data, parts, int(row_weight), bound.ctypes.data)
+    else:
+        call("gnncg_partition_rows", off.size - 1, off.ctypes.data, parts, bound.ctypes.data)
     return bound

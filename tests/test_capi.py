@@ -92,6 +92,22 @@ def test_partitioner_matches_oracle():
         np.testing.assert_array_equal(partition_rows(off, P), O.partition_rows(off, P))
 
 
+@pytest.mark.parametrize("w", [0, 1, 22, 32, 1000])
+def test_weighted_partitioner_matches_oracle(w):
+    """Cost-balanced blocks (edges + w per row) equal the restatement bit for bit; w = 0 is the
+    edge-balanced partitioner; a power-law graph's tail rank gets fewer rows as w grows."""
+    rng = np.random.default_rng(2)
+    deg = (4000.0 / (np.arange(3000) + 5.0)).astype(np.int64) + rng.integers(0, 3, 3000)
+    off = np.concatenate([[0], np.cumsum(deg)]).astype(np.uint64)
+    for P in (1, 2, 3, 8):
+        b = partition_rows(off, P, row_weight=w)
+        np.testing.assert_array_equal(b, O.partition_rows_weighted(off, P, w))
+        if w == 0:
+            np.testing.assert_array_equal(b, partition_rows(off, P))
+    if w:
+        assert np.diff(partition_rows(off, 8, row_weight=w))[-1] < np.diff(partition_rows(off, 8))[-1]
+
+
 def test_errors_map_to_reference_exceptions():
     assert issubclass(_lib.GraphError, RuntimeError) and issubclass(_lib.TensorError, RuntimeError)
     with pytest.raises(_lib.ArgumentError):
