@@ -63,12 +63,13 @@ def test_per_rank_chung_lu_equals_filtered_global_list(cuda, P):
     """Multi-GPU graph build: each rank's edges (gnncg_gen_chung_lu_rows) are the global edge
     list filtered to its destination block, in edge-id order; the in-degree histogram and the
     row bounds equal those of the global list; the local CSR is the global CSR's row block."""
-    from paper_2110_09524_b200.dist import partitioned_chung_lu
+    from paper_2110_09524_b200.dist import DEFAULT_ROW_WEIGHT, partitioned_chung_lu
 
     V, E, off, seed = 20000, 1_000_000, 100, 5
     src, dst = chung_lu_edges_host(V, E, off, seed)
     ref = O.host_graph(V, src, dst)
-    bounds = O.partition_rows(ref.dst_off, P)
+    # the multi-GPU default: cost-balanced blocks (gnncg_partition_rows_weighted)
+    bounds = O.partition_rows_weighted(ref.dst_off, P, DEFAULT_ROW_WEIGHT)
     total = 0
     for rank in range(P):
         lg = partitioned_chung_lu(V, E, offset=off, seed=seed, rank=rank, world=P, device=cuda)
