@@ -125,10 +125,26 @@ def build_local(plan: PartitionPlan, rank: int, src: torch.Tensor, dst: torch.Te
     del ps, ld, own
     csr_local = engine.build_index(n, ld_l, ps_l, Vp)
     csc_local = engine.build_index(n, ps_l - base, ld_l, n)
+    _gather_hint(csr_local, ps_l, Vp)  # K2's local pass reads Ht_all rows of the local sources
+    _gather_hint(csc_local, ld_l, n)  # K4f's local pass reads dOut rows of the owned destinations
     del ps_l, ld_l
     csr_remote = engine.build_index(n, ld_r, ps_r, Vp)
     csc_remote = engine.build_index(Vp, ps_r, ld_r, n)
+    _gather_hint(csr_remote, ps_r, Vp)
+    _gather_hint(csc_remote, ld_r, n)
     return LocalGraph(plan, rank, csr_local, csr_remote, csc_local, csc_remote)
+
+
+def _gather_hint(idx, gathered: torch.Tensor, rows: int):
+    """The L2 hint of a rank-local index (gnncg_sched_t.gather_off): how often its fused kernel
+    reads each row of the table it gathers, as host prefix sums (the padded Ht_all / A_l table
+    for the csr passes, the owned dOut rows for the csc passes)."""
+    if not hasattr(idx, "gather_off"):  # the oracle engine's indexes
+        return
+    cnt = torch.bincount(gathered.to(torch.int64), minlength=rows)
+    off = torch.zeros(rows + 1, dtype=torch.int64, device=cnt.device)
+    torch.cumsum(cnt, 0, out=off[1:])
+    idx.gather_off = np.ascontiguousarray(off.cpu().numpy().view(np.uint64))
 
 
 class NcclComm:
