@@ -663,7 +663,7 @@ class PartitionedGraph {
     two(csr_r_, csc_r_, kr, orr, Vp, 0);
     views_[0] = csr_l_.view(); views_[1] = csr_r_.view(); views_[2] = csc_l_.view(); views_[3] = csc_r_.view();
     part_ = gnncg_part_t{n_, maxrows_, P_, rank_, &views_[0], &csr_l_.sched, &views_[1], &csr_r_.sched,
-                         &views_[2], &csc_l_.sched, &views_[3], &csc_r_.sched};
+                         &views_[2], &csc_l_.sched, &views_[3], &csc_r_.sched, bounds_.data()};
   }
   PartitionedGraph(const PartitionedGraph&) = delete;
   PartitionedGraph& operator=(const PartitionedGraph&) = delete;

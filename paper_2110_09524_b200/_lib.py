@@ -88,7 +88,7 @@ class Part(C.Structure):
     _fields_ = [("num_local", i64), ("maxrows", i64), ("nparts", i32), ("rank", i32),
                 ("csr_local", P(Index)), ("csr_local_sched", P(Sched)), ("csr_remote", P(Index)),
                 ("csr_remote_sched", P(Sched)), ("csc_local", P(Index)), ("csc_local_sched", P(Sched)),
-                ("csc_remote", P(Index)), ("csc_remote_sched", P(Sched))]
+                ("csc_remote", P(Index)), ("csc_remote_sched", P(Sched)), ("bounds", vp)]
 
 
 _SIGS = {

@@ -45,6 +45,9 @@ struct NcclApi {
                                 cudaStream_t) = nullptr;
   ncclResult_t (*AllReduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, ncclComm_t,
                             cudaStream_t) = nullptr;
+  ncclResult_t (*Broadcast)(const void*, void*, size_t, ncclDataType_t, int, ncclComm_t, cudaStream_t) = nullptr;
+  ncclResult_t (*Reduce)(const void*, void*, size_t, ncclDataType_t, ncclRedOp_t, int, ncclComm_t,
+                         cudaStream_t) = nullptr;
   ncclResult_t (*GroupStart)() = nullptr;
   ncclResult_t (*GroupEnd)() = nullptr;
   const char* (*GetErrorString)(ncclResult_t) = nullptr;
@@ -75,6 +78,8 @@ const NcclApi& nccl() {
     sym(api.AllGather, "ncclAllGather");
     sym(api.ReduceScatter, "ncclReduceScatter");
     sym(api.AllReduce, "ncclAllReduce");
+    sym(api.Broadcast, "ncclBroadcast");
+    sym(api.Reduce, "ncclReduce");
     sym(api.GroupStart, "ncclGroupStart");
     sym(api.GroupEnd, "ncclGroupEnd");
     sym(api.GetErrorString, "ncclGetErrorString");
@@ -209,6 +214,13 @@ int check_part(const gnncg_part_t* p, int h, int f) {
                     p->csr_remote->num_edges == p->csc_remote->num_edges,
                 GNNCG_ERR_SHAPE, "gat_dist: csr / csc edge counts differ");
   GNNCG_REQUIRE(h >= 1 && h <= 32 && f >= 1, GNNCG_ERR_SHAPE, "gat_dist: bad heads / f");
+  if (p->bounds) {
+    GNNCG_REQUIRE(p->bounds[0] == 0 && (int64_t)(p->bounds[p->rank + 1] - p->bounds[p->rank]) == p->num_local,
+                  GNNCG_ERR_ARG, "gat_dist: bounds disagree with num_local");
+    for (int q = 0; q < p->nparts; ++q)
+      GNNCG_REQUIRE(p->bounds[q + 1] >= p->bounds[q] && (int64_t)(p->bounds[q + 1] - p->bounds[q]) <= p->maxrows,
+                    GNNCG_ERR_ARG, "gat_dist: block %d larger than maxrows", q);
+  }
   return GNNCG_OK;
 }
 
@@ -384,10 +396,20 @@ int gnncg_gat_fwd_dist(gnncg_comm_t* comm, const gnncg_part_t* p, int h, int f, 
     rc = fork_to_comm(comm, s);
     if (rc) return rc;
     GNNCG_NCCL_TRY(nccl().GroupStart());
-    GNNCG_NCCL_TRY(nccl().AllGather(Ht_all + p->rank * mr * hf, Ht_all, (size_t)(mr * hf), ncclFloat32, comm->nc,
-                                    comm->cs));
-    GNNCG_NCCL_TRY(nccl().AllGather(Al_all + p->rank * mr * h, Al_all, (size_t)(mr * h), ncclFloat32, comm->nc,
-                                    comm->cs));
+    if (p->bounds) {  // only the owned rows of each block: one in-place broadcast per root
+      for (int q = 0; q < p->nparts; ++q) {
+        const size_t nq = (size_t)(p->bounds[q + 1] - p->bounds[q]);
+        float* bh = Ht_all + (int64_t)q * mr * hf;
+        float* ba = Al_all + (int64_t)q * mr * h;
+        GNNCG_NCCL_TRY(nccl().Broadcast(bh, bh, nq * (size_t)hf, ncclFloat32, q, comm->nc, comm->cs));
+        GNNCG_NCCL_TRY(nccl().Broadcast(ba, ba, nq * (size_t)h, ncclFloat32, q, comm->nc, comm->cs));
+      }
+    } else {
+      GNNCG_NCCL_TRY(nccl().AllGather(Ht_all + p->rank * mr * hf, Ht_all, (size_t)(mr * hf), ncclFloat32, comm->nc,
+                                      comm->cs));
+      GNNCG_NCCL_TRY(nccl().AllGather(Al_all + p->rank * mr * h, Al_all, (size_t)(mr * h), ncclFloat32, comm->nc,
+                                      comm->cs));
+    }
     GNNCG_NCCL_TRY(nccl().GroupEnd());
   }
   if (n == 0) return gather ? join_from_comm(comm, s) : GNNCG_OK;
@@ -459,8 +481,20 @@ int gnncg_gat_bwd_dist(gnncg_comm_t* comm, const gnncg_part_t* p, int h, int f, 
     rc = fork_to_comm(comm, s);
     if (rc) return rc;
     GNNCG_NCCL_TRY(nccl().GroupStart());
-    GNNCG_NCCL_TRY(nccl().ReduceScatter(dHt_send, recvH, (size_t)(mr * hf), ncclFloat32, ncclSum, comm->nc, comm->cs));
-    GNNCG_NCCL_TRY(nccl().ReduceScatter(dAl_send, recvAl, (size_t)(mr * h), ncclFloat32, ncclSum, comm->nc, comm->cs));
+    if (p->bounds) {  // block q's partials summed onto rank q, owned rows only
+      for (int q = 0; q < p->nparts; ++q) {
+        const size_t nq = (size_t)(p->bounds[q + 1] - p->bounds[q]);
+        GNNCG_NCCL_TRY(nccl().Reduce(dHt_send + (int64_t)q * mr * hf, recvH, nq * (size_t)hf, ncclFloat32, ncclSum, q,
+                                     comm->nc, comm->cs));
+        GNNCG_NCCL_TRY(nccl().Reduce(dAl_send + (int64_t)q * mr * h, recvAl, nq * (size_t)h, ncclFloat32, ncclSum, q,
+                                     comm->nc, comm->cs));
+      }
+    } else {
+      GNNCG_NCCL_TRY(
+          nccl().ReduceScatter(dHt_send, recvH, (size_t)(mr * hf), ncclFloat32, ncclSum, comm->nc, comm->cs));
+      GNNCG_NCCL_TRY(
+          nccl().ReduceScatter(dAl_send, recvAl, (size_t)(mr * h), ncclFloat32, ncclSum, comm->nc, comm->cs));
+    }
     GNNCG_NCCL_TRY(nccl().GroupEnd());
   }
   // 3. ... while K4f walks the local-source edges (own rows of the tables, rebased)

@@ -202,9 +202,10 @@ class CudaEngine:
         if lg._part is None:
             idx = [lg.csr_local, lg.csr_remote, lg.csc_local, lg.csc_remote]
             keep = [(i.struct(), self._sched(i).struct()) for i in idx]
+            bounds = np.ascontiguousarray(lg.plan.bounds, dtype=np.uint64)  # unpadded collectives
             pt = Part(lg.num_local, lg.plan.maxrows, lg.plan.P, lg.rank,
-                      *[C.pointer(x) for pair in keep for x in pair])
-            lg._part = (pt, keep)
+                      *[C.pointer(x) for pair in keep for x in pair], bounds.ctypes.data)
+            lg._part = (pt, keep, bounds)
         return lg._part[0]
 
     def zeros(self, *shape):
