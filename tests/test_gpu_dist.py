@@ -163,3 +163,31 @@ def test_partitioned_world1_matches_single_gpu(cuda, nccl_world1):
         for a, b in ((dW, gr.dW), (da_l, gr.da_l), (da_r, gr.da_r)):
             assert _norm(a, b) < 1e-4
     pm.engine.comm.close()
+
+
+def test_part_bounds_are_validated(cuda):
+    """gnncg_part_t.bounds (the owned-rows collectives) must agree with num_local and maxrows:
+    a part whose bounds disagree is refused with GNNCG_ERR_ARG instead of moving wrong rows."""
+    from paper_2110_09524_b200 import _lib
+    from paper_2110_09524_b200.dist import CudaEngine, partitioned_chung_lu
+    from paper_2110_09524_b200.graph import _ptr, _stream
+
+    lg = partitioned_chung_lu(3000, 100_000, offset=40, seed=3, rank=1, world=2, device=cuda)
+    eng = CudaEngine(cuda)
+    pt = eng.part(lg)
+    h, f = 8, 16
+    n, mr = lg.num_local, lg.plan.maxrows
+    Ht_all = torch.zeros(2 * mr, h * f, device=cuda)
+    Al_all = torch.zeros(2 * mr, h, device=cuda)
+    Ar = torch.zeros(n, h, device=cuda)
+    out = torch.empty(n, h * f, device=cuda)
+    m, d = torch.empty(n, h, device=cuda), torch.empty(n, h, device=cuda)
+    ws = torch.empty(_lib.lib().gnncg_gat_dist_workspace(C.byref(pt), h, f), dtype=torch.uint8, device=cuda)
+    args = lambda: (None, C.byref(pt), h, f, 0.2, _ptr(Ht_all), _ptr(Al_all), _ptr(Ar), _ptr(out), _ptr(m),  # noqa: E731
+                    _ptr(d), _ptr(ws), ws.numel(), _stream())
+    _lib.call("gnncg_gat_fwd_dist", *args())  # consistent bounds: accepted
+    bad = np.ascontiguousarray(lg.plan.bounds, dtype=np.uint64).copy()
+    bad[1] += 1  # rank 1's block no longer matches num_local
+    pt.bounds = bad.ctypes.data
+    with pytest.raises(_lib.ArgumentError):
+        _lib.call("gnncg_gat_fwd_dist", *args())
