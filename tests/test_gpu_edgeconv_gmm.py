@@ -20,8 +20,9 @@ def np64(t):
     return t.detach().cpu().double().numpy()
 
 
-# C picks K6/K7's column width per lane: 64 -> 2, 96 -> 2 with a partial second pass,
-# 128 / 256 -> 4 (16-byte loads; two passes at 256), 33 -> 1
+# C picks K6/K7's column width per lane (VW) and lanes per row (L): 64 -> VW 8 / L 8 (4 rows per
+# warp), 96 -> 8 / 16 with 4 idle lanes, 128 -> 8 / 16, 256 -> 8 / 32, 33 -> 1 / 32 with a partial
+# second pass
 @pytest.mark.parametrize("clouds,points,k,C", [(2, 256, 20, 64), (4, 1024, 40, 64), (1, 64, 8, 33),
                                                (2, 256, 20, 128), (1, 512, 16, 256), (2, 128, 10, 96)])
 def test_edgeconv_region_argmax_bit_exact(cuda, clouds, points, k, C):
@@ -38,6 +39,45 @@ def test_edgeconv_region_argmax_bit_exact(cuda, clouds, points, k, C):
     torch.cuda.synchronize()
     np.testing.assert_array_equal(amax.cpu().numpy().view(np.uint32), ref_amax)
     np.testing.assert_array_equal(out.cpu().numpy(), ref_out)  # same fp32 RN expression -> bitwise
+
+
+@pytest.mark.parametrize("C", [8, 36, 64, 128, 200])
+def test_edgeconv_ragged_rows(cuda, C):
+    """Rows of different lengths (0 .. ~60 edges, some empty) side by side in one warp's lane groups:
+    each group runs its own trip count.  Forward bitwise; backward against the f64 oracle routed by
+    the shared argmax."""
+    rng = np.random.default_rng(C + 7)
+    V = 700
+    deg = rng.integers(0, 60, V)
+    deg[rng.random(V) < 0.1] = 0
+    dst = np.repeat(np.arange(V), deg)
+    src = rng.integers(0, V, dst.size)
+    perm = rng.permutation(dst.size)  # edge ids not in row order
+    src, dst = src[perm], dst[perm]
+    hg = O.host_graph(V, src, dst)
+    g = DeviceGraph.from_edges(V, src, dst, device=cuda)
+    Th = (rng.integers(-8, 8, (V, C)) / 4.0).astype(np.float32)
+    Ph = rng.uniform(-1, 1, (V, C)).astype(np.float32)
+    ref_out, ref_amax = O.edgeconv_fwd(hg, Th, Ph, np.float32)
+    out, amax = edgeconv_region_forward(g, t32(Th, cuda), t32(Ph, cuda))
+    torch.cuda.synchronize()
+    np.testing.assert_array_equal(amax.cpu().numpy().view(np.uint32), ref_amax)
+    np.testing.assert_array_equal(out.cpu().numpy(), ref_out)
+    Fin = 16
+    H = rng.uniform(-1, 1, (V, Fin))
+    Theta, Phi = rng.uniform(-0.25, 0.25, (Fin, C)), rng.uniform(-0.25, 0.25, (Fin, C))
+    dOut = rng.uniform(-1, 1, (V, C))
+    tH, tT, tP = t32(H, cuda), t32(Theta, cuda), t32(Phi, cuda)
+    _, st = edgeconv_forward(g, tH, tT, tP)
+    Y = st.Y.cpu().numpy()
+    _, ref_amax2 = O.edgeconv_fwd(hg, Y[:, :C], Y[:, C:], np.float32)
+    np.testing.assert_array_equal(st.argmax.cpu().numpy().view(np.uint32), ref_amax2)
+    dH, dTheta, dPhi = edgeconv_backward(g, tH, tT, tP, st, t32(dOut, cuda))
+    torch.cuda.synchronize()
+    bw = O.edgeconv_layer_bwd_f64(hg, H, Theta, Phi, ref_amax2, dOut)
+    for name, got in (("dH", dH), ("dTheta", dTheta), ("dPhi", dPhi)):
+        scale = max(1.0, np.abs(bw[name]).max())
+        assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name
 
 
 def test_edgeconv_empty_rows_and_ties(cuda):
