@@ -20,13 +20,6 @@ namespace {
 
 constexpr int MAXK = 8, MAXR = 4, MAXKF = 256, WARPS = 8;
 
-struct GmmSmem {
-  uint32_t nb[32];
-  float w[32 * (MAXK + 1)];
-  float red[MAXKF];
-  float row[MAXKF];
-};
-
 struct GmmArgs {
   int64_t rows;
   int K, r, f;
@@ -59,77 +52,117 @@ __device__ __forceinline__ void load_p(const float* p, int r, float (&x)[MAXR]) 
   for (int t = 0; t < MAXR; ++t) x[t] = t < r ? __ldg(p + t) : 0.f;
 }
 
+// Lane groups for the column passes (K8 forward, pass 2): L lanes own one row and a warp walks
+// 32 / L rows, L = 8 / 16 / 32 for K f <= 64 / 128 / 256 (each lane keeps 8 accumulators, columns
+// sl, sl + L, ...).  On Pubmed-shaped layers (4.5 edges per row, K f = 48) a whole warp per row left
+// most lanes idle in the per-edge weight stage and most of the warp's latency uncovered.
+template <int L>
+struct GmmGroupSmem {
+  uint32_t nb[L];
+  float w[L * (MAXK + 1)];
+  float red[8 * L];
+  float row[8 * L];
+};
+
+template <int L>
+struct GmmGroup {
+  int sub, sl;
+  unsigned mask;
+  __device__ __forceinline__ GmmGroup() {
+    const int lane = threadIdx.x & 31;
+    sub = lane / L;
+    sl = lane % L;
+    mask = L == 32 ? 0xffffffffu : (((1u << L) - 1u) << (sub * L));
+  }
+  __device__ __forceinline__ int slot() const { return (threadIdx.x >> 5) * (32 / L) + sub; }
+  __device__ __forceinline__ int64_t row() const { return ((int64_t)blockIdx.x * WARPS + (threadIdx.x >> 5)) * (32 / L) + sub; }
+  __device__ __forceinline__ float sum(float v) const {
+#pragma unroll
+    for (int o = L / 2; o > 0; o >>= 1) v += __shfl_xor_sync(mask, v, o);
+    return v;
+  }
+};
+
+template <int L>
 __global__ void __launch_bounds__(256, 4) gmm_fwd_kernel(GmmArgs a) {
-  __shared__ GmmSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  GmmSmem& sm = smem[wid];
-  const int64_t v = (int64_t)blockIdx.x * WARPS + wid;
+  constexpr int NA = 8;  // accumulators per lane: K f <= 8 L
+  __shared__ GmmGroupSmem<L> smem[WARPS * (32 / L)];
+  const GmmGroup<L> grp;
+  GmmGroupSmem<L>& sm = smem[grp.slot()];
+  const int64_t v = grp.row();
   if (v >= a.rows) return;
   const int K = a.K, r = a.r, f = a.f, Kf = K * f;
   float prv[MAXR];
   load_p(a.Y + v * a.ldy + Kf + r, r, prv);
-  float acc[MAXKF / 32];
+  float acc[NA];
 #pragma unroll
-  for (int i = 0; i < MAXKF / 32; ++i) acc[i] = 0.f;
+  for (int i = 0; i < NA; ++i) acc[i] = 0.f;
   const uint64_t e0 = a.off[v], e1 = a.off[v + 1];
-  for (uint64_t base = e0; base < e1; base += 32) {
-    const int n = (int)min((uint64_t)32, e1 - base);
-    if (lane < n) {
-      const uint32_t u = __ldg(a.nbr + base + lane);
-      sm.nb[lane] = u;
+  for (uint64_t base = e0; base < e1; base += L) {
+    const int n = (int)min((uint64_t)L, e1 - base);
+    if (grp.sl < n) {
+      const uint32_t u = __ldg(a.nbr + base + grp.sl);
+      sm.nb[grp.sl] = u;
       float plu[MAXR];
       load_p(a.Y + (int64_t)u * a.ldy + Kf, r, plu);
 #pragma unroll
       for (int k = 0; k < MAXK; ++k)
-        if (k < K) sm.w[lane * (MAXK + 1) + k] = gmm_w(a, k, plu, prv);
+        if (k < K) sm.w[grp.sl * (MAXK + 1) + k] = gmm_w(a, k, plu, prv);
     }
-    __syncwarp();
+    __syncwarp(grp.mask);
     for (int j = 0; j < n; ++j) {
       const float* y = a.Y + (int64_t)sm.nb[j] * a.ldy;
 #pragma unroll
-      for (int i = 0; i < MAXKF / 32; ++i) {
-        const int c = i * 32 + lane;
+      for (int i = 0; i < NA; ++i) {
+        const int c = i * L + grp.sl;
         if (c < Kf) acc[i] = fmaf(sm.w[j * (MAXK + 1) + c / f], __ldg(y + c), acc[i]);
       }
     }
-    __syncwarp();
+    __syncwarp(grp.mask);
   }
 #pragma unroll
-  for (int i = 0; i < MAXKF / 32; ++i) {
-    const int c = i * 32 + lane;
+  for (int i = 0; i < NA; ++i) {
+    const int c = i * L + grp.sl;
     if (c < Kf) sm.red[c] = acc[i];
   }
-  __syncwarp();
+  __syncwarp(grp.mask);
   const float invK = 1.f / (float)K;
-  for (int c = lane; c < f; c += 32) {
+  for (int c = grp.sl; c < f; c += L) {
     float s = 0.f;
     for (int k = 0; k < K; ++k) s += sm.red[k * f + c];
     a.out[v * f + c] = s * invK;
   }
 }
 
-// pass 1 over csr_dst: lane per edge.  The per-row dmu / dsinv partials (2 K r <= 64 values)
-// are reduced across the warp per 32-edge batch and held distributed: lane j keeps entries j
-// and 32 + j.
+// pass 1 over csr_dst, in lane groups (see gmm_fwd_kernel): lane per edge.  The per-row dmu / dsinv
+// partials (2 K r <= 64 values) are reduced across the group per L-edge batch and accumulated in
+// the group's shared-memory slot in batch order.
+template <int L>
+struct GmmDstSmem {
+  float row[8 * L];
+  float part[2 * MAXK * MAXR];
+};
+
+template <int L>
 __global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
-  __shared__ GmmSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  GmmSmem& sm = smem[wid];
-  const int64_t v = (int64_t)blockIdx.x * WARPS + wid;
+  __shared__ GmmDstSmem<L> smem[WARPS * (32 / L)];
+  const GmmGroup<L> grp;
+  GmmDstSmem<L>& sm = smem[grp.slot()];
+  const int64_t v = grp.row();
   if (v >= a.rows) return;
   const int K = a.K, r = a.r, f = a.f, Kf = K * f, Kr = K * r;
   const float invK = 1.f / (float)K;
-  for (int c = lane; c < f; c += 32) sm.row[c] = __ldg(a.dOut + v * f + c);
-  __syncwarp();
+  for (int c = grp.sl; c < f; c += L) sm.row[c] = __ldg(a.dOut + v * f + c);
+  for (int c = grp.sl; c < 2 * Kr; c += L) sm.part[c] = 0.f;
+  __syncwarp(grp.mask);
   float prv[MAXR], dpr[MAXR];
   load_p(a.Y + v * a.ldy + Kf + r, r, prv);
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) dpr[t] = 0.f;
-  float acc0 = 0.f, acc1 = 0.f;
   const uint64_t e0 = a.off[v], e1 = a.off[v + 1];
-  for (uint64_t base = e0; base < e1; base += 32) {
-    const bool valid = base + lane < e1;
-    const int64_t u = valid ? (int64_t)__ldg(a.nbr + base + lane) : 0;
+  for (uint64_t base = e0; base < e1; base += L) {
+    const bool valid = base + grp.sl < e1;
+    const int64_t u = valid ? (int64_t)__ldg(a.nbr + base + grp.sl) : 0;
     const float* y = a.Y + u * a.ldy;
     float plu[MAXR], dw[MAXK];
     load_p(y + Kf, r, plu);
@@ -152,52 +185,55 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
             const float s = __ldg(a.sinv + k * r + t), x = plu[t] + prv[t] - __ldg(a.mu + k * r + t);
             const float dmd = dq * 2.f * x * s * s;
             dpr[t] += dmd;
-            const float gm = warp_sum(-dmd), gs = warp_sum(dq * 2.f * x * x * s);
-            const int jm = k * r + t, js = Kr + jm;
-            if ((jm & 31) == lane) { if (jm < 32) acc0 += gm; else acc1 += gm; }
-            if ((js & 31) == lane) { if (js < 32) acc0 += gs; else acc1 += gs; }
+            const float gm = grp.sum(-dmd), gs = grp.sum(dq * 2.f * x * x * s);
+            if (grp.sl == 0) {
+              sm.part[k * r + t] += gm;
+              sm.part[Kr + k * r + t] += gs;
+            }
           }
         }
       }
     }
   }
+  __syncwarp(grp.mask);
   float* part = a.part + v * (int64_t)(2 * Kr);
-  if (lane < 2 * Kr) part[lane] = acc0;
-  if (32 + lane < 2 * Kr) part[32 + lane] = acc1;
+  for (int c = grp.sl; c < 2 * Kr; c += L) part[c] = sm.part[c];
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) {
     if (t < r) {
-      const float s = warp_sum(dpr[t]);
-      if (lane == 0) a.dY[v * a.ldy + Kf + r + t] = s;
+      const float s = grp.sum(dpr[t]);
+      if (grp.sl == 0) a.dY[v * a.ldy + Kf + r + t] = s;
     }
   }
 }
 
-// pass 2 over csc_src.
+// pass 2 over csc_src, in lane groups (see gmm_fwd_kernel).
+template <int L>
 __global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
-  __shared__ GmmSmem smem[WARPS];
-  const int lane = threadIdx.x & 31, wid = threadIdx.x >> 5;
-  GmmSmem& sm = smem[wid];
-  const int64_t u = (int64_t)blockIdx.x * WARPS + wid;
+  constexpr int NA = 8;
+  __shared__ GmmGroupSmem<L> smem[WARPS * (32 / L)];
+  const GmmGroup<L> grp;
+  GmmGroupSmem<L>& sm = smem[grp.slot()];
+  const int64_t u = grp.row();
   if (u >= a.rows) return;
   const int K = a.K, r = a.r, f = a.f, Kf = K * f;
   const float invK = 1.f / (float)K;
   const float* yu = a.Y + u * a.ldy;
-  for (int c = lane; c < Kf; c += 32) sm.row[c] = __ldg(yu + c);
+  for (int c = grp.sl; c < Kf; c += L) sm.row[c] = __ldg(yu + c);
   float plu[MAXR], dpl[MAXR];
   load_p(yu + Kf, r, plu);
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) dpl[t] = 0.f;
-  __syncwarp();
-  float acc[MAXKF / 32];
+  __syncwarp(grp.mask);
+  float acc[NA];
 #pragma unroll
-  for (int i = 0; i < MAXKF / 32; ++i) acc[i] = 0.f;
+  for (int i = 0; i < NA; ++i) acc[i] = 0.f;
   const uint64_t e0 = a.off[u], e1 = a.off[u + 1];
-  for (uint64_t base = e0; base < e1; base += 32) {
-    const int n = (int)min((uint64_t)32, e1 - base);
-    if (lane < n) {
-      const int64_t v = __ldg(a.nbr + base + lane);
-      sm.nb[lane] = (uint32_t)v;
+  for (uint64_t base = e0; base < e1; base += L) {
+    const int n = (int)min((uint64_t)L, e1 - base);
+    if (grp.sl < n) {
+      const int64_t v = __ldg(a.nbr + base + grp.sl);
+      sm.nb[grp.sl] = (uint32_t)v;
       float prv[MAXR], dw[MAXK];
       load_p(a.Y + v * a.ldy + Kf + r, r, prv);
       const float* g = a.dOut + v * f;
@@ -213,7 +249,7 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
       for (int k = 0; k < MAXK; ++k) {
         if (k < K) {
           const float w = gmm_w(a, k, plu, prv);
-          sm.w[lane * (MAXK + 1) + k] = w * invK;
+          sm.w[grp.sl * (MAXK + 1) + k] = w * invK;
           const float dq = -0.5f * w * dw[k] * invK;
 #pragma unroll
           for (int t = 0; t < MAXR; ++t)
@@ -224,34 +260,38 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
         }
       }
     }
-    __syncwarp();
+    __syncwarp(grp.mask);
     for (int j = 0; j < n; ++j) {
       const float* g = a.dOut + (int64_t)sm.nb[j] * f;
 #pragma unroll
-      for (int i = 0; i < MAXKF / 32; ++i) {
-        const int c = i * 32 + lane;
+      for (int i = 0; i < NA; ++i) {
+        const int c = i * L + grp.sl;
         if (c < Kf) acc[i] = fmaf(sm.w[j * (MAXK + 1) + c / f], __ldg(g + c % f), acc[i]);
       }
     }
-    __syncwarp();
+    __syncwarp(grp.mask);
   }
   float* dy = a.dY + u * a.ldy;
 #pragma unroll
-  for (int i = 0; i < MAXKF / 32; ++i) {
-    const int c = i * 32 + lane;
+  for (int i = 0; i < NA; ++i) {
+    const int c = i * L + grp.sl;
     if (c < Kf) dy[c] = acc[i];
   }
   // alignment columns past K f + 2 r (rows padded to 16 bytes for the TMA GEMM): zero, so
   // dWcat = H^T dY leaves the padding of [W | P_l | P_r] at zero
-  for (int64_t c = Kf + 2 * r + lane; c < a.ldy; c += 32) dy[c] = 0.f;
+  for (int64_t c = Kf + 2 * r + grp.sl; c < a.ldy; c += L) dy[c] = 0.f;
 #pragma unroll
   for (int t = 0; t < MAXR; ++t) {
     if (t < r) {
-      const float s = warp_sum(dpl[t]);
-      if (lane == 0) dy[Kf + t] = s;
+      const float s = grp.sum(dpl[t]);
+      if (grp.sl == 0) dy[Kf + t] = s;
     }
   }
 }
+
+// Lanes per row for the grouped passes and their grid.
+int gmm_lanes(int Kf) { return Kf <= 64 ? 8 : Kf <= 128 ? 16 : 32; }
+unsigned gmm_grid(int64_t rows, int L) { return (unsigned)ceil_div(rows, (int64_t)WARPS * (32 / L)); }
 
 // dmu / dsinv = sum over rows of the per-row partials, in a fixed order (deterministic):
 // stage 1: block b sums rows [b R, (b+1) R) -- thread t owns parameter t % n and rows
@@ -321,7 +361,11 @@ int gnncg_gmm_fwd(const gnncg_index_t* csr, int K, int r, int f, const float* Y,
   GNNCG_REQUIRE(csr->off && (csr->num_edges == 0 || csr->nbr) && Y && mu && sinv && out, GNNCG_ERR_ARG,
                 "gmm_fwd: null pointer");
   GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, nullptr, out, nullptr, nullptr};
-  gmm_fwd_kernel<<<(unsigned)ceil_div(csr->num_rows, WARPS), 256, 0, as_stream(stream)>>>(a);
+  const int L = gmm_lanes(K * f);
+  cudaStream_t s = as_stream(stream);
+  if (L == 8) gmm_fwd_kernel<8><<<gmm_grid(csr->num_rows, 8), 256, 0, s>>>(a);
+  else if (L == 16) gmm_fwd_kernel<16><<<gmm_grid(csr->num_rows, 16), 256, 0, s>>>(a);
+  else gmm_fwd_kernel<32><<<gmm_grid(csr->num_rows, 32), 256, 0, s>>>(a);
   GNNCG_LAUNCH_CHECK();
   return GNNCG_OK;
 }
@@ -355,12 +399,16 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr, const gnncg_index_t* csc, int K, int
                 "gmm_bwd: null pointer");
   GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, dOut, nullptr, dY,
             static_cast<float*>(ws)};
-  const unsigned grid = (unsigned)ceil_div(csr->num_rows, WARPS);
-  gmm_bwd_dst_kernel<<<grid, 256, 0, s>>>(a);
+  const int L = gmm_lanes(K * f);
+  if (L == 8) gmm_bwd_dst_kernel<8><<<gmm_grid(csr->num_rows, 8), 256, 0, s>>>(a);
+  else if (L == 16) gmm_bwd_dst_kernel<16><<<gmm_grid(csr->num_rows, 16), 256, 0, s>>>(a);
+  else gmm_bwd_dst_kernel<32><<<gmm_grid(csr->num_rows, 32), 256, 0, s>>>(a);
   GNNCG_LAUNCH_CHECK();
   a.off = csc->off;
   a.nbr = csc->nbr;
-  gmm_bwd_src_kernel<<<grid, 256, 0, s>>>(a);
+  if (L == 8) gmm_bwd_src_kernel<8><<<gmm_grid(csr->num_rows, 8), 256, 0, s>>>(a);
+  else if (L == 16) gmm_bwd_src_kernel<16><<<gmm_grid(csr->num_rows, 16), 256, 0, s>>>(a);
+  else gmm_bwd_src_kernel<32><<<gmm_grid(csr->num_rows, 32), 256, 0, s>>>(a);
   GNNCG_LAUNCH_CHECK();
   const int n = 2 * K * r, nblk = red_blocks(csr->num_rows);
   float* blk = a.part + align_up((size_t)csr->num_rows * n * sizeof(float)) / sizeof(float);

@@ -118,8 +118,10 @@ def test_edgeconv_layer_vs_oracle(cuda, k, C):
         assert O.max_rel_err(np64(got) / scale, bw[name] / scale) < TOL, name
 
 
+# K f picks K8's lanes per row: <= 64 -> 8 (4 rows per warp), <= 128 -> 16, else 32
 @pytest.mark.parametrize("V,E,Fin,K,r,f", [(200, 1500, 20, 3, 2, 16), (19717, 88648, 500, 3, 3, 16),
-                                           (500, 4000, 8, 2, 1, 16), (300, 2000, 10, 8, 4, 32)])
+                                           (500, 4000, 8, 2, 1, 16), (300, 2000, 10, 8, 4, 32),
+                                           (400, 6000, 12, 4, 3, 24), (350, 9000, 6, 1, 2, 5)])
 def test_gmm_layer_vs_oracle(cuda, V, E, Fin, K, r, f):
     rng = np.random.default_rng(V)
     src, dst = rng.integers(0, V, E), rng.integers(0, V, E)
