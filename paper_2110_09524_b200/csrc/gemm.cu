@@ -134,16 +134,40 @@ __global__ void __launch_bounds__(NT, 2)
   }
 }
 
-// C[m,n] = sum_z P[z][m][n] in ascending z (deterministic split-K merge).
-__global__ void splitk_reduce_kernel(int64_t M, int64_t N, int splits, const float* __restrict__ P, float* __restrict__ C,
-                                     int64_t ldc) {
+// C[m,n] = sum_z P[z][m][n] (deterministic split-K merge).
+#ifndef GNNCG_SPLITK_WARPS
+#define GNNCG_SPLITK_WARPS 8
+#endif
+// Split-K partials summed in a fixed order.  A block takes 32 outputs at a time; warp w adds splits
+// w, w + 8, ... (one coalesced 128-byte row per split) and the 8 warp sums are added in warp order.
+// (One thread per output walking all splits left each thread a chain of up to 64 loads: 14-16 us
+// per launch for the 8K-output weight gradients of EdgeConv / MoNet.)
+__global__ void __launch_bounds__(32 * GNNCG_SPLITK_WARPS) splitk_reduce_kernel(int64_t M, int64_t N, int splits,
+                                                                              const float* __restrict__ P,
+                                                                              float* __restrict__ C, int64_t ldc) {
+  constexpr int W = GNNCG_SPLITK_WARPS;
+  __shared__ float red[W][32];
+  const int lane = threadIdx.x & 31, w = threadIdx.x >> 5;
   const int64_t total = M * N;
-  for (int64_t i = blockIdx.x * (int64_t)blockDim.x + threadIdx.x; i < total; i += (int64_t)gridDim.x * blockDim.x) {
+  for (int64_t i0 = (int64_t)blockIdx.x * 32; i0 < total; i0 += (int64_t)gridDim.x * 32) {
+    const int64_t i = i0 + lane;
     float s = 0.f;
-    for (int z = 0; z < splits; ++z) s += P[(int64_t)z * total + i];
-    C[(i / N) * ldc + (i % N)] = s;
+    if (i < total) {
+#pragma unroll 4
+      for (int z = w; z < splits; z += W) s += P[(int64_t)z * total + i];
+    }
+    red[w][lane] = s;
+    __syncthreads();
+    if (w == 0 && i < total) {
+      float t = red[0][lane];
+#pragma unroll
+      for (int k = 1; k < W; ++k) t += red[k][lane];
+      C[(i / N) * ldc + (i % N)] = t;
+    }
+    __syncthreads();
   }
 }
+unsigned splitk_grid(int64_t total) { return (unsigned)std::min<int64_t>(ceil_div(total, (int64_t)32), 148 * 8); }
 
 int choose_splits(int64_t M, int64_t N, int64_t K) {
   const int64_t tiles = ceil_div(M, BM) * ceil_div(N, BN);
@@ -252,9 +276,8 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
                      AttnEpi{}, B_lo, ldb_lo);
     if (rc != GNNCG_OK) return rc;
     if (splits > 1) {
-      const int64_t total = M * N;
-      const int g = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
-      splitk_reduce_kernel<<<g, 256, 0, s>>>(M, N, splits, static_cast<float*>(ws), C, ldc);
+      splitk_reduce_kernel<<<splitk_grid(M * N), 32 * GNNCG_SPLITK_WARPS, 0, s>>>(M, N, splits, static_cast<float*>(ws),
+                                                                                C, ldc);
       GNNCG_LAUNCH_CHECK();
     }
     return GNNCG_OK;
@@ -274,9 +297,7 @@ int gnncg_gemm(int trans_a, int trans_b, int64_t M, int64_t N, int64_t K, const 
     sgemm_kernel<true, false><<<grid, NT, 0, s>>>(M, N, K, A, lda, B, ldb, out, ldo, kchunk, stride);
   GNNCG_LAUNCH_CHECK();
   if (splits > 1) {
-    const int64_t total = M * N;
-    const int g = (int)std::min<int64_t>(ceil_div(total, 256), 148 * 16);
-    splitk_reduce_kernel<<<g, 256, 0, s>>>(M, N, real_splits, out, C, ldc);
+    splitk_reduce_kernel<<<splitk_grid(M * N), 32 * GNNCG_SPLITK_WARPS, 0, s>>>(M, N, real_splits, out, C, ldc);
     GNNCG_LAUNCH_CHECK();
   }
   return GNNCG_OK;
