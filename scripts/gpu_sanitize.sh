@@ -16,7 +16,7 @@ echo "rc=$?" >> gpurun_out/san_gemm_$TAG.log
 for tool in memcheck racecheck synccheck; do
   timeout 900 compute-sanitizer --tool $tool --error-exitcode 99 --print-limit 20 \
     python -m pytest tests/test_gpu_edgeconv_gmm.py -q -x -p no:cacheprovider \
-    -k "1-64-8-33 or 2-128-10-96 or 2-256-20-128 or 200-1500 or 500-4000 or 12-36" > gpurun_out/san_ecgmm_${tool}_$TAG.log 2>&1
+    -k "1-64-8-33 or 2-128-10-96 or 2-256-20-128 or 200-1500 or 500-4000 or 12-36 or ragged or 400-6000 or 350-9000" > gpurun_out/san_ecgmm_${tool}_$TAG.log 2>&1
   echo "rc=$?" >> gpurun_out/san_ecgmm_${tool}_$TAG.log
 done
 # the work-counter item fetch of K2 / K4f forced on small graphs
