@@ -170,3 +170,41 @@ def test_edgeless_graph_edgeconv_and_gmm(cuda):
     for t in g2:
         if t is not None:
             assert torch.count_nonzero(t) == 0
+
+
+@pytest.mark.parametrize("C", [64, 128, 256])
+def test_edgeconv_column_alignment_paths_agree(cuda, C):
+    """K6 / K7 pick 32-byte columns for aligned tables and 16 / 8 / 4-byte ones for shifted views
+    (and with them the lanes per row); every column still walks its edges in the same order, so the
+    outputs are bitwise equal across the paths."""
+    from paper_2110_09524_b200._lib import call
+    from paper_2110_09524_b200.graph import _ptr, _stream
+
+    src, dst = knn_edges(2, 256, 20, seed=3)
+    V = 512
+    g = DeviceGraph.from_edges(V, src, dst, device=cuda)
+    rng = np.random.default_rng(C)
+    Th = t32((rng.integers(-8, 8, (V, C)) / 4.0).astype(np.float32), cuda)
+    Ph = t32(rng.uniform(-1, 1, (V, C)), cuda)
+    dOut = t32(rng.uniform(-1, 1, (V, C)), cuda)
+    ref_out, ref_amax = edgeconv_region_forward(g, Th, Ph)
+
+    def view(shift):
+        return torch.zeros(V, C + 8, device=cuda)[:, shift:shift + C]
+
+    def bwd(dTh, dPh):
+        call("gnncg_edgeconv_bwd", g.csc_src.struct(), g.csr_dst.struct(), C, _ptr(ref_amax), _ptr(dOut), _ptr(dTh),
+             dTh.stride(0), _ptr(dPh), dPh.stride(0), _stream())
+        torch.cuda.synchronize()
+        return dTh.clone(), dPh.clone()
+
+    base = bwd(torch.empty(V, C, device=cuda), torch.empty(V, C, device=cuda))
+    for shift in (1, 2, 4):  # 4 / 8 / 16-byte aligned rows
+        bt, bp = view(shift), view(shift)
+        bt.copy_(Th)
+        bp.copy_(Ph)
+        out, amax = edgeconv_region_forward(g, bt, bp)
+        torch.cuda.synchronize()
+        assert torch.equal(out, ref_out) and torch.equal(amax, ref_amax), shift
+        d = bwd(view(shift), view(shift))
+        assert torch.equal(d[0], base[0]) and torch.equal(d[1], base[1]), shift
