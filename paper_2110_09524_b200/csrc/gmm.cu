@@ -29,6 +29,7 @@ struct GmmArgs {
   int64_t ldy;
   const float *mu, *sinv, *dOut;
   float *out, *dY, *part;
+  bool vec4;  // f % 4 == 0 and 16-byte rows of Y / dOut: the per-edge f loops read float4s
 };
 
 // w_k of one edge: exp(-1/2 sum_t (pl_u + pr_v - mu_k)_t^2 sinv_kt^2).  k < K, t < r are runtime
@@ -57,7 +58,7 @@ __device__ __forceinline__ void load_p(const float* p, int r, float (&x)[MAXR]) 
 // sl, sl + L, ...).  On Pubmed-shaped layers (4.5 edges per row, K f = 48) a whole warp per row left
 // most lanes idle in the per-edge weight stage and most of the warp's latency uncovered.
 template <int L>
-struct GmmGroupSmem {
+struct alignas(16) GmmGroupSmem {
   uint32_t nb[L];
   float w[L * (MAXK + 1)];
   float red[8 * L];
@@ -138,7 +139,7 @@ __global__ void __launch_bounds__(256, 4) gmm_fwd_kernel(GmmArgs a) {
 // partials (2 K r <= 64 values) are reduced across the group per L-edge batch and accumulated in
 // the group's shared-memory slot in batch order.
 template <int L>
-struct GmmDstSmem {
+struct alignas(16) GmmDstSmem {
   float row[8 * L];
   float part[2 * MAXK * MAXR];
 };
@@ -168,13 +169,24 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
     load_p(y + Kf, r, plu);
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) dw[k] = 0.f;
-    if (valid)
+    if (valid && a.vec4) {
+      for (int c = 0; c < f; c += 4) {
+        const float4 g = *reinterpret_cast<const float4*>(sm.row + c);
+#pragma unroll
+        for (int k = 0; k < MAXK; ++k)
+          if (k < K) {
+            const float4 x = __ldg(reinterpret_cast<const float4*>(y + k * f + c));
+            dw[k] = fmaf(g.w, x.w, fmaf(g.z, x.z, fmaf(g.y, x.y, fmaf(g.x, x.x, dw[k]))));
+          }
+      }
+    } else if (valid) {
       for (int c = 0; c < f; ++c) {
         const float g = sm.row[c];
 #pragma unroll
         for (int k = 0; k < MAXK; ++k)
           if (k < K) dw[k] = fmaf(g, __ldg(y + k * f + c), dw[k]);
       }
+    }
 #pragma unroll
     for (int k = 0; k < MAXK; ++k) {
       if (k < K) {
@@ -239,11 +251,23 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
       const float* g = a.dOut + v * f;
 #pragma unroll
       for (int k = 0; k < MAXK; ++k) dw[k] = 0.f;
-      for (int c = 0; c < f; ++c) {
-        const float gc = __ldg(g + c);
+      if (a.vec4) {
+        for (int c = 0; c < f; c += 4) {
+          const float4 gc = __ldg(reinterpret_cast<const float4*>(g + c));
 #pragma unroll
-        for (int k = 0; k < MAXK; ++k)
-          if (k < K) dw[k] = fmaf(gc, sm.row[k * f + c], dw[k]);
+          for (int k = 0; k < MAXK; ++k)
+            if (k < K) {
+              const float4 x = *reinterpret_cast<const float4*>(sm.row + k * f + c);
+              dw[k] = fmaf(gc.w, x.w, fmaf(gc.z, x.z, fmaf(gc.y, x.y, fmaf(gc.x, x.x, dw[k]))));
+            }
+        }
+      } else {
+        for (int c = 0; c < f; ++c) {
+          const float gc = __ldg(g + c);
+#pragma unroll
+          for (int k = 0; k < MAXK; ++k)
+            if (k < K) dw[k] = fmaf(gc, sm.row[k * f + c], dw[k]);
+        }
       }
 #pragma unroll
       for (int k = 0; k < MAXK; ++k) {
@@ -360,7 +384,7 @@ int gnncg_gmm_fwd(const gnncg_index_t* csr, int K, int r, int f, const float* Y,
   if (csr->num_rows == 0) return GNNCG_OK;
   GNNCG_REQUIRE(csr->off && (csr->num_edges == 0 || csr->nbr) && Y && mu && sinv && out, GNNCG_ERR_ARG,
                 "gmm_fwd: null pointer");
-  GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, nullptr, out, nullptr, nullptr};
+  GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, nullptr, out, nullptr, nullptr, false};
   const int L = gmm_lanes(K * f);
   cudaStream_t s = as_stream(stream);
   if (L == 8) gmm_fwd_kernel<8><<<gmm_grid(csr->num_rows, 8), 256, 0, s>>>(a);
@@ -398,7 +422,8 @@ int gnncg_gmm_bwd(const gnncg_index_t* csr, const gnncg_index_t* csc, int K, int
                 GNNCG_ERR_ARG,
                 "gmm_bwd: null pointer");
   GmmArgs a{csr->num_rows, K, r, f, csr->off, csr->nbr, Y, ldy, mu, sinv, dOut, nullptr, dY,
-            static_cast<float*>(ws)};
+            static_cast<float*>(ws),
+            f % 4 == 0 && ldy % 4 == 0 && (uintptr_t)Y % 16 == 0 && (uintptr_t)dOut % 16 == 0};
   const int L = gmm_lanes(K * f);
   if (L == 8) gmm_bwd_dst_kernel<8><<<gmm_grid(csr->num_rows, 8), 256, 0, s>>>(a);
   else if (L == 16) gmm_bwd_dst_kernel<16><<<gmm_grid(csr->num_rows, 16), 256, 0, s>>>(a);
