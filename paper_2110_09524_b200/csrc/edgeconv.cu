@@ -18,7 +18,9 @@ namespace {
 
 constexpr uint32_t kNoEdge = 0xFFFFFFFFu;
 // Build-time A/B knobs (scripts/build_ab.sh): edges per gather batch forward / backward, 32-byte
-// column vectors, lane groups (0: one row per warp).
+// column vectors, lane groups (0: one row per warp), CTAs per SM the register allocation must allow
+// (4 forward / 5 backward: 64 / 48 registers, a few bytes of spill, more warps resident; C3 k = 20
+// step 0.787 -> 0.749 ms, k = 40 1.077 -> 1.025 ms on one box, profiles/r02_edgeconv_ab.txt).
 #ifndef GNNCG_EC_UF
 #define GNNCG_EC_UF 2
 #endif
@@ -30,6 +32,12 @@ constexpr uint32_t kNoEdge = 0xFFFFFFFFu;
 #endif
 #ifndef GNNCG_EC_GROUPS
 #define GNNCG_EC_GROUPS 1
+#endif
+#ifndef GNNCG_EC_MINB_FWD
+#define GNNCG_EC_MINB_FWD 4
+#endif
+#ifndef GNNCG_EC_MINB_BWD
+#define GNNCG_EC_MINB_BWD 5
 #endif
 
 template <int VW>
@@ -120,7 +128,7 @@ struct Group {
 // 0.761 ms, k = 40 1.218 -> 1.029 ms with the lane groups and 32-byte loads;
 // profiles/r02_edgeconv_ab.txt).  Edges are walked in the row's (edge-id) order.
 template <int VW, int L>
-__global__ void __launch_bounds__(256) edgeconv_fwd_kernel(int64_t rows, int C, int64_t row_base,
+__global__ void __launch_bounds__(256, GNNCG_EC_MINB_FWD) edgeconv_fwd_kernel(int64_t rows, int C, int64_t row_base,
                                                            const uint64_t* __restrict__ off,
                                                            const uint32_t* __restrict__ nbr,
                                                            const uint32_t* __restrict__ eid,
@@ -180,7 +188,7 @@ __global__ void __launch_bounds__(256) edgeconv_fwd_kernel(int64_t rows, int C, 
 // lane.  EAGER (the default; GNNCG_EC_EAGER=0 for the other) loads g with amax instead of after a
 // match: one dependent round trip per edge instead of two, for bytes that are L2-resident here.
 template <int VW, int L, bool EAGER>
-__global__ void __launch_bounds__(256) edgeconv_bwd_kernel(int64_t rows, int C, const uint64_t* __restrict__ soff,
+__global__ void __launch_bounds__(256, GNNCG_EC_MINB_BWD) edgeconv_bwd_kernel(int64_t rows, int C, const uint64_t* __restrict__ soff,
                                                            const uint32_t* __restrict__ snbr,
                                                            const uint32_t* __restrict__ seid,
                                                            const uint64_t* __restrict__ doff,
