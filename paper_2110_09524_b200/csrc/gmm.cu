@@ -19,6 +19,15 @@ namespace gnncg_b200 {
 namespace {
 
 constexpr int MAXK = 8, MAXR = 4, MAXKF = 256, WARPS = 8;
+// CTAs per SM the register allocation must allow (build-time A/B knobs): the backward passes spill
+// below 64 registers; the forward takes 48 at 5 CTAs without spilling (C4 step 0.304 -> 0.298 ms,
+// profiles/r02_gmm_ab.txt).
+#ifndef GNNCG_GMM_MINB
+#define GNNCG_GMM_MINB 4
+#endif
+#ifndef GNNCG_GMM_MINB_FWD
+#define GNNCG_GMM_MINB_FWD 5
+#endif
 
 struct GmmArgs {
   int64_t rows;
@@ -85,7 +94,7 @@ struct GmmGroup {
 };
 
 template <int L>
-__global__ void __launch_bounds__(256, 4) gmm_fwd_kernel(GmmArgs a) {
+__global__ void __launch_bounds__(256, GNNCG_GMM_MINB_FWD) gmm_fwd_kernel(GmmArgs a) {
   constexpr int NA = 8;  // accumulators per lane: K f <= 8 L
   __shared__ GmmGroupSmem<L> smem[WARPS * (32 / L)];
   const GmmGroup<L> grp;
@@ -145,7 +154,7 @@ struct alignas(16) GmmDstSmem {
 };
 
 template <int L>
-__global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
+__global__ void __launch_bounds__(256, GNNCG_GMM_MINB) gmm_bwd_dst_kernel(GmmArgs a) {
   __shared__ GmmDstSmem<L> smem[WARPS * (32 / L)];
   const GmmGroup<L> grp;
   GmmDstSmem<L>& sm = smem[grp.slot()];
@@ -221,7 +230,7 @@ __global__ void __launch_bounds__(256, 4) gmm_bwd_dst_kernel(GmmArgs a) {
 
 // pass 2 over csc_src, in lane groups (see gmm_fwd_kernel).
 template <int L>
-__global__ void __launch_bounds__(256, 4) gmm_bwd_src_kernel(GmmArgs a) {
+__global__ void __launch_bounds__(256, GNNCG_GMM_MINB) gmm_bwd_src_kernel(GmmArgs a) {
   constexpr int NA = 8;
   __shared__ GmmGroupSmem<L> smem[WARPS * (32 / L)];
   const GmmGroup<L> grp;
